@@ -1,0 +1,414 @@
+#!/usr/bin/env python3
+"""Benchmark: hybrid-dealiased convolution on B200 (BASELINE.json metric:
+"hybrid-dealiased conv output samples/s and % HBM roofline, 2D 4096^2 c128").
+
+Workload (BASELINE.json configs[2]): complex128
+4096x4096 image (re ~ U[0,1), im = 0) convolved with a 255x255 Gaussian kernel
+(sigma 40) plus 1e-3 uniform noise; full linear output 4350x4350.  A step is one
+complete hybrid-dealiased convolution (all three passes) through the C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--no-tune] [--no-cpu]
+
+N > 1 runs under torchrun (one process per GPU, NCCL); each rank convolves its
+own image (weak scaling, no data-path collective: the 2D problems are
+independent), timing is the max over ranks.  `--impl reference` times the CPU
+oracle (oracle/, plain direct convolution) on the host cores on a bounded
+sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "hybrid-dealiased conv output samples/s and % HBM roofline, 2D 4096² c128"
+UNIT = "output samples/s"
+FALLBACK_HBM = 6650.0
+
+
+# ---------------------------------------------------------------------------
+def workload(cfg: int):
+    d = synth.config_inputs(cfg)
+    f, g = d["f"], d["g"]
+    Lf, Lg = list(f[0].shape), list(g[0].shape)
+    Lout = [a + b - 1 for a, b in zip(Lf, Lg)]
+    name = {1: "config1_1d_c128_64x40", 2: "config2_1d_c128_batch4096_8192x3000",
+            3: "config3_2d_c128_4096sq_x_255sq_gauss", 4: "config4_3d_c64_512cube_x_129cube",
+            5: "config5_2d_c128_multiconv6_2048sq_x_1024x1536"}[cfg]
+    return d, f, g, Lf, Lg, Lout, name
+
+
+def alg_bytes(ndim, N, Lf, Lg, Lout, eb, batch=1):
+    """Algorithmic bytes per pass at minimal padding: each pass reads
+    its inputs once and writes its outputs once; intermediates sized by L_out."""
+    P = {}
+    if ndim == 1:
+        P["conv1d"] = batch * eb * N * (Lf[0] + Lg[0]) + batch * eb * Lout[0]
+    elif ndim == 2:
+        Xf = N * Lf[0] * Lout[1]
+        Xg = N * Lg[0] * Lout[1]
+        P["fwd_x_f"] = eb * (N * Lf[0] * Lf[1] + Xf)
+        P["fwd_x_g"] = eb * (N * Lg[0] * Lg[1] + Xg)
+        P["conv_y"] = eb * (Xf + Xg + Lout[0] * Lout[1])
+        P["inv_x"] = eb * 2 * Lout[0] * Lout[1]
+    else:
+        X1f = N * Lf[0] * Lf[1] * Lout[2]
+        X1g = N * Lg[0] * Lg[1] * Lout[2]
+        XYf = N * Lf[0] * Lout[1] * Lout[2]
+        XYg = N * Lg[0] * Lout[1] * Lout[2]
+        O3 = Lout[0] * Lout[1] * Lout[2]
+        P["fwd_x_f"] = eb * (N * np.prod(Lf) + X1f)
+        P["fwd_x_g"] = eb * (N * np.prod(Lg) + X1g)
+        P["fwd_y_f"] = eb * (X1f + XYf)
+        P["fwd_y_g"] = eb * (X1g + XYg)
+        P["conv_z"] = eb * (XYf + XYg + O3)
+        P["inv_y"] = eb * 2 * O3
+        P["inv_x"] = eb * 2 * O3
+    return {k: int(v) for k, v in P.items()}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_name):
+    """dram read+write bytes per launch of the kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("traffic_bytes_per_launch", {}).get(kernel_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms in the background."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.tmp = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def mark(self, which):
+        if which == 0:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.tmp.flush()
+        self.tmp.seek(0)
+        rows = [r.strip().split(", ") for r in self.tmp.read().splitlines() if r.strip()]
+        os.unlink(self.tmp.name)
+        sm, mx, reasons = [], [], set()
+        for r in rows:
+            try:
+                ts = time.mktime(time.strptime(r[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+            except Exception:
+                ts = None
+            if ts is not None and self.t0 is not None and not (self.t0 - 1.0 <= ts <= self.t1 + 1.0):
+                continue
+            try:
+                sm.append(float(r[2]))
+                mx.append(float(r[3]))
+            except Exception:
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_oracle_rate(f, g, Lout, target_s=12.0, seed=4242):
+    """Oracle (as it stands) on host cores: output samples/s on a bounded random
+    sample of output indices of the same workload."""
+    import oracle
+    n = 256
+    idx = synth.sample_indices(Lout, n_random=n, seed=seed, edge=0)
+    t = time.perf_counter()
+    oracle.multiconv_sampled(f, g, idx)
+    dt = time.perf_counter() - t
+    n2 = int(min(2_000_000, max(n, len(idx) * target_s / max(dt, 1e-6))))
+    idx = synth.sample_indices(Lout, n_random=n2, seed=seed + 1, edge=0)
+    t = time.perf_counter()
+    oracle.multiconv_sampled(f, g, idx)
+    dt = time.perf_counter() - t
+    return len(idx) / dt, len(idx), dt, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    d, f, g, Lf, Lg, Lout, name = workload(args.config)
+    import oracle
+    per_step = []
+    nsamp = None
+    # size each step to ~1/steps of a bounded budget
+    budget = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
+    rate0, n0, _, cores = cpu_oracle_rate(f, g, Lout, target_s=budget)
+    nsamp = n0
+    for s in range(args.warmup + args.steps):
+        idx = synth.sample_indices(Lout, n_random=nsamp, seed=9000 + s, edge=0)
+        t = time.perf_counter()
+        oracle.multiconv_sampled(f, g, idx)
+        dt = time.perf_counter() - t
+        if s >= args.warmup:
+            per_step.append((len(idx), dt))
+    tot_n = sum(n for n, _ in per_step)
+    tot_t = sum(t for _, t in per_step)
+    value = tot_n / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(per_step),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": name, "sample": f"{nsamp} random output indices per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{nsamp} random output samples per step of the {name} "
+                                   f"output (direct O(L_f L_g) sum per sample)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2306_10016_b200 import hdconv as H
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    d, f, g, Lf, Lg, Lout, name = workload(args.config)
+    ndim = d["ndim"]
+    N = len(f)
+    npdt = f[0].dtype
+    eb = 16 if npdt == np.complex128 else 8
+    dtc = H.HD_C128 if eb == 16 else H.HD_C64
+    batch = d["batch"] if ndim == 1 else 1
+    if ndim == 1:
+        Lf, Lg = [f[0].shape[-1]], [g[0].shape[-1]]
+        Lout = [Lf[0] + Lg[0] - 1]
+    ctx = H.Context(local_rank)
+    fh = [torch.from_numpy(a).pin_memory() for a in f]
+    gh = [torch.from_numpy(a).pin_memory() for a in g]
+    fd = [t.to(dev) for t in fh]
+    gd = [t.to(dev) for t in gh]
+    out_shape = ([batch] if ndim == 1 else []) + Lout
+    hd_ = torch.empty(out_shape, dtype=fd[0].dtype, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    tune_s = 0.0
+    plan = None
+    if d.get("plan"):
+        plan = H.Plan.make(ndim, [d["plan"]])
+    elif not args.no_tune:
+        t = time.perf_counter()
+        plan = ctx.tune(dtc, Lf, Lg, N=N, batch=batch, reps=3)
+        tune_s = time.perf_counter() - t
+    if plan is None:
+        plan = ctx.default_plan(dtc, Lf, Lg, npairs=N)
+    plan = H.hd_plan_complete(dtc, Lf, Lg, plan, npairs=N)
+
+    def step():
+        if N > 1:
+            ctx.multiconv(fd, gd, plan=plan, h=hd_)
+        else:
+            ctx.conv(fd[0], gd[0], plan=plan, h=hd_, batch=(ndim == 1))
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    for _ in range(args.warmup):
+        step()
+    # keep the clock sampler fed: >= 1 s of untimed load before timing
+    torch.cuda.synchronize()
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        step()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.profile_reset()
+    ctx.profile_enable(True)
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark(0)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark(1)
+    launches = ctx.launch_count() - l0
+    ctx.profile_enable(False)
+    prof = ctx.profile_read()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        dist.barrier()
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    clk = clocks.stop()
+    samples_per_step = batch * int(np.prod(Lout))
+    value = world * samples_per_step * args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (largest share of the step)
+    peak, peak_src = peaks()
+    ab = alg_bytes(ndim, N, Lf, Lg, Lout, eb, batch)
+    dom = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    roof = None
+    if dom:
+        dms, dl = prof[dom]
+        avg = dms / dl
+        achieved = ab.get(dom, 0) / (avg * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_src,
+                "alg_bytes_per_launch": ab.get(dom), "avg_launch_ms": avg,
+                "share_of_step": dms / sum(v[0] for v in prof.values())}
+    total_ab = sum(ab.values())
+    whole = {"alg_bytes_per_step": total_ab,
+             "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,
+             "frac_of_hbm": total_ab / (ms * 1e-3 / args.steps) / 1e9 / peak,
+             "per_kernel_ms": {k: v[0] / v[1] for k, v in prof.items()}}
+
+    # end to end through the host-buffer C-ABI entry point (copies inside)
+    e2e = None
+    if not args.no_e2e:
+        hh = torch.empty(out_shape, dtype=fd[0].dtype).pin_memory()
+        k2 = max(2, min(args.steps, 10))
+        ctx.hd_conv_host(fh, gh, hh, ndim=ndim, batch=batch, plan=plan)
+        if dist:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(k2):
+            ctx.hd_conv_host(fh, gh, hh, ndim=ndim, batch=batch, plan=plan)
+        te = time.perf_counter() - t
+        if dist:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * samples_per_step * k2 / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(a.nbytes for a in f) + sum(a.nbytes for a in g)),
+               "d2h_bytes_per_step": int(samples_per_step * eb), "steps": k2}
+
+    # explicit-padding GPU variant from the same kernels (context)
+    explicit = None
+    if not args.no_explicit and ndim >= 2:
+        try:
+            ctx.hd_conv_explicit(fd, gd, plan=plan, h=hd_)
+            torch.cuda.synchronize()
+            k3 = max(2, min(args.steps, 20))
+            e0.record(stream)
+            for _ in range(k3):
+                ctx.hd_conv_explicit(fd, gd, plan=plan, h=hd_)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            xms = e0.elapsed_time(e1) / k3
+            explicit = {"value": samples_per_step / (xms * 1e-3), "ms_per_step": xms,
+                        "hybrid_speedup": xms / (ms / args.steps)}
+        except Exception as ex:  # report, never hide
+            explicit = {"error": str(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, n, dt, cores = cpu_oracle_rate(f, g, Lout, target_s=args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{n} random output samples of {name} (direct sum per sample), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if eb == 16 else "f32",
+            "data": "synthetic",
+            "config": {"workload": name, "Lf": Lf, "Lg": Lg, "Lout": Lout, "pairs": N, "batch": batch,
+                       "plan": [{k: v for k, v in a.items()} for a in plan.as_dict()["axis"]],
+                       "tune_seconds": tune_s, "parallelism": f"weak x{world} (independent problems)",
+                       "l2": "inputs larger than L2 (image 268 MB > 126 MB L2); no flush needed"},
+            "roofline": roof, "whole_step": whole, "cpu_baseline": cpu, "e2e": e2e,
+            "explicit_variant": explicit, "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-explicit", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

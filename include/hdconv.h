@@ -1,0 +1,209 @@
+/*
+ * hdconv.h -- C ABI of libhdconv.so: hybrid-dealiased linear convolution
+ * (R. J. George, "Hybrid Dealiased Convolutions", arXiv 2306.10016) on NVIDIA
+ * B200 (sm_100a).
+ *
+ * The operation (Eq. 4, per axis per PAPER.md:716):
+ *     h = f * g,   h[o] = sum_a f[a] g[o - a],   extent L_f,i + L_g,i - 1,
+ * computed without materialised zero padding: each input of length L on an
+ * axis is explicitly padded to p*m (p = ceil(L/m)) and implicitly to
+ * M1 = q*m >= M >= L_f + L_g - 1 (q = ceil(M/m)) (hybrid padding,
+ * PAPER.md:641; parameters PAPER.md:564-567).  Per residue r < q the input is
+ * folded and pre-twiddled, w_s = zeta_{qm}^{rs} sum_t zeta_q^{rt} x_{tm+s}
+ * (Forward Eq. PAPER.md:528; Alg. "Forward Routine for 1D" PAPER.md:79-114),
+ * transformed by a size-m FFT, multiplied pointwise (and summed over pairs for
+ * multi-convolution), inverse transformed, untwiddled and accumulated into the
+ * outputs (Backward Eq. PAPER.md:531; Alg. "Backward Routine for 1D"
+ * PAPER.md:116-134; Alg. "Main Convolution for 1D" PAPER.md:136-204).
+ * N-D problems are separable passes along each axis.
+ *
+ * Conventions (all entry points):
+ *  - Complex data is interleaved (re, im): hd_dtype_t HD_C128 = 2 x double,
+ *    HD_C64 = 2 x float.  Arrays are row-major, last axis contiguous, batch
+ *    index outermost.  C128 buffers must be 16-byte aligned, C64 8-byte.
+ *  - Device entry points take caller-owned DEVICE pointers.  The library never
+ *    frees them; inputs are read-only; h must not alias f or g (out-of-place
+ *    only, the paper's I parameter is unsupported).
+ *  - Calls are asynchronous and ordered on `stream` (a cudaStream_t, NULL =
+ *    legacy default stream).  Kernel faults surface at the next sync.
+ *  - Status codes only; nothing is thrown across the ABI.  On any validation
+ *    failure h is left untouched and hd_last_error() describes the problem.
+ *  - Either input may be the longer one on any axis (convolution commutes,
+ *    PAPER.md:680 "we can always call the larger array g").
+ *  - M[i] = 0 selects the minimal padding M = L_f + L_g - 1 on axis i; a
+ *    non-zero M[i] must satisfy M[i] >= L_f,i + L_g,i - 1 (aliases are removed
+ *    only then) unless HD_FLAG_ALLOW_ALIAS is set.
+ *  - plan = NULL uses the tuned plan cached for this problem, else a default
+ *    plan; an explicit plan is honoured exactly (fields p_f, p_g, q, M1 are
+ *    recomputed and returned by hd_plan_complete).
+ *  - ws = NULL lets the context allocate (and cache) the workspace; otherwise
+ *    ws_bytes must be >= hd_workspace_bytes() for the same arguments.
+ *  - No CPU fallback exists: without a CUDA device every compute call returns
+ *    HD_ERR_CUDA.
+ */
+#ifndef HDCONV_H
+#define HDCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HD_ABI_VERSION 1
+#define HD_MAX_DIM 3
+#define HD_MAX_PAIRS 16
+
+typedef enum { HD_C64 = 1, HD_C128 = 2 } hd_dtype_t;
+
+typedef enum {
+  HD_OK = 0,
+  HD_ERR_INVALID = 1,      /* bad sizes, pointers, plan */
+  HD_ERR_UNSUPPORTED = 2,  /* valid request this build does not implement */
+  HD_ERR_CUDA = 3,         /* CUDA runtime error (or no device) */
+  HD_ERR_NCCL = 4,         /* reserved for the distributed entry points */
+  HD_ERR_WORKSPACE = 5     /* caller workspace too small */
+} hd_status_t;
+
+/* Plan flags */
+#define HD_FLAG_ALLOW_ALIAS 0x1u   /* test-only: accept M1 < L_out (aliased output, extent min(M1, L_out)) */
+#define HD_FLAG_SHARED_G    0x2u   /* batch > 1: one g shared by every batch entry */
+
+/* Per-axis parameters (L, M, C, m, D per dimension).
+ *  m  : FFT size, a power of two in [2, 4096]
+ *  p_f, p_g : ceil(L_f/m), ceil(L_g/m) (derived, PAPER.md:684-685 with Lambda = 1)
+ *  q  : ceil(M/m) residues (derived from M and m)
+ *  C  : lines (FFT copies) per CTA in passes along this axis when it
+ *       is the contiguous axis; S: lines per CTA (= tile width of the transposed
+ *       intermediate it reads) when the axis is strided.  1, 2, 4, 8 or 16.
+ *  D  : residues per group, 1 <= D <= q (0 = q)
+ *  M1 : q*m (derived) */
+typedef struct {
+  int32_t m, p_f, p_g, q, C, S, D, threads;
+  int64_t M1;
+} hd_axis_plan_t;
+
+typedef struct {
+  int32_t ndim;
+  uint32_t flags;
+  hd_axis_plan_t axis[HD_MAX_DIM];
+  double tuned_seconds;   /* median seconds of the plan when chosen by hd_tune, else 0 */
+} hd_plan_t;
+
+typedef struct hd_ctx* hd_ctx_t;  /* owns twiddle tables, plan cache, scratch; one device */
+
+/* ---- context --------------------------------------------------------------- */
+int         hd_abi_version(void);
+/* Create a context bound to CUDA device `device`.  Returns HD_ERR_CUDA if the
+ * device cannot be selected (e.g. no GPU).  *ctx is NULL on failure. */
+hd_status_t hd_create(hd_ctx_t* ctx, int device);
+hd_status_t hd_destroy(hd_ctx_t ctx);
+/* Message for the last failure on this context (or of hd_create when ctx is NULL). */
+const char* hd_last_error(hd_ctx_t ctx);
+
+/* ---- plans (host only, no GPU needed) -------------------------------------- */
+/* Default plan for a problem: per-axis m, C/S, D chosen by a static cost model.
+ * Lf, Lg, M: ndim extents each (M may be NULL = minimal). */
+hd_status_t hd_plan_default(hd_dtype_t dtype, int32_t ndim, int32_t npairs,
+                            const int64_t* Lf, const int64_t* Lg, const int64_t* M,
+                            hd_plan_t* out);
+/* Validate a plan against a problem and fill its derived fields (p_f, p_g, q, M1,
+ * D = 0 -> q).  Returns HD_ERR_INVALID with a message on inadmissible plans. */
+hd_status_t hd_plan_complete(hd_dtype_t dtype, int32_t ndim, int32_t npairs,
+                             const int64_t* Lf, const int64_t* Lg, const int64_t* M,
+                             hd_plan_t* plan);
+/* Internal spectral order: the forward transforms write residue r's size-m FFT
+ * output in digit-reversed order.  perm[pos] = l means slot pos of a residue
+ * block holds frequency q*l + r.  (perm has m entries.) */
+hd_status_t hd_spectral_permutation(int32_t m, int32_t* perm);
+
+/* Bytes of scratch the device entry points need for these arguments. */
+size_t hd_workspace_bytes(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t npairs,
+                          int64_t batch, const int64_t* Lf, const int64_t* Lg,
+                          const int64_t* M, const hd_plan_t* plan);
+
+/* ---- convolution (device pointers) ----------------------------------------- */
+/* 1D: batch independent pairs; f is [batch][Lf], g is [batch][Lg] (or [Lg] with
+ * HD_FLAG_SHARED_G), h is [batch][Lf+Lg-1]. */
+hd_status_t hd_conv1d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch,
+                      const void* f, int64_t Lf, const void* g, int64_t Lg,
+                      void* h, int64_t M, const hd_plan_t* plan,
+                      void* ws, size_t ws_bytes, void* stream);
+/* 2D: f [batch][Lf0][Lf1], g [batch][Lg0][Lg1], h [batch][Lf0+Lg0-1][Lf1+Lg1-1]. */
+hd_status_t hd_conv2d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch,
+                      const void* f, const int64_t Lf[2], const void* g, const int64_t Lg[2],
+                      void* h, const int64_t M[2], const hd_plan_t* plan,
+                      void* ws, size_t ws_bytes, void* stream);
+/* 3D: as 2D with three extents. */
+hd_status_t hd_conv3d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch,
+                      const void* f, const int64_t Lf[3], const void* g, const int64_t Lg[3],
+                      void* h, const int64_t M[3], const hd_plan_t* plan,
+                      void* ws, size_t ws_bytes, void* stream);
+/* Multi-convolution h = sum_{k<N} f[k] * g[k] (reading R9); every f[k]
+ * has extents Lf, every g[k] extents Lg; ndim in {1,2,3}; 1 <= N <= HD_MAX_PAIRS.
+ * f and g are host arrays of N device pointers. */
+hd_status_t hd_multiconv(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                         const void* const* f, const int64_t* Lf,
+                         const void* const* g, const int64_t* Lg,
+                         void* h, const int64_t* M, const hd_plan_t* plan,
+                         void* ws, size_t ws_bytes, void* stream);
+/* Explicit-dealiasing baseline: materialise zero padding to
+ * M_exp,i = next power of two >= L_f,i + L_g,i - 1 and run the same kernels with
+ * p = q (no pruned blocks); same output as hd_multiconv.  Measurement only. */
+hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                             const void* const* f, const int64_t* Lf,
+                             const void* const* g, const int64_t* Lg,
+                             void* h, const hd_plan_t* plan, void* stream);
+
+/* ---- end-to-end with HOST buffers ------------------------------------------ */
+/* Same as hd_multiconv with batch (N = 1 for plain conv) but f, g, h are HOST
+ * pointers (pinned for best speed).  Copies in, convolves, copies out and
+ * synchronises `stream` before returning.  Device buffers are context-owned. */
+hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                         int64_t batch, const void* const* f, const int64_t* Lf,
+                         const void* const* g, const int64_t* Lg, void* h,
+                         const int64_t* M, const hd_plan_t* plan, void* stream);
+
+/* ---- the paper's residue routines, batched (device pointers) --------------- */
+/* Forward: for each of nlines lines x[l][0..L) compute every residue block
+ * X[l][r*m + pos] = F_{q*perm[pos] + r} of x zero-padded to q*m (
+ * Alg. Forward PAPER.md:79-114 with lambda = 1). X is [nlines][q*m]. */
+hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
+                                const void* x, int64_t L, int32_t m, int32_t q,
+                                void* X, void* stream);
+/* Backward: x[l][j] = sum over residues of the Backward Eq. without
+ * the 1/(qm) factor, for j < Lout <= q*m (Alg. Backward).  Input
+ * in the internal order hd_forward_residues writes. */
+hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
+                                 const void* X, int32_t m, int32_t q, void* x,
+                                 int64_t Lout, void* stream);
+
+/* ---- tuning (the paper's "experience") -------------------- */
+#define HD_TUNE_PER_AXIS   0x0u   /* search each axis independently */
+#define HD_TUNE_EXHAUSTIVE 0x1u   /* full cross product (grid search A0) */
+/* Time candidate plans on the device (CUDA events, 2 warm-ups, median of `reps`
+ * >= 1 runs; 0 = 5) and return the fastest; ties break lexicographically on
+ * (m, C, S, D).  Inputs are synthetic scratch of the problem's shape.  The
+ * result is cached in the context for plan = NULL calls on the same problem. */
+hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                    int64_t batch, const int64_t* Lf, const int64_t* Lg, const int64_t* M,
+                    uint32_t flags, int32_t reps, void* stream, hd_plan_t* out);
+/* Number of candidates evaluated by the last hd_tune and their (plan, seconds). */
+int32_t     hd_tune_log(hd_ctx_t ctx, int32_t max, hd_plan_t* plans, double* seconds);
+
+/* ---- measurement hooks ------------------------------------------------------ */
+/* When enabled, each kernel launch of the compute entry points is bracketed by
+ * CUDA events on its stream; hd_profile_read returns (after a stream sync by the
+ * caller) the accumulated per-pass milliseconds, launch counts and names. */
+hd_status_t hd_profile_enable(hd_ctx_t ctx, int32_t enable);
+int32_t     hd_profile_read(hd_ctx_t ctx, int32_t max, double* ms, int64_t* launches,
+                            char* names /* max x 32 bytes */);
+hd_status_t hd_profile_reset(hd_ctx_t ctx);
+/* Total kernel launches issued by this context since creation. */
+int64_t     hd_launch_count(hd_ctx_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDCONV_H */

@@ -1,0 +1,1123 @@
+// hd_api.cu -- host side of libhdconv.so: plans,
+// twiddle tables, the multi-pass drivers for 1D/2D/3D/multiconv
+// (PAPER.md:716-739, 1438-1489), the explicit baseline, the
+// on-device tuning sweep and the C ABI (include/hdconv.h).
+#include "hdconv.h"
+#include "hd_device.cuh"
+#include "hd_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using hd::LineIn;
+using hd::LineOut;
+using hd::PassArgs;
+
+namespace {
+thread_local std::string g_tls_error;
+constexpr int kDefaultThreads = 256;
+constexpr int64_t kHugeTile = int64_t(1) << 30;
+}  // namespace
+
+struct hd_ctx {
+  int device = 0;
+  std::string err;
+  std::mutex mu;
+  std::map<int64_t, void*> tw64, tw32;  // N -> device zeta_N^k tables
+  void* ws = nullptr;
+  size_t ws_size = 0;
+  void* io = nullptr;                   // device buffers for hd_conv_host
+  size_t io_size = 0;
+  std::map<std::string, hd_plan_t> plan_cache;
+  std::vector<std::pair<hd_plan_t, double>> tune_log;
+  // profiling
+  bool profiling = false;
+  struct ProfEntry {
+    std::string name;
+    double ms = 0;
+    int64_t launches = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+  };
+  std::vector<ProfEntry> prof;
+  int64_t launches = 0;
+};
+
+namespace {
+
+hd_status_t fail(hd_ctx* ctx, hd_status_t st, const std::string& msg) {
+  if (ctx) ctx->err = msg; else g_tls_error = msg;
+  g_tls_error = msg;
+  return st;
+}
+hd_status_t cuda_fail(hd_ctx* ctx, cudaError_t e, const char* what) {
+  return fail(ctx, HD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int ilog2(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
+size_t elem_bytes(hd_dtype_t dt) { return dt == HD_C128 ? 16 : 8; }
+
+// ---------------------------------------------------------------------------
+// twiddle tables zeta_N^k = exp(2 pi i k / N), k < N, computed in long double
+// with the integer k reduced to the first octant's symmetric argument.
+// ---------------------------------------------------------------------------
+void host_twiddles(int64_t N, std::vector<double>& out) {
+  out.resize(2 * N);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int64_t k = 0; k < N; ++k) {
+    // reduce: angle = 2 pi k / N; use k' = min(k, N-k) for accuracy of sin/cos
+    long double ang = two_pi * (long double)k / (long double)N;
+    long double c = cosl(ang), s = sinl(ang);
+    if (4 * k == N) { c = 0; s = 1; }
+    if (2 * k == N) { c = -1; s = 0; }
+    if (4 * k == 3 * N) { c = 0; s = -1; }
+    out[2 * k] = (double)c;
+    out[2 * k + 1] = (double)s;
+  }
+}
+
+hd_status_t get_table(hd_ctx* ctx, int64_t N, bool dbl, const void** out) {
+  auto& cache = dbl ? ctx->tw64 : ctx->tw32;
+  auto it = cache.find(N);
+  if (it != cache.end()) { *out = it->second; return HD_OK; }
+  std::vector<double> h;
+  host_twiddles(N, h);
+  void* d = nullptr;
+  size_t bytes = dbl ? 16 * (size_t)N : 8 * (size_t)N;
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(twiddles)");
+  if (dbl) {
+    e = cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice);
+  } else {
+    std::vector<float> hf(2 * N);
+    for (int64_t i = 0; i < 2 * N; ++i) hf[i] = (float)h[i];
+    e = cudaMemcpy(d, hf.data(), bytes, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) { cudaFree(d); return cuda_fail(ctx, e, "cudaMemcpy(twiddles)"); }
+  cache[N] = d;
+  *out = d;
+  return HD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+struct AxisInfo {
+  int64_t Lf, Lg, Lout, M, M1, O;  // O: output extent (Lout, or M1 if aliased)
+  int m, q, pf, pg, T, C, S, D, lines, threads;
+};
+
+// lines per CTA used by passes along axis i: C on the contiguous axis, S otherwise
+int lines_for(const hd_axis_plan_t& a, int i, int ndim) { return i == ndim - 1 ? a.C : a.S; }
+
+int64_t round_slots(int64_t n, size_t eb) {
+  const int64_t epr = 128 / (int64_t)eb;
+  return (n + 8 * epr - 1) / (8 * epr) * (8 * epr);
+}
+size_t pass_smem(size_t eb, int q, int lines, int D, int m, int nbuf) {
+  return eb * (size_t)(round_slots(q, eb) + nbuf * round_slots((int64_t)lines * D * m, eb));
+}
+int conv_nbuf(int npairs) { return npairs == 1 ? 2 : 3; }
+
+bool valid_lines(int v) { return v == 1 || v == 2 || v == 4 || v == 8 || v == 16; }
+
+hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const int64_t* Lf,
+                          const int64_t* Lg, const int64_t* M, hd_plan_t* plan, AxisInfo* ax) {
+  if (dt != HD_C64 && dt != HD_C128) return fail(ctx, HD_ERR_INVALID, "dtype must be HD_C64 or HD_C128");
+  if (ndim < 1 || ndim > HD_MAX_DIM) return fail(ctx, HD_ERR_INVALID, "ndim must be 1, 2 or 3");
+  if (npairs < 1 || npairs > HD_MAX_PAIRS) return fail(ctx, HD_ERR_INVALID, "N must be in [1, 16]");
+  if (plan->ndim != ndim) return fail(ctx, HD_ERR_INVALID, "plan.ndim does not match ndim");
+  const size_t eb = elem_bytes(dt);
+  for (int i = 0; i < ndim; ++i) {
+    hd_axis_plan_t& a = plan->axis[i];
+    AxisInfo& x = ax[i];
+    if (Lf[i] < 1 || Lg[i] < 1) return fail(ctx, HD_ERR_INVALID, "extents must be >= 1");
+    x.Lf = Lf[i]; x.Lg = Lg[i];
+    x.Lout = Lf[i] + Lg[i] - 1;
+    x.M = (M && M[i] > 0) ? M[i] : x.Lout;
+    if (!is_pow2(a.m) || a.m < 2 || a.m > 4096)
+      return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": m must be a power of two in [2, 4096]");
+    x.m = a.m;
+    x.q = (int)cdiv(x.M, a.m);
+    x.M1 = (int64_t)x.q * a.m;
+    if (x.M1 < x.Lout && !(plan->flags & HD_FLAG_ALLOW_ALIAS))
+      return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": M < L_f + L_g - 1 would alias (PAPER.md:592)");
+    x.O = std::min(x.Lout, x.M1);
+    x.pf = (int)cdiv(x.Lf, a.m);
+    x.pg = (int)cdiv(x.Lg, a.m);
+    x.T = (int)cdiv(x.O, a.m);
+    if (a.C == 0) a.C = 1;
+    if (a.S == 0) a.S = 1;
+    if (!valid_lines(a.C) || !valid_lines(a.S)) return fail(ctx, HD_ERR_INVALID, "C and S must be 1, 2, 4, 8 or 16");
+    x.C = a.C; x.S = a.S;
+    if (a.D == 0) a.D = x.q;
+    if (a.D < 1 || a.D > x.q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
+    x.D = a.D;
+    if (a.threads == 0) a.threads = kDefaultThreads;
+    if (a.threads != kDefaultThreads) return fail(ctx, HD_ERR_UNSUPPORTED, "threads must be 256 in this build");
+    x.threads = a.threads;
+    x.lines = lines_for(a, i, ndim);
+    const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
+    if (pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
+      return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": lines*D*m too large for shared memory");
+    a.p_f = x.pf; a.p_g = x.pg; a.q = x.q; a.M1 = x.M1;
+  }
+  if (ndim == 3 && plan->axis[0].S != plan->axis[1].S)
+    return fail(ctx, HD_ERR_INVALID, "3D plans need S equal on axes 0 and 1");
+  return HD_OK;
+}
+
+// static cost model for the default plan (per line of the axis)
+double axis_cost(int64_t Lf, int64_t Lg, int64_t Lout, int64_t M, int m, bool conv) {
+  const int64_t q = cdiv(M, m), M1 = q * m;
+  const int64_t pf = cdiv(Lf, m), pg = cdiv(Lg, m), T = cdiv(Lout, m);
+  double fold = (double)M1 * (double)(pf + pg);
+  double fft = (double)M1 * 3.0 * 1.25 * ilog2(m);
+  double unfold = (double)T * m * (double)q;
+  double bytes = conv ? 0.0 : 10.0 * (double)M1;
+  return fold + fft + unfold + bytes;
+}
+
+hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const int64_t* Lf,
+                         const int64_t* Lg, const int64_t* M, hd_plan_t* out) {
+  if (ndim < 1 || ndim > HD_MAX_DIM) return fail(ctx, HD_ERR_INVALID, "ndim must be 1, 2 or 3");
+  const size_t eb = elem_bytes(dt);
+  hd_plan_t p;
+  std::memset(&p, 0, sizeof(p));
+  p.ndim = ndim;
+  for (int i = 0; i < ndim; ++i) {
+    if (Lf[i] < 1 || Lg[i] < 1) return fail(ctx, HD_ERR_INVALID, "extents must be >= 1");
+    const int64_t Lout = Lf[i] + Lg[i] - 1;
+    const int64_t Mi = (M && M[i] > 0) ? M[i] : Lout;
+    const bool conv = (i == 0);
+    const int nbuf = conv ? conv_nbuf(npairs) : 1;
+    const int lines = (ndim == 1) ? 1 : 2;
+    double best = 1e300;
+    int bm = 2, bD = 1;
+    for (int m = 2; m <= 4096; m *= 2) {
+      const int q = (int)cdiv(Mi, m);
+      int D = q;
+      while (D > 1 && pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) --D;
+      if (pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) continue;
+      double c = axis_cost(Lf[i], Lg[i], Lout, Mi, m, conv);
+      const int groups = (int)cdiv(q, D);
+      if (groups > 1) c += (double)(groups - 1) * (double)(Lf[i] + Lg[i] + 2 * Lout) * 4.0;
+      if (c < best) { best = c; bm = m; bD = D; }
+    }
+    p.axis[i].m = bm;
+    p.axis[i].D = bD;
+    p.axis[i].C = (i == ndim - 1) ? lines : 1;
+    p.axis[i].S = (i == ndim - 1) ? 1 : lines;
+    p.axis[i].threads = kDefaultThreads;
+  }
+  if (ndim == 3) p.axis[1].S = p.axis[0].S;
+  *out = p;
+  return HD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// launching
+// ---------------------------------------------------------------------------
+struct Launch {
+  int mode;
+  const char* name;
+  PassArgs a;
+  int m, lines, nbuf, threads;
+  int64_t ngroups, nbatch, narrays;
+};
+
+void init_in(LineIn& in) { std::memset(&in, 0, sizeof(in)); in.nbi = 1; }
+void init_out(LineOut& o) { std::memset(&o, 0, sizeof(o)); o.nbi = 1; o.So = 1; }
+
+hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
+  const bool dbl = dt == HD_C128;
+  hd::LaunchFn fn = hd::lookup_launcher(dbl, L.m, L.mode, L.threads);
+  if (!fn) return fail(ctx, HD_ERR_UNSUPPORTED, "no kernel instantiation for this m/threads");
+  const size_t smem = pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf);
+  if (smem > hd::kMaxSmem) return fail(ctx, HD_ERR_INVALID, "pass shared memory exceeds 227 KB");
+  dim3 grid;
+  if (L.a.batch_fastest) { grid.x = (unsigned)L.nbatch; grid.y = (unsigned)L.ngroups; }
+  else { grid.x = (unsigned)L.ngroups; grid.y = (unsigned)L.nbatch; }
+  grid.z = (unsigned)L.narrays;
+  if (grid.y > 65535 || grid.z > 65535 || L.ngroups < 1 || L.nbatch < 1)
+    return fail(ctx, HD_ERR_UNSUPPORTED, "grid too large for one launch");
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+  }
+  cudaError_t e = fn(L.a, grid, smem, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, L.name);
+  ctx->launches += 1;
+  if (ctx->profiling) {
+    cudaEventRecord(e1, st);
+    hd_ctx::ProfEntry* pe = nullptr;
+    for (auto& p : ctx->prof) if (p.name == L.name) pe = &p;
+    if (!pe) { ctx->prof.push_back({}); pe = &ctx->prof.back(); pe->name = L.name; }
+    pe->pending.push_back({e0, e1});
+    pe->launches += 1;
+  }
+  return HD_OK;
+}
+}  // namespace
+
+namespace {
+
+struct Problem {
+  hd_dtype_t dt = HD_C128;
+  int ndim = 1, N = 1;
+  int64_t batch = 1;
+  bool shared_g = false;
+  const void* f[HD_MAX_PAIRS] = {};
+  const void* g[HD_MAX_PAIRS] = {};
+  void* h = nullptr;
+  AxisInfo ax[HD_MAX_DIM] = {};
+  hd_plan_t plan{};
+};
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+// Workspace regions (elements) of the multi-pass pipeline; returns total bytes.
+size_t ws_regions(const Problem& P, std::vector<int64_t>& elems) {
+  elems.clear();
+  const int64_t B = P.batch, Bg = P.shared_g ? 1 : P.batch;
+  const AxisInfo* a = P.ax;
+  if (P.ndim == 2) {
+    const int64_t Kx = a[1].M1, Cx = a[1].lines;
+    const int64_t Oyp = cdiv(a[0].O, Cx) * Cx;
+    for (int k = 0; k < P.N; ++k) elems.push_back(B * Kx * a[0].Lf);
+    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * Kx * a[0].Lg);
+    elems.push_back(B * Oyp * Kx);
+  } else if (P.ndim == 3) {
+    const int64_t Kx = a[2].M1, Ky = a[1].M1, Cx = a[2].lines;
+    const int64_t Oyp = cdiv(a[1].O, Cx) * Cx;
+    for (int k = 0; k < P.N; ++k) elems.push_back(B * a[0].Lf * Kx * a[1].Lf);
+    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * a[0].Lg * Kx * a[1].Lg);
+    for (int k = 0; k < P.N; ++k) elems.push_back(B * Ky * Kx * a[0].Lf);
+    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * Ky * Kx * a[0].Lg);
+    elems.push_back(B * a[0].O * Kx * Ky);
+    elems.push_back(B * a[0].O * Oyp * Kx);
+  }
+  size_t total = 0;
+  for (int64_t e : elems) total += align256((size_t)e * elem_bytes(P.dt));
+  return total;
+}
+
+Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, int axis,
+                   const void* twm, const void* twM1) {
+  const AxisInfo& x = P.ax[axis];
+  Launch L;
+  std::memset(&L, 0, sizeof(L));
+  L.mode = mode;
+  L.name = name;
+  L.m = x.m;
+  L.lines = x.lines;
+  L.threads = x.threads;
+  L.nbuf = (mode == hd::MODE_CONV) ? conv_nbuf(P.N) : 1;
+  init_in(L.a.in_f);
+  init_in(L.a.in_g);
+  init_out(L.a.out);
+  L.a.tw_m = twm;
+  L.a.tw_M1 = twM1;
+  L.a.q = x.q;
+  L.a.D = x.D;
+  L.a.C = x.lines;
+  L.a.M1 = x.M1;
+  L.a.npairs = (mode == hd::MODE_CONV) ? P.N : 1;
+  L.a.scale = 1.0;
+  L.narrays = 1;
+  (void)ctx;
+  return L;
+}
+
+hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const bool dbl = P.dt == HD_C128;
+  const size_t eb = elem_bytes(P.dt);
+  const void* twm[HD_MAX_DIM] = {};
+  const void* twM1[HD_MAX_DIM] = {};
+  for (int i = 0; i < P.ndim; ++i) {
+    hd_status_t s = get_table(ctx, P.ax[i].m, dbl, &twm[i]);
+    if (s != HD_OK) return s;
+    s = get_table(ctx, P.ax[i].M1, dbl, &twM1[i]);
+    if (s != HD_OK) return s;
+  }
+  double scale = 1.0;
+  for (int i = 0; i < P.ndim; ++i) scale /= (double)P.ax[i].M1;
+
+  std::vector<int64_t> el;
+  const size_t need = ws_regions(P, el);
+  if (need > 0) {
+    if (!ws) {
+      if (ctx->ws_size < need) {
+        if (ctx->ws) cudaFree(ctx->ws);
+        ctx->ws = nullptr; ctx->ws_size = 0;
+        cudaError_t e = cudaMalloc(&ctx->ws, need);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(workspace)");
+        ctx->ws_size = need;
+      }
+      ws = ctx->ws;
+    } else if (ws_bytes < need) {
+      return fail(ctx, HD_ERR_WORKSPACE, "workspace too small");
+    }
+  }
+  std::vector<char*> reg;
+  {
+    char* base = (char*)ws;
+    for (int64_t e : el) { reg.push_back(base); base += align256((size_t)e * eb); }
+  }
+  const int64_t B = P.batch, Bg = P.shared_g ? 1 : P.batch;
+  const int N = P.N;
+  const AxisInfo* a = P.ax;
+
+  if (P.ndim == 1) {
+    const AxisInfo& x = a[0];
+    Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv1d", 0, twm[0], twM1[0]);
+    const int64_t c = x.lines;
+    for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = P.f[k]; L.a.in_g.ptr[k] = P.g[k]; }
+    L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; L.a.in_f.s_g = c * x.Lf; L.a.in_f.s_c = x.Lf; L.a.in_f.s_j = 1;
+    L.a.in_g.L = x.Lg; L.a.in_g.p = x.pg;
+    L.a.in_g.s_g = P.shared_g ? 0 : c * x.Lg; L.a.in_g.s_c = P.shared_g ? 0 : x.Lg; L.a.in_g.s_j = 1;
+    L.a.out.ptr[0] = P.h; L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.So = (int32_t)kHugeTile;
+    L.a.out.s_g = c * x.O; L.a.out.s_c = x.O; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+    L.a.scale = scale;
+    L.a.nlines = B; L.a.nbatch = 1;
+    L.a.in_f.nbi = L.a.in_g.nbi = L.a.out.nbi = 1;
+    L.ngroups = cdiv(B, c); L.nbatch = 1;
+    return launch(ctx, P.dt, L, st);
+  }
+
+  if (P.ndim == 2) {
+    const AxisInfo &y = a[0], &x = a[1];
+    const int64_t Kx = x.M1, Cx = x.lines, Sy = y.lines;
+    const int64_t Oyp = cdiv(y.O, Cx) * Cx;
+    char** Xf = &reg[0];
+    char** Xg = &reg[N];
+    char* Y = reg[2 * N];
+    // pass A: forward along x for the rows of every f_k, then every g_k
+    for (int which = 0; which < 2; ++which) {
+      const int64_t rows = which == 0 ? y.Lf : y.Lg;
+      const int64_t len = which == 0 ? x.Lf : x.Lg;
+      const int64_t nb = which == 0 ? B : Bg;
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_x_f" : "fwd_x_g", 1, twm[1], twM1[1]);
+      for (int k = 0; k < N; ++k) {
+        L.a.in_f.ptr[k] = which == 0 ? P.f[k] : P.g[k];
+        L.a.out.ptr[k] = which == 0 ? Xf[k] : Xg[k];
+      }
+      L.a.in_f.L = len; L.a.in_f.p = which == 0 ? x.pf : x.pg;
+      L.a.in_f.nbi = nb; L.a.in_f.s_b = rows * len; L.a.in_f.s_g = Cx * len; L.a.in_f.s_c = len; L.a.in_f.s_j = 1;
+      L.a.out.nbi = nb; L.a.out.s_b = Kx * rows; L.a.out.s_g = Cx * Sy; L.a.out.s_c = Sy;
+      L.a.out.So = (int32_t)Sy; L.a.out.s_jt = rows * Sy; L.a.out.s_js = 1; L.a.out.L = Kx;
+      L.a.nlines = rows; L.a.nbatch = nb;
+      L.ngroups = cdiv(rows, Cx); L.nbatch = nb; L.narrays = N;
+      hd_status_t s = launch(ctx, P.dt, L, st);
+      if (s != HD_OK) return s;
+    }
+    // pass B: convolution along y for every spectral column (sum over pairs)
+    {
+      Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_y", 0, twm[0], twM1[0]);
+      for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = Xf[k]; L.a.in_g.ptr[k] = Xg[k]; }
+      L.a.in_f.L = y.Lf; L.a.in_f.p = y.pf; L.a.in_f.nbi = B;
+      L.a.in_f.s_b = Kx * y.Lf; L.a.in_f.s_g = y.Lf * Sy; L.a.in_f.s_c = 1; L.a.in_f.s_j = Sy;
+      L.a.in_g.L = y.Lg; L.a.in_g.p = y.pg; L.a.in_g.nbi = B;
+      L.a.in_g.s_b = P.shared_g ? 0 : Kx * y.Lg; L.a.in_g.s_g = y.Lg * Sy; L.a.in_g.s_c = 1; L.a.in_g.s_j = Sy;
+      L.a.out.ptr[0] = Y; L.a.out.nbi = B; L.a.out.s_b = Oyp * Kx; L.a.out.s_g = Sy * Cx; L.a.out.s_c = Cx;
+      L.a.out.So = (int32_t)Cx; L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1; L.a.out.L = y.O; L.a.out.T = y.T;
+      L.a.scale = scale;
+      L.a.nlines = Kx; L.a.nbatch = B;
+      L.ngroups = cdiv(Kx, Sy); L.nbatch = B;
+      hd_status_t s = launch(ctx, P.dt, L, st);
+      if (s != HD_OK) return s;
+    }
+    // pass C: inverse along x for every output row
+    {
+      Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 1, twm[1], twM1[1]);
+      L.a.in_f.ptr[0] = Y; L.a.in_f.nbi = B; L.a.in_f.s_b = Oyp * Kx; L.a.in_f.s_g = Kx * Cx;
+      L.a.in_f.s_c = 1; L.a.in_f.s_j = Cx; L.a.in_f.L = Kx;
+      L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; L.a.out.s_g = Cx * x.O;
+      L.a.out.s_c = x.O; L.a.out.So = (int32_t)kHugeTile; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+      L.a.out.L = x.O; L.a.out.T = x.T;
+      L.a.nlines = y.O; L.a.nbatch = B;
+      L.ngroups = cdiv(y.O, Cx); L.nbatch = B;
+      return launch(ctx, P.dt, L, st);
+    }
+  }
+
+  // ndim == 3: axes z (0), y (1), x (2)
+  const AxisInfo &z = a[0], &y = a[1], &x = a[2];
+  const int64_t Kx = x.M1, Ky = y.M1, Cx = x.lines, S = y.lines;
+  const int64_t Oyp = cdiv(y.O, Cx) * Cx;
+  char** X1f = &reg[0];
+  char** X1g = &reg[N];
+  char** XYf = &reg[2 * N];
+  char** XYg = &reg[3 * N];
+  char* Zl = reg[4 * N];
+  char* W = reg[4 * N + 1];
+  for (int which = 0; which < 2; ++which) {
+    const int64_t Fz = which == 0 ? z.Lf : z.Lg, Fy = which == 0 ? y.Lf : y.Lg, Fx = which == 0 ? x.Lf : x.Lg;
+    const int64_t nb = which == 0 ? B : Bg;
+    // pass 1: forward along x; batch = (b, z) combined, lines = y
+    {
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_x_f" : "fwd_x_g", 2, twm[2], twM1[2]);
+      for (int k = 0; k < N; ++k) {
+        L.a.in_f.ptr[k] = which == 0 ? P.f[k] : P.g[k];
+        L.a.out.ptr[k] = which == 0 ? X1f[k] : X1g[k];
+      }
+      L.a.in_f.L = Fx; L.a.in_f.p = which == 0 ? x.pf : x.pg;
+      L.a.in_f.nbi = nb * Fz; L.a.in_f.s_b = Fy * Fx; L.a.in_f.s_g = Cx * Fx; L.a.in_f.s_c = Fx; L.a.in_f.s_j = 1;
+      L.a.out.nbi = nb * Fz; L.a.out.s_b = Kx * Fy; L.a.out.s_g = Cx * S; L.a.out.s_c = S;
+      L.a.out.So = (int32_t)S; L.a.out.s_jt = Fy * S; L.a.out.s_js = 1; L.a.out.L = Kx;
+      L.a.nlines = Fy; L.a.nbatch = nb * Fz;
+      L.ngroups = cdiv(Fy, Cx); L.nbatch = nb * Fz; L.narrays = N;
+      hd_status_t s = launch(ctx, P.dt, L, st);
+      if (s != HD_OK) return s;
+    }
+    // pass 2: forward along y; batch = (b, z), lines = kx (S per CTA)
+    {
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_y_f" : "fwd_y_g", 1, twm[1], twM1[1]);
+      for (int k = 0; k < N; ++k) {
+        L.a.in_f.ptr[k] = which == 0 ? X1f[k] : X1g[k];
+        L.a.out.ptr[k] = which == 0 ? XYf[k] : XYg[k];
+      }
+      L.a.in_f.L = Fy; L.a.in_f.p = which == 0 ? y.pf : y.pg;
+      L.a.in_f.nbi = Fz; L.a.in_f.s_bo = Fz * Kx * Fy; L.a.in_f.s_b = Kx * Fy;
+      L.a.in_f.s_g = Fy * S; L.a.in_f.s_c = 1; L.a.in_f.s_j = S;
+      L.a.out.nbi = Fz; L.a.out.s_bo = Ky * Kx * Fz; L.a.out.s_b = S; L.a.out.s_g = Fz * S; L.a.out.s_c = 1;
+      L.a.out.So = 1; L.a.out.s_jt = Kx * Fz; L.a.out.s_js = 0; L.a.out.L = Ky;
+      L.a.batch_fastest = 1;
+      L.a.nlines = Kx; L.a.nbatch = nb * Fz;
+      L.ngroups = cdiv(Kx, S); L.nbatch = nb * Fz; L.narrays = N;
+      hd_status_t s = launch(ctx, P.dt, L, st);
+      if (s != HD_OK) return s;
+    }
+  }
+  // pass 3: convolution along z; batch = (b, ky), lines = kx
+  {
+    Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_z", 0, twm[0], twM1[0]);
+    for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = XYf[k]; L.a.in_g.ptr[k] = XYg[k]; }
+    L.a.in_f.L = z.Lf; L.a.in_f.p = z.pf; L.a.in_f.nbi = Ky; L.a.in_f.s_bo = Ky * Kx * z.Lf;
+    L.a.in_f.s_b = Kx * z.Lf; L.a.in_f.s_g = z.Lf * S; L.a.in_f.s_c = 1; L.a.in_f.s_j = S;
+    L.a.in_g.L = z.Lg; L.a.in_g.p = z.pg; L.a.in_g.nbi = Ky; L.a.in_g.s_bo = P.shared_g ? 0 : Ky * Kx * z.Lg;
+    L.a.in_g.s_b = Kx * z.Lg; L.a.in_g.s_g = z.Lg * S; L.a.in_g.s_c = 1; L.a.in_g.s_j = S;
+    L.a.out.ptr[0] = Zl; L.a.out.nbi = Ky; L.a.out.s_bo = z.O * Kx * Ky; L.a.out.s_b = S;
+    L.a.out.s_g = Ky * S; L.a.out.s_c = 1; L.a.out.So = 1; L.a.out.s_jt = Kx * Ky; L.a.out.s_js = 0;
+    L.a.out.L = z.O; L.a.out.T = z.T;
+    L.a.scale = scale;
+    L.a.batch_fastest = 1;
+    L.a.nlines = Kx; L.a.nbatch = B * Ky;
+    L.ngroups = cdiv(Kx, S); L.nbatch = B * Ky;
+    hd_status_t s = launch(ctx, P.dt, L, st);
+    if (s != HD_OK) return s;
+  }
+  // pass 4: inverse along y; batch = (b, z_out) combined, lines = kx
+  {
+    Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_y", 1, twm[1], twM1[1]);
+    L.a.in_f.ptr[0] = Zl; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Kx * Ky; L.a.in_f.s_g = Ky * S;
+    L.a.in_f.s_c = 1; L.a.in_f.s_j = S; L.a.in_f.L = Ky;
+    L.a.out.ptr[0] = W; L.a.out.nbi = B * z.O; L.a.out.s_b = Oyp * Kx; L.a.out.s_g = S * Cx;
+    L.a.out.s_c = Cx; L.a.out.So = (int32_t)Cx; L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1;
+    L.a.out.L = y.O; L.a.out.T = y.T;
+    L.a.nlines = Kx; L.a.nbatch = B * z.O;
+    L.ngroups = cdiv(Kx, S); L.nbatch = B * z.O;
+    hd_status_t s = launch(ctx, P.dt, L, st);
+    if (s != HD_OK) return s;
+  }
+  // pass 5: inverse along x; batch = (b, z_out), lines = y_out
+  {
+    Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 2, twm[2], twM1[2]);
+    L.a.in_f.ptr[0] = W; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Oyp * Kx; L.a.in_f.s_g = Kx * Cx;
+    L.a.in_f.s_c = 1; L.a.in_f.s_j = Cx; L.a.in_f.L = Kx;
+    L.a.out.ptr[0] = P.h; L.a.out.nbi = B * z.O; L.a.out.s_b = y.O * x.O; L.a.out.s_g = Cx * x.O;
+    L.a.out.s_c = x.O; L.a.out.So = (int32_t)kHugeTile; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+    L.a.out.L = x.O; L.a.out.T = x.T;
+    L.a.nlines = y.O; L.a.nbatch = B * z.O;
+    L.ngroups = cdiv(y.O, Cx); L.nbatch = B * z.O;
+    return launch(ctx, P.dt, L, st);
+  }
+}
+
+std::string problem_key(hd_dtype_t dt, int ndim, int N, int64_t batch, const int64_t* Lf,
+                        const int64_t* Lg, const int64_t* M, uint32_t flags) {
+  std::string k = std::to_string((int)dt) + "|" + std::to_string(ndim) + "|" + std::to_string(N) +
+                  "|" + std::to_string(batch) + "|" + std::to_string(flags);
+  for (int i = 0; i < ndim; ++i)
+    k += "|" + std::to_string(Lf[i]) + "," + std::to_string(Lg[i]) + "," +
+         std::to_string(M ? M[i] : 0);
+  return k;
+}
+
+// Build a Problem from the public arguments (plan: explicit, cached or default).
+hd_status_t setup(hd_ctx* ctx, Problem& P, hd_dtype_t dt, int ndim, int N, int64_t batch,
+                  const void* const* f, const int64_t* Lf, const void* const* g, const int64_t* Lg,
+                  void* h, const int64_t* M, const hd_plan_t* plan, bool need_ptrs = true) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (dt != HD_C64 && dt != HD_C128) return fail(ctx, HD_ERR_INVALID, "dtype must be HD_C64 or HD_C128");
+  if (ndim < 1 || ndim > HD_MAX_DIM) return fail(ctx, HD_ERR_INVALID, "ndim must be 1, 2 or 3");
+  if (N < 1 || N > HD_MAX_PAIRS) return fail(ctx, HD_ERR_INVALID, "N must be in [1, 16]");
+  if (batch < 1) return fail(ctx, HD_ERR_INVALID, "batch must be >= 1");
+  if (!Lf || !Lg) return fail(ctx, HD_ERR_INVALID, "null extents");
+  P.dt = dt; P.ndim = ndim; P.N = N; P.batch = batch;
+  if (need_ptrs) {
+    if (!f || !g || !h) return fail(ctx, HD_ERR_INVALID, "null data pointer");
+    for (int k = 0; k < N; ++k) {
+      if (!f[k] || !g[k]) return fail(ctx, HD_ERR_INVALID, "null input pointer");
+      const uintptr_t al = elem_bytes(dt);
+      if (((uintptr_t)f[k] % al) || ((uintptr_t)g[k] % al) || ((uintptr_t)h % al))
+        return fail(ctx, HD_ERR_INVALID, "misaligned data pointer");
+      if (f[k] == h || g[k] == h) return fail(ctx, HD_ERR_INVALID, "h must not alias f or g");
+      P.f[k] = f[k]; P.g[k] = g[k];
+    }
+    P.h = h;
+  }
+  hd_plan_t pl;
+  if (plan) {
+    pl = *plan;
+  } else {
+    auto it = ctx->plan_cache.find(problem_key(dt, ndim, N, batch, Lf, Lg, M, 0));
+    if (it != ctx->plan_cache.end()) pl = it->second;
+    else {
+      hd_status_t s = default_plan(ctx, dt, ndim, N, Lf, Lg, M, &pl);
+      if (s != HD_OK) return s;
+    }
+  }
+  P.shared_g = (pl.flags & HD_FLAG_SHARED_G) != 0;
+  hd_status_t s = complete_plan(ctx, dt, ndim, N, Lf, Lg, M, &pl, P.ax);
+  if (s != HD_OK) return s;
+  P.plan = pl;
+  return HD_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int hd_abi_version(void) { return HD_ABI_VERSION; }
+
+hd_status_t hd_create(hd_ctx_t* out, int device) {
+  if (!out) return fail(nullptr, HD_ERR_INVALID, "null ctx pointer");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(nullptr, HD_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= n) return fail(nullptr, HD_ERR_INVALID, "device ordinal out of range");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  hd_ctx* c = new hd_ctx();
+  c->device = device;
+  *out = c;
+  return HD_OK;
+}
+
+hd_status_t hd_destroy(hd_ctx_t ctx) {
+  if (!ctx) return HD_OK;
+  cudaSetDevice(ctx->device);
+  for (auto& kv : ctx->tw64) cudaFree(kv.second);
+  for (auto& kv : ctx->tw32) cudaFree(kv.second);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->io) cudaFree(ctx->io);
+  for (auto& p : ctx->prof)
+    for (auto& ev : p.pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+  delete ctx;
+  return HD_OK;
+}
+
+const char* hd_last_error(hd_ctx_t ctx) {
+  return ctx ? ctx->err.c_str() : g_tls_error.c_str();
+}
+
+hd_status_t hd_plan_default(hd_dtype_t dtype, int32_t ndim, int32_t npairs, const int64_t* Lf,
+                            const int64_t* Lg, const int64_t* M, hd_plan_t* out) {
+  if (!Lf || !Lg || !out) return fail(nullptr, HD_ERR_INVALID, "null argument");
+  if (dtype != HD_C64 && dtype != HD_C128) return fail(nullptr, HD_ERR_INVALID, "bad dtype");
+  if (npairs < 1 || npairs > HD_MAX_PAIRS) return fail(nullptr, HD_ERR_INVALID, "N must be in [1, 16]");
+  return default_plan(nullptr, dtype, ndim, npairs, Lf, Lg, M, out);
+}
+
+hd_status_t hd_plan_complete(hd_dtype_t dtype, int32_t ndim, int32_t npairs, const int64_t* Lf,
+                             const int64_t* Lg, const int64_t* M, hd_plan_t* plan) {
+  if (!Lf || !Lg || !plan) return fail(nullptr, HD_ERR_INVALID, "null argument");
+  AxisInfo ax[HD_MAX_DIM];
+  return complete_plan(nullptr, dtype, ndim, npairs, Lf, Lg, M, plan, ax);
+}
+
+hd_status_t hd_spectral_permutation(int32_t m, int32_t* perm) {
+  if (!perm || !is_pow2(m) || m < 2 || m > 4096)
+    return fail(nullptr, HD_ERR_INVALID, "m must be a power of two in [2, 4096]");
+  // radix schedule of hd_device.cuh Sched<m>: radix-8 stages then one radix-4/2
+  const int lg = ilog2(m);
+  std::vector<int> rad;
+  for (int i = 0; i < lg / 3; ++i) rad.push_back(8);
+  if (lg % 3 == 1) rad.push_back(2);
+  if (lg % 3 == 2) rad.push_back(4);
+  // DIF: position j*(n/R) + o' of a size-n block holds R*perm_{n/R}(o') + j
+  for (int pos = 0; pos < m; ++pos) {
+    int n = m, p = pos, mul = 1, freq = 0;
+    for (size_t s = 0; s < rad.size(); ++s) {
+      const int R = rad[s];
+      const int sub = n / R;
+      const int j = p / sub;
+      freq += mul * j;
+      mul *= R;
+      p %= sub;
+      n = sub;
+    }
+    perm[pos] = freq;
+  }
+  return HD_OK;
+}
+
+size_t hd_workspace_bytes(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t npairs, int64_t batch,
+                          const int64_t* Lf, const int64_t* Lg, const int64_t* M,
+                          const hd_plan_t* plan) {
+  Problem P;
+  if (setup(ctx, P, dtype, ndim, npairs, batch, nullptr, Lf, nullptr, Lg, nullptr, M, plan, false) != HD_OK)
+    return 0;
+  std::vector<int64_t> el;
+  return ws_regions(P, el);
+}
+
+static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64_t batch,
+                             const void* const* f, const int64_t* Lf, const void* const* g,
+                             const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan,
+                             void* ws, size_t ws_bytes, void* stream) {
+  Problem P;
+  hd_status_t s = setup(ctx, P, dt, ndim, N, batch, f, Lf, g, Lg, h, M, plan);
+  if (s != HD_OK) return s;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  return run_pipeline(ctx, P, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+hd_status_t hd_conv1d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
+                      const void* g, int64_t Lg, void* h, int64_t M, const hd_plan_t* plan,
+                      void* ws, size_t ws_bytes, void* stream) {
+  const void* fa[1] = {f};
+  const void* ga[1] = {g};
+  int64_t Mv[1] = {M};
+  return run_entry(ctx, dtype, 1, 1, batch, fa, &Lf, ga, &Lg, h, Mv, plan, ws, ws_bytes, stream);
+}
+
+hd_status_t hd_conv2d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, const int64_t Lf[2],
+                      const void* g, const int64_t Lg[2], void* h, const int64_t M[2],
+                      const hd_plan_t* plan, void* ws, size_t ws_bytes, void* stream) {
+  const void* fa[1] = {f};
+  const void* ga[1] = {g};
+  return run_entry(ctx, dtype, 2, 1, batch, fa, Lf, ga, Lg, h, M, plan, ws, ws_bytes, stream);
+}
+
+hd_status_t hd_conv3d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, const int64_t Lf[3],
+                      const void* g, const int64_t Lg[3], void* h, const int64_t M[3],
+                      const hd_plan_t* plan, void* ws, size_t ws_bytes, void* stream) {
+  const void* fa[1] = {f};
+  const void* ga[1] = {g};
+  return run_entry(ctx, dtype, 3, 1, batch, fa, Lf, ga, Lg, h, M, plan, ws, ws_bytes, stream);
+}
+
+hd_status_t hd_multiconv(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                         const void* const* f, const int64_t* Lf, const void* const* g,
+                         const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan,
+                         void* ws, size_t ws_bytes, void* stream) {
+  return run_entry(ctx, dtype, ndim, N, 1, f, Lf, g, Lg, h, M, plan, ws, ws_bytes, stream);
+}
+
+hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                             const void* const* f, const int64_t* Lf, const void* const* g,
+                             const int64_t* Lg, void* h, const hd_plan_t* plan, void* stream) {
+  // Validate against the hybrid problem first (also gives the user's m, C, S).
+  Problem H;
+  hd_status_t s = setup(ctx, H, dtype, ndim, N, 1, f, Lf, g, Lg, h, nullptr, plan);
+  if (s != HD_OK) return s;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t eb = elem_bytes(dtype);
+  int64_t Me[HD_MAX_DIM], Lo[HD_MAX_DIM];
+  int64_t nin = 1;
+  for (int i = 0; i < ndim; ++i) {
+    Lo[i] = Lf[i] + Lg[i] - 1;
+    Me[i] = 1;
+    while (Me[i] < Lo[i]) Me[i] *= 2;
+    nin *= Me[i];
+  }
+  // explicit plan: same m (capped by M_exp), same C/S, D reduced until it fits
+  hd_plan_t pe = H.plan;
+  pe.flags = HD_FLAG_ALLOW_ALIAS;
+  for (int i = 0; i < ndim; ++i) {
+    hd_axis_plan_t& a = pe.axis[i];
+    a.m = (int)std::min<int64_t>(a.m, Me[i]);
+    const int q = (int)(Me[i] / a.m);
+    const int lines = lines_for(a, i, ndim);
+    const int nbuf = (i == 0) ? conv_nbuf(N) : 1;
+    a.D = q;
+    while (a.D > 1 && pass_smem(eb, q, lines, a.D, a.m, nbuf) > hd::kMaxSmem) --a.D;
+  }
+  // scratch: N padded f, N padded g, padded output, pipeline workspace
+  Problem E;
+  E.dt = dtype; E.ndim = ndim; E.N = N; E.batch = 1;
+  s = complete_plan(ctx, dtype, ndim, N, Me, Me, Me, &pe, E.ax);
+  if (s != HD_OK) return s;
+  E.plan = pe;
+  std::vector<int64_t> el;
+  const size_t wsb = ws_regions(E, el);
+  const size_t inb = align256((size_t)nin * eb);
+  const size_t need = (2 * N + 1) * inb + wsb;
+  if (ctx->io_size < need) {
+    if (ctx->io) cudaFree(ctx->io);
+    ctx->io = nullptr; ctx->io_size = 0;
+    cudaError_t e = cudaMalloc(&ctx->io, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(explicit scratch)");
+    ctx->io_size = need;
+  }
+  char* base = (char*)ctx->io;
+  int64_t L3[3], P3[3];
+  auto to3 = [&](const int64_t* v, int64_t* o) {
+    for (int i = 0; i < 3; ++i) o[i] = 1;
+    for (int i = 0; i < ndim; ++i) o[3 - ndim + i] = v[i];
+  };
+  to3(Me, P3);
+  for (int k = 0; k < N; ++k) {
+    to3(Lf, L3);
+    cudaError_t e = hd::launch_pad(dtype == HD_C128, f[k], base + k * inb, L3, P3, 1, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "pad_copy");
+    to3(Lg, L3);
+    e = hd::launch_pad(dtype == HD_C128, g[k], base + (N + k) * inb, L3, P3, 1, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "pad_copy");
+    ctx->launches += 2;
+    E.f[k] = base + k * inb;
+    E.g[k] = base + (N + k) * inb;
+  }
+  E.h = base + 2 * N * inb;
+  s = run_pipeline(ctx, E, base + (2 * N + 1) * inb, wsb, st);
+  if (s != HD_OK) return s;
+  to3(Lo, L3);
+  cudaError_t e = hd::launch_crop(dtype == HD_C128, E.h, h, L3, P3, 1, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "crop_copy");
+  ctx->launches += 1;
+  return HD_OK;
+}
+
+hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
+                         const void* const* f, const int64_t* Lf, const void* const* g,
+                         const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan,
+                         void* stream) {
+  Problem P;
+  hd_status_t s = setup(ctx, P, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan);
+  if (s != HD_OK) return s;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t eb = elem_bytes(dtype);
+  int64_t nf = batch, ng = P.shared_g ? 1 : batch, nh = batch;
+  for (int i = 0; i < ndim; ++i) { nf *= Lf[i]; ng *= Lg[i]; nh *= P.ax[i].O; }
+  const size_t bf = align256((size_t)nf * eb), bg = align256((size_t)ng * eb), bh = align256((size_t)nh * eb);
+  const size_t need = N * (bf + bg) + bh;
+  if (ctx->io_size < need) {
+    if (ctx->io) cudaFree(ctx->io);
+    ctx->io = nullptr; ctx->io_size = 0;
+    cudaError_t e = cudaMalloc(&ctx->io, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(host io)");
+    ctx->io_size = need;
+  }
+  char* base = (char*)ctx->io;
+  for (int k = 0; k < N; ++k) {
+    char* df = base + k * bf;
+    char* dg = base + N * bf + k * bg;
+    cudaError_t e = cudaMemcpyAsync(df, f[k], (size_t)nf * eb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(f)");
+    e = cudaMemcpyAsync(dg, g[k], (size_t)ng * eb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(g)");
+    P.f[k] = df;
+    P.g[k] = dg;
+  }
+  void* hh = h;
+  P.h = base + N * (bf + bg);
+  s = run_pipeline(ctx, P, nullptr, 0, st);
+  if (s != HD_OK) return s;
+  cudaError_t e = cudaMemcpyAsync(hh, P.h, (size_t)nh * eb, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(h)");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamSynchronize");
+  return HD_OK;
+}
+
+hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* x,
+                                int64_t L, int32_t m, int32_t q, void* X, void* stream) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (!x || !X || nlines < 1 || L < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
+  if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < L)
+    return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= L");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const bool dbl = dtype == HD_C128;
+  const size_t eb = elem_bytes(dtype);
+  Problem P;
+  P.dt = dtype; P.N = 1;
+  AxisInfo& a = P.ax[0];
+  a.m = m; a.q = q; a.M1 = (int64_t)q * m; a.Lf = L; a.pf = (int)cdiv(L, m);
+  a.lines = 1; a.threads = kDefaultThreads;
+  a.D = q;
+  while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
+  const void *twm, *twM1;
+  hd_status_t s = get_table(ctx, m, dbl, &twm);
+  if (s != HD_OK) return s;
+  s = get_table(ctx, a.M1, dbl, &twM1);
+  if (s != HD_OK) return s;
+  Launch Lh = make_launch(ctx, P, hd::MODE_FWD, "fwd_residues", 0, twm, twM1);
+  Lh.a.in_f.ptr[0] = x; Lh.a.in_f.L = L; Lh.a.in_f.p = a.pf; Lh.a.in_f.s_g = L; Lh.a.in_f.s_c = L; Lh.a.in_f.s_j = 1;
+  Lh.a.out.ptr[0] = X; Lh.a.out.So = (int32_t)kHugeTile; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
+  Lh.a.out.s_g = a.M1; Lh.a.out.s_c = a.M1; Lh.a.out.L = a.M1;
+  Lh.a.nlines = nlines; Lh.a.nbatch = 1;
+  Lh.ngroups = nlines; Lh.nbatch = 1;
+  return launch(ctx, dtype, Lh, (cudaStream_t)stream);
+}
+
+hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* X,
+                                 int32_t m, int32_t q, void* x, int64_t Lout, void* stream) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (!x || !X || nlines < 1 || Lout < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
+  if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < Lout)
+    return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= Lout");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const bool dbl = dtype == HD_C128;
+  const size_t eb = elem_bytes(dtype);
+  Problem P;
+  P.dt = dtype; P.N = 1;
+  AxisInfo& a = P.ax[0];
+  a.m = m; a.q = q; a.M1 = (int64_t)q * m; a.O = Lout; a.T = (int)cdiv(Lout, m);
+  a.lines = 1; a.threads = kDefaultThreads;
+  a.D = q;
+  while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
+  const void *twm, *twM1;
+  hd_status_t s = get_table(ctx, m, dbl, &twm);
+  if (s != HD_OK) return s;
+  s = get_table(ctx, a.M1, dbl, &twM1);
+  if (s != HD_OK) return s;
+  Launch Lh = make_launch(ctx, P, hd::MODE_INV, "bwd_residues", 0, twm, twM1);
+  Lh.a.in_f.ptr[0] = X; Lh.a.in_f.s_g = a.M1; Lh.a.in_f.s_c = a.M1; Lh.a.in_f.s_j = 1; Lh.a.in_f.L = a.M1;
+  Lh.a.out.ptr[0] = x; Lh.a.out.So = (int32_t)kHugeTile; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
+  Lh.a.out.s_g = Lout; Lh.a.out.s_c = Lout; Lh.a.out.L = Lout; Lh.a.out.T = a.T;
+  Lh.a.nlines = nlines; Lh.a.nbatch = 1;
+  Lh.ngroups = nlines; Lh.nbatch = 1;
+  return launch(ctx, dtype, Lh, (cudaStream_t)stream);
+}
+
+hd_status_t hd_profile_enable(hd_ctx_t ctx, int32_t enable) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  ctx->profiling = enable != 0;
+  return HD_OK;
+}
+
+int32_t hd_profile_read(hd_ctx_t ctx, int32_t max, double* ms, int64_t* launches, char* names) {
+  if (!ctx) return -1;
+  int32_t n = 0;
+  for (auto& p : ctx->prof) {
+    for (auto& ev : p.pending) {
+      float t = 0;
+      if (cudaEventElapsedTime(&t, ev.first, ev.second) == cudaSuccess) p.ms += t;
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    p.pending.clear();
+    if (n < max) {
+      if (ms) ms[n] = p.ms;
+      if (launches) launches[n] = p.launches;
+      if (names) { std::strncpy(names + 32 * n, p.name.c_str(), 31); names[32 * n + 31] = 0; }
+    }
+    ++n;
+  }
+  return n;
+}
+
+hd_status_t hd_profile_reset(hd_ctx_t ctx) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  for (auto& p : ctx->prof)
+    for (auto& ev : p.pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+  ctx->prof.clear();
+  return HD_OK;
+}
+
+int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
+}  // extern "C"
+
+// ===========================================================================
+// On-device tuning sweep: the paper's "experience" search,
+// per dimension independently, scored by measured time of
+// the whole convolution (CUDA events, median of reps after 2 warm-ups), first
+// strict minimum wins with a lexicographic (m, C, S, D) tie-break
+// (SPEC.md:350).
+// ===========================================================================
+namespace {
+
+struct AxisCand { int m, C, S, D; };
+
+bool cand_less(const AxisCand& a, const AxisCand& b) {
+  if (a.m != b.m) return a.m < b.m;
+  if (a.C != b.C) return a.C < b.C;
+  if (a.S != b.S) return a.S < b.S;
+  return a.D < b.D;
+}
+
+std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, int npairs,
+                                      const int64_t* Lf, const int64_t* Lg, const int64_t* M,
+                                      size_t eb) {
+  std::vector<AxisCand> out;
+  const int64_t Lout = Lf[i] + Lg[i] - 1;
+  const int64_t Mi = (M && M[i] > 0) ? M[i] : Lout;
+  const int m0 = base.axis[i].m;
+  const bool contig = (i == ndim - 1);
+  const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
+  for (int m = std::max(2, m0 / 4); m <= std::min(4096, m0 * 4); m *= 2) {
+    const int q = (int)cdiv(Mi, m);
+    for (int lines : {1, 2, 4}) {
+      std::vector<int> Ds = {q};
+      if (q > 1) Ds.push_back((q + 1) / 2);
+      for (int D : Ds) {
+        if (pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) continue;
+        AxisCand c{m, contig ? lines : base.axis[i].C, contig ? base.axis[i].S : lines, D};
+        out.push_back(c);
+      }
+    }
+  }
+  return out;
+}
+
+void apply_cand(hd_plan_t& p, int i, int ndim, const AxisCand& c) {
+  p.axis[i].m = c.m; p.axis[i].C = c.C; p.axis[i].S = c.S; p.axis[i].D = c.D;
+  if (ndim == 3 && (i == 0 || i == 1)) { p.axis[0].S = c.S; p.axis[1].S = c.S; }
+}
+
+}  // namespace
+
+extern "C" {
+
+hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
+                    const int64_t* Lf, const int64_t* Lg, const int64_t* M, uint32_t flags,
+                    int32_t reps, void* stream, hd_plan_t* out) {
+  if (!ctx || !out) return fail(ctx, HD_ERR_INVALID, "null argument");
+  Problem P0;
+  hd_status_t s = setup(ctx, P0, dtype, ndim, N, batch, nullptr, Lf, nullptr, Lg, nullptr, M, nullptr, false);
+  if (s != HD_OK) return s;
+  hd_plan_t base;
+  s = default_plan(ctx, dtype, ndim, N, Lf, Lg, M, &base);
+  if (s != HD_OK) return s;
+  if (reps <= 0) reps = 5;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t eb = elem_bytes(dtype);
+  // synthetic scratch operands of the problem's shape (timing is value independent)
+  int64_t nf = batch, ng = batch, nh = batch;
+  for (int i = 0; i < ndim; ++i) { nf *= Lf[i]; ng *= Lg[i]; nh *= Lf[i] + Lg[i] - 1; }
+  const size_t bf = align256((size_t)nf * eb), bg = align256((size_t)ng * eb), bh = align256((size_t)nh * eb);
+  char* scratch = nullptr;
+  cudaError_t e = cudaMalloc(&scratch, N * (bf + bg) + bh);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(tune scratch)");
+  cudaMemsetAsync(scratch, 0, N * (bf + bg) + bh, st);
+  const void* fp[HD_MAX_PAIRS];
+  const void* gp[HD_MAX_PAIRS];
+  for (int k = 0; k < N; ++k) { fp[k] = scratch + k * bf; gp[k] = scratch + N * bf + k * bg; }
+  void* hp = scratch + N * (bf + bg);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  ctx->tune_log.clear();
+  const bool prof_was = ctx->profiling;
+  ctx->profiling = false;
+
+  auto time_plan = [&](hd_plan_t pl, double* secs) -> bool {
+    Problem P;
+    P.dt = dtype; P.ndim = ndim; P.N = N; P.batch = batch; P.shared_g = false;
+    for (int k = 0; k < N; ++k) { P.f[k] = fp[k]; P.g[k] = gp[k]; }
+    P.h = hp;
+    if (complete_plan(ctx, dtype, ndim, N, Lf, Lg, M, &pl, P.ax) != HD_OK) return false;
+    P.plan = pl;
+    for (int w = 0; w < 2; ++w)
+      if (run_pipeline(ctx, P, nullptr, 0, st) != HD_OK) return false;
+    std::vector<double> ts;
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(e0, st);
+      if (run_pipeline(ctx, P, nullptr, 0, st) != HD_OK) return false;
+      cudaEventRecord(e1, st);
+      if (cudaEventSynchronize(e1) != cudaSuccess) return false;
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms * 1e-3);
+    }
+    std::sort(ts.begin(), ts.end());
+    *secs = ts[ts.size() / 2];
+    ctx->tune_log.push_back({pl, *secs});
+    return true;
+  };
+
+  hd_plan_t best = base;
+  double best_t = 1e300;
+  if (!time_plan(best, &best_t)) best_t = 1e300;
+  if (flags & HD_TUNE_EXHAUSTIVE) {
+    std::vector<std::vector<AxisCand>> lists;
+    size_t combos = 1;
+    for (int i = 0; i < ndim; ++i) {
+      lists.push_back(axis_candidates(base, i, ndim, N, Lf, Lg, M, eb));
+      combos *= std::max<size_t>(1, lists.back().size());
+    }
+    combos = std::min<size_t>(combos, 4096);
+    for (size_t c = 0; c < combos; ++c) {
+      hd_plan_t pl = base;
+      size_t r = c;
+      for (int i = 0; i < ndim; ++i) {
+        if (lists[i].empty()) continue;
+        apply_cand(pl, i, ndim, lists[i][r % lists[i].size()]);
+        r /= lists[i].size();
+      }
+      double t;
+      if (time_plan(pl, &t) && t < best_t) { best_t = t; best = pl; }
+    }
+  } else {
+    for (int i = 0; i < ndim; ++i) {
+      std::vector<AxisCand> cands = axis_candidates(best, i, ndim, N, Lf, Lg, M, eb);
+      AxisCand bc{best.axis[i].m, best.axis[i].C, best.axis[i].S, best.axis[i].D};
+      for (const AxisCand& c : cands) {
+        hd_plan_t pl = best;
+        apply_cand(pl, i, ndim, c);
+        double t;
+        if (!time_plan(pl, &t)) continue;
+        const bool tie = std::fabs(t - best_t) <= 1e-12 * best_t;
+        if (t < best_t && !tie) { best_t = t; best = pl; bc = c; }
+        else if (tie && cand_less(c, bc)) { best = pl; bc = c; }
+      }
+    }
+  }
+  ctx->profiling = prof_was;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(scratch);
+  AxisInfo ax[HD_MAX_DIM];
+  s = complete_plan(ctx, dtype, ndim, N, Lf, Lg, M, &best, ax);
+  if (s != HD_OK) return s;
+  best.tuned_seconds = best_t;
+  ctx->plan_cache[problem_key(dtype, ndim, N, batch, Lf, Lg, M, 0)] = best;
+  *out = best;
+  return HD_OK;
+}
+
+int32_t hd_tune_log(hd_ctx_t ctx, int32_t max, hd_plan_t* plans, double* seconds) {
+  if (!ctx) return -1;
+  const int32_t n = (int32_t)ctx->tune_log.size();
+  for (int32_t i = 0; i < n && i < max; ++i) {
+    if (plans) plans[i] = ctx->tune_log[i].first;
+    if (seconds) seconds[i] = ctx->tune_log[i].second;
+  }
+  return n;
+}
+
+}  // extern "C"

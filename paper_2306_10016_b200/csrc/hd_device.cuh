@@ -1,0 +1,463 @@
+// hd_device.cuh -- device building blocks of the hybrid-dealiased convolution
+// passes (sm_100a).  One CTA owns C lines of one axis (a "line group") and walks
+// the q residues of that axis D at a time:
+//
+//   fold      w_r[s] = zeta_{qm}^{rs} * sum_{t<p} zeta_q^{rt} x[tm+s]
+//             (Forward Eq. PAPER.md:528; Alg. Forward PAPER.md:90-102 incl. the
+//             partial last block PAPER.md:100-101)               -> SMEM [c][d][s]
+//   fft_fwd   size-m DIF FFT, positive exponent, unnormalised ("W <- m F(W)",
+//             PAPER.md:104), radix-8/4/2 register butterflies, output left in
+//             digit-reversed order (the internal spectral order)
+//   product   H = (1/prod M1) * sum_k F_k G_k
+//   fft_inv   size-m DIT FFT, negative exponent, digit-reversed in,
+//             natural out -- the exact adjoint of fft_fwd
+//   unfold    h[tm+s] += zeta_q^{-tr} zeta_{qm}^{-rs} V_r[s] for t < T
+//             (Backward Eq. PAPER.md:531; Alg. Backward)
+//
+// Shared memory holds complex values in an XOR-swizzled layout so that both the
+// unit-stride and the radix-strided butterfly accesses are bank-conflict free.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hd {
+
+constexpr int kMaxPairs = 16;
+constexpr int kFoldChunk = 8;  // residues held in registers by one fold/unfold sweep
+
+template <typename T> struct cplx_of;
+template <> struct cplx_of<double> { using type = double2; };
+template <> struct cplx_of<float> { using type = float2; };
+
+template <typename V> __device__ __forceinline__ V cmk(decltype(V::x) re, decltype(V::x) im) {
+  V r; r.x = re; r.y = im; return r;
+}
+template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return cmk<V>(a.x + b.x, a.y + b.y); }
+template <typename V> __device__ __forceinline__ V csub(V a, V b) { return cmk<V>(a.x - b.x, a.y - b.y); }
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+  return cmk<V>(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+template <typename V> __device__ __forceinline__ V cmulc(V a, V b) {
+  return cmk<V>(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+// acc + a*b
+template <typename V> __device__ __forceinline__ V cfma(V acc, V a, V b) {
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+// acc + a*conj(b)
+template <typename V> __device__ __forceinline__ V cfmac(V acc, V a, V b) {
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.y, b.x, acc.y); acc.y = fma(-a.x, b.y, acc.y);
+  return acc;
+}
+template <typename V> __device__ __forceinline__ V cscale(V a, decltype(V::x) s) { return cmk<V>(a.x * s, a.y * s); }
+// multiply by (s * i), s = +-1
+template <typename V, int S> __device__ __forceinline__ V cmul_si(V a) {
+  return S > 0 ? cmk<V>(-a.y, a.x) : cmk<V>(a.y, -a.x);
+}
+
+// Read-only global load through the non-coherent path.
+template <typename V> __device__ __forceinline__ V ldg(const V* p) { return __ldg(p); }
+
+// XOR swizzle: permute the complex slots inside each 128-byte row by the row index.
+template <typename V> __device__ __forceinline__ int swz(int i) {
+  constexpr int EPR = 128 / (int)sizeof(V);  // 8 (double2) or 16 (float2)
+  return i ^ ((i / EPR) & (EPR - 1));
+}
+
+// ---------------------------------------------------------------------------
+// Radix schedule for m = 2^k: radix-8 stages, then one radix-4 or radix-2 stage.
+// DIF stage s works on sub-transforms of size NK(s) with butterfly span NK/R.
+// ---------------------------------------------------------------------------
+template <int M> struct Sched {
+  static constexpr int LOG = (M <= 1) ? 0 : 1 + Sched<M / 2>::LOG;
+  static constexpr int N8 = LOG / 3;
+  static constexpr int REM = LOG % 3;
+  static constexpr int NST = N8 + (REM ? 1 : 0);
+  __host__ __device__ static constexpr int radix(int s) { return s < N8 ? 8 : (REM == 1 ? 2 : 4); }
+  __host__ __device__ static constexpr int nk(int s) {
+    int n = M;
+    for (int i = 0; i < s; ++i) n /= radix(i);
+    return n;
+  }
+};
+template <> struct Sched<1> { static constexpr int LOG = 0; };
+
+// In-register DFT of size R with exponent sign S: y_j = sum_i v_i zeta_R^{S i j}.
+template <typename V, int S> __device__ __forceinline__ void dft2(V& a, V& b) {
+  V t = a; a = cadd(t, b); b = csub(t, b);
+}
+template <typename V, int S> __device__ __forceinline__ void dft4(V* v) {
+  V a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+  V b0 = cadd(v[1], v[3]), b1 = cmul_si<V, S>(csub(v[1], v[3]));
+  v[0] = cadd(a0, b0); v[2] = csub(a0, b0);
+  v[1] = cadd(a1, b1); v[3] = csub(a1, b1);
+}
+template <typename V, int S> __device__ __forceinline__ void dft8(V* v) {
+  using R = decltype(V::x);
+  const R h = (R)0.70710678118654752440084436210484903928;
+  // radix-2 DIF split: b_n = v_n + v_{n+4}, c_n = (v_n - v_{n+4}) zeta_8^{S n}
+  V b[4], c[4];
+#pragma unroll
+  for (int n = 0; n < 4; ++n) { b[n] = cadd(v[n], v[n + 4]); c[n] = csub(v[n], v[n + 4]); }
+  // zeta_8^{S} = h(1 + S i); zeta_8^{2S} = S i; zeta_8^{3S} = h(-1 + S i)
+  c[1] = cmk<V>(h * (c[1].x - S * c[1].y), h * (c[1].y + S * c[1].x));
+  c[2] = cmul_si<V, S>(c[2]);
+  c[3] = cmk<V>(h * (-c[3].x - S * c[3].y), h * (-c[3].y + S * c[3].x));
+  dft4<V, S>(b);
+  dft4<V, S>(c);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { v[2 * k] = b[k]; v[2 * k + 1] = c[k]; }
+}
+template <typename V, int R, int S> __device__ __forceinline__ void dftR(V* v) {
+  if constexpr (R == 2) dft2<V, S>(v[0], v[1]);
+  else if constexpr (R == 4) dft4<V, S>(v);
+  else dft8<V, S>(v);
+}
+
+// One DIF (forward) or DIT (inverse) stage over nrows rows of M in SMEM.
+template <typename V, int M, int NT, int ST, bool INV>
+__device__ __forceinline__ void fft_stage(V* buf, int nrows, const V* __restrict__ twm) {
+  constexpr int R = Sched<M>::radix(ST);
+  constexpr int NK = Sched<M>::nk(ST);
+  constexpr int SPAN = NK / R;
+  constexpr int PER_ROW = M / R;
+  constexpr int TWSTEP = M / NK;
+  const int items = nrows * PER_ROW;
+  for (int it = threadIdx.x; it < items; it += NT) {
+    const int row = it / PER_ROW;
+    const int w = it % PER_ROW;
+    const int b = w / SPAN, o = w % SPAN;
+    const int base = row * M + b * NK + o;
+    V v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[swz<V>(base + i * SPAN)];
+    if constexpr (!INV) {
+      dftR<V, R, +1>(v);
+      if (SPAN > 1 && o > 0) {
+#pragma unroll
+        for (int j = 1; j < R; ++j) v[j] = cmul(v[j], ldg(twm + o * j * TWSTEP));
+      }
+    } else {
+      if (SPAN > 1 && o > 0) {
+#pragma unroll
+        for (int j = 1; j < R; ++j) v[j] = cmulc(v[j], ldg(twm + o * j * TWSTEP));
+      }
+      dftR<V, R, -1>(v);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) buf[swz<V>(base + i * SPAN)] = v[i];
+  }
+}
+
+template <typename V, int M, int NT, int ST>
+__device__ __forceinline__ void fft_fwd_from(V* buf, int nrows, const V* twm) {
+  if constexpr (ST < Sched<M>::NST) {
+    fft_stage<V, M, NT, ST, false>(buf, nrows, twm);
+    __syncthreads();
+    fft_fwd_from<V, M, NT, ST + 1>(buf, nrows, twm);
+  }
+}
+template <typename V, int M, int NT, int ST>
+__device__ __forceinline__ void fft_inv_from(V* buf, int nrows, const V* twm) {
+  if constexpr (ST >= 0) {
+    fft_stage<V, M, NT, ST, true>(buf, nrows, twm);
+    __syncthreads();
+    fft_inv_from<V, M, NT, ST - 1>(buf, nrows, twm);
+  }
+}
+// Forward FFT of nrows rows (ends with a CTA barrier).
+template <typename V, int M, int NT>
+__device__ __forceinline__ void fft_fwd(V* buf, int nrows, const V* twm) {
+  if constexpr (M > 1) fft_fwd_from<V, M, NT, 0>(buf, nrows, twm);
+}
+template <typename V, int M, int NT>
+__device__ __forceinline__ void fft_inv(V* buf, int nrows, const V* twm) {
+  if constexpr (M > 1) fft_inv_from<V, M, NT, Sched<M>::NST - 1>(buf, nrows, twm);
+}
+
+// ---------------------------------------------------------------------------
+// Pass arguments
+// ---------------------------------------------------------------------------
+struct LineIn {            // element j of line c of group g, batch b, array k:
+  const void* ptr[kMaxPairs];  //   ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b + g*s_g + c*s_c + j*s_j
+  int64_t L;               // valid elements per line (zero beyond)
+  int64_t nbi, s_bo;       // two-level batch index (nbi = nbatch: one level)
+  int64_t s_b, s_g, s_c, s_j;
+  int32_t p;               // ceil(L/m) blocks (fold)
+  int32_t pad_;
+};
+struct LineOut {           // element j of line c: ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b
+  void* ptr[kMaxPairs];    //   + g*s_g + c*s_c + (j/So)*s_jt + (j%So)*s_js
+  int64_t L;               // elements written per line
+  int64_t nbi, s_bo;
+  int64_t s_b, s_g, s_c, s_jt, s_js;
+  int32_t So;              // tile width of the output layout (>= m: plain rows)
+  int32_t T;               // output blocks ceil(L/m) (unfold)
+};
+struct PassArgs {
+  LineIn in_f, in_g;
+  LineOut out;
+  const void* tw_m;        // zeta_m^k,  k < m
+  const void* tw_M1;       // zeta_M1^k, k < M1
+  int64_t nlines;          // lines per batch entry
+  int64_t nbatch;
+  int64_t M1;
+  double scale;            // 1 / prod M1 (CONV)
+  int32_t q, D, C;
+  int32_t npairs;
+  int32_t batch_fastest;
+  int32_t pad_;
+};
+
+enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2 };
+
+// fold residues [r0, r0+nd) of the C lines of this group into buf[c][d][s]
+template <typename V, int M, int NT>
+__device__ __forceinline__ void fold(V* buf, const LineIn& in, int k, int64_t b, int64_t g,
+                                     int64_t nlines, int C, int r0, int nd, int q,
+                                     const V* zq, const V* __restrict__ twM1) {
+  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
+  const int items = C * M;
+  const bool cfast = (in.s_j != 1);
+  const int p = in.p;
+  const int64_t L = in.L;
+  for (int it = threadIdx.x; it < items; it += NT) {
+    int c, s;
+    if (cfast) { c = it % C; s = it / C; } else { s = it % M; c = it / M; }
+    const bool live = (g * C + c) < nlines;
+    const V* xl = x + c * in.s_c;
+    for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
+      V acc[kFoldChunk];
+      int e[kFoldChunk];  // (r * t) mod q, updated incrementally over t
+#pragma unroll
+      for (int d = 0; d < kFoldChunk; ++d) { acc[d] = cmk<V>(0, 0); e[d] = 0; }
+      if (live) {
+        for (int t = 0; t < p; ++t) {
+          const int64_t j = (int64_t)t * M + s;
+          if (j >= L) break;
+          const V u = xl[j * in.s_j];
+#pragma unroll
+          for (int d = 0; d < kFoldChunk; ++d) {
+            if (d0 + d < nd) {
+              acc[d] = cfma(acc[d], u, zq[e[d]]);
+              e[d] += r0 + d0 + d;
+              if (e[d] >= q) e[d] -= q;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < kFoldChunk; ++d) {
+        if (d0 + d < nd) {
+          const int r = r0 + d0 + d;
+          const V w = cmul(acc[d], ldg(twM1 + (int64_t)r * s));
+          buf[swz<V>((c * nd + d0 + d) * M + s)] = w;
+        }
+      }
+    }
+  }
+}
+
+// unfold residues [r0, r0+nd) from buf[c][d][s] into the output lines
+template <typename V, int M, int NT>
+__device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, int64_t b, int64_t g,
+                                       int64_t nlines, int C, int r0, int nd, int q, bool accumulate,
+                                       const V* zq, const V* __restrict__ twM1) {
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
+  const int items = C * M;
+  const int so = out.So < M ? out.So : M;
+  const int64_t L = out.L;
+  const int T = out.T;
+  for (int it = threadIdx.x; it < items; it += NT) {
+    const int s_lo = it % so;
+    const int rest = it / so;
+    const int c = rest % C;
+    const int s = (rest / C) * so + s_lo;
+    if ((g * C + c) >= nlines) continue;
+    V* yl = y + c * out.s_c;
+    for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
+      V v[kFoldChunk];
+#pragma unroll
+      for (int d = 0; d < kFoldChunk; ++d) {
+        v[d] = cmk<V>(0, 0);
+        if (d0 + d < nd) {
+          const int r = r0 + d0 + d;
+          v[d] = cmulc(buf[swz<V>((c * nd + d0 + d) * M + s)], ldg(twM1 + (int64_t)r * s));
+        }
+      }
+      int e[kFoldChunk];
+#pragma unroll
+      for (int d = 0; d < kFoldChunk; ++d) e[d] = 0;
+      const bool add = accumulate || d0 > 0;
+      for (int t = 0; t < T; ++t) {
+        const int64_t j = (int64_t)t * M + s;
+        if (j >= L) break;
+        V val = cmk<V>(0, 0);
+#pragma unroll
+        for (int d = 0; d < kFoldChunk; ++d) {
+          if (d0 + d < nd) {
+            val = cfmac(val, v[d], zq[e[d]]);
+            e[d] += r0 + d0 + d;
+            if (e[d] >= q) e[d] -= q;
+          }
+        }
+        V* dst = yl + (j / out.So) * out.s_jt + (j % out.So) * out.s_js;
+        if (add) { V o = *dst; val = cadd(o, val); }
+        *dst = val;
+      }
+    }
+  }
+}
+
+// store residue group spectrum buf[c][d][pos] -> out element kappa = r0*m + d*m + pos
+template <typename V, int M, int NT>
+__device__ __forceinline__ void store_spectrum(const V* buf, const LineOut& out, int k, int64_t b,
+                                               int64_t g, int64_t nlines, int C, int r0, int nd) {
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
+  const int so = out.So < M ? out.So : M;
+  const int items = C * nd * M;
+  for (int it = threadIdx.x; it < items; it += NT) {
+    const int e_lo = it % so;
+    const int rest = it / so;
+    const int c = rest % C;
+    const int e = (rest / C) * so + e_lo;
+    if ((g * C + c) >= nlines) continue;
+    const int d = e / M, pos = e % M;
+    const int64_t kap = (int64_t)r0 * M + e;
+    y[c * out.s_c + (kap / out.So) * out.s_jt + (kap % out.So) * out.s_js] =
+        buf[swz<V>((c * nd + d) * M + pos)];
+  }
+}
+
+// load residue group spectrum (internal order) into buf[c][d][pos]
+template <typename V, int M, int NT>
+__device__ __forceinline__ void load_spectrum(V* buf, const LineIn& in, int64_t b, int64_t g,
+                                              int64_t nlines, int C, int r0, int nd) {
+  const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
+  const int items = C * nd * M;
+  const bool cfast = (in.s_j != 1);
+  for (int it = threadIdx.x; it < items; it += NT) {
+    int c, e;
+    if (cfast) { c = it % C; e = it / C; } else { e = it % (nd * M); c = it / (nd * M); }
+    const int d = e / M, pos = e % M;
+    V v = cmk<V>(0, 0);
+    if ((g * C + c) < nlines) v = x[c * in.s_c + ((int64_t)r0 * M + e) * in.s_j];
+    buf[swz<V>((c * nd + d) * M + pos)] = v;
+  }
+}
+
+template <int EPR> __host__ __device__ constexpr int64_t round_slots(int64_t n) {
+  return (n + 8 * EPR - 1) / (8 * EPR) * (8 * EPR);
+}
+
+// ---------------------------------------------------------------------------
+// The pass kernel.  MODE_FWD: fold+FFT -> spectrum; MODE_INV: spectrum ->
+// IFFT+unfold; MODE_CONV: fold+FFT both inputs, sum of products, IFFT+unfold.
+// ---------------------------------------------------------------------------
+template <typename T, int M, int NT, int MODE>
+__global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassArgs a) {
+  using V = typename cplx_of<T>::type;
+  constexpr int EPR = 128 / (int)sizeof(V);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  V* smem = reinterpret_cast<V*>(smem_raw);
+
+  const int64_t g = a.batch_fastest ? blockIdx.y : blockIdx.x;
+  const int64_t b = a.batch_fastest ? blockIdx.x : blockIdx.y;
+  const int k_arr = blockIdx.z;
+  const int C = a.C, D = a.D, q = a.q;
+  const int64_t bufn = round_slots<EPR>((int64_t)C * D * M);
+
+  V* zq = smem;                                  // zeta_q^k, k < q
+  V* bufF = smem + round_slots<EPR>(q);
+  V* bufG = bufF + bufn;
+  V* bufA = bufG + bufn;
+  const V* twm = reinterpret_cast<const V*>(a.tw_m);
+  const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
+  for (int i = threadIdx.x; i < q; i += NT) zq[i] = ldg(twM1 + (int64_t)i * M);
+  __syncthreads();
+
+  for (int r0 = 0; r0 < q; r0 += D) {
+    const int nd = (q - r0) < D ? (q - r0) : D;
+    if constexpr (MODE == MODE_FWD) {
+      fold<V, M, NT>(bufF, a.in_f, k_arr, b, g, a.nlines, C, r0, nd, q, zq, twM1);
+      __syncthreads();
+      fft_fwd<V, M, NT>(bufF, C * nd, twm);
+      store_spectrum<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, r0, nd);
+      __syncthreads();
+    } else if constexpr (MODE == MODE_INV) {
+      load_spectrum<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, r0, nd);
+      __syncthreads();
+      fft_inv<V, M, NT>(bufF, C * nd, twm);
+      unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, r0, nd, q, r0 > 0, zq, twM1);
+      __syncthreads();
+    } else {
+      const T scale = (T)a.scale;
+      const int n = C * nd * M;
+      V* P = (a.npairs == 1) ? bufF : bufA;
+      for (int kk = 0; kk < a.npairs; ++kk) {
+        fold<V, M, NT>(bufF, a.in_f, kk, b, g, a.nlines, C, r0, nd, q, zq, twM1);
+        fold<V, M, NT>(bufG, a.in_g, kk, b, g, a.nlines, C, r0, nd, q, zq, twM1);
+        __syncthreads();
+        // bufF and bufG are adjacent: one FFT sweep over both
+        if (bufn == (int64_t)C * nd * M) {
+          fft_fwd<V, M, NT>(bufF, 2 * C * nd, twm);
+        } else {
+          fft_fwd<V, M, NT>(bufF, C * nd, twm);
+          fft_fwd<V, M, NT>(bufG, C * nd, twm);
+        }
+        for (int i = threadIdx.x; i < n; i += NT) {
+          const int si = swz<V>(i);
+          V pr = cmul(bufF[si], bufG[si]);
+          if (a.npairs == 1) P[si] = cscale(pr, scale);
+          else P[si] = (kk == 0) ? pr : cadd(P[si], pr);
+        }
+        __syncthreads();
+      }
+      if (a.npairs > 1) {
+        for (int i = threadIdx.x; i < n; i += NT) { const int si = swz<V>(i); P[si] = cscale(P[si], scale); }
+        __syncthreads();
+      }
+      fft_inv<V, M, NT>(P, C * nd, twm);
+      unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, r0, nd, q, r0 > 0, zq, twM1);
+      __syncthreads();
+    }
+  }
+}
+
+// Materialise explicit zero padding: dst[b][i0][i1][i2] = src[..] inside L, else 0.
+template <typename V>
+__global__ void pad_copy_kernel(const V* __restrict__ src, V* __restrict__ dst,
+                                int64_t L0, int64_t L1, int64_t L2,
+                                int64_t P0, int64_t P1, int64_t P2, int64_t nb) {
+  const int64_t total = nb * P0 * P1 * P2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i2 = i % P2, r = i / P2;
+    int64_t i1 = r % P1; r /= P1;
+    int64_t i0 = r % P0; int64_t bb = r / P0;
+    V v = cmk<V>(0, 0);
+    if (i0 < L0 && i1 < L1 && i2 < L2) v = src[((bb * L0 + i0) * L1 + i1) * L2 + i2];
+    dst[i] = v;
+  }
+}
+
+// Crop: dst[b][o0][o1][o2] = src[b][o0][o1][o2] with src extents P, dst extents O.
+template <typename V>
+__global__ void crop_copy_kernel(const V* __restrict__ src, V* __restrict__ dst,
+                                 int64_t O0, int64_t O1, int64_t O2,
+                                 int64_t P0, int64_t P1, int64_t P2, int64_t nb) {
+  const int64_t total = nb * O0 * O1 * O2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i2 = i % O2, r = i / O2;
+    int64_t i1 = r % O1; r /= O1;
+    int64_t i0 = r % O0; int64_t bb = r / O0;
+    dst[i] = src[((bb * P0 + i0) * P1 + i1) * P2 + i2];
+  }
+}
+
+}  // namespace hd

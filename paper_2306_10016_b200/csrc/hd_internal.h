@@ -1,0 +1,17 @@
+// hd_internal.h -- declarations shared by the host driver (hd_api.cu) and the
+// kernel instantiations (hd_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hd {
+struct PassArgs;
+using LaunchFn = cudaError_t (*)(const PassArgs&, dim3, size_t, cudaStream_t);
+// nullptr if (m, mode, threads) has no instantiation
+LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
+cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
+                       const int64_t P[3], int64_t nb, cudaStream_t st);
+cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],
+                        const int64_t P[3], int64_t nb, cudaStream_t st);
+constexpr size_t kMaxSmem = 227 * 1024;
+}  // namespace hd

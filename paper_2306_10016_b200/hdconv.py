@@ -1,0 +1,373 @@
+"""Thin ctypes binding of libhdconv.so (include/hdconv.h).
+
+Argument marshalling only: every step of the convolution runs in the CUDA
+kernels of libhdconv.so.  There is no CPU fallback: importing this module
+without the built library raises, and every compute call on a machine without
+a CUDA device raises HDError(HD_ERR_CUDA).
+
+Tensors are torch tensors on the context's device (complex128 -> HD_C128,
+complex64 -> HD_C64), row-major and contiguous.  The function names mirror the
+C entry points (hd_conv1d, hd_conv2d, ...).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhdconv.so")
+
+HD_C64, HD_C128 = 1, 2
+HD_OK, HD_ERR_INVALID, HD_ERR_UNSUPPORTED, HD_ERR_CUDA, HD_ERR_NCCL, HD_ERR_WORKSPACE = range(6)
+HD_FLAG_ALLOW_ALIAS = 0x1
+HD_FLAG_SHARED_G = 0x2
+HD_TUNE_PER_AXIS = 0x0
+HD_TUNE_EXHAUSTIVE = 0x1
+HD_MAX_DIM = 3
+HD_MAX_PAIRS = 16
+
+STATUS_NAMES = {0: "HD_OK", 1: "HD_ERR_INVALID", 2: "HD_ERR_UNSUPPORTED", 3: "HD_ERR_CUDA",
+                4: "HD_ERR_NCCL", 5: "HD_ERR_WORKSPACE"}
+
+EXPORTED = [
+    "hd_abi_version", "hd_create", "hd_destroy", "hd_last_error", "hd_plan_default",
+    "hd_plan_complete", "hd_spectral_permutation", "hd_workspace_bytes", "hd_conv1d",
+    "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host",
+    "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_log",
+    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count",
+]
+
+
+class AxisPlan(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("p_f", ctypes.c_int32), ("p_g", ctypes.c_int32),
+                ("q", ctypes.c_int32), ("C", ctypes.c_int32), ("S", ctypes.c_int32),
+                ("D", ctypes.c_int32), ("threads", ctypes.c_int32), ("M1", ctypes.c_int64)]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("axis", AxisPlan * HD_MAX_DIM), ("tuned_seconds", ctypes.c_double)]
+
+    def as_dict(self):
+        return {"ndim": self.ndim, "flags": self.flags, "tuned_seconds": self.tuned_seconds,
+                "axis": [{f: getattr(self.axis[i], f) for f, _ in AxisPlan._fields_}
+                         for i in range(self.ndim)]}
+
+    @staticmethod
+    def make(ndim, axes, flags=0):
+        """axes: list of dicts with m and optional C, S, D (0 = default)."""
+        p = Plan()
+        p.ndim = ndim
+        p.flags = flags
+        for i, a in enumerate(axes):
+            p.axis[i].m = int(a["m"])
+            p.axis[i].C = int(a.get("C", 0))
+            p.axis[i].S = int(a.get("S", 0))
+            p.axis[i].D = int(a.get("D", 0))
+            p.axis[i].threads = int(a.get("threads", 0))
+        return p
+
+
+class HDError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2306_10016_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
+    PP = ctypes.POINTER(Plan)
+    sig = {
+        "hd_abi_version": ([], ctypes.c_int),
+        "hd_create": ([ctypes.POINTER(P), ctypes.c_int], ctypes.c_int),
+        "hd_destroy": ([P], ctypes.c_int),
+        "hd_last_error": ([P], ctypes.c_char_p),
+        "hd_plan_default": ([ctypes.c_int, I32, I32, P, P, P, PP], ctypes.c_int),
+        "hd_plan_complete": ([ctypes.c_int, I32, I32, P, P, P, PP], ctypes.c_int),
+        "hd_spectral_permutation": ([I32, P], ctypes.c_int),
+        "hd_workspace_bytes": ([P, ctypes.c_int, I32, I32, I64, P, P, P, PP], SZ),
+        "hd_conv1d": ([P, ctypes.c_int, I64, P, I64, P, I64, P, I64, PP, P, SZ, P], ctypes.c_int),
+        "hd_conv2d": ([P, ctypes.c_int, I64, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
+        "hd_conv3d": ([P, ctypes.c_int, I64, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
+        "hd_multiconv": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
+        "hd_conv_explicit": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, PP, P], ctypes.c_int),
+        "hd_conv_host": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, PP, P], ctypes.c_int),
+        "hd_forward_residues": ([P, ctypes.c_int, I64, P, I64, I32, I32, P, P], ctypes.c_int),
+        "hd_backward_residues": ([P, ctypes.c_int, I64, P, I32, I32, P, I64, P], ctypes.c_int),
+        "hd_tune": ([P, ctypes.c_int, I32, I32, I64, P, P, P, U32, I32, P, PP], ctypes.c_int),
+        "hd_tune_log": ([P, I32, PP, P], I32),
+        "hd_profile_enable": ([P, I32], ctypes.c_int),
+        "hd_profile_read": ([P, I32, P, P, P], I32),
+        "hd_profile_reset": ([P], ctypes.c_int),
+        "hd_launch_count": ([P], I64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _i64arr(v):
+    a = (ctypes.c_int64 * len(v))(*[int(x) for x in v])
+    return a
+
+
+def _check(status, ctx=None):
+    if status != HD_OK:
+        msg = _lib.hd_last_error(ctx)
+        raise HDError(status, msg.decode() if msg else "")
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.complex128:
+        return HD_C128
+    if t.dtype == torch.complex64:
+        return HD_C64
+    raise TypeError(f"unsupported dtype {t.dtype} (complex64 / complex128 only)")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _ptr(t):
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------------------
+# host-only helpers (no GPU required)
+# ---------------------------------------------------------------------------
+def hd_plan_default(dtype, Lf, Lg, M=None, npairs=1):
+    ndim = len(Lf)
+    p = Plan()
+    Mv = _i64arr(M) if M is not None else None
+    _check(_lib.hd_plan_default(dtype, ndim, npairs, _i64arr(Lf), _i64arr(Lg), Mv, ctypes.byref(p)))
+    return p
+
+
+def hd_plan_complete(dtype, Lf, Lg, plan, M=None, npairs=1):
+    Mv = _i64arr(M) if M is not None else None
+    _check(_lib.hd_plan_complete(dtype, len(Lf), npairs, _i64arr(Lf), _i64arr(Lg), Mv,
+                                 ctypes.byref(plan)))
+    return plan
+
+
+def hd_spectral_permutation(m):
+    perm = np.zeros(m, dtype=np.int32)
+    _check(_lib.hd_spectral_permutation(m, perm.ctypes.data_as(ctypes.c_void_p)))
+    return perm
+
+
+def hd_abi_version():
+    return _lib.hd_abi_version()
+
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+class Context:
+    """One hd_ctx_t bound to a CUDA device (owns twiddle tables, plan cache, scratch)."""
+
+    def __init__(self, device=0):
+        h = ctypes.c_void_p()
+        _check(_lib.hd_create(ctypes.byref(h), int(device)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _lib.hd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        _check(st, self.h)
+
+    # ---- convolution (device tensors) --------------------------------------
+    def _out(self, like, shape):
+        import torch
+        return torch.empty(shape, dtype=like.dtype, device=like.device)
+
+    def conv(self, f, g, M=None, plan=None, h=None, batch=False, shared_g=False, stream=None):
+        """Full linear convolution of torch tensors f, g (1-3 dims, leading batch
+        axis when batch=True)."""
+        nd = f.dim() - (1 if batch else 0)
+        B = f.shape[0] if batch else 1
+        Lf = list(f.shape[-nd:])
+        Lg = list(g.shape[-nd:])
+        if plan is None and shared_g:
+            plan = self.default_plan(_dtype_code(f), Lf, Lg, M)
+        if plan is not None and shared_g:
+            plan.flags |= HD_FLAG_SHARED_G
+        out_shape = ([B] if batch else []) + [a + b - 1 for a, b in zip(Lf, Lg)]
+        if plan is not None and (plan.flags & HD_FLAG_ALLOW_ALIAS):
+            pc = hd_plan_complete(_dtype_code(f), Lf, Lg, Plan.from_buffer_copy(plan), M)
+            out_shape = ([B] if batch else []) + [min(a + b - 1, pc.axis[i].M1)
+                                                  for i, (a, b) in enumerate(zip(Lf, Lg))]
+        if h is None:
+            h = self._out(f, out_shape)
+        dt = _dtype_code(f)
+        Mv = _i64arr(M) if M is not None else _i64arr([0] * nd)
+        pp = ctypes.byref(plan) if plan is not None else None
+        st = _stream_ptr(stream)
+        if nd == 1:
+            self._chk(_lib.hd_conv1d(self.h, dt, B, _ptr(f), Lf[0], _ptr(g), Lg[0], _ptr(h),
+                                     int(M[0]) if M is not None else 0, pp, None, 0, st))
+        elif nd == 2:
+            self._chk(_lib.hd_conv2d(self.h, dt, B, _ptr(f), _i64arr(Lf), _ptr(g), _i64arr(Lg),
+                                     _ptr(h), Mv, pp, None, 0, st))
+        elif nd == 3:
+            self._chk(_lib.hd_conv3d(self.h, dt, B, _ptr(f), _i64arr(Lf), _ptr(g), _i64arr(Lg),
+                                     _ptr(h), Mv, pp, None, 0, st))
+        else:
+            raise ValueError("ndim must be 1, 2 or 3")
+        return h
+
+    def hd_conv1d(self, f, g, **kw):
+        return self.conv(f, g, **kw)
+
+    def hd_conv2d(self, f, g, **kw):
+        return self.conv(f, g, **kw)
+
+    def hd_conv3d(self, f, g, **kw):
+        return self.conv(f, g, **kw)
+
+    def hd_multiconv(self, fs, gs, M=None, plan=None, h=None, stream=None):
+        """h = sum_k fs[k] * gs[k]."""
+        N = len(fs)
+        nd = fs[0].dim()
+        Lf, Lg = list(fs[0].shape), list(gs[0].shape)
+        if h is None:
+            h = self._out(fs[0], [a + b - 1 for a, b in zip(Lf, Lg)])
+        fp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in fs])
+        gp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in gs])
+        Mv = _i64arr(M) if M is not None else None
+        pp = ctypes.byref(plan) if plan is not None else None
+        self._chk(_lib.hd_multiconv(self.h, _dtype_code(fs[0]), nd, N, fp, _i64arr(Lf), gp,
+                                    _i64arr(Lg), _ptr(h), Mv, pp, None, 0, _stream_ptr(stream)))
+        return h
+
+    multiconv = hd_multiconv
+
+    def hd_conv_explicit(self, fs, gs, plan=None, h=None, stream=None):
+        N = len(fs)
+        nd = fs[0].dim()
+        Lf, Lg = list(fs[0].shape), list(gs[0].shape)
+        if h is None:
+            h = self._out(fs[0], [a + b - 1 for a, b in zip(Lf, Lg)])
+        fp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in fs])
+        gp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in gs])
+        pp = ctypes.byref(plan) if plan is not None else None
+        self._chk(_lib.hd_conv_explicit(self.h, _dtype_code(fs[0]), nd, N, fp, _i64arr(Lf), gp,
+                                        _i64arr(Lg), _ptr(h), pp, _stream_ptr(stream)))
+        return h
+
+    def hd_conv_host(self, fs, gs, h, ndim, batch=1, M=None, plan=None, stream=None):
+        """End-to-end with HOST buffers: fs, gs lists of (pinned) CPU tensors or numpy
+        arrays ([batch] + extents), h a CPU tensor / numpy array receiving the result."""
+        N = len(fs)
+        def hp(a):
+            return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+        nd = int(ndim)
+        Lf = list(fs[0].shape)[-nd:]
+        Lg = list(gs[0].shape)[-nd:]
+        is128 = (fs[0].dtype == np.complex128) if isinstance(fs[0], np.ndarray) else \
+            (str(fs[0].dtype) == "torch.complex128")
+        dt = HD_C128 if is128 else HD_C64
+        fp = (ctypes.c_void_p * N)(*[hp(t) for t in fs])
+        gp = (ctypes.c_void_p * N)(*[hp(t) for t in gs])
+        Mv = _i64arr(M) if M is not None else None
+        pp = ctypes.byref(plan) if plan is not None else None
+        self._chk(_lib.hd_conv_host(self.h, dt, nd, N, batch, fp, _i64arr(Lf), gp, _i64arr(Lg),
+                                    ctypes.c_void_p(hp(h)), Mv, pp, _stream_ptr(stream)))
+        return h
+
+    def hd_forward_residues(self, x, m, q, X=None, stream=None):
+        """x: [nlines, L] -> X: [nlines, q*m] (internal residue order)."""
+        nl, L = x.shape
+        if X is None:
+            X = self._out(x, [nl, q * m])
+        self._chk(_lib.hd_forward_residues(self.h, _dtype_code(x), nl, _ptr(x), L, m, q, _ptr(X),
+                                           _stream_ptr(stream)))
+        return X
+
+    def hd_backward_residues(self, X, m, q, Lout, x=None, stream=None):
+        nl = X.shape[0]
+        if x is None:
+            x = self._out(X, [nl, Lout])
+        self._chk(_lib.hd_backward_residues(self.h, _dtype_code(X), nl, _ptr(X), m, q, _ptr(x),
+                                            Lout, _stream_ptr(stream)))
+        return x
+
+    def default_plan(self, dtype, Lf, Lg, M=None, npairs=1):
+        return hd_plan_default(dtype, Lf, Lg, M, npairs)
+
+    def hd_tune(self, dtype, Lf, Lg, M=None, N=1, batch=1, exhaustive=False, reps=5, stream=None):
+        p = Plan()
+        Mv = _i64arr(M) if M is not None else None
+        self._chk(_lib.hd_tune(self.h, dtype, len(Lf), N, batch, _i64arr(Lf), _i64arr(Lg), Mv,
+                               HD_TUNE_EXHAUSTIVE if exhaustive else HD_TUNE_PER_AXIS, reps,
+                               _stream_ptr(stream), ctypes.byref(p)))
+        return p
+
+    tune = hd_tune
+
+    def hd_tune_log(self):
+        n = _lib.hd_tune_log(self.h, 0, None, None)
+        plans = (Plan * max(n, 1))()
+        secs = np.zeros(max(n, 1), dtype=np.float64)
+        _lib.hd_tune_log(self.h, n, plans, secs.ctypes.data_as(ctypes.c_void_p))
+        return [(plans[i], float(secs[i])) for i in range(n)]
+
+    def hd_workspace_bytes(self, dtype, Lf, Lg, M=None, npairs=1, batch=1, plan=None):
+        Mv = _i64arr(M) if M is not None else None
+        pp = ctypes.byref(plan) if plan is not None else None
+        return _lib.hd_workspace_bytes(self.h, dtype, len(Lf), npairs, batch, _i64arr(Lf),
+                                       _i64arr(Lg), Mv, pp)
+
+    def profile_enable(self, on=True):
+        self._chk(_lib.hd_profile_enable(self.h, 1 if on else 0))
+
+    def profile_reset(self):
+        self._chk(_lib.hd_profile_reset(self.h))
+
+    def profile_read(self):
+        n = _lib.hd_profile_read(self.h, 0, None, None, None)
+        ms = np.zeros(max(n, 1))
+        la = np.zeros(max(n, 1), dtype=np.int64)
+        names = ctypes.create_string_buffer(32 * max(n, 1))
+        _lib.hd_profile_read(self.h, n, ms.ctypes.data_as(ctypes.c_void_p),
+                             la.ctypes.data_as(ctypes.c_void_p), names)
+        out = {}
+        for i in range(n):
+            nm = names.raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode()
+            out[nm] = (float(ms[i]), int(la[i]))
+        return out
+
+    def launch_count(self):
+        return int(_lib.hd_launch_count(self.h))

@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Tolerance (north_star): relative L2 <= 1e-11 for complex128 and
+<= 1e-5 for complex64.  Run with -m gpu on a B200."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {np.complex128: 1e-11, np.complex64: 1e-5}
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2306_10016_b200 import hdconv
+    return hdconv
+
+
+@pytest.fixture(scope="module")
+def ctx(H):
+    c = H.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------- residue routines
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("m", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
+def test_fft_m_vs_naive_dft(ctx, H, dtype, m):
+    # U1: q = 1, L = m: the residue transform is the size-m DFT
+    x = synth.random_pair(m, (3, m), (1,))[0].astype(dtype)
+    X = host(ctx.hd_forward_residues(dev(x), m, 1))
+    perm = H.hd_spectral_permutation(m)
+    for l in range(3):
+        ref = oracle.dft(x[l], m, +1)
+        got = np.empty(m, complex)
+        got[perm] = X[l]
+        assert oracle.rel_l2(got, ref) < TOL[dtype] / 10
+
+
+@pytest.mark.parametrize("L,m,q", [(3, 2, 2), (13, 4, 5), (100, 16, 9), (255, 512, 9),
+                                   (4096, 512, 9), (3000, 1024, 11), (129, 128, 5),
+                                   (1000, 64, 17), (64, 32, 4), (5, 8, 1)])
+def test_residue_blocks_vs_dft(ctx, H, L, m, q):
+    # U2: block r equals DFT_{qm}(x padded)[q l + r]
+    x = synth.random_pair(L + 7 * m, (2, L), (1,))[0]
+    X = host(ctx.hd_forward_residues(dev(x), m, q))
+    perm = H.hd_spectral_permutation(m)
+    for l in range(2):
+        full = oracle.dft(x[l], q * m, +1)
+        for r in range(q):
+            got = np.empty(m, complex)
+            got[perm] = X[l, r * m:(r + 1) * m]
+            assert oracle.rel_l2(got, full[r::q]) < 1e-12
+
+
+@pytest.mark.parametrize("L,m,q", [(3, 2, 2), (100, 16, 9), (4096, 512, 9), (129, 128, 5)])
+def test_round_trip(ctx, L, m, q):
+    # U3: backward(forward(x)) = q m x
+    x = synth.random_pair(L, (2, L), (1,))[0]
+    X = ctx.hd_forward_residues(dev(x), m, q)
+    y = host(ctx.hd_backward_residues(X, m, q, L)) / (q * m)
+    assert oracle.rel_l2(y, x) < 1e-13
+
+
+def test_spec_worked_residue_example(ctx, H, golden):
+    d = golden("residue_forward.json")
+    X = host(ctx.hd_forward_residues(dev(np.array([d["x"]], complex)), d["m"], d["q"]))
+    perm = H.hd_spectral_permutation(d["m"])
+    for r in (0, 1):
+        got = np.empty(2, complex)
+        got[perm] = X[0, 2 * r:2 * r + 2]
+        want = np.array([complex(a, b) for a, b in d[f"r{r}"]])
+        assert np.allclose(got, want, atol=1e-13)
+
+
+# ---------------------------------------------------------------- 1D
+def test_worked_example(ctx, H, golden):
+    d = golden("worked_example_1d.json")
+    for m in (2, 4, 8):
+        h = host(ctx.conv(dev(np.array(d["f"], complex)), dev(np.array(d["g"], complex)),
+                          plan=H.Plan.make(1, [{"m": m}])))
+        assert np.allclose(h, d["h"], atol=1e-13)
+
+
+def test_alias_fold(ctx, H, golden):
+    d = golden("alias_fold_1d.json")
+    p = H.Plan.make(1, [{"m": 2}], flags=H.HD_FLAG_ALLOW_ALIAS)
+    h = host(ctx.conv(dev(np.array(d["f"], complex)), dev(np.array(d["g"], complex)),
+                      M=[d["M"]], plan=p))
+    assert np.allclose(h, d["h"], atol=1e-13)
+
+
+def test_config1(ctx, H):
+    d = synth.config_inputs(1)
+    f, g = d["f"][0], d["g"][0]
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(1, [{"m": 32, "D": 4}])))
+    assert h.shape == (103,)
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
+
+
+def test_random_1d_sweep(ctx, H):
+    # randomised small problems, every admissible plan shape (SPEC.md:202 style)
+    s = synth.Stream(99)
+    for case in range(60):
+        Lf = 1 + int(s.uniform(1)[0] * 64)
+        Lg = 1 + int(s.uniform(1)[0] * 64)
+        f, g = synth.random_pair(1000 + case, (Lf,), (Lg,))
+        ref = oracle.conv(f, g)
+        m = 2 ** (1 + case % 7)
+        q = -(-(Lf + Lg - 1) // m)
+        D = 1 + case % q
+        C = 1 << (case % 3)
+        h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(1, [{"m": m, "D": D, "C": C}])))
+        assert oracle.rel_l2(h, ref) < 1e-11, (Lf, Lg, m, D, C)
+
+
+@pytest.mark.parametrize("C,D", [(1, 0), (2, 3), (4, 1)])
+def test_batched_1d(ctx, H, C, D):
+    f, g = synth.random_pair(5, (7, 300), (7, 77))
+    h = host(ctx.conv(dev(f), dev(g), batch=True,
+                      plan=H.Plan.make(1, [{"m": 64, "C": C, "D": D}])))
+    assert oracle.rel_l2(h, oracle.conv_batch(f, g)) < 1e-11
+    # shared g
+    hs = host(ctx.conv(dev(f), dev(g[0]), batch=True, shared_g=True))
+    ref = np.stack([oracle.conv(f[b], g[0]) for b in range(7)])
+    assert oracle.rel_l2(hs, ref) < 1e-11
+
+
+def test_padding_monotonicity(ctx, H):
+    # any M >= L_out gives the same first L_out outputs
+    f, g = synth.random_pair(8, (37,), (21,))
+    ref = oracle.conv(f, g)
+    for M in (57, 58, 64, 100, 200):
+        h = host(ctx.conv(dev(f), dev(g), M=[M], plan=H.Plan.make(1, [{"m": 8}])))
+        assert oracle.rel_l2(h, ref) < 1e-11
+
+
+def test_integer_exactness(ctx):
+    f, g = synth.integer_pair(4, (500,), (300,))
+    h = host(ctx.conv(dev(f), dev(g)))
+    ref = oracle.conv(f, g)
+    assert np.array_equal(np.round(h.real), ref.real) and np.array_equal(np.round(h.imag), ref.imag)
+    assert np.max(np.abs(h - ref)) < 1e-9
+
+
+def test_c64_1d(ctx):
+    f, g = synth.random_pair(6, (1000,), (333,))
+    h = host(ctx.conv(dev(f.astype(np.complex64)), dev(g.astype(np.complex64))))
+    ref = oracle.conv(f.astype(np.complex64), g.astype(np.complex64))
+    assert oracle.rel_l2(h, ref) < 1e-5
+
+
+# ---------------------------------------------------------------- 2D / 3D / multiconv
+PLANS_2D = [None,
+            [{"m": 8, "S": 1, "D": 0}, {"m": 16, "C": 1, "D": 0}],
+            [{"m": 16, "S": 2, "D": 2}, {"m": 8, "C": 2, "D": 3}],
+            [{"m": 32, "S": 4, "D": 1}, {"m": 64, "C": 4, "D": 1}],
+            [{"m": 4, "S": 8, "D": 5}, {"m": 4, "C": 8, "D": 2}]]
+
+
+@pytest.mark.parametrize("pi", range(len(PLANS_2D)))
+def test_2d_plans(ctx, H, pi):
+    f, g = synth.random_pair(20 + pi, (45, 70), (13, 9))
+    ref = oracle.conv(f, g)
+    plan = None if PLANS_2D[pi] is None else H.Plan.make(2, PLANS_2D[pi])
+    h = host(ctx.conv(dev(f), dev(g), plan=plan))
+    assert oracle.rel_l2(h, ref) < 1e-11
+
+
+def test_2d_batched_and_swapped(ctx):
+    f, g = synth.random_pair(30, (3, 20, 33), (3, 41, 7))  # g longer on axis 0
+    h = host(ctx.conv(dev(f), dev(g), batch=True))
+    ref = np.stack([oracle.conv(f[b], g[b]) for b in range(3)])
+    assert oracle.rel_l2(h, ref) < 1e-11
+
+
+def test_2d_separability_and_delta(ctx):
+    s = synth.Stream(31)
+    a, b, c, d = (s.complex_uniform((n,)) for n in (30, 25, 7, 12))
+    h = host(ctx.conv(dev(np.outer(a, b)), dev(np.outer(c, d))))
+    assert oracle.rel_l2(h, np.outer(np.convolve(a, c), np.convolve(b, d))) < 1e-11
+    g = s.complex_uniform((17, 19))
+    delta = np.zeros((2, 3), complex)
+    delta[1, 2] = 1
+    h2 = host(ctx.conv(dev(delta), dev(g)))
+    assert np.allclose(h2[1:, 2:], g, atol=1e-13) and np.max(np.abs(h2[0])) < 1e-13
+
+
+def test_2d_c64(ctx):
+    f, g = synth.random_pair(32, (100, 90), (20, 31), dtype=np.complex64)
+    h = host(ctx.conv(dev(f), dev(g)))
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-5
+
+
+PLANS_3D = [None,
+            [{"m": 8, "S": 2, "D": 0}, {"m": 4, "S": 2, "D": 3}, {"m": 16, "C": 2, "D": 0}],
+            [{"m": 16, "S": 1, "D": 1}, {"m": 8, "S": 1, "D": 0}, {"m": 8, "C": 4, "D": 2}],
+            [{"m": 4, "S": 4, "D": 2}, {"m": 16, "S": 4, "D": 1}, {"m": 4, "C": 1, "D": 0}]]
+
+
+@pytest.mark.parametrize("pi", range(len(PLANS_3D)))
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_3d_plans(ctx, H, pi, dtype):
+    f, g = synth.random_pair(40 + pi, (19, 14, 23), (6, 9, 4), dtype=dtype)
+    ref = oracle.conv(f, g)
+    plan = None if PLANS_3D[pi] is None else H.Plan.make(3, PLANS_3D[pi])
+    h = host(ctx.conv(dev(f), dev(g), plan=plan))
+    assert oracle.rel_l2(h, ref) < TOL[dtype]
+
+
+def test_multiconv(ctx, H):
+    s = synth.Stream(50)
+    fs = [s.complex_uniform((30, 41)) for _ in range(5)]
+    gs = [s.complex_uniform((12, 23)) for _ in range(5)]
+    ref = oracle.multiconv(fs, gs)
+    h = host(ctx.multiconv([dev(a) for a in fs], [dev(a) for a in gs]))
+    assert oracle.rel_l2(h, ref) < 1e-11
+    p = H.Plan.make(2, [{"m": 8, "S": 2, "D": 2}, {"m": 16, "C": 2, "D": 1}])
+    h = host(ctx.multiconv([dev(a) for a in fs], [dev(a) for a in gs], plan=p))
+    assert oracle.rel_l2(h, ref) < 1e-11
+    f1 = [s.complex_uniform((50,)) for _ in range(3)]
+    g1 = [s.complex_uniform((20,)) for _ in range(3)]
+    h1 = host(ctx.multiconv([dev(a) for a in f1], [dev(a) for a in g1]))
+    assert oracle.rel_l2(h1, oracle.multiconv(f1, g1)) < 1e-11
+    f3 = [s.complex_uniform((7, 8, 9)) for _ in range(2)]
+    g3 = [s.complex_uniform((3, 4, 5)) for _ in range(2)]
+    h3 = host(ctx.multiconv([dev(a) for a in f3], [dev(a) for a in g3]))
+    assert oracle.rel_l2(h3, oracle.multiconv(f3, g3)) < 1e-11
+
+
+def test_explicit_variant(ctx):
+    f, g = synth.random_pair(60, (40, 33), (11, 20))
+    h = host(ctx.hd_conv_explicit([dev(f)], [dev(g)]))
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
+    f1, g1 = synth.random_pair(61, (300,), (45,))
+    h1 = host(ctx.hd_conv_explicit([dev(f1)], [dev(g1)]))
+    assert oracle.rel_l2(h1, oracle.conv(f1, g1)) < 1e-11
+
+
+def test_host_entry_point(ctx):
+    f, g = synth.random_pair(70, (64, 50), (10, 12))
+    h = np.zeros((73, 61), complex)
+    ctx.hd_conv_host([f], [g], h, ndim=2)
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
+
+
+def test_alias_2d(ctx, H):
+    f, g = synth.random_pair(71, (10, 12), (7, 5))
+    p = H.Plan.make(2, [{"m": 4}, {"m": 4}], flags=H.HD_FLAG_ALLOW_ALIAS)
+    h = host(ctx.conv(dev(f), dev(g), M=[12, 8], plan=p))
+    want = oracle.alias_fold(oracle.conv(f, g), [12, 8])
+    assert h.shape == want.shape and oracle.rel_l2(h, want) < 1e-11
+
+
+def test_tune_small(ctx, H):
+    p = ctx.tune(H.HD_C128, [200, 300], [31, 17], reps=2)
+    log = ctx.hd_tune_log()
+    assert len(log) >= 2 and p.tuned_seconds > 0
+    assert abs(p.tuned_seconds - min(t for _, t in log)) <= 1e-9 * p.tuned_seconds
+    f, g = synth.random_pair(80, (200, 300), (31, 17))
+    h = host(ctx.conv(dev(f), dev(g), plan=p))
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
