@@ -122,11 +122,14 @@ int64_t round_slots(int64_t n, size_t eb) {
   return (n + 8 * epr - 1) / (8 * epr) * (8 * epr);
 }
 size_t pass_smem(size_t eb, int q, int lines, int D, int m, int nbuf) {
-  return eb * (size_t)(round_slots(q, eb) + nbuf * round_slots((int64_t)lines * D * m, eb));
+  return eb * (size_t)(round_slots(q, eb) + round_slots(hd::kQF * hd::kQF, eb) +
+                       nbuf * round_slots((int64_t)lines * D * m, eb));
 }
 int conv_nbuf(int npairs) { return npairs == 1 ? 2 : 3; }
 
 bool valid_lines(int v) { return v == 1 || v == 2 || v == 4 || v == 8 || v == 16; }
+// 512 threads when one pass sweep has at least 512 independent (line, s) items
+int default_threads(int lines, int m) { return (int64_t)lines * m >= 512 ? 512 : 256; }
 
 hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const int64_t* Lf,
                           const int64_t* Lg, const int64_t* M, hd_plan_t* plan, AxisInfo* ax) {
@@ -160,8 +163,9 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     if (a.D == 0) a.D = x.q;
     if (a.D < 1 || a.D > x.q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
     x.D = a.D;
-    if (a.threads == 0) a.threads = kDefaultThreads;
-    if (a.threads != kDefaultThreads) return fail(ctx, HD_ERR_UNSUPPORTED, "threads must be 256 in this build");
+    if (a.threads == 0) a.threads = default_threads(lines_for(a, i, ndim), a.m);
+    if (a.threads != 256 && a.threads != 512)
+      return fail(ctx, HD_ERR_UNSUPPORTED, "threads must be 256 or 512 in this build");
     x.threads = a.threads;
     x.lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
@@ -215,7 +219,7 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
     p.axis[i].D = bD;
     p.axis[i].C = (i == ndim - 1) ? lines : 1;
     p.axis[i].S = (i == ndim - 1) ? 1 : lines;
-    p.axis[i].threads = kDefaultThreads;
+    p.axis[i].threads = default_threads(lines, bm);
   }
   if (ndim == 3) p.axis[1].S = p.axis[0].S;
   *out = p;
@@ -234,7 +238,7 @@ struct Launch {
 };
 
 void init_in(LineIn& in) { std::memset(&in, 0, sizeof(in)); in.nbi = 1; }
-void init_out(LineOut& o) { std::memset(&o, 0, sizeof(o)); o.nbi = 1; o.So = 1; }
+void init_out(LineOut& o) { std::memset(&o, 0, sizeof(o)); o.nbi = 1; o.so_log2 = 0; }
 
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
@@ -329,6 +333,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   L.a.q = x.q;
   L.a.D = x.D;
   L.a.C = x.lines;
+  L.a.c_log2 = ilog2(x.lines);
   L.a.M1 = x.M1;
   L.a.npairs = (mode == hd::MODE_CONV) ? P.N : 1;
   L.a.scale = 1.0;
@@ -384,7 +389,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; L.a.in_f.s_g = c * x.Lf; L.a.in_f.s_c = x.Lf; L.a.in_f.s_j = 1;
     L.a.in_g.L = x.Lg; L.a.in_g.p = x.pg;
     L.a.in_g.s_g = P.shared_g ? 0 : c * x.Lg; L.a.in_g.s_c = P.shared_g ? 0 : x.Lg; L.a.in_g.s_j = 1;
-    L.a.out.ptr[0] = P.h; L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.So = (int32_t)kHugeTile;
+    L.a.out.ptr[0] = P.h; L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.so_log2 = 40;
     L.a.out.s_g = c * x.O; L.a.out.s_c = x.O; L.a.out.s_jt = 0; L.a.out.s_js = 1;
     L.a.scale = scale;
     L.a.nlines = B; L.a.nbatch = 1;
@@ -413,7 +418,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_f.L = len; L.a.in_f.p = which == 0 ? x.pf : x.pg;
       L.a.in_f.nbi = nb; L.a.in_f.s_b = rows * len; L.a.in_f.s_g = Cx * len; L.a.in_f.s_c = len; L.a.in_f.s_j = 1;
       L.a.out.nbi = nb; L.a.out.s_b = Kx * rows; L.a.out.s_g = Cx * Sy; L.a.out.s_c = Sy;
-      L.a.out.So = (int32_t)Sy; L.a.out.s_jt = rows * Sy; L.a.out.s_js = 1; L.a.out.L = Kx;
+      L.a.out.so_log2 = ilog2(Sy); L.a.out.s_jt = rows * Sy; L.a.out.s_js = 1; L.a.out.L = Kx;
       L.a.nlines = rows; L.a.nbatch = nb;
       L.ngroups = cdiv(rows, Cx); L.nbatch = nb; L.narrays = N;
       hd_status_t s = launch(ctx, P.dt, L, st);
@@ -428,7 +433,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_g.L = y.Lg; L.a.in_g.p = y.pg; L.a.in_g.nbi = B;
       L.a.in_g.s_b = P.shared_g ? 0 : Kx * y.Lg; L.a.in_g.s_g = y.Lg * Sy; L.a.in_g.s_c = 1; L.a.in_g.s_j = Sy;
       L.a.out.ptr[0] = Y; L.a.out.nbi = B; L.a.out.s_b = Oyp * Kx; L.a.out.s_g = Sy * Cx; L.a.out.s_c = Cx;
-      L.a.out.So = (int32_t)Cx; L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1; L.a.out.L = y.O; L.a.out.T = y.T;
+      L.a.out.so_log2 = ilog2(Cx); L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1; L.a.out.L = y.O; L.a.out.T = y.T;
       L.a.scale = scale;
       L.a.nlines = Kx; L.a.nbatch = B;
       L.ngroups = cdiv(Kx, Sy); L.nbatch = B;
@@ -441,7 +446,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_f.ptr[0] = Y; L.a.in_f.nbi = B; L.a.in_f.s_b = Oyp * Kx; L.a.in_f.s_g = Kx * Cx;
       L.a.in_f.s_c = 1; L.a.in_f.s_j = Cx; L.a.in_f.L = Kx;
       L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; L.a.out.s_g = Cx * x.O;
-      L.a.out.s_c = x.O; L.a.out.So = (int32_t)kHugeTile; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+      L.a.out.s_c = x.O; L.a.out.so_log2 = 40; L.a.out.s_jt = 0; L.a.out.s_js = 1;
       L.a.out.L = x.O; L.a.out.T = x.T;
       L.a.nlines = y.O; L.a.nbatch = B;
       L.ngroups = cdiv(y.O, Cx); L.nbatch = B;
@@ -472,7 +477,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_f.L = Fx; L.a.in_f.p = which == 0 ? x.pf : x.pg;
       L.a.in_f.nbi = nb * Fz; L.a.in_f.s_b = Fy * Fx; L.a.in_f.s_g = Cx * Fx; L.a.in_f.s_c = Fx; L.a.in_f.s_j = 1;
       L.a.out.nbi = nb * Fz; L.a.out.s_b = Kx * Fy; L.a.out.s_g = Cx * S; L.a.out.s_c = S;
-      L.a.out.So = (int32_t)S; L.a.out.s_jt = Fy * S; L.a.out.s_js = 1; L.a.out.L = Kx;
+      L.a.out.so_log2 = ilog2(S); L.a.out.s_jt = Fy * S; L.a.out.s_js = 1; L.a.out.L = Kx;
       L.a.nlines = Fy; L.a.nbatch = nb * Fz;
       L.ngroups = cdiv(Fy, Cx); L.nbatch = nb * Fz; L.narrays = N;
       hd_status_t s = launch(ctx, P.dt, L, st);
@@ -489,7 +494,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_f.nbi = Fz; L.a.in_f.s_bo = Fz * Kx * Fy; L.a.in_f.s_b = Kx * Fy;
       L.a.in_f.s_g = Fy * S; L.a.in_f.s_c = 1; L.a.in_f.s_j = S;
       L.a.out.nbi = Fz; L.a.out.s_bo = Ky * Kx * Fz; L.a.out.s_b = S; L.a.out.s_g = Fz * S; L.a.out.s_c = 1;
-      L.a.out.So = 1; L.a.out.s_jt = Kx * Fz; L.a.out.s_js = 0; L.a.out.L = Ky;
+      L.a.out.so_log2 = 0; L.a.out.s_jt = Kx * Fz; L.a.out.s_js = 0; L.a.out.L = Ky;
       L.a.batch_fastest = 1;
       L.a.nlines = Kx; L.a.nbatch = nb * Fz;
       L.ngroups = cdiv(Kx, S); L.nbatch = nb * Fz; L.narrays = N;
@@ -506,7 +511,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_g.L = z.Lg; L.a.in_g.p = z.pg; L.a.in_g.nbi = Ky; L.a.in_g.s_bo = P.shared_g ? 0 : Ky * Kx * z.Lg;
     L.a.in_g.s_b = Kx * z.Lg; L.a.in_g.s_g = z.Lg * S; L.a.in_g.s_c = 1; L.a.in_g.s_j = S;
     L.a.out.ptr[0] = Zl; L.a.out.nbi = Ky; L.a.out.s_bo = z.O * Kx * Ky; L.a.out.s_b = S;
-    L.a.out.s_g = Ky * S; L.a.out.s_c = 1; L.a.out.So = 1; L.a.out.s_jt = Kx * Ky; L.a.out.s_js = 0;
+    L.a.out.s_g = Ky * S; L.a.out.s_c = 1; L.a.out.so_log2 = 0; L.a.out.s_jt = Kx * Ky; L.a.out.s_js = 0;
     L.a.out.L = z.O; L.a.out.T = z.T;
     L.a.scale = scale;
     L.a.batch_fastest = 1;
@@ -521,7 +526,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_f.ptr[0] = Zl; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Kx * Ky; L.a.in_f.s_g = Ky * S;
     L.a.in_f.s_c = 1; L.a.in_f.s_j = S; L.a.in_f.L = Ky;
     L.a.out.ptr[0] = W; L.a.out.nbi = B * z.O; L.a.out.s_b = Oyp * Kx; L.a.out.s_g = S * Cx;
-    L.a.out.s_c = Cx; L.a.out.So = (int32_t)Cx; L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1;
+    L.a.out.s_c = Cx; L.a.out.so_log2 = ilog2(Cx); L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1;
     L.a.out.L = y.O; L.a.out.T = y.T;
     L.a.nlines = Kx; L.a.nbatch = B * z.O;
     L.ngroups = cdiv(Kx, S); L.nbatch = B * z.O;
@@ -534,7 +539,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_f.ptr[0] = W; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Oyp * Kx; L.a.in_f.s_g = Kx * Cx;
     L.a.in_f.s_c = 1; L.a.in_f.s_j = Cx; L.a.in_f.L = Kx;
     L.a.out.ptr[0] = P.h; L.a.out.nbi = B * z.O; L.a.out.s_b = y.O * x.O; L.a.out.s_g = Cx * x.O;
-    L.a.out.s_c = x.O; L.a.out.So = (int32_t)kHugeTile; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+    L.a.out.s_c = x.O; L.a.out.so_log2 = 40; L.a.out.s_jt = 0; L.a.out.s_js = 1;
     L.a.out.L = x.O; L.a.out.T = x.T;
     L.a.nlines = y.O; L.a.nbatch = B * z.O;
     L.ngroups = cdiv(y.O, Cx); L.nbatch = B * z.O;
@@ -873,7 +878,7 @@ hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, 
   if (s != HD_OK) return s;
   Launch Lh = make_launch(ctx, P, hd::MODE_FWD, "fwd_residues", 0, twm, twM1);
   Lh.a.in_f.ptr[0] = x; Lh.a.in_f.L = L; Lh.a.in_f.p = a.pf; Lh.a.in_f.s_g = L; Lh.a.in_f.s_c = L; Lh.a.in_f.s_j = 1;
-  Lh.a.out.ptr[0] = X; Lh.a.out.So = (int32_t)kHugeTile; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
+  Lh.a.out.ptr[0] = X; Lh.a.out.so_log2 = 40; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
   Lh.a.out.s_g = a.M1; Lh.a.out.s_c = a.M1; Lh.a.out.L = a.M1;
   Lh.a.nlines = nlines; Lh.a.nbatch = 1;
   Lh.ngroups = nlines; Lh.nbatch = 1;
@@ -904,7 +909,7 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
   if (s != HD_OK) return s;
   Launch Lh = make_launch(ctx, P, hd::MODE_INV, "bwd_residues", 0, twm, twM1);
   Lh.a.in_f.ptr[0] = X; Lh.a.in_f.s_g = a.M1; Lh.a.in_f.s_c = a.M1; Lh.a.in_f.s_j = 1; Lh.a.in_f.L = a.M1;
-  Lh.a.out.ptr[0] = x; Lh.a.out.So = (int32_t)kHugeTile; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
+  Lh.a.out.ptr[0] = x; Lh.a.out.so_log2 = 40; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
   Lh.a.out.s_g = Lout; Lh.a.out.s_c = Lout; Lh.a.out.L = Lout; Lh.a.out.T = a.T;
   Lh.a.nlines = nlines; Lh.a.nbatch = 1;
   Lh.ngroups = nlines; Lh.nbatch = 1;
@@ -959,13 +964,14 @@ int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 // ===========================================================================
 namespace {
 
-struct AxisCand { int m, C, S, D; };
+struct AxisCand { int m, C, S, D, threads; };
 
 bool cand_less(const AxisCand& a, const AxisCand& b) {
   if (a.m != b.m) return a.m < b.m;
   if (a.C != b.C) return a.C < b.C;
   if (a.S != b.S) return a.S < b.S;
-  return a.D < b.D;
+  if (a.D != b.D) return a.D < b.D;
+  return a.threads < b.threads;
 }
 
 std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, int npairs,
@@ -984,8 +990,10 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
       if (q > 1) Ds.push_back((q + 1) / 2);
       for (int D : Ds) {
         if (pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) continue;
-        AxisCand c{m, contig ? lines : base.axis[i].C, contig ? base.axis[i].S : lines, D};
-        out.push_back(c);
+        for (int th : {256, 512}) {
+          AxisCand c{m, contig ? lines : base.axis[i].C, contig ? base.axis[i].S : lines, D, th};
+          out.push_back(c);
+        }
       }
     }
   }
@@ -994,6 +1002,7 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
 
 void apply_cand(hd_plan_t& p, int i, int ndim, const AxisCand& c) {
   p.axis[i].m = c.m; p.axis[i].C = c.C; p.axis[i].S = c.S; p.axis[i].D = c.D;
+  p.axis[i].threads = c.threads;
   if (ndim == 3 && (i == 0 || i == 1)) { p.axis[0].S = c.S; p.axis[1].S = c.S; }
 }
 
@@ -1085,7 +1094,7 @@ hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int
   } else {
     for (int i = 0; i < ndim; ++i) {
       std::vector<AxisCand> cands = axis_candidates(best, i, ndim, N, Lf, Lg, M, eb);
-      AxisCand bc{best.axis[i].m, best.axis[i].C, best.axis[i].S, best.axis[i].D};
+      AxisCand bc{best.axis[i].m, best.axis[i].C, best.axis[i].S, best.axis[i].D, best.axis[i].threads};
       for (const AxisCand& c : cands) {
         hd_plan_t pl = best;
         apply_cand(pl, i, ndim, c);

@@ -191,11 +191,11 @@ struct LineIn {            // element j of line c of group g, batch b, array k:
   int32_t pad_;
 };
 struct LineOut {           // element j of line c: ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b
-  void* ptr[kMaxPairs];    //   + g*s_g + c*s_c + (j/So)*s_jt + (j%So)*s_js
+  void* ptr[kMaxPairs];    //   + g*s_g + c*s_c + (j>>so_log2)*s_jt + (j&(2^so_log2-1))*s_js
   int64_t L;               // elements written per line
   int64_t nbi, s_bo;
   int64_t s_b, s_g, s_c, s_jt, s_js;
-  int32_t So;              // tile width of the output layout (>= m: plain rows)
+  int32_t so_log2;         // log2 tile width of the output layout (>= 30: plain rows)
   int32_t T;               // output blocks ceil(L/m) (unfold)
 };
 struct PassArgs {
@@ -207,78 +207,197 @@ struct PassArgs {
   int64_t nbatch;
   int64_t M1;
   double scale;            // 1 / prod M1 (CONV)
-  int32_t q, D, C;
+  int32_t q, D, C, c_log2; // residues, residues per group, lines per CTA (power of two)
   int32_t npairs;
   int32_t batch_fastest;
-  int32_t pad_;
 };
 
 enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2 };
 
-// fold residues [r0, r0+nd) of the C lines of this group into buf[c][d][s]
+constexpr int kQF = 16;    // fast q-point DFT paths: q <= 16
+constexpr int kPF = 8;     // fast fold path: p <= 8
+
+__device__ __forceinline__ int64_t jt_off(int64_t j, int sl, int64_t s_jt, int64_t s_js) {
+  if (sl >= 30) return j * s_js;
+  return (j >> sl) * s_jt + (j & ((int64_t(1) << sl) - 1)) * s_js;
+}
+
+// ---------------------------------------------------------------------------
+// fold: w_r[s] = zeta_{M1}^{rs} sum_{t<p} zeta_q^{rt} x[tm+s] for r in [r0, r0+nd)
+// Fast path (all residues, q <= 16, p <= 8): the q-point DFT over t is evaluated
+// in symmetric pairs r, q-r (shared real products), the zeta_{M1}^{rs} twiddles
+// by recurrence from one table entry.  Generic path: direct sums.
+// ---------------------------------------------------------------------------
 template <typename V, int M, int NT>
 __device__ __forceinline__ void fold(V* buf, const LineIn& in, int k, int64_t b, int64_t g,
-                                     int64_t nlines, int C, int r0, int nd, int q,
-                                     const V* zq, const V* __restrict__ twM1) {
+                                     int64_t nlines, int C, int clog, int r0, int nd, int q,
+                                     const V* zq, const V* zt, const V* __restrict__ twm,
+                                     const V* __restrict__ twM1) {
+  using R = decltype(V::x);
   const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
   const int items = C * M;
   const bool cfast = (in.s_j != 1);
   const int p = in.p;
   const int64_t L = in.L;
+  const bool fast = (nd == q) && (q <= kQF) && (p <= kPF);
   for (int it = threadIdx.x; it < items; it += NT) {
     int c, s;
-    if (cfast) { c = it % C; s = it / C; } else { s = it % M; c = it / M; }
+    if (cfast) { c = it & (C - 1); s = it >> clog; } else { s = it % M; c = it / M; }
     const bool live = (g * C + c) < nlines;
     const V* xl = x + c * in.s_c;
-    for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
-      V acc[kFoldChunk];
-      int e[kFoldChunk];  // (r * t) mod q, updated incrementally over t
+    const int cb = c * nd * M;  // swizzle indices are relative to buf
+    if (fast) {
+      V u[kPF];
 #pragma unroll
-      for (int d = 0; d < kFoldChunk; ++d) { acc[d] = cmk<V>(0, 0); e[d] = 0; }
-      if (live) {
-        for (int t = 0; t < p; ++t) {
-          const int64_t j = (int64_t)t * M + s;
-          if (j >= L) break;
-          const V u = xl[j * in.s_j];
+      for (int t = 0; t < kPF; ++t) {
+        u[t] = cmk<V>(0, 0);
+        const int64_t j = (int64_t)t * M + s;
+        if (live && t < p && j < L) u[t] = xl[j * in.s_j];
+      }
+      V a0 = u[0];
 #pragma unroll
-          for (int d = 0; d < kFoldChunk; ++d) {
-            if (d0 + d < nd) {
-              acc[d] = cfma(acc[d], u, zq[e[d]]);
-              e[d] += r0 + d0 + d;
-              if (e[d] >= q) e[d] -= q;
+      for (int t = 1; t < kPF; ++t) a0 = cadd(a0, u[t]);
+      buf[swz<V>(cb + s)] = a0;
+      const V w1 = ldg(twM1 + s);                 // zeta_{M1}^{s}
+      const V wq = ldg(twm + s);                  // zeta_{M1}^{q s} = zeta_m^{s}
+      V wr = w1;
+#pragma unroll
+      for (int r = 1; r <= kQF / 2; ++r) {
+        if (2 * r > q) break;
+        V A = cmk<V>(0, 0), B = cmk<V>(0, 0);
+#pragma unroll
+        for (int t = 0; t < kPF; ++t) {
+          const V z = zt[r * kQF + t];            // zeta_q^{r t}
+          A.x = fma(u[t].x, z.x, A.x); A.y = fma(u[t].y, z.x, A.y);
+          B.x = fma(u[t].x, z.y, B.x); B.y = fma(u[t].y, z.y, B.y);
+        }
+        // a_r = A + iB, a_{q-r} = A - iB
+        const V ar = cmk<V>(A.x - B.y, A.y + B.x);
+        buf[swz<V>(cb + r * M + s)] = cmul(ar, wr);
+        if (2 * r < q) {
+          const V aq = cmk<V>(A.x + B.y, A.y - B.x);
+          buf[swz<V>(cb + (q - r) * M + s)] = cmul(aq, cmulc(wq, wr));  // zeta^{(q-r)s} = zeta_m^s conj(zeta^{rs})
+        }
+        wr = cmul(wr, w1);
+      }
+      (void)sizeof(R);
+    } else {
+      for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
+        V acc[kFoldChunk];
+        int e[kFoldChunk];  // (r * t) mod q, updated incrementally over t
+#pragma unroll
+        for (int d = 0; d < kFoldChunk; ++d) { acc[d] = cmk<V>(0, 0); e[d] = 0; }
+        if (live) {
+          for (int t = 0; t < p; ++t) {
+            const int64_t j = (int64_t)t * M + s;
+            if (j >= L) break;
+            const V u = xl[j * in.s_j];
+#pragma unroll
+            for (int d = 0; d < kFoldChunk; ++d) {
+              if (d0 + d < nd) {
+                acc[d] = cfma(acc[d], u, zq[e[d]]);
+                e[d] += r0 + d0 + d;
+                if (e[d] >= q) e[d] -= q;
+              }
             }
           }
         }
-      }
 #pragma unroll
-      for (int d = 0; d < kFoldChunk; ++d) {
-        if (d0 + d < nd) {
-          const int r = r0 + d0 + d;
-          const V w = cmul(acc[d], ldg(twM1 + (int64_t)r * s));
-          buf[swz<V>((c * nd + d0 + d) * M + s)] = w;
+        for (int d = 0; d < kFoldChunk; ++d) {
+          if (d0 + d < nd) {
+            const int r = r0 + d0 + d;
+            buf[swz<V>(cb + (d0 + d) * M + s)] = cmul(acc[d], ldg(twM1 + (int64_t)r * s));
+          }
         }
       }
     }
   }
 }
 
-// unfold residues [r0, r0+nd) from buf[c][d][s] into the output lines
-template <typename V, int M, int NT>
-__device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, int64_t b, int64_t g,
-                                       int64_t nlines, int C, int r0, int nd, int q, bool accumulate,
-                                       const V* zq, const V* __restrict__ twM1) {
-  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
+// ---------------------------------------------------------------------------
+// unfold: h[tm+s] (+)= sum_{r in group} zeta_q^{-tr} zeta_{M1}^{-rs} V_r[s], t < T
+// Fast path (all residues, q <= 16): v_r in registers, output blocks in pairs t, q-t.
+// ---------------------------------------------------------------------------
+template <typename V, int M, int NT, int QM>
+__device__ __forceinline__ void unfold_fast(const V* buf, V* y, const LineOut& out, int64_t g,
+                                            int64_t nlines, int C, int clog, int q,
+                                            const V* zt, const V* __restrict__ twm,
+                                            const V* __restrict__ twM1) {
   const int items = C * M;
-  const int so = out.So < M ? out.So : M;
+  const int sl = out.so_log2;
+  const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
   for (int it = threadIdx.x; it < items; it += NT) {
-    const int s_lo = it % so;
-    const int rest = it / so;
-    const int c = rest % C;
-    const int s = (rest / C) * so + s_lo;
+    const int s_lo = it & ((1 << so_l) - 1);
+    const int rest = it >> so_l;
+    const int c = rest & (C - 1);
+    const int s = ((rest >> clog) << so_l) + s_lo;
+    if ((g * C + c) >= nlines) continue;
+    const int cb = c * q * M;
+    V* yl = y + c * out.s_c;
+    V v[QM];
+    const V w1 = ldg(twM1 + s);
+    V wr = cmk<V>(1, 0);
+#pragma unroll
+    for (int r = 0; r < QM; ++r) {
+      v[r] = cmk<V>(0, 0);
+      if (r < q) {
+        v[r] = cmulc(buf[swz<V>(cb + r * M + s)], wr);
+        wr = cmul(wr, w1);
+      }
+    }
+    // t = 0
+    {
+      V h0 = v[0];
+#pragma unroll
+      for (int r = 1; r < QM; ++r) h0 = cadd(h0, v[r]);
+      if (s < L) yl[jt_off(s, sl, out.s_jt, out.s_js)] = h0;
+    }
+#pragma unroll
+    for (int t = 1; t <= QM / 2; ++t) {
+      if (2 * t > q) break;
+      V A = cmk<V>(0, 0), B = cmk<V>(0, 0);
+#pragma unroll
+      for (int r = 0; r < QM; ++r) {
+        const V z = zt[t * kQF + r];              // zeta_q^{t r}
+        A.x = fma(v[r].x, z.x, A.x); A.y = fma(v[r].y, z.x, A.y);
+        B.x = fma(v[r].x, z.y, B.x); B.y = fma(v[r].y, z.y, B.y);
+      }
+      // h_t = sum v_r conj(z) = A - iB ; h_{q-t} = A + iB
+      const int64_t j1 = (int64_t)t * M + s;
+      if (t < T && j1 < L) yl[jt_off(j1, sl, out.s_jt, out.s_js)] = cmk<V>(A.x + B.y, A.y - B.x);
+      if (2 * t < q) {
+        const int64_t j2 = (int64_t)(q - t) * M + s;
+        if (q - t < T && j2 < L) yl[jt_off(j2, sl, out.s_jt, out.s_js)] = cmk<V>(A.x - B.y, A.y + B.x);
+      }
+    }
+  }
+}
+
+template <typename V, int M, int NT>
+__device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, int64_t b, int64_t g,
+                                       int64_t nlines, int C, int clog, int r0, int nd, int q,
+                                       bool accumulate, const V* zq, const V* zt,
+                                       const V* __restrict__ twm, const V* __restrict__ twM1) {
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
+  if (nd == q && !accumulate) {
+    if (q <= 8) { unfold_fast<V, M, NT, 8>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
+    if (q <= kQF) { unfold_fast<V, M, NT, kQF>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
+  }
+  const int items = C * M;
+  const int sl = out.so_log2;
+  const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
+  const int64_t L = out.L;
+  const int T = out.T;
+  for (int it = threadIdx.x; it < items; it += NT) {
+    const int s_lo = it & ((1 << so_l) - 1);
+    const int rest = it >> so_l;
+    const int c = rest & (C - 1);
+    const int s = ((rest >> clog) << so_l) + s_lo;
     if ((g * C + c) >= nlines) continue;
     V* yl = y + c * out.s_c;
+    const int cb = c * nd * M;
     for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
       V v[kFoldChunk];
 #pragma unroll
@@ -286,7 +405,7 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
         v[d] = cmk<V>(0, 0);
         if (d0 + d < nd) {
           const int r = r0 + d0 + d;
-          v[d] = cmulc(buf[swz<V>((c * nd + d0 + d) * M + s)], ldg(twM1 + (int64_t)r * s));
+          v[d] = cmulc(buf[swz<V>(cb + (d0 + d) * M + s)], ldg(twM1 + (int64_t)r * s));
         }
       }
       int e[kFoldChunk];
@@ -305,7 +424,7 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
             if (e[d] >= q) e[d] -= q;
           }
         }
-        V* dst = yl + (j / out.So) * out.s_jt + (j % out.So) * out.s_js;
+        V* dst = yl + jt_off(j, sl, out.s_jt, out.s_js);
         if (add) { V o = *dst; val = cadd(o, val); }
         *dst = val;
       }
@@ -316,37 +435,35 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
 // store residue group spectrum buf[c][d][pos] -> out element kappa = r0*m + d*m + pos
 template <typename V, int M, int NT>
 __device__ __forceinline__ void store_spectrum(const V* buf, const LineOut& out, int k, int64_t b,
-                                               int64_t g, int64_t nlines, int C, int r0, int nd) {
+                                               int64_t g, int64_t nlines, int C, int clog, int r0, int nd) {
   V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
-  const int so = out.So < M ? out.So : M;
+  const int sl = out.so_log2;
+  const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int items = C * nd * M;
   for (int it = threadIdx.x; it < items; it += NT) {
-    const int e_lo = it % so;
-    const int rest = it / so;
-    const int c = rest % C;
-    const int e = (rest / C) * so + e_lo;
+    const int e_lo = it & ((1 << so_l) - 1);
+    const int rest = it >> so_l;
+    const int c = rest & (C - 1);
+    const int e = ((rest >> clog) << so_l) + e_lo;
     if ((g * C + c) >= nlines) continue;
-    const int d = e / M, pos = e % M;
     const int64_t kap = (int64_t)r0 * M + e;
-    y[c * out.s_c + (kap / out.So) * out.s_jt + (kap % out.So) * out.s_js] =
-        buf[swz<V>((c * nd + d) * M + pos)];
+    y[c * out.s_c + jt_off(kap, sl, out.s_jt, out.s_js)] = buf[swz<V>(c * nd * M + e)];
   }
 }
 
 // load residue group spectrum (internal order) into buf[c][d][pos]
 template <typename V, int M, int NT>
 __device__ __forceinline__ void load_spectrum(V* buf, const LineIn& in, int64_t b, int64_t g,
-                                              int64_t nlines, int C, int r0, int nd) {
+                                              int64_t nlines, int C, int clog, int r0, int nd) {
   const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
   const int items = C * nd * M;
   const bool cfast = (in.s_j != 1);
   for (int it = threadIdx.x; it < items; it += NT) {
     int c, e;
-    if (cfast) { c = it % C; e = it / C; } else { e = it % (nd * M); c = it / (nd * M); }
-    const int d = e / M, pos = e % M;
+    if (cfast) { c = it & (C - 1); e = it >> clog; } else { e = it % (nd * M); c = it / (nd * M); }
     V v = cmk<V>(0, 0);
     if ((g * C + c) < nlines) v = x[c * in.s_c + ((int64_t)r0 * M + e) * in.s_j];
-    buf[swz<V>((c * nd + d) * M + pos)] = v;
+    buf[swz<V>(c * nd * M + e)] = v;
   }
 }
 
@@ -357,6 +474,7 @@ template <int EPR> __host__ __device__ constexpr int64_t round_slots(int64_t n) 
 // ---------------------------------------------------------------------------
 // The pass kernel.  MODE_FWD: fold+FFT -> spectrum; MODE_INV: spectrum ->
 // IFFT+unfold; MODE_CONV: fold+FFT both inputs, sum of products, IFFT+unfold.
+// Shared memory: [zq: q][zt: 16x16][bufF][bufG][bufA]
 // ---------------------------------------------------------------------------
 template <typename T, int M, int NT, int MODE>
 __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassArgs a) {
@@ -368,39 +486,44 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
   const int64_t g = a.batch_fastest ? blockIdx.y : blockIdx.x;
   const int64_t b = a.batch_fastest ? blockIdx.x : blockIdx.y;
   const int k_arr = blockIdx.z;
-  const int C = a.C, D = a.D, q = a.q;
+  const int C = a.C, clog = a.c_log2, D = a.D, q = a.q;
   const int64_t bufn = round_slots<EPR>((int64_t)C * D * M);
 
   V* zq = smem;                                  // zeta_q^k, k < q
-  V* bufF = smem + round_slots<EPR>(q);
+  V* zt = zq + round_slots<EPR>(q);              // zeta_q^{(r t) mod q}, r, t < 16
+  V* bufF = zt + round_slots<EPR>(kQF * kQF);
   V* bufG = bufF + bufn;
   V* bufA = bufG + bufn;
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
   for (int i = threadIdx.x; i < q; i += NT) zq[i] = ldg(twM1 + (int64_t)i * M);
+  for (int i = threadIdx.x; i < kQF * kQF; i += NT) {
+    const int r = i / kQF, t = i % kQF;
+    zt[i] = ldg(twM1 + (int64_t)((r * t) % q) * M);
+  }
   __syncthreads();
 
   for (int r0 = 0; r0 < q; r0 += D) {
     const int nd = (q - r0) < D ? (q - r0) : D;
     if constexpr (MODE == MODE_FWD) {
-      fold<V, M, NT>(bufF, a.in_f, k_arr, b, g, a.nlines, C, r0, nd, q, zq, twM1);
+      fold<V, M, NT>(bufF, a.in_f, k_arr, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
       __syncthreads();
       fft_fwd<V, M, NT>(bufF, C * nd, twm);
-      store_spectrum<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, r0, nd);
+      store_spectrum<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, clog, r0, nd);
       __syncthreads();
     } else if constexpr (MODE == MODE_INV) {
-      load_spectrum<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, r0, nd);
+      load_spectrum<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, clog, r0, nd);
       __syncthreads();
       fft_inv<V, M, NT>(bufF, C * nd, twm);
-      unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, r0, nd, q, r0 > 0, zq, twM1);
+      unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
       __syncthreads();
     } else {
       const T scale = (T)a.scale;
       const int n = C * nd * M;
       V* P = (a.npairs == 1) ? bufF : bufA;
       for (int kk = 0; kk < a.npairs; ++kk) {
-        fold<V, M, NT>(bufF, a.in_f, kk, b, g, a.nlines, C, r0, nd, q, zq, twM1);
-        fold<V, M, NT>(bufG, a.in_g, kk, b, g, a.nlines, C, r0, nd, q, zq, twM1);
+        fold<V, M, NT>(bufF, a.in_f, kk, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
+        fold<V, M, NT>(bufG, a.in_g, kk, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
         __syncthreads();
         // bufF and bufG are adjacent: one FFT sweep over both
         if (bufn == (int64_t)C * nd * M) {
@@ -422,7 +545,7 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
         __syncthreads();
       }
       fft_inv<V, M, NT>(P, C * nd, twm);
-      unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, r0, nd, q, r0 > 0, zq, twM1);
+      unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
       __syncthreads();
     }
   }
