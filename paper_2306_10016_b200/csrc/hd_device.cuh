@@ -118,49 +118,79 @@ template <typename V, int R, int S> __device__ __forceinline__ void dftR(V* v) {
   else dft8<V, S>(v);
 }
 
-// One DIF (forward) or DIT (inverse) stage over nrows rows of M in SMEM.
-template <typename V, int M, int NT, int ST, bool INV>
-__device__ __forceinline__ void fft_stage(V* buf, int nrows, const V* __restrict__ twm) {
-  constexpr int R = Sched<M>::radix(ST);
-  constexpr int NK = Sched<M>::nk(ST);
-  constexpr int SPAN = NK / R;
-  constexpr int PER_ROW = M / R;
-  constexpr int TWSTEP = M / NK;
-  const int items = nrows * PER_ROW;
-  for (int it = threadIdx.x; it < items; it += NT) {
-    const int row = it / PER_ROW;
-    const int w = it % PER_ROW;
-    const int b = w / SPAN, o = w % SPAN;
-    const int base = row * M + b * NK + o;
-    V v[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = buf[swz<V>(base + i * SPAN)];
-    if constexpr (!INV) {
-      dftR<V, R, +1>(v);
-      if (SPAN > 1 && o > 0) {
-#pragma unroll
-        for (int j = 1; j < R; ++j) v[j] = cmul(v[j], ldg(twm + o * j * TWSTEP));
-      }
-    } else {
-      if (SPAN > 1 && o > 0) {
-#pragma unroll
-        for (int j = 1; j < R; ++j) v[j] = cmulc(v[j], ldg(twm + o * j * TWSTEP));
-      }
-      dftR<V, R, -1>(v);
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) buf[swz<V>(base + i * SPAN)] = v[i];
+// Twiddle powers w[j] = w1^j, j < R (w[0] unused), by repeated products of the
+// one table entry w1 = zeta_NK^{o} (coalesced load; <= 3 products deep).
+template <typename V, int R> __device__ __forceinline__ void tw_powers(V w1, V* w) {
+  w[1] = w1;
+  if constexpr (R >= 4) { w[2] = cmul(w1, w1); w[3] = cmul(w[2], w1); }
+  if constexpr (R >= 8) {
+    w[4] = cmul(w[2], w[2]); w[5] = cmul(w[4], w1); w[6] = cmul(w[4], w[2]); w[7] = cmul(w[4], w[3]);
   }
 }
 
-template <typename V, int M, int NT, int ST>
-__device__ __forceinline__ void fft_fwd_from(V* buf, int nrows, const V* twm) {
-  if constexpr (ST < Sched<M>::NST) {
-    fft_stage<V, M, NT, ST, false>(buf, nrows, twm);
-    __syncthreads();
-    fft_fwd_from<V, M, NT, ST + 1>(buf, nrows, twm);
+template <int M, int ST> struct StageC {
+  static constexpr int R = Sched<M>::radix(ST);
+  static constexpr int NK = Sched<M>::nk(ST);
+  static constexpr int SPAN = NK / R;
+  static constexpr int PER_ROW = M / R;
+  static constexpr int TWSTEP = M / NK;
+};
+
+// DIF butterfly of stage ST (forward, +exponent) on registers, offset o inside its block
+template <typename V, int M, int ST>
+__device__ __forceinline__ void dif_bfly(V* v, int o, const V* __restrict__ twm) {
+  using S = StageC<M, ST>;
+  dftR<V, S::R, +1>(v);
+  if (S::SPAN > 1 && o > 0) {
+    V w[S::R];
+    tw_powers<V, S::R>(ldg(twm + o * S::TWSTEP), w);
+#pragma unroll
+    for (int j = 1; j < S::R; ++j) v[j] = cmul(v[j], w[j]);
   }
 }
+// DIT butterfly of stage ST (inverse, -exponent): adjoint of dif_bfly
+template <typename V, int M, int ST>
+__device__ __forceinline__ void dit_bfly(V* v, int o, const V* __restrict__ twm) {
+  using S = StageC<M, ST>;
+  if (S::SPAN > 1 && o > 0) {
+    V w[S::R];
+    tw_powers<V, S::R>(ldg(twm + o * S::TWSTEP), w);
+#pragma unroll
+    for (int j = 1; j < S::R; ++j) v[j] = cmulc(v[j], w[j]);
+  }
+  dftR<V, S::R, -1>(v);
+}
+
+// One DIF (forward) or DIT (inverse) stage over nrows rows of M in SMEM.
+template <typename V, int M, int NT, int ST, bool INV>
+__device__ __forceinline__ void fft_stage(V* buf, int nrows, const V* __restrict__ twm) {
+  using S = StageC<M, ST>;
+  const int items = nrows * S::PER_ROW;
+  for (int it = threadIdx.x; it < items; it += NT) {
+    const int row = it / S::PER_ROW;
+    const int w = it % S::PER_ROW;
+    const int b = w / S::SPAN, o = w % S::SPAN;
+    const int base = row * M + b * S::NK + o;
+    V v[S::R];
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) v[i] = buf[swz<V>(base + i * S::SPAN)];
+    if constexpr (!INV) dif_bfly<V, M, ST>(v, o, twm);
+    else dit_bfly<V, M, ST>(v, o, twm);
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) buf[swz<V>(base + i * S::SPAN)] = v[i];
+  }
+}
+
+// forward stages [ST, STOP) with a barrier after each
+template <typename V, int M, int NT, int ST, int STOP>
+__device__ __forceinline__ void fft_fwd_range(V* buf, int nrows, const V* twm) {
+  if constexpr (ST < STOP) {
+    fft_stage<V, M, NT, ST, false>(buf, nrows, twm);
+    __syncthreads();
+    fft_fwd_range<V, M, NT, ST + 1, STOP>(buf, nrows, twm);
+  }
+}
+// inverse stages ST, ST-1, ..., 0 with a barrier after each
 template <typename V, int M, int NT, int ST>
 __device__ __forceinline__ void fft_inv_from(V* buf, int nrows, const V* twm) {
   if constexpr (ST >= 0) {
@@ -168,15 +198,6 @@ __device__ __forceinline__ void fft_inv_from(V* buf, int nrows, const V* twm) {
     __syncthreads();
     fft_inv_from<V, M, NT, ST - 1>(buf, nrows, twm);
   }
-}
-// Forward FFT of nrows rows (ends with a CTA barrier).
-template <typename V, int M, int NT>
-__device__ __forceinline__ void fft_fwd(V* buf, int nrows, const V* twm) {
-  if constexpr (M > 1) fft_fwd_from<V, M, NT, 0>(buf, nrows, twm);
-}
-template <typename V, int M, int NT>
-__device__ __forceinline__ void fft_inv(V* buf, int nrows, const V* twm) {
-  if constexpr (M > 1) fft_inv_from<V, M, NT, Sched<M>::NST - 1>(buf, nrows, twm);
 }
 
 // ---------------------------------------------------------------------------
@@ -382,7 +403,9 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
                                        const V* __restrict__ twm, const V* __restrict__ twM1) {
   V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
   if (nd == q && !accumulate) {
+    if (q <= 4) { unfold_fast<V, M, NT, 4>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
     if (q <= 8) { unfold_fast<V, M, NT, 8>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
+    if (q <= 12) { unfold_fast<V, M, NT, 12>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
     if (q <= kQF) { unfold_fast<V, M, NT, kQF>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
   }
   const int items = C * M;
@@ -432,38 +455,109 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
   }
 }
 
-// store residue group spectrum buf[c][d][pos] -> out element kappa = r0*m + d*m + pos
+// Last forward stage fused with the spectrum store: DIF stage NST-1 (span 1) on
+// buf rows (c, d), results written straight to the output element
+// kappa = (r0 + d) m + pos of line c.  Line index fastest across threads so
+// that the C lines of one kappa land in one contiguous tile segment.
 template <typename V, int M, int NT>
-__device__ __forceinline__ void store_spectrum(const V* buf, const LineOut& out, int k, int64_t b,
-                                               int64_t g, int64_t nlines, int C, int clog, int r0, int nd) {
+__device__ __forceinline__ void fwd_last_store(const V* buf, const LineOut& out, int k, int64_t b,
+                                               int64_t g, int64_t nlines, int C, int clog, int r0,
+                                               int nd, const V* __restrict__ twm) {
+  constexpr int ST = Sched<M>::NST - 1;
+  using S = StageC<M, ST>;
+  static_assert(S::SPAN == 1, "last stage has unit span");
   V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
   const int sl = out.so_log2;
-  const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
-  const int items = C * nd * M;
+  const int items = C * nd * S::PER_ROW;
   for (int it = threadIdx.x; it < items; it += NT) {
-    const int e_lo = it & ((1 << so_l) - 1);
-    const int rest = it >> so_l;
-    const int c = rest & (C - 1);
-    const int e = ((rest >> clog) << so_l) + e_lo;
-    if ((g * C + c) >= nlines) continue;
-    const int64_t kap = (int64_t)r0 * M + e;
-    y[c * out.s_c + jt_off(kap, sl, out.s_jt, out.s_js)] = buf[swz<V>(c * nd * M + e)];
+    const int c = it & (C - 1);
+    const int rest = it >> clog;
+    const int w = rest % S::PER_ROW;
+    const int d = rest / S::PER_ROW;
+    const int base = (c * nd + d) * M + w * S::R;
+    V v[S::R];
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) v[i] = buf[swz<V>(base + i)];
+    dif_bfly<V, M, ST>(v, 0, twm);
+    if ((g * C + c) < nlines) {
+      V* yl = y + c * out.s_c;
+      const int64_t k0 = (int64_t)(r0 + d) * M + w * S::R;
+#pragma unroll
+      for (int i = 0; i < S::R; ++i) yl[jt_off(k0 + i, sl, out.s_jt, out.s_js)] = v[i];
+    }
   }
 }
 
-// load residue group spectrum (internal order) into buf[c][d][pos]
+// First inverse stage fused with the spectrum load: reads kappa = (r0+d) m + pos
+// of line c from global, DIT stage NST-1 (span 1), writes buf rows (c, d).
 template <typename V, int M, int NT>
-__device__ __forceinline__ void load_spectrum(V* buf, const LineIn& in, int64_t b, int64_t g,
-                                              int64_t nlines, int C, int clog, int r0, int nd) {
+__device__ __forceinline__ void inv_first_load(V* buf, const LineIn& in, int64_t b, int64_t g,
+                                               int64_t nlines, int C, int clog, int r0, int nd,
+                                               const V* __restrict__ twm) {
+  constexpr int ST = Sched<M>::NST - 1;
+  using S = StageC<M, ST>;
   const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
-  const int items = C * nd * M;
+  const int items = C * nd * S::PER_ROW;
   const bool cfast = (in.s_j != 1);
   for (int it = threadIdx.x; it < items; it += NT) {
-    int c, e;
-    if (cfast) { c = it & (C - 1); e = it >> clog; } else { e = it % (nd * M); c = it / (nd * M); }
-    V v = cmk<V>(0, 0);
-    if ((g * C + c) < nlines) v = x[c * in.s_c + ((int64_t)r0 * M + e) * in.s_j];
-    buf[swz<V>(c * nd * M + e)] = v;
+    int c, w, d;
+    if (cfast) {
+      c = it & (C - 1);
+      const int rest = it >> clog;
+      w = rest % S::PER_ROW;
+      d = rest / S::PER_ROW;
+    } else {
+      w = it % S::PER_ROW;
+      const int rest = it / S::PER_ROW;
+      d = rest % nd;
+      c = rest / nd;
+    }
+    V v[S::R];
+    const int64_t k0 = (int64_t)(r0 + d) * M + w * S::R;
+    const bool live = (g * C + c) < nlines;
+    const V* xl = x + c * in.s_c;
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) v[i] = live ? xl[(k0 + i) * in.s_j] : cmk<V>(0, 0);
+    dit_bfly<V, M, ST>(v, 0, twm);
+    const int base = (c * nd + d) * M + w * S::R;
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) buf[swz<V>(base + i)] = v[i];
+  }
+}
+
+// The pointwise (multi-)product fused between the last forward stage and the
+// first inverse stage: for every group of R positions,
+// DIF_last(F) * DIF_last(G) is accumulated over the pairs k, scaled by 1/prod M1
+// on the last pair and put through DIT_last, all in registers.
+//   npairs == 1: result -> bufF;  else accumulator -> bufA
+template <typename V, int M, int NT>
+__device__ __forceinline__ void conv_mid(V* bufF, const V* bufG, V* bufA, int nrows, int kk,
+                                         int npairs, decltype(V::x) scale, const V* __restrict__ twm) {
+  constexpr int ST = Sched<M>::NST - 1;
+  using S = StageC<M, ST>;
+  const int items = nrows * S::PER_ROW;
+  const bool last = (kk == npairs - 1);
+  for (int it = threadIdx.x; it < items; it += NT) {
+    const int base = it * S::R;  // rows are contiguous: row*M + w*R == it*R
+    V f[S::R], h[S::R];
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) { f[i] = bufF[swz<V>(base + i)]; h[i] = bufG[swz<V>(base + i)]; }
+    dif_bfly<V, M, ST>(f, 0, twm);
+    dif_bfly<V, M, ST>(h, 0, twm);
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) f[i] = cmul(f[i], h[i]);
+    if (npairs > 1 && kk > 0) {
+#pragma unroll
+      for (int i = 0; i < S::R; ++i) f[i] = cadd(f[i], bufA[swz<V>(base + i)]);
+    }
+    V* dst = (npairs == 1) ? bufF : bufA;
+    if (last) {
+#pragma unroll
+      for (int i = 0; i < S::R; ++i) f[i] = cscale(f[i], scale);
+      dit_bfly<V, M, ST>(f, 0, twm);
+    }
+#pragma unroll
+    for (int i = 0; i < S::R; ++i) dst[swz<V>(base + i)] = f[i];
   }
 }
 
@@ -480,6 +574,7 @@ template <typename T, int M, int NT, int MODE>
 __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassArgs a) {
   using V = typename cplx_of<T>::type;
   constexpr int EPR = 128 / (int)sizeof(V);
+  constexpr int NST = Sched<M>::NST;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V* smem = reinterpret_cast<V*>(smem_raw);
 
@@ -508,43 +603,33 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
     if constexpr (MODE == MODE_FWD) {
       fold<V, M, NT>(bufF, a.in_f, k_arr, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
       __syncthreads();
-      fft_fwd<V, M, NT>(bufF, C * nd, twm);
-      store_spectrum<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, clog, r0, nd);
+      fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, C * nd, twm);
+      fwd_last_store<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, clog, r0, nd, twm);
       __syncthreads();
     } else if constexpr (MODE == MODE_INV) {
-      load_spectrum<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, clog, r0, nd);
+      inv_first_load<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, clog, r0, nd, twm);
       __syncthreads();
-      fft_inv<V, M, NT>(bufF, C * nd, twm);
+      fft_inv_from<V, M, NT, NST - 2>(bufF, C * nd, twm);
       unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
       __syncthreads();
     } else {
       const T scale = (T)a.scale;
-      const int n = C * nd * M;
       V* P = (a.npairs == 1) ? bufF : bufA;
       for (int kk = 0; kk < a.npairs; ++kk) {
         fold<V, M, NT>(bufF, a.in_f, kk, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
         fold<V, M, NT>(bufG, a.in_g, kk, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
         __syncthreads();
-        // bufF and bufG are adjacent: one FFT sweep over both
+        // bufF and bufG are adjacent when the group is full: one sweep over both
         if (bufn == (int64_t)C * nd * M) {
-          fft_fwd<V, M, NT>(bufF, 2 * C * nd, twm);
+          fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, 2 * C * nd, twm);
         } else {
-          fft_fwd<V, M, NT>(bufF, C * nd, twm);
-          fft_fwd<V, M, NT>(bufG, C * nd, twm);
+          fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, C * nd, twm);
+          fft_fwd_range<V, M, NT, 0, NST - 1>(bufG, C * nd, twm);
         }
-        for (int i = threadIdx.x; i < n; i += NT) {
-          const int si = swz<V>(i);
-          V pr = cmul(bufF[si], bufG[si]);
-          if (a.npairs == 1) P[si] = cscale(pr, scale);
-          else P[si] = (kk == 0) ? pr : cadd(P[si], pr);
-        }
+        conv_mid<V, M, NT>(bufF, bufG, bufA, C * nd, kk, a.npairs, scale, twm);
         __syncthreads();
       }
-      if (a.npairs > 1) {
-        for (int i = threadIdx.x; i < n; i += NT) { const int si = swz<V>(i); P[si] = cscale(P[si], scale); }
-        __syncthreads();
-      }
-      fft_inv<V, M, NT>(P, C * nd, twm);
+      fft_inv_from<V, M, NT, NST - 2>(P, C * nd, twm);
       unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
       __syncthreads();
     }
