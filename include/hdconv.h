@@ -69,15 +69,19 @@ typedef enum {
 /* Plan flags */
 #define HD_FLAG_ALLOW_ALIAS 0x1u   /* test-only: accept M1 < L_out (aliased output, extent min(M1, L_out)) */
 #define HD_FLAG_SHARED_G    0x2u   /* batch > 1: one g shared by every batch entry */
+#define HD_FLAG_GENERIC_FFT 0x4u   /* force the generic radix-8 shared-memory FFT engine
+                                      (default: the warp-level engine where it applies) */
 
 /* Per-axis parameters (L, M, C, m, D per dimension).
  *  m  : FFT size, a power of two in [2, 4096]
  *  p_f, p_g : ceil(L_f/m), ceil(L_g/m) (derived, PAPER.md:684-685 with Lambda = 1)
  *  q  : ceil(M/m) residues (derived from M and m)
- *  C  : lines (FFT copies) per CTA in passes along this axis when it
- *       is the contiguous axis; S: lines per CTA (= tile width of the transposed
- *       intermediate it reads) when the axis is strided.  1, 2, 4, 8 or 16.
+ *  C  : lines (copies of the FFT computed simultaneously) per CTA in
+ *       the passes along this axis: 1, 2, 4, 8 or 16
+ *  S  : tile width of the transposed intermediate read by the passes along this
+ *       axis (adjacent lines staged together; 1, 2, 4, 8 or 16; unused in 1D)
  *  D  : residues per group, 1 <= D <= q (0 = q)
+ *  threads : CTA size of the generic engine (multiple of 32, 0 = automatic)
  *  M1 : q*m (derived) */
 typedef struct {
   int32_t m, p_f, p_g, q, C, S, D, threads;

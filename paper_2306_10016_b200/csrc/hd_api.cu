@@ -21,7 +21,6 @@ using hd::PassArgs;
 
 namespace {
 thread_local std::string g_tls_error;
-constexpr int kDefaultThreads = 256;
 constexpr int64_t kHugeTile = int64_t(1) << 30;
 }  // namespace
 
@@ -30,6 +29,8 @@ struct hd_ctx {
   std::string err;
   std::mutex mu;
   std::map<int64_t, void*> tw64, tw32;  // N -> device zeta_N^k tables
+  std::map<int64_t, void*> st64, st32;  // m -> device stage twiddle tables
+  void* w512tw = nullptr;               // [15][32] zeta_512^{t j} for the warp engine
   void* ws = nullptr;
   size_t ws_size = 0;
   void* io = nullptr;                   // device buffers for hd_conv_host
@@ -106,6 +107,71 @@ hd_status_t get_table(hd_ctx* ctx, int64_t N, bool dbl, const void** out) {
   return HD_OK;
 }
 
+// Stage twiddle table of the size-m FFT (layout of hd_device.cuh StageOff): for
+// every DIF stage s with span SP > 1 (radix-8 stages, then one radix-4/2), the
+// entries [j-1][o] = zeta_NK^{o j}, j = 1..R-1, o < SP, NK = m / prod(radix < s).
+hd_status_t get_stage_table(hd_ctx* ctx, int m, bool dbl, const void** out) {
+  auto& cache = dbl ? ctx->st64 : ctx->st32;
+  auto it = cache.find(m);
+  if (it != cache.end()) { *out = it->second; return HD_OK; }
+  const int lg = ilog2(m);
+  std::vector<int> rad;
+  for (int i = 0; i < lg / 3; ++i) rad.push_back(8);
+  if (lg % 3 == 1) rad.push_back(2);
+  if (lg % 3 == 2) rad.push_back(4);
+  std::vector<double> full;
+  host_twiddles(m, full);  // zeta_m^k
+  std::vector<double> tab;
+  int NK = m;
+  for (size_t st = 0; st < rad.size(); ++st) {
+    const int R = rad[st], SP = NK / R;
+    if (SP > 1)
+      for (int j = 1; j < R; ++j)
+        for (int o = 0; o < SP; ++o) {
+          const int64_t e = (int64_t)o * j * (m / NK);  // zeta_NK^{o j} = zeta_m^{o j m/NK}
+          tab.push_back(full[2 * e]);
+          tab.push_back(full[2 * e + 1]);
+        }
+    NK = SP;
+  }
+  if (tab.empty()) { tab.push_back(1.0); tab.push_back(0.0); }
+  const size_t n = tab.size() / 2;
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, dbl ? 16 * n : 8 * n);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(stage twiddles)");
+  if (dbl) e = cudaMemcpy(d, tab.data(), 16 * n, cudaMemcpyHostToDevice);
+  else {
+    std::vector<float> f(tab.begin(), tab.end());
+    e = cudaMemcpy(d, f.data(), 8 * n, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) { cudaFree(d); return cuda_fail(ctx, e, "cudaMemcpy(stage twiddles)"); }
+  cache[m] = d;
+  *out = d;
+  return HD_OK;
+}
+
+// [15][32] table zeta_512^{t j}, j = 1..15, t < 32 (warp engine, hd_w512.cuh)
+hd_status_t get_w512_table(hd_ctx* ctx, const void** out) {
+  if (!ctx->w512tw) {
+    std::vector<double> full, tab;
+    host_twiddles(512, full);
+    for (int j = 1; j < 16; ++j)
+      for (int t = 0; t < 32; ++t) {
+        const int e = (t * j) % 512;
+        tab.push_back(full[2 * e]);
+        tab.push_back(full[2 * e + 1]);
+      }
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, tab.size() * sizeof(double));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(w512 twiddles)");
+    e = cudaMemcpy(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(d); return cuda_fail(ctx, e, "cudaMemcpy(w512 twiddles)"); }
+    ctx->w512tw = d;
+  }
+  *out = ctx->w512tw;
+  return HD_OK;
+}
+
 // ---------------------------------------------------------------------------
 // plans
 // ---------------------------------------------------------------------------
@@ -114,8 +180,10 @@ struct AxisInfo {
   int m, q, pf, pg, T, C, S, D, lines, threads;
 };
 
-// lines per CTA used by passes along axis i: C on the contiguous axis, S otherwise
-int lines_for(const hd_axis_plan_t& a, int i, int ndim) { return i == ndim - 1 ? a.C : a.S; }
+// lines per CTA used by passes along axis i (the paper's C, "copies of the FFT
+// computed simultaneously"); S is the tile width of the transposed
+// intermediate those passes read (strided-pass staging width)
+int lines_for(const hd_axis_plan_t& a, int i, int ndim) { (void)i; (void)ndim; return a.C; }
 
 int64_t round_slots(int64_t n, size_t eb) {
   const int64_t epr = 128 / (int64_t)eb;
@@ -128,8 +196,20 @@ size_t pass_smem(size_t eb, int q, int lines, int D, int m, int nbuf) {
 int conv_nbuf(int npairs) { return npairs == 1 ? 2 : 3; }
 
 bool valid_lines(int v) { return v == 1 || v == 2 || v == 4 || v == 8 || v == 16; }
-// 512 threads when one pass sweep has at least 512 independent (line, s) items
-int default_threads(int lines, int m) { return (int64_t)lines * m >= 512 ? 512 : 256; }
+// Block size matched to the FFT butterfly sweep (lines * D * m / R items): the
+// multiple of 32 in [128, 576] that wastes the fewest thread slots, largest first.
+int default_threads(int lines, int D, int m) {
+  const int R = m >= 8 ? 8 : m;
+  const int64_t items = (int64_t)lines * D * (m / R);
+  int best = 576;
+  double best_eff = 0;
+  for (int nt = 576; nt >= 128; nt -= 32) {
+    const double eff = (double)items / (double)(cdiv(items, nt) * nt);
+    if (eff > best_eff + 0.01) { best_eff = eff; best = nt; }
+  }
+  return best;
+}
+bool valid_threads(int t) { return t >= 32 && t <= 1024 && t % 32 == 0; }
 
 hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const int64_t* Lf,
                           const int64_t* Lg, const int64_t* M, hd_plan_t* plan, AxisInfo* ax) {
@@ -163,9 +243,10 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     if (a.D == 0) a.D = x.q;
     if (a.D < 1 || a.D > x.q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
     x.D = a.D;
-    if (a.threads == 0) a.threads = default_threads(lines_for(a, i, ndim), a.m);
-    if (a.threads != 256 && a.threads != 512)
-      return fail(ctx, HD_ERR_UNSUPPORTED, "threads must be 256 or 512 in this build");
+    if (a.D == 0) a.D = x.q;
+    if (a.threads == 0) a.threads = default_threads(lines_for(a, i, ndim), a.D, a.m);
+    if (!valid_threads(a.threads))
+      return fail(ctx, HD_ERR_INVALID, "threads must be a multiple of 32 in [32, 1024]");
     x.threads = a.threads;
     x.lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
@@ -173,8 +254,6 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
       return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": lines*D*m too large for shared memory");
     a.p_f = x.pf; a.p_g = x.pg; a.q = x.q; a.M1 = x.M1;
   }
-  if (ndim == 3 && plan->axis[0].S != plan->axis[1].S)
-    return fail(ctx, HD_ERR_INVALID, "3D plans need S equal on axes 0 and 1");
   return HD_OK;
 }
 
@@ -202,26 +281,28 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
     const int64_t Mi = (M && M[i] > 0) ? M[i] : Lout;
     const bool conv = (i == 0);
     const int nbuf = conv ? conv_nbuf(npairs) : 1;
-    const int lines = (ndim == 1) ? 1 : 2;
     double best = 1e300;
-    int bm = 2, bD = 1;
-    for (int m = 2; m <= 4096; m *= 2) {
-      const int q = (int)cdiv(Mi, m);
-      int D = q;
-      while (D > 1 && pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) --D;
-      if (pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) continue;
-      double c = axis_cost(Lf[i], Lg[i], Lout, Mi, m, conv);
-      const int groups = (int)cdiv(q, D);
-      if (groups > 1) c += (double)(groups - 1) * (double)(Lf[i] + Lg[i] + 2 * Lout) * 4.0;
-      if (c < best) { best = c; bm = m; bD = D; }
+    int bm = 2, bD = 1, bl = 1;
+    for (int lines : {2, 1}) {
+      if (ndim == 1 && lines > 1) continue;
+      for (int m = 2; m <= 4096; m *= 2) {
+        const int q = (int)cdiv(Mi, m);
+        int D = q;
+        while (D > 1 && pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) --D;
+        if (pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) continue;
+        double c = axis_cost(Lf[i], Lg[i], Lout, Mi, m, conv);
+        const int groups = (int)cdiv(q, D);
+        if (groups > 1) c += (double)(groups - 1) * (double)(Lf[i] + Lg[i] + 2 * Lout) * 16.0;
+        if (c < best * 0.999) { best = c; bm = m; bD = D; bl = lines; }
+      }
     }
+    const int lines = bl;
     p.axis[i].m = bm;
     p.axis[i].D = bD;
-    p.axis[i].C = (i == ndim - 1) ? lines : 1;
-    p.axis[i].S = (i == ndim - 1) ? 1 : lines;
-    p.axis[i].threads = default_threads(lines, bm);
+    p.axis[i].C = lines;
+    p.axis[i].S = (ndim == 1) ? 1 : 2;
+    p.axis[i].threads = default_threads(lines, bD, bm);
   }
-  if (ndim == 3) p.axis[1].S = p.axis[0].S;
   *out = p;
   return HD_OK;
 }
@@ -230,6 +311,7 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
 // launching
 // ---------------------------------------------------------------------------
 struct Launch {
+  uint32_t flags;
   int mode;
   const char* name;
   PassArgs a;
@@ -240,24 +322,51 @@ struct Launch {
 void init_in(LineIn& in) { std::memset(&in, 0, sizeof(in)); in.nbi = 1; }
 void init_out(LineOut& o) { std::memset(&o, 0, sizeof(o)); o.nbi = 1; o.so_log2 = 0; }
 
+// The warp-level m = 512 engine applies to one line per CTA, all residues at once
+// (D = q <= 9), the fast fold (p <= 8) and, for the convolution pass, one pair with
+// a short input of a single block (p_g = 1).
+bool use_w512(hd_dtype_t dt, const Launch& L) {
+  if (dt != HD_C128 || L.m != 512 || L.lines != 1 || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
+  if (L.a.D != L.a.q || L.a.q > 9) return false;
+  if (L.mode == hd::MODE_FWD) return L.a.in_f.p <= 8;
+  if (L.mode == hd::MODE_CONV) return L.a.npairs == 1 && L.a.in_f.p <= 8 && L.a.in_g.p == 1;
+  return true;
+}
+
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
-  hd::LaunchFn fn = hd::lookup_launcher(dbl, L.m, L.mode, L.threads);
+  hd::LaunchFn fn;
+  size_t smem;
+  int threads = L.threads;
+  if (use_w512(dt, L)) {
+    fn = hd::lookup_w512(L.mode);
+    threads = 32 * L.a.q;
+    smem = 16 * (size_t)(round_slots(L.a.q, 16) + round_slots(hd::kQF * hd::kQF, 16) +
+                         round_slots((int64_t)L.a.q * 512, 16));
+    const void* tw1;
+    hd_status_t s = get_w512_table(ctx, &tw1);
+    if (s != HD_OK) return s;
+    L.a.tw_st = tw1;
+  } else {
+    fn = hd::lookup_launcher(dbl, L.m, L.mode, L.threads);
+    smem = pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf);
+  }
   if (!fn) return fail(ctx, HD_ERR_UNSUPPORTED, "no kernel instantiation for this m/threads");
-  const size_t smem = pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf);
   if (smem > hd::kMaxSmem) return fail(ctx, HD_ERR_INVALID, "pass shared memory exceeds 227 KB");
   dim3 grid;
-  if (L.a.batch_fastest) { grid.x = (unsigned)L.nbatch; grid.y = (unsigned)L.ngroups; }
-  else { grid.x = (unsigned)L.ngroups; grid.y = (unsigned)L.nbatch; }
-  grid.z = (unsigned)L.narrays;
-  if (grid.y > 65535 || grid.z > 65535 || L.ngroups < 1 || L.nbatch < 1)
+  const int64_t total = L.ngroups * L.nbatch;
+  if (L.ngroups < 1 || L.nbatch < 1 || L.narrays > 65535 || total > 0x7fffffffLL)
     return fail(ctx, HD_ERR_UNSUPPORTED, "grid too large for one launch");
+  L.a.ngroups = L.ngroups;
+  grid.x = (unsigned)total;  // capped to the persistent CTA count by the launcher
+  grid.y = 1;
+  grid.z = (unsigned)L.narrays;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->profiling) {
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
   }
-  cudaError_t e = fn(L.a, grid, smem, st);
+  cudaError_t e = fn(L.a, grid, threads, smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, L.name);
   ctx->launches += 1;
   if (ctx->profiling) {
@@ -289,33 +398,48 @@ struct Problem {
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 // Workspace regions (elements) of the multi-pass pipeline; returns total bytes.
+// Spectral extents tiled by a tile width <= 16 are padded to a multiple of 16.
+int64_t pad16(int64_t v) { return cdiv(v, 16) * 16; }
 size_t ws_regions(const Problem& P, std::vector<int64_t>& elems) {
   elems.clear();
   const int64_t B = P.batch, Bg = P.shared_g ? 1 : P.batch;
   const AxisInfo* a = P.ax;
   if (P.ndim == 2) {
-    const int64_t Kx = a[1].M1, Cx = a[1].lines;
-    const int64_t Oyp = cdiv(a[0].O, Cx) * Cx;
-    for (int k = 0; k < P.N; ++k) elems.push_back(B * Kx * a[0].Lf);
-    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * Kx * a[0].Lg);
-    elems.push_back(B * Oyp * Kx);
+    const int64_t Kxp = pad16(a[1].M1), Sx = a[1].S;
+    const int64_t Oyp = cdiv(a[0].O, Sx) * Sx;
+    for (int k = 0; k < P.N; ++k) elems.push_back(B * Kxp * a[0].Lf);
+    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * Kxp * a[0].Lg);
+    elems.push_back(B * Oyp * Kxp);
   } else if (P.ndim == 3) {
-    const int64_t Kx = a[2].M1, Ky = a[1].M1, Cx = a[2].lines;
-    const int64_t Oyp = cdiv(a[1].O, Cx) * Cx;
-    for (int k = 0; k < P.N; ++k) elems.push_back(B * a[0].Lf * Kx * a[1].Lf);
-    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * a[0].Lg * Kx * a[1].Lg);
-    for (int k = 0; k < P.N; ++k) elems.push_back(B * Ky * Kx * a[0].Lf);
-    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * Ky * Kx * a[0].Lg);
-    elems.push_back(B * a[0].O * Kx * Ky);
-    elems.push_back(B * a[0].O * Oyp * Kx);
+    const int64_t Kxp = pad16(a[2].M1), Ky = a[1].M1, Sx = a[2].S;
+    const int64_t Oyp = cdiv(a[1].O, Sx) * Sx;
+    for (int k = 0; k < P.N; ++k) elems.push_back(B * a[0].Lf * Kxp * a[1].Lf);
+    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * a[0].Lg * Kxp * a[1].Lg);
+    for (int k = 0; k < P.N; ++k) elems.push_back(B * Ky * Kxp * a[0].Lf);
+    for (int k = 0; k < P.N; ++k) elems.push_back(Bg * Ky * Kxp * a[0].Lg);
+    elems.push_back(B * a[0].O * Kxp * Ky);
+    elems.push_back(B * a[0].O * Oyp * Kxp);
   }
   size_t total = 0;
   for (int64_t e : elems) total += align256((size_t)e * elem_bytes(P.dt));
   return total;
 }
 
+// layout helpers (strides in elements)
+void in_rows(LineIn& in, int64_t row) { in.tl = 40; in.s_l = row; in.s_j = 1; }
+void in_tiled(LineIn& in, int64_t S, int64_t tile) { in.tl = ilog2(S); in.s_t = tile; in.s_l = 1; in.s_j = S; }
+void out_rows(LineOut& o, int64_t row) { o.tl = 40; o.s_l = row; o.so_log2 = 40; o.s_jt = 0; o.s_js = 1; }
+// lines linear (stride line), element axis tiled by S with tile stride `tile`
+void out_elem_tiled(LineOut& o, int64_t line, int64_t S, int64_t tile) {
+  o.tl = 40; o.s_l = line; o.so_log2 = ilog2(S); o.s_jt = tile; o.s_js = 1;
+}
+// lines tiled by S (tile stride `tile`, lane stride 1), element axis plain (stride `elem`)
+void out_line_tiled(LineOut& o, int64_t S, int64_t tile, int64_t elem) {
+  o.tl = ilog2(S); o.s_t = tile; o.s_l = 1; o.so_log2 = 40; o.s_jt = 0; o.s_js = elem;
+}
+
 Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, int axis,
-                   const void* twm, const void* twM1) {
+                   const void* twm, const void* twM1, const void* twst) {
   const AxisInfo& x = P.ax[axis];
   Launch L;
   std::memset(&L, 0, sizeof(L));
@@ -330,6 +454,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   init_out(L.a.out);
   L.a.tw_m = twm;
   L.a.tw_M1 = twM1;
+  L.a.tw_st = twst;
   L.a.q = x.q;
   L.a.D = x.D;
   L.a.C = x.lines;
@@ -338,6 +463,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   L.a.npairs = (mode == hd::MODE_CONV) ? P.N : 1;
   L.a.scale = 1.0;
   L.narrays = 1;
+  L.flags = P.plan.flags;
   (void)ctx;
   return L;
 }
@@ -347,8 +473,11 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
   const size_t eb = elem_bytes(P.dt);
   const void* twm[HD_MAX_DIM] = {};
   const void* twM1[HD_MAX_DIM] = {};
+  const void* twst[HD_MAX_DIM] = {};
   for (int i = 0; i < P.ndim; ++i) {
     hd_status_t s = get_table(ctx, P.ax[i].m, dbl, &twm[i]);
+    if (s != HD_OK) return s;
+    s = get_stage_table(ctx, P.ax[i].m, dbl, &twst[i]);
     if (s != HD_OK) return s;
     s = get_table(ctx, P.ax[i].M1, dbl, &twM1[i]);
     if (s != HD_OK) return s;
@@ -383,70 +512,67 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
 
   if (P.ndim == 1) {
     const AxisInfo& x = a[0];
-    Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv1d", 0, twm[0], twM1[0]);
-    const int64_t c = x.lines;
+    Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv1d", 0, twm[0], twM1[0], twst[0]);
     for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = P.f[k]; L.a.in_g.ptr[k] = P.g[k]; }
-    L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; L.a.in_f.s_g = c * x.Lf; L.a.in_f.s_c = x.Lf; L.a.in_f.s_j = 1;
-    L.a.in_g.L = x.Lg; L.a.in_g.p = x.pg;
-    L.a.in_g.s_g = P.shared_g ? 0 : c * x.Lg; L.a.in_g.s_c = P.shared_g ? 0 : x.Lg; L.a.in_g.s_j = 1;
-    L.a.out.ptr[0] = P.h; L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.so_log2 = 40;
-    L.a.out.s_g = c * x.O; L.a.out.s_c = x.O; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+    L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; in_rows(L.a.in_f, x.Lf);
+    L.a.in_g.L = x.Lg; L.a.in_g.p = x.pg; in_rows(L.a.in_g, P.shared_g ? 0 : x.Lg);
+    L.a.out.ptr[0] = P.h; L.a.out.L = x.O; L.a.out.T = x.T; out_rows(L.a.out, x.O);
     L.a.scale = scale;
     L.a.nlines = B; L.a.nbatch = 1;
-    L.a.in_f.nbi = L.a.in_g.nbi = L.a.out.nbi = 1;
-    L.ngroups = cdiv(B, c); L.nbatch = 1;
+    L.ngroups = cdiv(B, x.lines); L.nbatch = 1;
     return launch(ctx, P.dt, L, st);
   }
 
   if (P.ndim == 2) {
     const AxisInfo &y = a[0], &x = a[1];
-    const int64_t Kx = x.M1, Cx = x.lines, Sy = y.lines;
-    const int64_t Oyp = cdiv(y.O, Cx) * Cx;
+    const int64_t Kx = x.M1, Kxp = pad16(Kx), Cx = x.lines, Cy = y.lines;
+    const int64_t Sy = y.S, Sx = x.S;           // X tiles (read by conv_y), Y tiles (read by inv_x)
+    const int64_t Oyp = cdiv(y.O, Sx) * Sx;
     char** Xf = &reg[0];
     char** Xg = &reg[N];
     char* Y = reg[2 * N];
-    // pass A: forward along x for the rows of every f_k, then every g_k
+    // pass A: forward along x for the rows of every f_k, then every g_k -> X[kx/Sy][y][kx%Sy]
     for (int which = 0; which < 2; ++which) {
       const int64_t rows = which == 0 ? y.Lf : y.Lg;
       const int64_t len = which == 0 ? x.Lf : x.Lg;
       const int64_t nb = which == 0 ? B : Bg;
-      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_x_f" : "fwd_x_g", 1, twm[1], twM1[1]);
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_x_f" : "fwd_x_g", 1, twm[1], twM1[1], twst[1]);
       for (int k = 0; k < N; ++k) {
         L.a.in_f.ptr[k] = which == 0 ? P.f[k] : P.g[k];
         L.a.out.ptr[k] = which == 0 ? Xf[k] : Xg[k];
       }
       L.a.in_f.L = len; L.a.in_f.p = which == 0 ? x.pf : x.pg;
-      L.a.in_f.nbi = nb; L.a.in_f.s_b = rows * len; L.a.in_f.s_g = Cx * len; L.a.in_f.s_c = len; L.a.in_f.s_j = 1;
-      L.a.out.nbi = nb; L.a.out.s_b = Kx * rows; L.a.out.s_g = Cx * Sy; L.a.out.s_c = Sy;
-      L.a.out.so_log2 = ilog2(Sy); L.a.out.s_jt = rows * Sy; L.a.out.s_js = 1; L.a.out.L = Kx;
+      L.a.in_f.nbi = nb; L.a.in_f.s_b = rows * len; in_rows(L.a.in_f, len);
+      L.a.out.nbi = nb; L.a.out.s_b = Kxp * rows; out_elem_tiled(L.a.out, Sy, Sy, rows * Sy);
+      L.a.out.L = Kx;
       L.a.nlines = rows; L.a.nbatch = nb;
       L.ngroups = cdiv(rows, Cx); L.nbatch = nb; L.narrays = N;
       hd_status_t s = launch(ctx, P.dt, L, st);
       if (s != HD_OK) return s;
     }
-    // pass B: convolution along y for every spectral column (sum over pairs)
+    // pass B: convolution along y for every spectral column (sum over pairs) -> Y[y/Sx][kx][y%Sx]
     {
-      Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_y", 0, twm[0], twM1[0]);
+      Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_y", 0, twm[0], twM1[0], twst[0]);
       for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = Xf[k]; L.a.in_g.ptr[k] = Xg[k]; }
       L.a.in_f.L = y.Lf; L.a.in_f.p = y.pf; L.a.in_f.nbi = B;
-      L.a.in_f.s_b = Kx * y.Lf; L.a.in_f.s_g = y.Lf * Sy; L.a.in_f.s_c = 1; L.a.in_f.s_j = Sy;
+      L.a.in_f.s_b = Kxp * y.Lf; in_tiled(L.a.in_f, Sy, y.Lf * Sy);
       L.a.in_g.L = y.Lg; L.a.in_g.p = y.pg; L.a.in_g.nbi = B;
-      L.a.in_g.s_b = P.shared_g ? 0 : Kx * y.Lg; L.a.in_g.s_g = y.Lg * Sy; L.a.in_g.s_c = 1; L.a.in_g.s_j = Sy;
-      L.a.out.ptr[0] = Y; L.a.out.nbi = B; L.a.out.s_b = Oyp * Kx; L.a.out.s_g = Sy * Cx; L.a.out.s_c = Cx;
-      L.a.out.so_log2 = ilog2(Cx); L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1; L.a.out.L = y.O; L.a.out.T = y.T;
+      L.a.in_g.s_b = P.shared_g ? 0 : Kxp * y.Lg; in_tiled(L.a.in_g, Sy, y.Lg * Sy);
+      L.a.out.ptr[0] = Y; L.a.out.nbi = B; L.a.out.s_b = Oyp * Kxp;
+      out_elem_tiled(L.a.out, Sx, Sx, Kxp * Sx);
+      L.a.out.L = y.O; L.a.out.T = y.T;
       L.a.scale = scale;
       L.a.nlines = Kx; L.a.nbatch = B;
-      L.ngroups = cdiv(Kx, Sy); L.nbatch = B;
+      L.ngroups = cdiv(Kx, Cy); L.nbatch = B;
       hd_status_t s = launch(ctx, P.dt, L, st);
       if (s != HD_OK) return s;
     }
     // pass C: inverse along x for every output row
     {
-      Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 1, twm[1], twM1[1]);
-      L.a.in_f.ptr[0] = Y; L.a.in_f.nbi = B; L.a.in_f.s_b = Oyp * Kx; L.a.in_f.s_g = Kx * Cx;
-      L.a.in_f.s_c = 1; L.a.in_f.s_j = Cx; L.a.in_f.L = Kx;
-      L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; L.a.out.s_g = Cx * x.O;
-      L.a.out.s_c = x.O; L.a.out.so_log2 = 40; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+      Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 1, twm[1], twM1[1], twst[1]);
+      L.a.in_f.ptr[0] = Y; L.a.in_f.nbi = B; L.a.in_f.s_b = Oyp * Kxp; in_tiled(L.a.in_f, Sx, Kxp * Sx);
+      L.a.in_f.L = Kx;
+      L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; out_rows(L.a.out, x.O);
       L.a.out.L = x.O; L.a.out.T = x.T;
       L.a.nlines = y.O; L.a.nbatch = B;
       L.ngroups = cdiv(y.O, Cx); L.nbatch = B;
@@ -456,8 +582,10 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
 
   // ndim == 3: axes z (0), y (1), x (2)
   const AxisInfo &z = a[0], &y = a[1], &x = a[2];
-  const int64_t Kx = x.M1, Ky = y.M1, Cx = x.lines, S = y.lines;
-  const int64_t Oyp = cdiv(y.O, Cx) * Cx;
+  const int64_t Kx = x.M1, Kxp = pad16(Kx), Ky = y.M1;
+  const int64_t Cx = x.lines, Cy = y.lines, Cz = z.lines;
+  const int64_t S1 = y.S, S0 = z.S, Sx = x.S;  // X1 / Zl kx-tiles, XY kx-tiles, W y-tiles
+  const int64_t Oyp = cdiv(y.O, Sx) * Sx;
   char** X1f = &reg[0];
   char** X1g = &reg[N];
   char** XYf = &reg[2 * N];
@@ -467,79 +595,78 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
   for (int which = 0; which < 2; ++which) {
     const int64_t Fz = which == 0 ? z.Lf : z.Lg, Fy = which == 0 ? y.Lf : y.Lg, Fx = which == 0 ? x.Lf : x.Lg;
     const int64_t nb = which == 0 ? B : Bg;
-    // pass 1: forward along x; batch = (b, z) combined, lines = y
+    // pass 1: forward along x; batch = (b, z) combined, lines = y -> X1[b][z][kx/S1][y][kx%S1]
     {
-      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_x_f" : "fwd_x_g", 2, twm[2], twM1[2]);
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_x_f" : "fwd_x_g", 2, twm[2], twM1[2], twst[2]);
       for (int k = 0; k < N; ++k) {
         L.a.in_f.ptr[k] = which == 0 ? P.f[k] : P.g[k];
         L.a.out.ptr[k] = which == 0 ? X1f[k] : X1g[k];
       }
       L.a.in_f.L = Fx; L.a.in_f.p = which == 0 ? x.pf : x.pg;
-      L.a.in_f.nbi = nb * Fz; L.a.in_f.s_b = Fy * Fx; L.a.in_f.s_g = Cx * Fx; L.a.in_f.s_c = Fx; L.a.in_f.s_j = 1;
-      L.a.out.nbi = nb * Fz; L.a.out.s_b = Kx * Fy; L.a.out.s_g = Cx * S; L.a.out.s_c = S;
-      L.a.out.so_log2 = ilog2(S); L.a.out.s_jt = Fy * S; L.a.out.s_js = 1; L.a.out.L = Kx;
+      L.a.in_f.nbi = nb * Fz; L.a.in_f.s_b = Fy * Fx; in_rows(L.a.in_f, Fx);
+      L.a.out.nbi = nb * Fz; L.a.out.s_b = Kxp * Fy; out_elem_tiled(L.a.out, S1, S1, Fy * S1);
+      L.a.out.L = Kx;
       L.a.nlines = Fy; L.a.nbatch = nb * Fz;
       L.ngroups = cdiv(Fy, Cx); L.nbatch = nb * Fz; L.narrays = N;
       hd_status_t s = launch(ctx, P.dt, L, st);
       if (s != HD_OK) return s;
     }
-    // pass 2: forward along y; batch = (b, z), lines = kx (S per CTA)
+    // pass 2: forward along y; batch = (b, z), lines = kx -> XY[b][ky][kx/S0][z][kx%S0]
     {
-      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_y_f" : "fwd_y_g", 1, twm[1], twM1[1]);
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, which == 0 ? "fwd_y_f" : "fwd_y_g", 1, twm[1], twM1[1], twst[1]);
       for (int k = 0; k < N; ++k) {
         L.a.in_f.ptr[k] = which == 0 ? X1f[k] : X1g[k];
         L.a.out.ptr[k] = which == 0 ? XYf[k] : XYg[k];
       }
       L.a.in_f.L = Fy; L.a.in_f.p = which == 0 ? y.pf : y.pg;
-      L.a.in_f.nbi = Fz; L.a.in_f.s_bo = Fz * Kx * Fy; L.a.in_f.s_b = Kx * Fy;
-      L.a.in_f.s_g = Fy * S; L.a.in_f.s_c = 1; L.a.in_f.s_j = S;
-      L.a.out.nbi = Fz; L.a.out.s_bo = Ky * Kx * Fz; L.a.out.s_b = S; L.a.out.s_g = Fz * S; L.a.out.s_c = 1;
-      L.a.out.so_log2 = 0; L.a.out.s_jt = Kx * Fz; L.a.out.s_js = 0; L.a.out.L = Ky;
+      L.a.in_f.nbi = Fz; L.a.in_f.s_bo = Fz * Kxp * Fy; L.a.in_f.s_b = Kxp * Fy;
+      in_tiled(L.a.in_f, S1, Fy * S1);
+      L.a.out.nbi = Fz; L.a.out.s_bo = Ky * Kxp * Fz; L.a.out.s_b = S0;
+      out_line_tiled(L.a.out, S0, Fz * S0, Kxp * Fz);
+      L.a.out.L = Ky;
       L.a.batch_fastest = 1;
       L.a.nlines = Kx; L.a.nbatch = nb * Fz;
-      L.ngroups = cdiv(Kx, S); L.nbatch = nb * Fz; L.narrays = N;
+      L.ngroups = cdiv(Kx, Cy); L.nbatch = nb * Fz; L.narrays = N;
       hd_status_t s = launch(ctx, P.dt, L, st);
       if (s != HD_OK) return s;
     }
   }
-  // pass 3: convolution along z; batch = (b, ky), lines = kx
+  // pass 3: convolution along z; batch = (b, ky), lines = kx -> Zl[b][z][kx/S1][ky][kx%S1]
   {
-    Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_z", 0, twm[0], twM1[0]);
+    Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_z", 0, twm[0], twM1[0], twst[0]);
     for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = XYf[k]; L.a.in_g.ptr[k] = XYg[k]; }
-    L.a.in_f.L = z.Lf; L.a.in_f.p = z.pf; L.a.in_f.nbi = Ky; L.a.in_f.s_bo = Ky * Kx * z.Lf;
-    L.a.in_f.s_b = Kx * z.Lf; L.a.in_f.s_g = z.Lf * S; L.a.in_f.s_c = 1; L.a.in_f.s_j = S;
-    L.a.in_g.L = z.Lg; L.a.in_g.p = z.pg; L.a.in_g.nbi = Ky; L.a.in_g.s_bo = P.shared_g ? 0 : Ky * Kx * z.Lg;
-    L.a.in_g.s_b = Kx * z.Lg; L.a.in_g.s_g = z.Lg * S; L.a.in_g.s_c = 1; L.a.in_g.s_j = S;
-    L.a.out.ptr[0] = Zl; L.a.out.nbi = Ky; L.a.out.s_bo = z.O * Kx * Ky; L.a.out.s_b = S;
-    L.a.out.s_g = Ky * S; L.a.out.s_c = 1; L.a.out.so_log2 = 0; L.a.out.s_jt = Kx * Ky; L.a.out.s_js = 0;
+    L.a.in_f.L = z.Lf; L.a.in_f.p = z.pf; L.a.in_f.nbi = Ky; L.a.in_f.s_bo = Ky * Kxp * z.Lf;
+    L.a.in_f.s_b = Kxp * z.Lf; in_tiled(L.a.in_f, S0, z.Lf * S0);
+    L.a.in_g.L = z.Lg; L.a.in_g.p = z.pg; L.a.in_g.nbi = Ky; L.a.in_g.s_bo = P.shared_g ? 0 : Ky * Kxp * z.Lg;
+    L.a.in_g.s_b = Kxp * z.Lg; in_tiled(L.a.in_g, S0, z.Lg * S0);
+    L.a.out.ptr[0] = Zl; L.a.out.nbi = Ky; L.a.out.s_bo = z.O * Kxp * Ky; L.a.out.s_b = S1;
+    out_line_tiled(L.a.out, S1, Ky * S1, Kxp * Ky);
     L.a.out.L = z.O; L.a.out.T = z.T;
     L.a.scale = scale;
     L.a.batch_fastest = 1;
     L.a.nlines = Kx; L.a.nbatch = B * Ky;
-    L.ngroups = cdiv(Kx, S); L.nbatch = B * Ky;
+    L.ngroups = cdiv(Kx, Cz); L.nbatch = B * Ky;
     hd_status_t s = launch(ctx, P.dt, L, st);
     if (s != HD_OK) return s;
   }
-  // pass 4: inverse along y; batch = (b, z_out) combined, lines = kx
+  // pass 4: inverse along y; batch = (b, z_out) combined, lines = kx -> W[b][z][y/Sx][kx][y%Sx]
   {
-    Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_y", 1, twm[1], twM1[1]);
-    L.a.in_f.ptr[0] = Zl; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Kx * Ky; L.a.in_f.s_g = Ky * S;
-    L.a.in_f.s_c = 1; L.a.in_f.s_j = S; L.a.in_f.L = Ky;
-    L.a.out.ptr[0] = W; L.a.out.nbi = B * z.O; L.a.out.s_b = Oyp * Kx; L.a.out.s_g = S * Cx;
-    L.a.out.s_c = Cx; L.a.out.so_log2 = ilog2(Cx); L.a.out.s_jt = Kx * Cx; L.a.out.s_js = 1;
+    Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_y", 1, twm[1], twM1[1], twst[1]);
+    L.a.in_f.ptr[0] = Zl; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Kxp * Ky; in_tiled(L.a.in_f, S1, Ky * S1);
+    L.a.in_f.L = Ky;
+    L.a.out.ptr[0] = W; L.a.out.nbi = B * z.O; L.a.out.s_b = Oyp * Kxp; out_elem_tiled(L.a.out, Sx, Sx, Kxp * Sx);
     L.a.out.L = y.O; L.a.out.T = y.T;
     L.a.nlines = Kx; L.a.nbatch = B * z.O;
-    L.ngroups = cdiv(Kx, S); L.nbatch = B * z.O;
+    L.ngroups = cdiv(Kx, Cy); L.nbatch = B * z.O;
     hd_status_t s = launch(ctx, P.dt, L, st);
     if (s != HD_OK) return s;
   }
   // pass 5: inverse along x; batch = (b, z_out), lines = y_out
   {
-    Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 2, twm[2], twM1[2]);
-    L.a.in_f.ptr[0] = W; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Oyp * Kx; L.a.in_f.s_g = Kx * Cx;
-    L.a.in_f.s_c = 1; L.a.in_f.s_j = Cx; L.a.in_f.L = Kx;
-    L.a.out.ptr[0] = P.h; L.a.out.nbi = B * z.O; L.a.out.s_b = y.O * x.O; L.a.out.s_g = Cx * x.O;
-    L.a.out.s_c = x.O; L.a.out.so_log2 = 40; L.a.out.s_jt = 0; L.a.out.s_js = 1;
+    Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 2, twm[2], twM1[2], twst[2]);
+    L.a.in_f.ptr[0] = W; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Oyp * Kxp; in_tiled(L.a.in_f, Sx, Kxp * Sx);
+    L.a.in_f.L = Kx;
+    L.a.out.ptr[0] = P.h; L.a.out.nbi = B * z.O; L.a.out.s_b = y.O * x.O; out_rows(L.a.out, x.O);
     L.a.out.L = x.O; L.a.out.T = x.T;
     L.a.nlines = y.O; L.a.nbatch = B * z.O;
     L.ngroups = cdiv(y.O, Cx); L.nbatch = B * z.O;
@@ -627,6 +754,9 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   cudaSetDevice(ctx->device);
   for (auto& kv : ctx->tw64) cudaFree(kv.second);
   for (auto& kv : ctx->tw32) cudaFree(kv.second);
+  for (auto& kv : ctx->st64) cudaFree(kv.second);
+  for (auto& kv : ctx->st32) cudaFree(kv.second);
+  if (ctx->w512tw) cudaFree(ctx->w512tw);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
   for (auto& p : ctx->prof)
@@ -868,18 +998,21 @@ hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, 
   P.dt = dtype; P.N = 1;
   AxisInfo& a = P.ax[0];
   a.m = m; a.q = q; a.M1 = (int64_t)q * m; a.Lf = L; a.pf = (int)cdiv(L, m);
-  a.lines = 1; a.threads = kDefaultThreads;
+  a.lines = 1;
   a.D = q;
   while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
+  a.threads = default_threads(1, a.D, m);
   const void *twm, *twM1;
   hd_status_t s = get_table(ctx, m, dbl, &twm);
   if (s != HD_OK) return s;
   s = get_table(ctx, a.M1, dbl, &twM1);
   if (s != HD_OK) return s;
-  Launch Lh = make_launch(ctx, P, hd::MODE_FWD, "fwd_residues", 0, twm, twM1);
-  Lh.a.in_f.ptr[0] = x; Lh.a.in_f.L = L; Lh.a.in_f.p = a.pf; Lh.a.in_f.s_g = L; Lh.a.in_f.s_c = L; Lh.a.in_f.s_j = 1;
-  Lh.a.out.ptr[0] = X; Lh.a.out.so_log2 = 40; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
-  Lh.a.out.s_g = a.M1; Lh.a.out.s_c = a.M1; Lh.a.out.L = a.M1;
+  const void* twst;
+  s = get_stage_table(ctx, m, dbl, &twst);
+  if (s != HD_OK) return s;
+  Launch Lh = make_launch(ctx, P, hd::MODE_FWD, "fwd_residues", 0, twm, twM1, twst);
+  Lh.a.in_f.ptr[0] = x; Lh.a.in_f.L = L; Lh.a.in_f.p = a.pf; in_rows(Lh.a.in_f, L);
+  Lh.a.out.ptr[0] = X; out_rows(Lh.a.out, a.M1); Lh.a.out.L = a.M1;
   Lh.a.nlines = nlines; Lh.a.nbatch = 1;
   Lh.ngroups = nlines; Lh.nbatch = 1;
   return launch(ctx, dtype, Lh, (cudaStream_t)stream);
@@ -899,18 +1032,21 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
   P.dt = dtype; P.N = 1;
   AxisInfo& a = P.ax[0];
   a.m = m; a.q = q; a.M1 = (int64_t)q * m; a.O = Lout; a.T = (int)cdiv(Lout, m);
-  a.lines = 1; a.threads = kDefaultThreads;
+  a.lines = 1;
   a.D = q;
   while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
+  a.threads = default_threads(1, a.D, m);
   const void *twm, *twM1;
   hd_status_t s = get_table(ctx, m, dbl, &twm);
   if (s != HD_OK) return s;
   s = get_table(ctx, a.M1, dbl, &twM1);
   if (s != HD_OK) return s;
-  Launch Lh = make_launch(ctx, P, hd::MODE_INV, "bwd_residues", 0, twm, twM1);
-  Lh.a.in_f.ptr[0] = X; Lh.a.in_f.s_g = a.M1; Lh.a.in_f.s_c = a.M1; Lh.a.in_f.s_j = 1; Lh.a.in_f.L = a.M1;
-  Lh.a.out.ptr[0] = x; Lh.a.out.so_log2 = 40; Lh.a.out.s_jt = 0; Lh.a.out.s_js = 1;
-  Lh.a.out.s_g = Lout; Lh.a.out.s_c = Lout; Lh.a.out.L = Lout; Lh.a.out.T = a.T;
+  const void* twst;
+  s = get_stage_table(ctx, m, dbl, &twst);
+  if (s != HD_OK) return s;
+  Launch Lh = make_launch(ctx, P, hd::MODE_INV, "bwd_residues", 0, twm, twM1, twst);
+  Lh.a.in_f.ptr[0] = X; in_rows(Lh.a.in_f, a.M1); Lh.a.in_f.L = a.M1;
+  Lh.a.out.ptr[0] = x; out_rows(Lh.a.out, Lout); Lh.a.out.L = Lout; Lh.a.out.T = a.T;
   Lh.a.nlines = nlines; Lh.a.nbatch = 1;
   Lh.ngroups = nlines; Lh.nbatch = 1;
   return launch(ctx, dtype, Lh, (cudaStream_t)stream);
@@ -981,19 +1117,20 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
   const int64_t Lout = Lf[i] + Lg[i] - 1;
   const int64_t Mi = (M && M[i] > 0) ? M[i] : Lout;
   const int m0 = base.axis[i].m;
-  const bool contig = (i == ndim - 1);
   const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
-  for (int m = std::max(2, m0 / 4); m <= std::min(4096, m0 * 4); m *= 2) {
+  std::vector<int> Ss = (ndim == 1) ? std::vector<int>{1} : std::vector<int>{1, 2, 4};
+  for (int m = std::max(2, m0 / 2); m <= std::min(4096, m0 * 2); m *= 2) {
     const int q = (int)cdiv(Mi, m);
-    for (int lines : {1, 2, 4}) {
+    for (int C : {1, 2}) {
       std::vector<int> Ds = {q};
       if (q > 1) Ds.push_back((q + 1) / 2);
       for (int D : Ds) {
-        if (pass_smem(eb, q, lines, D, m, nbuf) > hd::kMaxSmem) continue;
-        for (int th : {256, 512}) {
-          AxisCand c{m, contig ? lines : base.axis[i].C, contig ? base.axis[i].S : lines, D, th};
-          out.push_back(c);
-        }
+        if (pass_smem(eb, q, C, D, m, nbuf) > hd::kMaxSmem) continue;
+        const int dt = default_threads(C, D, m);
+        std::vector<int> ths = {dt};
+        if (dt != 256) ths.push_back(256);
+        for (int S : Ss)
+          for (int th : ths) out.push_back(AxisCand{m, C, S, D, th});
       }
     }
   }
@@ -1001,9 +1138,9 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
 }
 
 void apply_cand(hd_plan_t& p, int i, int ndim, const AxisCand& c) {
+  (void)ndim;
   p.axis[i].m = c.m; p.axis[i].C = c.C; p.axis[i].S = c.S; p.axis[i].D = c.D;
   p.axis[i].threads = c.threads;
-  if (ndim == 3 && (i == 0 || i == 1)) { p.axis[0].S = c.S; p.axis[1].S = c.S; }
 }
 
 }  // namespace

@@ -136,25 +136,56 @@ template <int M, int ST> struct StageC {
   static constexpr int TWSTEP = M / NK;
 };
 
+// Stage twiddle table (host-built per m, see hd_api.cu stage_table): for every
+// stage with span > 1, a block [j-1][o] = zeta_NK^{o j}, j = 1..R-1, o < span,
+// so that consecutive threads (consecutive o) load consecutive entries.
+template <int M, int ST> struct StageOff {
+  __host__ __device__ static constexpr int value() {
+    int off = 0;
+    for (int s = 0; s < ST; ++s) {
+      const int R = Sched<M>::radix(s), NK = Sched<M>::nk(s), SP = NK / R;
+      if (SP > 1) off += (R - 1) * SP;
+    }
+    return off;
+  }
+};
+
+#ifndef HD_TW_LOADS
+#define HD_TW_LOADS 1   // stage twiddles per butterfly loaded from the table (1: w1 only, 7: all)
+#endif
+// Stage twiddles w[j] = zeta_NK^{o j}, j = 1..R-1: HD_TW_LOADS == 1 loads w1 (coalesced
+// across o) and forms the rest by <= 3-deep products; otherwise all R-1 are loaded.
+template <typename V, int M, int ST>
+__device__ __forceinline__ void stage_tw(int o, const V* __restrict__ twst, V* w) {
+  using S = StageC<M, ST>;
+  const V* tw = twst + StageOff<M, ST>::value() + o;
+  if constexpr (HD_TW_LOADS == 1 && S::R > 2) {
+    tw_powers<V, S::R>(ldg(tw), w);
+  } else {
+#pragma unroll
+    for (int j = 1; j < S::R; ++j) w[j] = ldg(tw + (j - 1) * S::SPAN);
+  }
+}
+
 // DIF butterfly of stage ST (forward, +exponent) on registers, offset o inside its block
 template <typename V, int M, int ST>
-__device__ __forceinline__ void dif_bfly(V* v, int o, const V* __restrict__ twm) {
+__device__ __forceinline__ void dif_bfly(V* v, int o, const V* __restrict__ twst) {
   using S = StageC<M, ST>;
   dftR<V, S::R, +1>(v);
   if (S::SPAN > 1 && o > 0) {
     V w[S::R];
-    tw_powers<V, S::R>(ldg(twm + o * S::TWSTEP), w);
+    stage_tw<V, M, ST>(o, twst, w);
 #pragma unroll
     for (int j = 1; j < S::R; ++j) v[j] = cmul(v[j], w[j]);
   }
 }
 // DIT butterfly of stage ST (inverse, -exponent): adjoint of dif_bfly
 template <typename V, int M, int ST>
-__device__ __forceinline__ void dit_bfly(V* v, int o, const V* __restrict__ twm) {
+__device__ __forceinline__ void dit_bfly(V* v, int o, const V* __restrict__ twst) {
   using S = StageC<M, ST>;
   if (S::SPAN > 1 && o > 0) {
     V w[S::R];
-    tw_powers<V, S::R>(ldg(twm + o * S::TWSTEP), w);
+    stage_tw<V, M, ST>(o, twst, w);
 #pragma unroll
     for (int j = 1; j < S::R; ++j) v[j] = cmulc(v[j], w[j]);
   }
@@ -166,7 +197,7 @@ template <typename V, int M, int NT, int ST, bool INV>
 __device__ __forceinline__ void fft_stage(V* buf, int nrows, const V* __restrict__ twm) {
   using S = StageC<M, ST>;
   const int items = nrows * S::PER_ROW;
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     const int row = it / S::PER_ROW;
     const int w = it % S::PER_ROW;
     const int b = w / S::SPAN, o = w % S::SPAN;
@@ -203,29 +234,41 @@ __device__ __forceinline__ void fft_inv_from(V* buf, int nrows, const V* twm) {
 // ---------------------------------------------------------------------------
 // Pass arguments
 // ---------------------------------------------------------------------------
-struct LineIn {            // element j of line c of group g, batch b, array k:
-  const void* ptr[kMaxPairs];  //   ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b + g*s_g + c*s_c + j*s_j
-  int64_t L;               // valid elements per line (zero beyond)
+struct LineIn {            // element j of line l = g*C + c, batch b, array k:
+  const void* ptr[kMaxPairs];  //   ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b
+  int64_t L;               //   + (l >> tl)*s_t + (l & (2^tl-1))*s_l + j*s_j
   int64_t nbi, s_bo;       // two-level batch index (nbi = nbatch: one level)
-  int64_t s_b, s_g, s_c, s_j;
+  int64_t s_b, s_t, s_l, s_j;
   int32_t p;               // ceil(L/m) blocks (fold)
-  int32_t pad_;
+  int32_t tl;              // log2 line-tile width of the layout (>= 30: untiled, l*s_l)
 };
-struct LineOut {           // element j of line c: ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b
-  void* ptr[kMaxPairs];    //   + g*s_g + c*s_c + (j>>so_log2)*s_jt + (j&(2^so_log2-1))*s_js
+__device__ __forceinline__ int64_t line_off(const LineIn& in, int64_t l) {
+  if (in.tl >= 30) return l * in.s_l;
+  return (l >> in.tl) * in.s_t + (l & ((int64_t(1) << in.tl) - 1)) * in.s_l;
+}
+struct LineOut {           // element j of line l = g*C + c: ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b
+  void* ptr[kMaxPairs];    //   + (l >> tl)*s_t + (l & (2^tl-1))*s_l + (j>>so_log2)*s_jt + (j&(2^so_log2-1))*s_js
   int64_t L;               // elements written per line
   int64_t nbi, s_bo;
-  int64_t s_b, s_g, s_c, s_jt, s_js;
-  int32_t so_log2;         // log2 tile width of the output layout (>= 30: plain rows)
+  int64_t s_b, s_t, s_l, s_jt, s_js;
+  int32_t so_log2;         // log2 tile width of the element axis (>= 30: plain, j*s_js)
   int32_t T;               // output blocks ceil(L/m) (unfold)
+  int32_t tl;              // log2 line-tile width (>= 30: untiled)
+  int32_t pad_;
 };
+__device__ __forceinline__ int64_t line_off(const LineOut& o, int64_t l) {
+  if (o.tl >= 30) return l * o.s_l;
+  return (l >> o.tl) * o.s_t + (l & ((int64_t(1) << o.tl) - 1)) * o.s_l;
+}
 struct PassArgs {
   LineIn in_f, in_g;
   LineOut out;
   const void* tw_m;        // zeta_m^k,  k < m
   const void* tw_M1;       // zeta_M1^k, k < M1
+  const void* tw_st;       // stage twiddle table of m (see StageOff)
   int64_t nlines;          // lines per batch entry
   int64_t nbatch;
+  int64_t ngroups;         // line groups per batch entry (work items = nbatch * ngroups)
   int64_t M1;
   double scale;            // 1 / prod M1 (CONV)
   int32_t q, D, C, c_log2; // residues, residues per group, lines per CTA (power of two)
@@ -243,6 +286,46 @@ __device__ __forceinline__ int64_t jt_off(int64_t j, int sl, int64_t s_jt, int64
   return (j >> sl) * s_jt + (j & ((int64_t(1) << sl) - 1)) * s_js;
 }
 
+// One (line, s) of the fast fold: P = compile-time bound on p (<= 8)
+template <typename V, int M, int P>
+__device__ __forceinline__ void fold_fast_one(V* buf, int cb, const V* xl, int64_t s_j, int64_t L,
+                                              int s, bool live, int q, const V* zt,
+                                              const V* __restrict__ twm, const V* __restrict__ twM1) {
+  V u[P];
+#pragma unroll
+  for (int t = 0; t < P; ++t) {
+    u[t] = cmk<V>(0, 0);
+    const int64_t j = (int64_t)t * M + s;
+    if (live && j < L) u[t] = xl[j * s_j];
+  }
+  V a0 = u[0];
+#pragma unroll
+  for (int t = 1; t < P; ++t) a0 = cadd(a0, u[t]);
+  buf[swz<V>(cb + s)] = a0;
+  const V w1 = ldg(twM1 + s);                 // zeta_{M1}^{s}
+  const V wq = ldg(twm + s);                  // zeta_{M1}^{q s} = zeta_m^{s}
+  V wr = w1;
+#pragma unroll
+  for (int r = 1; r <= kQF / 2; ++r) {
+    if (2 * r > q) break;
+    V A = u[0], B = cmk<V>(0, 0);             // t = 0 term: zeta^0 = 1
+#pragma unroll
+    for (int t = 1; t < P; ++t) {
+      const V z = zt[r * kQF + t];            // zeta_q^{r t}
+      A.x = fma(u[t].x, z.x, A.x); A.y = fma(u[t].y, z.x, A.y);
+      B.x = fma(u[t].x, z.y, B.x); B.y = fma(u[t].y, z.y, B.y);
+    }
+    // a_r = A + iB, a_{q-r} = A - iB
+    const V ar = cmk<V>(A.x - B.y, A.y + B.x);
+    buf[swz<V>(cb + r * M + s)] = cmul(ar, wr);
+    if (2 * r < q) {
+      const V aq = cmk<V>(A.x + B.y, A.y - B.x);
+      buf[swz<V>(cb + (q - r) * M + s)] = cmul(aq, cmulc(wq, wr));  // zeta^{(q-r)s} = zeta_m^s conj(zeta^{rs})
+    }
+    wr = cmul(wr, w1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fold: w_r[s] = zeta_{M1}^{rs} sum_{t<p} zeta_q^{rt} x[tm+s] for r in [r0, r0+nd)
 // Fast path (all residues, q <= 16, p <= 8): the q-point DFT over t is evaluated
@@ -255,53 +338,23 @@ __device__ __forceinline__ void fold(V* buf, const LineIn& in, int k, int64_t b,
                                      const V* zq, const V* zt, const V* __restrict__ twm,
                                      const V* __restrict__ twM1) {
   using R = decltype(V::x);
-  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
+  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b;
   const int items = C * M;
   const bool cfast = (in.s_j != 1);
   const int p = in.p;
   const int64_t L = in.L;
   const bool fast = (nd == q) && (q <= kQF) && (p <= kPF);
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     int c, s;
     if (cfast) { c = it & (C - 1); s = it >> clog; } else { s = it % M; c = it / M; }
     const bool live = (g * C + c) < nlines;
-    const V* xl = x + c * in.s_c;
+    const V* xl = x + line_off(in, g * C + c);
     const int cb = c * nd * M;  // swizzle indices are relative to buf
     if (fast) {
-      V u[kPF];
-#pragma unroll
-      for (int t = 0; t < kPF; ++t) {
-        u[t] = cmk<V>(0, 0);
-        const int64_t j = (int64_t)t * M + s;
-        if (live && t < p && j < L) u[t] = xl[j * in.s_j];
-      }
-      V a0 = u[0];
-#pragma unroll
-      for (int t = 1; t < kPF; ++t) a0 = cadd(a0, u[t]);
-      buf[swz<V>(cb + s)] = a0;
-      const V w1 = ldg(twM1 + s);                 // zeta_{M1}^{s}
-      const V wq = ldg(twm + s);                  // zeta_{M1}^{q s} = zeta_m^{s}
-      V wr = w1;
-#pragma unroll
-      for (int r = 1; r <= kQF / 2; ++r) {
-        if (2 * r > q) break;
-        V A = cmk<V>(0, 0), B = cmk<V>(0, 0);
-#pragma unroll
-        for (int t = 0; t < kPF; ++t) {
-          const V z = zt[r * kQF + t];            // zeta_q^{r t}
-          A.x = fma(u[t].x, z.x, A.x); A.y = fma(u[t].y, z.x, A.y);
-          B.x = fma(u[t].x, z.y, B.x); B.y = fma(u[t].y, z.y, B.y);
-        }
-        // a_r = A + iB, a_{q-r} = A - iB
-        const V ar = cmk<V>(A.x - B.y, A.y + B.x);
-        buf[swz<V>(cb + r * M + s)] = cmul(ar, wr);
-        if (2 * r < q) {
-          const V aq = cmk<V>(A.x + B.y, A.y - B.x);
-          buf[swz<V>(cb + (q - r) * M + s)] = cmul(aq, cmulc(wq, wr));  // zeta^{(q-r)s} = zeta_m^s conj(zeta^{rs})
-        }
-        wr = cmul(wr, w1);
-      }
-      (void)sizeof(R);
+      if (p <= 1) fold_fast_one<V, M, 1>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
+      else if (p <= 2) fold_fast_one<V, M, 2>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
+      else if (p <= 4) fold_fast_one<V, M, 4>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
+      else fold_fast_one<V, M, kPF>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
     } else {
       for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
         V acc[kFoldChunk];
@@ -349,14 +402,14 @@ __device__ __forceinline__ void unfold_fast(const V* buf, V* y, const LineOut& o
   const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     const int s_lo = it & ((1 << so_l) - 1);
     const int rest = it >> so_l;
     const int c = rest & (C - 1);
     const int s = ((rest >> clog) << so_l) + s_lo;
     if ((g * C + c) >= nlines) continue;
     const int cb = c * q * M;
-    V* yl = y + c * out.s_c;
+    V* yl = y + line_off(out, g * C + c);
     V v[QM];
     const V w1 = ldg(twM1 + s);
     V wr = cmk<V>(1, 0);
@@ -401,7 +454,7 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
                                        int64_t nlines, int C, int clog, int r0, int nd, int q,
                                        bool accumulate, const V* zq, const V* zt,
                                        const V* __restrict__ twm, const V* __restrict__ twM1) {
-  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b;
   if (nd == q && !accumulate) {
     if (q <= 4) { unfold_fast<V, M, NT, 4>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
     if (q <= 8) { unfold_fast<V, M, NT, 8>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
@@ -413,13 +466,13 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
   const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     const int s_lo = it & ((1 << so_l) - 1);
     const int rest = it >> so_l;
     const int c = rest & (C - 1);
     const int s = ((rest >> clog) << so_l) + s_lo;
     if ((g * C + c) >= nlines) continue;
-    V* yl = y + c * out.s_c;
+    V* yl = y + line_off(out, g * C + c);
     const int cb = c * nd * M;
     for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
       V v[kFoldChunk];
@@ -455,6 +508,17 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
   }
 }
 
+// 256-bit global store of two adjacent complex values (STG.E.ENL2.256 on sm_100a);
+// p must be 32-byte aligned.  Falls back to two stores for float2.
+template <typename V> __device__ __forceinline__ void st256(V* p, V a, V b) {
+  if constexpr (sizeof(V) == 16) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(p), "d"((double)a.x), "d"((double)a.y),
+                 "d"((double)b.x), "d"((double)b.y) : "memory");
+  } else {
+    p[0] = a; p[1] = b;
+  }
+}
+
 // Last forward stage fused with the spectrum store: DIF stage NST-1 (span 1) on
 // buf rows (c, d), results written straight to the output element
 // kappa = (r0 + d) m + pos of line c.  Line index fastest across threads so
@@ -466,10 +530,10 @@ __device__ __forceinline__ void fwd_last_store(const V* buf, const LineOut& out,
   constexpr int ST = Sched<M>::NST - 1;
   using S = StageC<M, ST>;
   static_assert(S::SPAN == 1, "last stage has unit span");
-  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b + g * out.s_g;
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b;
   const int sl = out.so_log2;
   const int items = C * nd * S::PER_ROW;
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     const int c = it & (C - 1);
     const int rest = it >> clog;
     const int w = rest % S::PER_ROW;
@@ -480,10 +544,16 @@ __device__ __forceinline__ void fwd_last_store(const V* buf, const LineOut& out,
     for (int i = 0; i < S::R; ++i) v[i] = buf[swz<V>(base + i)];
     dif_bfly<V, M, ST>(v, 0, twm);
     if ((g * C + c) < nlines) {
-      V* yl = y + c * out.s_c;
+      V* yl = y + line_off(out, g * C + c);
       const int64_t k0 = (int64_t)(r0 + d) * M + w * S::R;
+      if (sizeof(V) == 16 && S::R >= 2 && sl >= 1 && out.s_js == 1) {
+        // kappa pairs (even, odd) are adjacent: one 256-bit store per pair
 #pragma unroll
-      for (int i = 0; i < S::R; ++i) yl[jt_off(k0 + i, sl, out.s_jt, out.s_js)] = v[i];
+        for (int i = 0; i < S::R; i += 2) st256(yl + jt_off(k0 + i, sl, out.s_jt, out.s_js), v[i], v[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < S::R; ++i) yl[jt_off(k0 + i, sl, out.s_jt, out.s_js)] = v[i];
+      }
     }
   }
 }
@@ -496,10 +566,10 @@ __device__ __forceinline__ void inv_first_load(V* buf, const LineIn& in, int64_t
                                                const V* __restrict__ twm) {
   constexpr int ST = Sched<M>::NST - 1;
   using S = StageC<M, ST>;
-  const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b + g * in.s_g;
+  const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b;
   const int items = C * nd * S::PER_ROW;
   const bool cfast = (in.s_j != 1);
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     int c, w, d;
     if (cfast) {
       c = it & (C - 1);
@@ -515,7 +585,7 @@ __device__ __forceinline__ void inv_first_load(V* buf, const LineIn& in, int64_t
     V v[S::R];
     const int64_t k0 = (int64_t)(r0 + d) * M + w * S::R;
     const bool live = (g * C + c) < nlines;
-    const V* xl = x + c * in.s_c;
+    const V* xl = x + line_off(in, g * C + c);
 #pragma unroll
     for (int i = 0; i < S::R; ++i) v[i] = live ? xl[(k0 + i) * in.s_j] : cmk<V>(0, 0);
     dit_bfly<V, M, ST>(v, 0, twm);
@@ -537,7 +607,7 @@ __device__ __forceinline__ void conv_mid(V* bufF, const V* bufG, V* bufA, int nr
   using S = StageC<M, ST>;
   const int items = nrows * S::PER_ROW;
   const bool last = (kk == npairs - 1);
-  for (int it = threadIdx.x; it < items; it += NT) {
+  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     const int base = it * S::R;  // rows are contiguous: row*M + w*R == it*R
     V f[S::R], h[S::R];
 #pragma unroll
@@ -561,6 +631,34 @@ __device__ __forceinline__ void conv_mid(V* bufF, const V* bufG, V* bufA, int nr
   }
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (UBLKPF); p 16-byte aligned.
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  for (uintptr_t a = a0; a < a1; a += (uintptr_t(1) << 20)) {
+    const uint32_t n = (uint32_t)((a1 - a) < (uintptr_t(1) << 20) ? (a1 - a) : (uintptr_t(1) << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a), "r"(n) : "memory");
+  }
+}
+
+// Prefetch the input lines of work item (b, g) of array k into L2 (one thread).
+template <typename V>
+__device__ __forceinline__ void prefetch_lines(const LineIn& in, int k, int64_t b, int64_t g, int C,
+                                               int64_t nlines) {
+  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b;
+  const int64_t l0 = g * C;
+  const int64_t l1 = (l0 + C < nlines ? l0 + C : nlines) - 1;
+  if (l1 < l0) return;
+  if (in.tl >= 30) {
+    for (int64_t l = l0; l <= l1; ++l)
+      prefetch_l2(x + l * in.s_l, ((in.L - 1) * in.s_j + 1) * (int64_t)sizeof(V));
+  } else {
+    const int64_t S = int64_t(1) << in.tl;
+    for (int64_t t = l0 >> in.tl; t <= (l1 >> in.tl); ++t)
+      prefetch_l2(x + t * in.s_t, in.L * S * (int64_t)sizeof(V));
+  }
+}
+
 template <int EPR> __host__ __device__ constexpr int64_t round_slots(int64_t n) {
   return (n + 8 * EPR - 1) / (8 * EPR) * (8 * EPR);
 }
@@ -578,8 +676,6 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V* smem = reinterpret_cast<V*>(smem_raw);
 
-  const int64_t g = a.batch_fastest ? blockIdx.y : blockIdx.x;
-  const int64_t b = a.batch_fastest ? blockIdx.x : blockIdx.y;
   const int k_arr = blockIdx.z;
   const int C = a.C, clog = a.c_log2, D = a.D, q = a.q;
   const int64_t bufn = round_slots<EPR>((int64_t)C * D * M);
@@ -591,25 +687,45 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
   V* bufA = bufG + bufn;
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
-  for (int i = threadIdx.x; i < q; i += NT) zq[i] = ldg(twM1 + (int64_t)i * M);
-  for (int i = threadIdx.x; i < kQF * kQF; i += NT) {
+  const V* twst = reinterpret_cast<const V*>(a.tw_st);
+  for (int i = threadIdx.x; i < q; i += (int)blockDim.x) zq[i] = ldg(twM1 + (int64_t)i * M);
+  for (int i = threadIdx.x; i < kQF * kQF; i += (int)blockDim.x) {
     const int r = i / kQF, t = i % kQF;
     zt[i] = ldg(twM1 + (int64_t)((r * t) % q) * M);
   }
   __syncthreads();
 
+  // persistent loop over work items (batch entry b, line group g); the next item's
+  // input is prefetched into L2 by a TMA bulk prefetch while this one computes
+  const int64_t total = a.nbatch * a.ngroups;
+  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+  const int64_t g = a.batch_fastest ? w / a.nbatch : w % a.ngroups;
+  const int64_t b = a.batch_fastest ? w % a.nbatch : w / a.ngroups;
+  if (threadIdx.x == 0 && w + gridDim.x < total) {
+    const int64_t wn = w + gridDim.x;
+    const int64_t gn = a.batch_fastest ? wn / a.nbatch : wn % a.ngroups;
+    const int64_t bn = a.batch_fastest ? wn % a.nbatch : wn / a.ngroups;
+    if constexpr (MODE == MODE_CONV) {
+      for (int kk = 0; kk < a.npairs; ++kk) {
+        prefetch_lines<V>(a.in_f, kk, bn, gn, C, a.nlines);
+        prefetch_lines<V>(a.in_g, kk, bn, gn, C, a.nlines);
+      }
+    } else {
+      prefetch_lines<V>(a.in_f, MODE == MODE_FWD ? k_arr : 0, bn, gn, C, a.nlines);
+    }
+  }
   for (int r0 = 0; r0 < q; r0 += D) {
     const int nd = (q - r0) < D ? (q - r0) : D;
     if constexpr (MODE == MODE_FWD) {
       fold<V, M, NT>(bufF, a.in_f, k_arr, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
       __syncthreads();
-      fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, C * nd, twm);
-      fwd_last_store<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, clog, r0, nd, twm);
+      fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, C * nd, twst);
+      fwd_last_store<V, M, NT>(bufF, a.out, k_arr, b, g, a.nlines, C, clog, r0, nd, twst);
       __syncthreads();
     } else if constexpr (MODE == MODE_INV) {
-      inv_first_load<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, clog, r0, nd, twm);
+      inv_first_load<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, clog, r0, nd, twst);
       __syncthreads();
-      fft_inv_from<V, M, NT, NST - 2>(bufF, C * nd, twm);
+      fft_inv_from<V, M, NT, NST - 2>(bufF, C * nd, twst);
       unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
       __syncthreads();
     } else {
@@ -621,19 +737,20 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
         __syncthreads();
         // bufF and bufG are adjacent when the group is full: one sweep over both
         if (bufn == (int64_t)C * nd * M) {
-          fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, 2 * C * nd, twm);
+          fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, 2 * C * nd, twst);
         } else {
-          fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, C * nd, twm);
-          fft_fwd_range<V, M, NT, 0, NST - 1>(bufG, C * nd, twm);
+          fft_fwd_range<V, M, NT, 0, NST - 1>(bufF, C * nd, twst);
+          fft_fwd_range<V, M, NT, 0, NST - 1>(bufG, C * nd, twst);
         }
-        conv_mid<V, M, NT>(bufF, bufG, bufA, C * nd, kk, a.npairs, scale, twm);
+        conv_mid<V, M, NT>(bufF, bufG, bufA, C * nd, kk, a.npairs, scale, twst);
         __syncthreads();
       }
-      fft_inv_from<V, M, NT, NST - 2>(P, C * nd, twm);
+      fft_inv_from<V, M, NT, NST - 2>(P, C * nd, twst);
       unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
       __syncthreads();
     }
   }
+  }  // work items
 }
 
 // Materialise explicit zero padding: dst[b][i0][i1][i2] = src[..] inside L, else 0.

@@ -6,9 +6,11 @@
 
 namespace hd {
 struct PassArgs;
-using LaunchFn = cudaError_t (*)(const PassArgs&, dim3, size_t, cudaStream_t);
-// nullptr if (m, mode, threads) has no instantiation
+using LaunchFn = cudaError_t (*)(const PassArgs&, dim3, int, size_t, cudaStream_t);
+// nullptr if (m, mode) has no instantiation or threads exceeds every slice bound
 LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
+// warp-level m = 512 complex-double engine (hd_w512.cuh); blockDim = 32 q <= 288
+LaunchFn lookup_w512(int mode);
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],

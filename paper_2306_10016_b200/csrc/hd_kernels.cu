@@ -7,13 +7,17 @@
 namespace hd {
 
 LaunchFn lookup_f64_256(int m, int mode);
-LaunchFn lookup_f64_512(int m, int mode);
+LaunchFn lookup_f64_576(int m, int mode);
+LaunchFn lookup_f64_1024(int m, int mode);
 LaunchFn lookup_f32_256(int m, int mode);
-LaunchFn lookup_f32_512(int m, int mode);
+LaunchFn lookup_f32_576(int m, int mode);
+LaunchFn lookup_f32_1024(int m, int mode);
 
+// the slice with the smallest register bound that admits `threads`
 LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads) {
-  if (threads == 256) return is_double ? lookup_f64_256(m, mode) : lookup_f32_256(m, mode);
-  if (threads == 512) return is_double ? lookup_f64_512(m, mode) : lookup_f32_512(m, mode);
+  if (threads <= 256) return is_double ? lookup_f64_256(m, mode) : lookup_f32_256(m, mode);
+  if (threads <= 576) return is_double ? lookup_f64_576(m, mode) : lookup_f32_576(m, mode);
+  if (threads <= 1024) return is_double ? lookup_f64_1024(m, mode) : lookup_f32_1024(m, mode);
   return nullptr;
 }
 

@@ -1,5 +1,6 @@
-// hd_kernels.cuh -- launcher templates; each hd_k_<dtype>_<threads>.cu instantiates
-// one (precision, threads-per-CTA) slice so the slices compile in parallel.
+// hd_kernels.cuh -- launcher templates; each hd_k_<dtype>_<NT>.cu instantiates one
+// (precision, max threads-per-CTA) slice so the slices compile in parallel.  The
+// template NT only bounds registers (__launch_bounds__); the block size is runtime.
 #pragma once
 #include "hd_device.cuh"
 #include "hd_internal.h"
@@ -7,7 +8,7 @@
 namespace hd {
 
 template <typename T, int M, int NT, int MODE>
-static cudaError_t launch_pass_impl(const PassArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+static cudaError_t launch_pass_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   auto kern = pass_kernel<T, M, NT, MODE>;
   static size_t configured = 0;  // largest dynamic smem size already allowed
   if (smem > 48 * 1024 && smem > configured) {
@@ -15,7 +16,25 @@ static cudaError_t launch_pass_impl(const PassArgs& a, dim3 grid, size_t smem, c
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  kern<<<grid, NT, smem, st>>>(a);
+  if (nt < 32 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
+  // persistent grid: every SM gets as many CTAs as fit; grid.x work items are
+  // strided over them (grid.x on entry = total work items)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static int occ_nt = -1, occ_val = 1;
+  static size_t occ_smem = 0;
+  if (occ_nt != nt || occ_smem != smem) {
+    int nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem) != cudaSuccess || nb < 1) nb = 1;
+    occ_nt = nt; occ_smem = smem; occ_val = nb;
+  }
+  const int64_t cap = (int64_t)sms * occ_val;
+  if ((int64_t)grid.x > cap) grid.x = (unsigned)cap;
+  kern<<<grid, nt, smem, st>>>(a);
   return cudaGetLastError();
 }
 

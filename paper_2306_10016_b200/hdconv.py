@@ -23,6 +23,7 @@ HD_C64, HD_C128 = 1, 2
 HD_OK, HD_ERR_INVALID, HD_ERR_UNSUPPORTED, HD_ERR_CUDA, HD_ERR_NCCL, HD_ERR_WORKSPACE = range(6)
 HD_FLAG_ALLOW_ALIAS = 0x1
 HD_FLAG_SHARED_G = 0x2
+HD_FLAG_GENERIC_FFT = 0x4
 HD_TUNE_PER_AXIS = 0x0
 HD_TUNE_EXHAUSTIVE = 0x1
 HD_MAX_DIM = 3

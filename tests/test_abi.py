@@ -62,9 +62,11 @@ def test_plan_validation(H):
         H.hd_plan_complete(H.HD_C128, [10], [10], H.Plan.make(1, [{"m": 4, "D": 9}]))
     with pytest.raises(H.HDError):  # lines*D*m beyond shared memory
         H.hd_plan_complete(H.HD_C128, [4096], [4096], H.Plan.make(1, [{"m": 4096, "C": 4}]))
-    with pytest.raises(H.HDError):  # 3D needs equal S on axes 0, 1
+    with pytest.raises(H.HDError):  # tile width S must be a power of two <= 16
         H.hd_plan_complete(H.HD_C64, [8, 8, 8], [3, 3, 3],
-                           H.Plan.make(3, [{"m": 8, "S": 2}, {"m": 8, "S": 1}, {"m": 8}]))
+                           H.Plan.make(3, [{"m": 8, "S": 3}, {"m": 8, "S": 1}, {"m": 8}]))
+    with pytest.raises(H.HDError):  # threads must be a multiple of 32
+        H.hd_plan_complete(H.HD_C128, [10], [10], H.Plan.make(1, [{"m": 4, "threads": 100}]))
 
 
 def test_default_plans_are_admissible(H):

@@ -273,3 +273,29 @@ def test_tune_small(ctx, H):
     f, g = synth.random_pair(80, (200, 300), (31, 17))
     h = host(ctx.conv(dev(f), dev(g), plan=p))
     assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
+
+
+# ---------------------------------------------------------------- warp engine (m = 512)
+@pytest.mark.parametrize("shape", [((600, 700), (100, 90)), ((1000, 513), (255, 300))])
+def test_w512_engine_matches_oracle_and_generic(ctx, H, shape):
+    (sf, sg) = shape
+    f, g = synth.random_pair(90, sf, sg)
+    ref = oracle.conv(f, g)
+    axes = [{"m": 512, "C": 1, "S": 2}, {"m": 512, "C": 1, "S": 2}]
+    hw = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes)))
+    hg = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes, flags=H.HD_FLAG_GENERIC_FFT)))
+    assert oracle.rel_l2(hw, ref) < 1e-11
+    assert oracle.rel_l2(hg, ref) < 1e-11
+
+
+@pytest.mark.parametrize("L,q", [(512, 1), (1000, 2), (4000, 8), (4096, 9)])
+def test_w512_residues_match_generic(ctx, H, L, q):
+    x = synth.random_pair(L, (3, L), (1,))[0]
+    X = host(ctx.hd_forward_residues(dev(x), 512, q))
+    perm = H.hd_spectral_permutation(512)
+    full = [oracle.dft(x[l], q * 512, +1) for l in range(3)]
+    for l in range(3):
+        for r in range(q):
+            got = np.empty(512, complex)
+            got[perm] = X[l, r * 512:(r + 1) * 512]
+            assert oracle.rel_l2(got, full[l][r::q]) < 1e-12
