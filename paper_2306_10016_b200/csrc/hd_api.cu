@@ -178,6 +178,7 @@ hd_status_t get_w512_table(hd_ctx* ctx, const void** out) {
 struct AxisInfo {
   int64_t Lf, Lg, Lout, M, M1, O;  // O: output extent (Lout, or M1 if aliased)
   int m, q, pf, pg, T, C, S, D, lines, threads;
+  bool auto_engine;                // plan threads == 0: warp engine where it applies
 };
 
 // lines per CTA used by passes along axis i (the paper's C, "copies of the FFT
@@ -244,10 +245,10 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     if (a.D < 1 || a.D > x.q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
     x.D = a.D;
     if (a.D == 0) a.D = x.q;
-    if (a.threads == 0) a.threads = default_threads(lines_for(a, i, ndim), a.D, a.m);
-    if (!valid_threads(a.threads))
-      return fail(ctx, HD_ERR_INVALID, "threads must be a multiple of 32 in [32, 1024]");
-    x.threads = a.threads;
+    x.auto_engine = (a.threads == 0);
+    x.threads = a.threads ? a.threads : default_threads(lines_for(a, i, ndim), a.D, a.m);
+    if (!valid_threads(x.threads))
+      return fail(ctx, HD_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 1024]");
     x.lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
     if (pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
@@ -301,7 +302,7 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
     p.axis[i].D = bD;
     p.axis[i].C = lines;
     p.axis[i].S = (ndim == 1) ? 1 : 2;
-    p.axis[i].threads = default_threads(lines, bD, bm);
+    p.axis[i].threads = 0;  // automatic engine choice
   }
   *out = p;
   return HD_OK;
@@ -312,6 +313,7 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
 // ---------------------------------------------------------------------------
 struct Launch {
   uint32_t flags;
+  bool auto_engine;
   int mode;
   const char* name;
   PassArgs a;
@@ -327,6 +329,7 @@ void init_out(LineOut& o) { std::memset(&o, 0, sizeof(o)); o.nbi = 1; o.so_log2 
 // a short input of a single block (p_g = 1).
 bool use_w512(hd_dtype_t dt, const Launch& L) {
   if (dt != HD_C128 || L.m != 512 || L.lines != 1 || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
+  if (!L.auto_engine) return false;
   if (L.a.D != L.a.q || L.a.q > 9) return false;
   if (L.mode == hd::MODE_FWD) return L.a.in_f.p <= 8;
   if (L.mode == hd::MODE_CONV) return L.a.npairs == 1 && L.a.in_f.p <= 8 && L.a.in_g.p == 1;
@@ -448,6 +451,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   L.m = x.m;
   L.lines = x.lines;
   L.threads = x.threads;
+  L.auto_engine = x.auto_engine;
   L.nbuf = (mode == hd::MODE_CONV) ? conv_nbuf(P.N) : 1;
   init_in(L.a.in_f);
   init_in(L.a.in_g);
@@ -1002,6 +1006,7 @@ hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, 
   a.D = q;
   while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
   a.threads = default_threads(1, a.D, m);
+  a.auto_engine = true;
   const void *twm, *twM1;
   hd_status_t s = get_table(ctx, m, dbl, &twm);
   if (s != HD_OK) return s;
@@ -1036,6 +1041,7 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
   a.D = q;
   while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
   a.threads = default_threads(1, a.D, m);
+  a.auto_engine = true;
   const void *twm, *twM1;
   hd_status_t s = get_table(ctx, m, dbl, &twm);
   if (s != HD_OK) return s;
@@ -1127,7 +1133,7 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
       for (int D : Ds) {
         if (pass_smem(eb, q, C, D, m, nbuf) > hd::kMaxSmem) continue;
         const int dt = default_threads(C, D, m);
-        std::vector<int> ths = {dt};
+        std::vector<int> ths = {0, dt};  // 0: automatic engine (warp engine where it applies)
         if (dt != 256) ths.push_back(256);
         for (int S : Ss)
           for (int th : ths) out.push_back(AxisCand{m, C, S, D, th});

@@ -35,6 +35,6 @@ for _ in range(a.steps):
     elif len(fd) > 1:
         ctx.multiconv(fd, gd, plan=plan)
     else:
-        ctx.conv(fd[0], gd[0], plan=plan, batch=(nd == 1))
+        ctx.conv(fd[0], gd[0], plan=plan, batch=(nd == 1 and d["batch"] > 1))
 torch.cuda.synchronize()
 print("ok launches", ctx.launch_count())

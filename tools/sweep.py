@@ -34,12 +34,12 @@ dt = H.HD_C128 if fd[0].dtype == torch.complex128 else H.HD_C64
 Lf = list(d["f"][0].shape[-nd:])
 Lg = list(d["g"][0].shape[-nd:])
 Lout = [x + y - 1 for x, y in zip(Lf, Lg)]
-nout = int(np.prod(Lout)) * (d["batch"] if nd == 1 else 1)
+nout = int(np.prod(Lout)) * d["batch"]
 plans = [H.Plan.make(nd, p) for p in json.loads(a.plans)]
 if a.default:
     plans.insert(0, H.hd_plan_default(dt, Lf, Lg, npairs=N))
 if a.tune:
-    plans.append(ctx.tune(dt, Lf, Lg, N=N, batch=d["batch"] if nd == 1 else 1, reps=3))
+    plans.append(ctx.tune(dt, Lf, Lg, N=N, batch=d["batch"], reps=3))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
@@ -47,7 +47,7 @@ def run(p):
     if N > 1:
         ctx.multiconv(fd, gd, plan=p)
     else:
-        ctx.conv(fd[0], gd[0], plan=p, batch=(nd == 1))
+        ctx.conv(fd[0], gd[0], plan=p, batch=(nd == 1 and d["batch"] > 1))
 
 
 for p in plans:
