@@ -242,6 +242,12 @@ struct LineIn {            // element j of line l = g*C + c, batch b, array k:
   int32_t p;               // ceil(L/m) blocks (fold)
   int32_t tl;              // log2 line-tile width of the layout (>= 30: untiled, l*s_l)
 };
+// two-level batch offset with 32-bit division (batch indices < 2^31)
+__device__ __forceinline__ int64_t boff(int64_t b, int64_t nbi, int64_t s_bo, int64_t s_b) {
+  const uint32_t ub = (uint32_t)b, un = (uint32_t)nbi;
+  const uint32_t hi = ub / un;
+  return (int64_t)hi * s_bo + (int64_t)(ub - hi * un) * s_b;
+}
 __device__ __forceinline__ int64_t line_off(const LineIn& in, int64_t l) {
   if (in.tl >= 30) return l * in.s_l;
   return (l >> in.tl) * in.s_t + (l & ((int64_t(1) << in.tl) - 1)) * in.s_l;
@@ -292,12 +298,11 @@ __device__ __forceinline__ void fold_fast_one(V* buf, int cb, const V* xl, int64
                                               int s, bool live, int q, const V* zt,
                                               const V* __restrict__ twm, const V* __restrict__ twM1) {
   V u[P];
+  const V* xs = xl + (int64_t)s * s_j;
+  const int64_t step = (int64_t)M * s_j;
+  const int64_t rem = live ? L - s : 0;   // block t is valid while t*M < rem
 #pragma unroll
-  for (int t = 0; t < P; ++t) {
-    u[t] = cmk<V>(0, 0);
-    const int64_t j = (int64_t)t * M + s;
-    if (live && j < L) u[t] = xl[j * s_j];
-  }
+  for (int t = 0; t < P; ++t) u[t] = ((int64_t)t * M < rem) ? xs[t * step] : cmk<V>(0, 0);
   V a0 = u[0];
 #pragma unroll
   for (int t = 1; t < P; ++t) a0 = cadd(a0, u[t]);
@@ -336,15 +341,16 @@ template <typename V, int M, int NT>
 __device__ __forceinline__ void fold(V* buf, const LineIn& in, int k, int64_t b, int64_t g,
                                      int64_t nlines, int C, int clog, int r0, int nd, int q,
                                      const V* zq, const V* zt, const V* __restrict__ twm,
-                                     const V* __restrict__ twM1) {
+                                     const V* __restrict__ twM1, int tid = -1, int nth = 0) {
+  if (tid < 0) { tid = threadIdx.x; nth = blockDim.x; }
   using R = decltype(V::x);
-  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b;
+  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + boff(b, in.nbi, in.s_bo, in.s_b);
   const int items = C * M;
   const bool cfast = (in.s_j != 1);
   const int p = in.p;
   const int64_t L = in.L;
   const bool fast = (nd == q) && (q <= kQF) && (p <= kPF);
-  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
+  for (int it = tid; it < items; it += nth) {
     int c, s;
     if (cfast) { c = it & (C - 1); s = it >> clog; } else { s = it % M; c = it / M; }
     const bool live = (g * C + c) < nlines;
@@ -396,13 +402,13 @@ template <typename V, int M, int NT, int QM>
 __device__ __forceinline__ void unfold_fast(const V* buf, V* y, const LineOut& out, int64_t g,
                                             int64_t nlines, int C, int clog, int q,
                                             const V* zt, const V* __restrict__ twm,
-                                            const V* __restrict__ twM1) {
+                                            const V* __restrict__ twM1, int tid, int nth) {
   const int items = C * M;
   const int sl = out.so_log2;
   const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
-  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
+  for (int it = tid; it < items; it += nth) {
     const int s_lo = it & ((1 << so_l) - 1);
     const int rest = it >> so_l;
     const int c = rest & (C - 1);
@@ -453,20 +459,22 @@ template <typename V, int M, int NT>
 __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, int64_t b, int64_t g,
                                        int64_t nlines, int C, int clog, int r0, int nd, int q,
                                        bool accumulate, const V* zq, const V* zt,
-                                       const V* __restrict__ twm, const V* __restrict__ twM1) {
-  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b;
+                                       const V* __restrict__ twm, const V* __restrict__ twM1,
+                                       int tid = -1, int nth = 0) {
+  if (tid < 0) { tid = threadIdx.x; nth = blockDim.x; }
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + boff(b, out.nbi, out.s_bo, out.s_b);
   if (nd == q && !accumulate) {
-    if (q <= 4) { unfold_fast<V, M, NT, 4>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
-    if (q <= 8) { unfold_fast<V, M, NT, 8>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
-    if (q <= 12) { unfold_fast<V, M, NT, 12>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
-    if (q <= kQF) { unfold_fast<V, M, NT, kQF>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1); return; }
+    if (q <= 4) { unfold_fast<V, M, NT, 4>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1, tid, nth); return; }
+    if (q <= 8) { unfold_fast<V, M, NT, 8>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1, tid, nth); return; }
+    if (q <= 12) { unfold_fast<V, M, NT, 12>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1, tid, nth); return; }
+    if (q <= kQF) { unfold_fast<V, M, NT, kQF>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1, tid, nth); return; }
   }
   const int items = C * M;
   const int sl = out.so_log2;
   const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
-  for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
+  for (int it = tid; it < items; it += nth) {
     const int s_lo = it & ((1 << so_l) - 1);
     const int rest = it >> so_l;
     const int c = rest & (C - 1);
@@ -530,7 +538,7 @@ __device__ __forceinline__ void fwd_last_store(const V* buf, const LineOut& out,
   constexpr int ST = Sched<M>::NST - 1;
   using S = StageC<M, ST>;
   static_assert(S::SPAN == 1, "last stage has unit span");
-  V* y = reinterpret_cast<V*>(out.ptr[k]) + (b / out.nbi) * out.s_bo + (b % out.nbi) * out.s_b;
+  V* y = reinterpret_cast<V*>(out.ptr[k]) + boff(b, out.nbi, out.s_bo, out.s_b);
   const int sl = out.so_log2;
   const int items = C * nd * S::PER_ROW;
   for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
@@ -566,7 +574,7 @@ __device__ __forceinline__ void inv_first_load(V* buf, const LineIn& in, int64_t
                                                const V* __restrict__ twm) {
   constexpr int ST = Sched<M>::NST - 1;
   using S = StageC<M, ST>;
-  const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b;
+  const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b);
   const int items = C * nd * S::PER_ROW;
   const bool cfast = (in.s_j != 1);
   for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
@@ -631,6 +639,14 @@ __device__ __forceinline__ void conv_mid(V* bufF, const V* bufG, V* bufA, int nr
   }
 }
 
+// work item w -> (batch b, line group g) with 32-bit division
+__device__ __forceinline__ void split_item(int64_t w, int64_t nbatch, int64_t ngroups, int bf,
+                                           int64_t& b, int64_t& g) {
+  const uint32_t uw = (uint32_t)w;
+  if (bf) { const uint32_t n = (uint32_t)nbatch; const uint32_t hi = uw / n; g = hi; b = uw - hi * n; }
+  else { const uint32_t n = (uint32_t)ngroups; const uint32_t hi = uw / n; b = hi; g = uw - hi * n; }
+}
+
 // TMA bulk prefetch of [p, p + bytes) into L2 (UBLKPF); p 16-byte aligned.
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
@@ -645,7 +661,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
 template <typename V>
 __device__ __forceinline__ void prefetch_lines(const LineIn& in, int k, int64_t b, int64_t g, int C,
                                                int64_t nlines) {
-  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b;
+  const V* x = reinterpret_cast<const V*>(in.ptr[k]) + boff(b, in.nbi, in.s_bo, in.s_b);
   const int64_t l0 = g * C;
   const int64_t l1 = (l0 + C < nlines ? l0 + C : nlines) - 1;
   if (l1 < l0) return;
@@ -699,12 +715,11 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
   // input is prefetched into L2 by a TMA bulk prefetch while this one computes
   const int64_t total = a.nbatch * a.ngroups;
   for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-  const int64_t g = a.batch_fastest ? w / a.nbatch : w % a.ngroups;
-  const int64_t b = a.batch_fastest ? w % a.nbatch : w / a.ngroups;
+  int64_t g, b;
+  split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
   if (threadIdx.x == 0 && w + gridDim.x < total) {
-    const int64_t wn = w + gridDim.x;
-    const int64_t gn = a.batch_fastest ? wn / a.nbatch : wn % a.ngroups;
-    const int64_t bn = a.batch_fastest ? wn % a.nbatch : wn / a.ngroups;
+    int64_t gn, bn;
+    split_item(w + gridDim.x, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
     if constexpr (MODE == MODE_CONV) {
       for (int kk = 0; kk < a.npairs; ++kk) {
         prefetch_lines<V>(a.in_f, kk, bn, gn, C, a.nlines);

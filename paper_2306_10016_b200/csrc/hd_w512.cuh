@@ -198,12 +198,11 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
   V* Fr = F + r * M;  // this warp's residue row (also its exchange region)
   const int64_t total = a.nbatch * a.ngroups;
   for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const int64_t g = a.batch_fastest ? w / a.nbatch : w % a.ngroups;
-    const int64_t b = a.batch_fastest ? w % a.nbatch : w / a.ngroups;
+    int64_t g, b;
+    split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
     if (threadIdx.x == 0 && w + gridDim.x < total) {
-      const int64_t wn = w + gridDim.x;
-      const int64_t gn = a.batch_fastest ? wn / a.nbatch : wn % a.ngroups;
-      const int64_t bn = a.batch_fastest ? wn % a.nbatch : wn / a.ngroups;
+      int64_t gn, bn;
+      split_item(w + gridDim.x, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
       prefetch_lines<V>(a.in_f, MODE == MODE_FWD ? k_arr : 0, bn, gn, 1, a.nlines);
       if (MODE == MODE_CONV) prefetch_lines<V>(a.in_g, 0, bn, gn, 1, a.nlines);
     }
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
       fft_fwd(v, Fr, lane, w1l);
       if (live) {
         const LineOut& o = a.out;
-        V* y = reinterpret_cast<V*>(o.ptr[k_arr]) + (b / o.nbi) * o.s_bo + (b % o.nbi) * o.s_b +
+        V* y = reinterpret_cast<V*>(o.ptr[k_arr]) + boff(b, o.nbi, o.s_bo, o.s_b) +
                line_off(o, g);
         const int sl = o.so_log2;
         const int64_t k0 = (int64_t)r * M;
@@ -239,7 +238,7 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
     } else if constexpr (MODE == MODE_INV) {
       {
         const LineIn& in = a.in_f;
-        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b +
+        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b) +
                      line_off(in, g);
         V v[16];
         const int64_t k0 = (int64_t)r * M;
@@ -265,7 +264,7 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
       V v[16];
       {
         const LineIn& in = a.in_g;
-        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + (b / in.nbi) * in.s_bo + (b % in.nbi) * in.s_b +
+        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b) +
                      line_off(in, g);
         V wr = ldg(twM1 + (int64_t)r * lane);
         const V step = ldg(twM1 + (int64_t)r * 32);

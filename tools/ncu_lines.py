@@ -12,7 +12,11 @@ stall = defaultdict(float)
 inst = defaultdict(float)
 text = {}
 cur = None
+fname = ""
 for r in rows:
+    if r and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
     if r and r[0] == "Line No":
         hdr = r
         iS = hdr.index("Warp Stall Sampling (All Samples)")
@@ -21,7 +25,7 @@ for r in rows:
     if hdr is None or len(r) < len(hdr):
         continue
     if r[0]:
-        cur = int(r[0])
+        cur = (fname, int(r[0]))
         text[cur] = r[1]
     if cur is None:
         continue
@@ -32,4 +36,4 @@ for r in rows:
         pass
 ts, ti = sum(stall.values()) or 1, sum(inst.values()) or 1
 for ln in sorted(stall, key=lambda k: -stall[k])[:top]:
-    print(f"{100 * stall[ln] / ts:5.1f}% stall {100 * inst[ln] / ti:5.1f}% inst  L{ln:<5d} {text.get(ln, '').strip()[:100]}")
+    print(f"{100 * stall[ln] / ts:5.1f}% stall {100 * inst[ln] / ti:5.1f}% inst  {ln[0][:12]}:{ln[1]:<5d} {text.get(ln, '').strip()[:90]}")
