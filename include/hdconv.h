@@ -183,6 +183,47 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
                                  const void* X, int32_t m, int32_t q, void* x,
                                  int64_t Lout, void* stream);
 
+/* ---- one pass with explicit layouts (building block of the distributed paths) */
+/* A pass runs along ONE axis over `nlines` lines (x `nbatch` batch entries) of
+ * m-point residue transforms, exactly as one launch of the multi-pass pipeline:
+ *   HD_PASS_FWD : fold + forward FFT of every line of in_f (array k = 0..npairs-1)
+ *                 -> out (array k): q*m spectral values per line, internal order
+ *   HD_PASS_INV : inverse FFT + unfold of every spectral line of in_f -> out
+ *                 (out.L values per line; no 1/(qm) factor)
+ *   HD_PASS_CONV: fold + FFT of in_f[k] and in_g[k], sum_k product x scale,
+ *                 inverse FFT + unfold -> out (one array)
+ * Addressing (elements, not bytes), for line l (0..nlines-1) and element j:
+ *   ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b + line(l) + elem(j)
+ *   line(l) = tl < 30 ? (l >> tl)*s_t + (l & (2^tl-1))*s_l : l*s_l
+ *   elem(j) = jd > 0  ? (j / jd)*s_jt + (j % jd)*s_j       : j*s_j
+ * Inputs are zero beyond L; outputs write elements j < L only.  The plan axis
+ * gives m, C, D, threads; q = ceil(M/m) for the descriptor's M. */
+#define HD_PASS_FWD  0
+#define HD_PASS_INV  1
+#define HD_PASS_CONV 2
+typedef struct {
+  void* ptr[HD_MAX_PAIRS];
+  int64_t L;
+  int64_t nbi, s_bo, s_b;     /* nbi = 0: one batch level (nbi = nbatch) */
+  int32_t tl, pad_;
+  int64_t s_t, s_l;
+  int64_t jd, s_jt, s_j;
+} hd_lines_t;
+typedef struct {
+  int32_t mode;               /* HD_PASS_* */
+  int32_t npairs;             /* arrays (FWD/INV) or pairs (CONV), 1..16 */
+  int64_t nlines, nbatch;
+  int64_t M;                  /* padded length along this axis; q = ceil(M/m) */
+  hd_axis_plan_t axis;        /* m, C, D (0 = q), threads (0 = automatic) */
+  hd_lines_t in_f, in_g, out;
+  double scale;               /* CONV: product scale (1 / prod M1 over all axes) */
+  int32_t batch_fastest;      /* 1: consecutive CTAs take consecutive batch entries */
+  uint32_t flags;             /* HD_FLAG_GENERIC_FFT */
+} hd_pass_desc_t;
+/* Validate and launch one pass on `stream`.  Device pointers.  Returns
+ * HD_ERR_INVALID on bad sizes/layouts, HD_ERR_UNSUPPORTED if no kernel exists. */
+hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* desc, void* stream);
+
 /* ---- tuning (the paper's "experience") -------------------- */
 #define HD_TUNE_PER_AXIS   0x0u   /* search each axis independently */
 #define HD_TUNE_EXHAUSTIVE 0x1u   /* full cross product (grid search A0) */

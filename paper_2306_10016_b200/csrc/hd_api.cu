@@ -1095,6 +1095,100 @@ hd_status_t hd_profile_reset(hd_ctx_t ctx) {
 
 int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
+static bool conv_lines_in(const hd_lines_t& d, LineIn& in, int64_t nbatch, int n, bool need_ptr) {
+  for (int k = 0; k < n; ++k) {
+    if (need_ptr && !d.ptr[k]) return false;
+    in.ptr[k] = d.ptr[k];
+  }
+  if (d.L < 1) return false;
+  in.L = d.L;
+  in.nbi = d.nbi > 0 ? d.nbi : nbatch;
+  in.s_bo = d.s_bo; in.s_b = d.s_b;
+  in.tl = d.tl; in.s_t = d.s_t; in.s_l = d.s_l;
+  in.jd = d.jd > 0 ? d.jd : 0; in.s_jt = d.s_jt; in.s_j = d.s_j;
+  return true;
+}
+static bool conv_lines_out(const hd_lines_t& d, LineOut& o, int64_t nbatch, int n) {
+  for (int k = 0; k < n; ++k) {
+    if (!d.ptr[k]) return false;
+    o.ptr[k] = d.ptr[k];
+  }
+  if (d.L < 1) return false;
+  o.L = d.L;
+  o.nbi = d.nbi > 0 ? d.nbi : nbatch;
+  o.s_bo = d.s_bo; o.s_b = d.s_b;
+  o.tl = d.tl; o.s_t = d.s_t; o.s_l = d.s_l;
+  if (d.jd > 0 && is_pow2(d.jd) && d.jd < (int64_t(1) << 29)) {
+    o.so_log2 = ilog2(d.jd); o.jd = 0;
+  } else if (d.jd > 0) {
+    if (d.jd > 0x7fffffff) return false;
+    o.so_log2 = 40; o.jd = d.jd;
+  } else {
+    o.so_log2 = 40; o.jd = 0;
+  }
+  o.s_jt = d.s_jt; o.s_js = d.s_j;
+  return true;
+}
+
+hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, void* stream) {
+  if (!ctx || !d) return fail(ctx, HD_ERR_INVALID, "null argument");
+  if (dtype != HD_C64 && dtype != HD_C128) return fail(ctx, HD_ERR_INVALID, "bad dtype");
+  if (d->mode < HD_PASS_FWD || d->mode > HD_PASS_CONV) return fail(ctx, HD_ERR_INVALID, "bad pass mode");
+  if (d->npairs < 1 || d->npairs > HD_MAX_PAIRS) return fail(ctx, HD_ERR_INVALID, "npairs must be in [1, 16]");
+  if (d->nlines < 1 || d->nbatch < 1 || d->M < 1) return fail(ctx, HD_ERR_INVALID, "nlines, nbatch, M must be >= 1");
+  const hd_axis_plan_t& ap = d->axis;
+  if (!is_pow2(ap.m) || ap.m < 2 || ap.m > 4096) return fail(ctx, HD_ERR_INVALID, "m must be a power of two in [2, 4096]");
+  const int C = ap.C ? ap.C : 1;
+  if (!valid_lines(C)) return fail(ctx, HD_ERR_INVALID, "C must be 1, 2, 4, 8 or 16");
+  const int q = (int)cdiv(d->M, ap.m);
+  const int D = ap.D ? ap.D : q;
+  if (D < 1 || D > q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
+  if (ap.threads && !valid_threads(ap.threads)) return fail(ctx, HD_ERR_INVALID, "bad threads");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const bool dbl = dtype == HD_C128;
+  const int64_t M1 = (int64_t)q * ap.m;
+  const void *twm, *twM1, *twst;
+  hd_status_t s = get_table(ctx, ap.m, dbl, &twm);
+  if (s != HD_OK) return s;
+  s = get_table(ctx, M1, dbl, &twM1);
+  if (s != HD_OK) return s;
+  s = get_stage_table(ctx, ap.m, dbl, &twst);
+  if (s != HD_OK) return s;
+  Launch L;
+  std::memset(&L, 0, sizeof(L));
+  L.flags = d->flags;
+  L.mode = d->mode;
+  L.name = d->mode == HD_PASS_FWD ? "pass_fwd" : (d->mode == HD_PASS_INV ? "pass_inv" : "pass_conv");
+  L.m = ap.m;
+  L.lines = C;
+  L.threads = ap.threads ? ap.threads : default_threads(C, D, ap.m);
+  L.auto_engine = ap.threads == 0;
+  L.nbuf = d->mode == HD_PASS_CONV ? conv_nbuf(d->npairs) : 1;
+  init_in(L.a.in_f);
+  init_in(L.a.in_g);
+  init_out(L.a.out);
+  const int narr = d->mode == HD_PASS_CONV ? d->npairs : (d->mode == HD_PASS_FWD ? d->npairs : 1);
+  if (!conv_lines_in(d->in_f, L.a.in_f, d->nbatch, narr, true))
+    return fail(ctx, HD_ERR_INVALID, "bad in_f description");
+  if (d->mode == HD_PASS_CONV && !conv_lines_in(d->in_g, L.a.in_g, d->nbatch, narr, true))
+    return fail(ctx, HD_ERR_INVALID, "bad in_g description");
+  if (!conv_lines_out(d->out, L.a.out, d->nbatch, d->mode == HD_PASS_FWD ? narr : 1))
+    return fail(ctx, HD_ERR_INVALID, "bad out description");
+  L.a.in_f.p = (int)cdiv(L.a.in_f.L, ap.m);
+  L.a.in_g.p = (int)cdiv(L.a.in_g.L, ap.m);
+  L.a.out.T = (int)cdiv(std::min<int64_t>(L.a.out.L, M1), ap.m);
+  if (d->mode != HD_PASS_FWD && L.a.out.L > M1) return fail(ctx, HD_ERR_INVALID, "out.L exceeds q*m");
+  L.a.tw_m = twm; L.a.tw_M1 = twM1; L.a.tw_st = twst;
+  L.a.q = q; L.a.D = D; L.a.C = C; L.a.c_log2 = ilog2(C); L.a.M1 = M1;
+  L.a.npairs = d->mode == HD_PASS_CONV ? d->npairs : 1;
+  L.a.scale = d->mode == HD_PASS_CONV ? d->scale : 1.0;
+  L.a.nlines = d->nlines; L.a.nbatch = d->nbatch; L.a.batch_fastest = d->batch_fastest ? 1 : 0;
+  L.narrays = d->mode == HD_PASS_FWD ? narr : 1;
+  L.ngroups = cdiv(d->nlines, C); L.nbatch = d->nbatch;
+  return launch(ctx, dtype, L, (cudaStream_t)stream);
+}
+
 }  // extern "C"
 
 // ===========================================================================

@@ -241,7 +241,14 @@ struct LineIn {            // element j of line l = g*C + c, batch b, array k:
   int64_t s_b, s_t, s_l, s_j;
   int32_t p;               // ceil(L/m) blocks (fold)
   int32_t tl;              // log2 line-tile width of the layout (>= 30: untiled, l*s_l)
+  int64_t jd, s_jt;        // element tiling: jd > 0: j -> (j / jd)*s_jt + (j % jd)*s_j
 };
+// offset of element j of an input line
+__device__ __forceinline__ int64_t in_el(const LineIn& in, int64_t j) {
+  if (in.jd <= 0) return j * in.s_j;
+  const int64_t hi = j / in.jd;
+  return hi * in.s_jt + (j - hi * in.jd) * in.s_j;
+}
 // two-level batch offset with 32-bit division (batch indices < 2^31)
 __device__ __forceinline__ int64_t boff(int64_t b, int64_t nbi, int64_t s_bo, int64_t s_b) {
   const uint32_t ub = (uint32_t)b, un = (uint32_t)nbi;
@@ -261,7 +268,10 @@ struct LineOut {           // element j of line l = g*C + c: ptr[k] + (b/nbi)*s_
   int32_t T;               // output blocks ceil(L/m) (unfold)
   int32_t tl;              // log2 line-tile width (>= 30: untiled)
   int32_t pad_;
+  int64_t jd;              // > 0: element j -> (j / jd)*s_jt + (j % jd)*s_js (overrides so_log2)
 };
+// element-axis tile code for jt_off: log2 tile (0..29), plain (>= 30), or -width (general)
+__device__ __forceinline__ int out_sl(const LineOut& o) { return o.jd > 0 ? -(int)o.jd : o.so_log2; }
 __device__ __forceinline__ int64_t line_off(const LineOut& o, int64_t l) {
   if (o.tl >= 30) return l * o.s_l;
   return (l >> o.tl) * o.s_t + (l & ((int64_t(1) << o.tl) - 1)) * o.s_l;
@@ -289,20 +299,34 @@ constexpr int kPF = 8;     // fast fold path: p <= 8
 
 __device__ __forceinline__ int64_t jt_off(int64_t j, int sl, int64_t s_jt, int64_t s_js) {
   if (sl >= 30) return j * s_js;
+  if (sl < 0) {  // general tile width -sl (division)
+    const int64_t hi = j / (-sl);
+    return hi * s_jt + (j + hi * sl) * s_js;
+  }
   return (j >> sl) * s_jt + (j & ((int64_t(1) << sl) - 1)) * s_js;
 }
 
 // One (line, s) of the fast fold: P = compile-time bound on p (<= 8)
 template <typename V, int M, int P>
-__device__ __forceinline__ void fold_fast_one(V* buf, int cb, const V* xl, int64_t s_j, int64_t L,
+__device__ __forceinline__ void fold_fast_one(V* buf, int cb, const V* xl, int64_t s_j, int64_t jd,
+                                              int64_t s_jt, int64_t L,
                                               int s, bool live, int q, const V* zt,
                                               const V* __restrict__ twm, const V* __restrict__ twM1) {
   V u[P];
-  const V* xs = xl + (int64_t)s * s_j;
-  const int64_t step = (int64_t)M * s_j;
   const int64_t rem = live ? L - s : 0;   // block t is valid while t*M < rem
+  if (jd <= 0) {
+    const V* xs = xl + (int64_t)s * s_j;
+    const int64_t step = (int64_t)M * s_j;
 #pragma unroll
-  for (int t = 0; t < P; ++t) u[t] = ((int64_t)t * M < rem) ? xs[t * step] : cmk<V>(0, 0);
+    for (int t = 0; t < P; ++t) u[t] = ((int64_t)t * M < rem) ? xs[t * step] : cmk<V>(0, 0);
+  } else {
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const int64_t j = (int64_t)t * M + s;
+      const int64_t hi = j / jd;
+      u[t] = ((int64_t)t * M < rem) ? xl[hi * s_jt + (j - hi * jd) * s_j] : cmk<V>(0, 0);
+    }
+  }
   V a0 = u[0];
 #pragma unroll
   for (int t = 1; t < P; ++t) a0 = cadd(a0, u[t]);
@@ -357,10 +381,10 @@ __device__ __forceinline__ void fold(V* buf, const LineIn& in, int k, int64_t b,
     const V* xl = x + line_off(in, g * C + c);
     const int cb = c * nd * M;  // swizzle indices are relative to buf
     if (fast) {
-      if (p <= 1) fold_fast_one<V, M, 1>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
-      else if (p <= 2) fold_fast_one<V, M, 2>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
-      else if (p <= 4) fold_fast_one<V, M, 4>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
-      else fold_fast_one<V, M, kPF>(buf, cb, xl, in.s_j, L, s, live, q, zt, twm, twM1);
+      if (p <= 1) fold_fast_one<V, M, 1>(buf, cb, xl, in.s_j, in.jd, in.s_jt, L, s, live, q, zt, twm, twM1);
+      else if (p <= 2) fold_fast_one<V, M, 2>(buf, cb, xl, in.s_j, in.jd, in.s_jt, L, s, live, q, zt, twm, twM1);
+      else if (p <= 4) fold_fast_one<V, M, 4>(buf, cb, xl, in.s_j, in.jd, in.s_jt, L, s, live, q, zt, twm, twM1);
+      else fold_fast_one<V, M, kPF>(buf, cb, xl, in.s_j, in.jd, in.s_jt, L, s, live, q, zt, twm, twM1);
     } else {
       for (int d0 = 0; d0 < nd; d0 += kFoldChunk) {
         V acc[kFoldChunk];
@@ -371,7 +395,7 @@ __device__ __forceinline__ void fold(V* buf, const LineIn& in, int k, int64_t b,
           for (int t = 0; t < p; ++t) {
             const int64_t j = (int64_t)t * M + s;
             if (j >= L) break;
-            const V u = xl[j * in.s_j];
+            const V u = xl[in_el(in, j)];
 #pragma unroll
             for (int d = 0; d < kFoldChunk; ++d) {
               if (d0 + d < nd) {
@@ -404,8 +428,8 @@ __device__ __forceinline__ void unfold_fast(const V* buf, V* y, const LineOut& o
                                             const V* zt, const V* __restrict__ twm,
                                             const V* __restrict__ twM1, int tid, int nth) {
   const int items = C * M;
-  const int sl = out.so_log2;
-  const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
+  const int sl = out_sl(out);
+  const int so_l = (sl >= 0 && sl < 30) ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
   for (int it = tid; it < items; it += nth) {
@@ -470,8 +494,8 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
     if (q <= kQF) { unfold_fast<V, M, NT, kQF>(buf, y, out, g, nlines, C, clog, q, zt, twm, twM1, tid, nth); return; }
   }
   const int items = C * M;
-  const int sl = out.so_log2;
-  const int so_l = sl < 30 ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
+  const int sl = out_sl(out);
+  const int so_l = (sl >= 0 && sl < 30) ? (sl < Sched<M>::LOG ? sl : Sched<M>::LOG) : Sched<M>::LOG;
   const int64_t L = out.L;
   const int T = out.T;
   for (int it = tid; it < items; it += nth) {
@@ -539,7 +563,7 @@ __device__ __forceinline__ void fwd_last_store(const V* buf, const LineOut& out,
   using S = StageC<M, ST>;
   static_assert(S::SPAN == 1, "last stage has unit span");
   V* y = reinterpret_cast<V*>(out.ptr[k]) + boff(b, out.nbi, out.s_bo, out.s_b);
-  const int sl = out.so_log2;
+  const int sl = out_sl(out);
   const int items = C * nd * S::PER_ROW;
   for (int it = threadIdx.x; it < items; it += (int)blockDim.x) {
     const int c = it & (C - 1);
@@ -595,7 +619,7 @@ __device__ __forceinline__ void inv_first_load(V* buf, const LineIn& in, int64_t
     const bool live = (g * C + c) < nlines;
     const V* xl = x + line_off(in, g * C + c);
 #pragma unroll
-    for (int i = 0; i < S::R; ++i) v[i] = live ? xl[(k0 + i) * in.s_j] : cmk<V>(0, 0);
+    for (int i = 0; i < S::R; ++i) v[i] = live ? xl[in_el(in, k0 + i)] : cmk<V>(0, 0);
     dit_bfly<V, M, ST>(v, 0, twm);
     const int base = (c * nd + d) * M + w * S::R;
 #pragma unroll

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
         const LineOut& o = a.out;
         V* y = reinterpret_cast<V*>(o.ptr[k_arr]) + boff(b, o.nbi, o.s_bo, o.s_b) +
                line_off(o, g);
-        const int sl = o.so_log2;
+        const int sl = out_sl(o);
         const int64_t k0 = (int64_t)r * M;
         if (sl >= 1 && sl < 30 && o.s_js == 1) {
           // positions pos(f) and pos(f)+1 = pos(f+64): registers k2 and k2+4, k2 in {0..3, 8..11}
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
         const int64_t k0 = (int64_t)r * M;
 #pragma unroll
         for (int k2 = 0; k2 < 16; ++k2)
-          v[k2] = live ? x[(k0 + pos_of_freq(freq_of(lane, k2))) * in.s_j] : cmk<V>(0, 0);
+          v[k2] = live ? x[in_el(in, k0 + pos_of_freq(freq_of(lane, k2)))] : cmk<V>(0, 0);
         fft_inv(v, Fr, lane, w1l);
         __syncwarp();
 #pragma unroll
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int s = lane + 32 * i;
-          const V u = (live && s < in.L) ? x[(int64_t)s * in.s_j] : cmk<V>(0, 0);
+          const V u = (live && s < in.L) ? x[in_el(in, s)] : cmk<V>(0, 0);
           v[i] = cmul(u, wr);
           wr = cmul(wr, step);
         }

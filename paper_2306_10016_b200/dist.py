@@ -1,0 +1,210 @@
+"""Multi-GPU hybrid-dealiased 2D convolution by slab decomposition.
+
+SURVEY §8(e): rank k holds a contiguous slab of f's rows (g is replicated);
+  1. forward along x of the local rows (pass A)       -> X[dest][kx_local][y_local]
+  2. all-to-all (exchange 1): rank k' receives the spectral columns of its slab
+  3. convolution along y of the local columns (pass B) -> Y[dest][kx_local][yo_local]
+  4. all-to-all (exchange 2): rank k receives its output rows for every column
+  5. inverse along x of the local output rows (pass C) -> h rows
+Every arithmetic step runs in libhdconv.so (`hd_pass`); this module only computes
+partitions and layouts (plain integers) and calls the caller's all-to-all, which is
+`torch.distributed.all_to_all_single` (NCCL over NVLink) in production.  The
+layouts make every per-destination block contiguous, so the exchange needs no
+packing.  The partition/exchange logic is shared with a CPU test backend
+(tests/test_dist_gloo.py) that runs it on 2 gloo ranks.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+
+def cdiv(a, b):
+    return -(-a // b)
+
+
+@dataclass
+class SlabPlan2D:
+    """Partition of a 2D problem f [Lf0][Lf1] * g [Lg0][Lg1] over `world` ranks.
+    Kx = M1 along x (spectral columns), Oy/Ox the output extents."""
+    world: int
+    Lf: tuple
+    Lg: tuple
+    Kx: int
+
+    def __post_init__(self):
+        self.Oy = self.Lf[0] + self.Lg[0] - 1
+        self.Ox = self.Lf[1] + self.Lg[1] - 1
+        self.R = cdiv(self.Lf[0], self.world)     # f rows per rank
+        self.Ro = cdiv(self.Oy, self.world)       # output rows per rank
+        self.Ks = cdiv(self.Kx, self.world)       # spectral columns per rank
+
+    def rows(self, k):
+        return k * self.R, min((k + 1) * self.R, self.Lf[0])
+
+    def out_rows(self, k):
+        return min(k * self.Ro, self.Oy), min((k + 1) * self.Ro, self.Oy)
+
+    def cols(self, k):
+        return min(k * self.Ks, self.Kx), min((k + 1) * self.Ks, self.Kx)
+
+    # element counts of the exchange buffers (all per-destination blocks equal)
+    @property
+    def x_block(self):
+        return self.Ks * self.R
+
+    @property
+    def y_block(self):
+        return self.Ks * self.Ro
+
+    def bytes_sent_per_rank(self, elem_bytes):
+        """Bytes leaving one rank in the two exchanges (block to itself excluded)."""
+        return (self.world - 1) * (self.x_block + self.y_block) * elem_bytes
+
+
+class SlabConv2D:
+    """Slab-decomposed 2D convolution on one rank of `world`.
+
+    backend: object with
+      fwd_rows(x_rows, nrows, Lx, out, plan)            pass A on local rows
+      fwd_full(g, out)                                   pass A on the replicated g
+      conv_cols(xrecv, xg, ncols, col0, out, plan)       pass B on local columns
+      inv_rows(yrecv, nrows, out_rows, plan)             pass C on local output rows
+      empty(n) -> buffer of n complex elements
+    exchange(send, recv, block): all-to-all of `world` equal blocks of `block` elements.
+    """
+
+    def __init__(self, backend, exchange, world, rank, Lf, Lg, Kx):
+        self.b = backend
+        self.exchange = exchange
+        self.rank = rank
+        self.plan = SlabPlan2D(world, tuple(Lf), tuple(Lg), Kx)
+
+    # the three compute stages between the two exchanges
+    def stage1(self, f_rows, g):
+        P, k, b = self.plan, self.rank, self.b
+        r0, r1 = P.rows(k)
+        xsend = b.empty(P.world * P.x_block)
+        b.fwd_rows(f_rows, r1 - r0, xsend, P)
+        xg = b.empty(P.Kx * P.Lg[0])
+        b.fwd_full(g, xg, P)
+        return xsend, xg
+
+    def stage2(self, xrecv, xg):
+        P, k, b = self.plan, self.rank, self.b
+        c0, c1 = P.cols(k)
+        ysend = b.empty(P.world * P.y_block)
+        b.conv_cols(xrecv, xg, c1 - c0, c0, ysend, P)
+        return ysend
+
+    def stage3(self, yrecv):
+        P, k = self.plan, self.rank
+        o0, o1 = P.out_rows(k)
+        return self.b.inv_rows(yrecv, o1 - o0, P)
+
+    def __call__(self, f_rows, g):
+        P, b = self.plan, self.b
+        xsend, xg = self.stage1(f_rows, g)
+        xrecv = b.empty(P.world * P.x_block)
+        self.exchange(xsend, xrecv, P.x_block)
+        ysend = self.stage2(xrecv, xg)
+        yrecv = b.empty(P.world * P.y_block)
+        self.exchange(ysend, yrecv, P.y_block)
+        return self.stage3(yrecv)
+
+
+def emulate_ranks(convs, f, g, empty):
+    """Run `world` SlabConv2D instances in one process (test/validation tool): the
+    all-to-all is replaced by block copies between the ranks' buffers."""
+    world = len(convs)
+    P = convs[0].plan
+    xs = []
+    for k, c in enumerate(convs):
+        r0, r1 = P.rows(k)
+        xs.append(c.stage1(f[r0:r1], g))
+    def a2a(sends, block):
+        recvs = [empty(world * block) for _ in range(world)]
+        for src in range(world):
+            for dst in range(world):
+                recvs[dst][src * block:(src + 1) * block] = sends[src][dst * block:(dst + 1) * block]
+        return recvs
+    xr = a2a([x for x, _ in xs], P.x_block)
+    ys = [c.stage2(xr[k], xs[k][1]) for k, c in enumerate(convs)]
+    yr = a2a(ys, P.y_block)
+    return [c.stage3(yr[k]) for k, c in enumerate(convs)]
+
+
+class GpuBackend:
+    """Passes on libhdconv.so through hd_pass descriptors (device tensors)."""
+
+    def __init__(self, ctx, plan, dtype):
+        import torch
+        from . import hdconv as H
+        self.H, self.torch, self.ctx = H, torch, ctx
+        self.dt = dtype
+        self.tdt = torch.complex128 if dtype == H.HD_C128 else torch.complex64
+        p = plan.as_dict()["axis"]
+        self.ax = p           # [y, x] completed axis plans (m, q, M1, C, D, threads)
+        self.scale = 1.0 / (p[0]["M1"] * p[1]["M1"])
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, n):
+        return self.torch.empty(max(1, n), dtype=self.tdt, device=self.dev)
+
+    def _desc(self, mode, axis, nlines, M):
+        H = self.H
+        d = H.PassDesc()
+        d.mode, d.npairs, d.nlines, d.nbatch, d.M = mode, 1, nlines, 1, M
+        a = self.ax[axis]
+        d.axis.m, d.axis.C, d.axis.D, d.axis.threads = a["m"], 1, 0, 0
+        return d
+
+    def fwd_rows(self, f_rows, nrows, out, P):
+        if nrows <= 0:
+            return
+        H = self.H
+        d = self._desc(H.HD_PASS_FWD, 1, nrows, self.ax[1]["M1"])
+        d.in_f = H.Lines.make([f_rows.data_ptr()], P.Lf[1], s_l=P.Lf[1])
+        # element kx of local row y -> (kx / Ks)*(Ks*R) + (kx % Ks)*R + y
+        d.out = H.Lines.make([out.data_ptr()], P.Kx, s_l=1, s_j=P.R, jd=P.Ks, s_jt=P.Ks * P.R)
+        self.ctx.hd_pass(self.dt, d)
+
+    def fwd_full(self, g, out, P):
+        H = self.H
+        d = self._desc(H.HD_PASS_FWD, 1, P.Lg[0], self.ax[1]["M1"])
+        d.in_f = H.Lines.make([g.data_ptr()], P.Lg[1], s_l=P.Lg[1])
+        d.out = H.Lines.make([out.data_ptr()], P.Kx, s_l=1, s_j=P.Lg[0])   # X_g[kx][y]
+        self.ctx.hd_pass(self.dt, d)
+
+    def conv_cols(self, xrecv, xg, ncols, col0, out, P):
+        if ncols <= 0:
+            return
+        H = self.H
+        d = self._desc(H.HD_PASS_CONV, 0, ncols, self.ax[0]["M1"])
+        d.in_f = H.Lines.make([xrecv.data_ptr()], P.Lf[0], s_l=P.R, s_j=1, jd=P.R, s_jt=P.Ks * P.R)
+        eb = xg.element_size()
+        d.in_g = H.Lines.make([xg.data_ptr() + col0 * P.Lg[0] * eb], P.Lg[0], s_l=P.Lg[0])
+        d.out = H.Lines.make([out.data_ptr()], P.Oy, s_l=P.Ro, s_j=1, jd=P.Ro, s_jt=P.Ks * P.Ro)
+        d.scale = self.scale
+        self.ctx.hd_pass(self.dt, d)
+
+    def inv_rows(self, yrecv, nrows, P):
+        h = self.torch.empty((max(nrows, 0), P.Ox), dtype=self.tdt, device=self.dev)
+        if nrows <= 0:
+            return h
+        H = self.H
+        d = self._desc(H.HD_PASS_INV, 1, nrows, self.ax[1]["M1"])
+        d.in_f = H.Lines.make([yrecv.data_ptr()], P.Kx, s_l=1, s_j=P.Ro, jd=P.Ks, s_jt=P.Ks * P.Ro)
+        d.out = H.Lines.make([h.data_ptr()], P.Ox, s_l=P.Ox)
+        self.ctx.hd_pass(self.dt, d)
+        return h
+
+
+def torch_exchange(group=None):
+    """all-to-all of equal contiguous blocks with torch.distributed (NCCL on GPU)."""
+    import torch.distributed as dist
+
+    def ex(send, recv, block):
+        n = dist.get_world_size(group)
+        dist.all_to_all_single(recv[: n * block], send[: n * block], group=group)
+    return ex

@@ -37,8 +37,9 @@ EXPORTED = [
     "hd_plan_complete", "hd_spectral_permutation", "hd_workspace_bytes", "hd_conv1d",
     "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_log",
-    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count",
+    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_pass",
 ]
+HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
 
 
 class AxisPlan(ctypes.Structure):
@@ -69,6 +70,32 @@ class Plan(ctypes.Structure):
             p.axis[i].D = int(a.get("D", 0))
             p.axis[i].threads = int(a.get("threads", 0))
         return p
+
+
+class Lines(ctypes.Structure):
+    """hd_lines_t: element j of line l, batch b, array k at
+    ptr[k] + (b/nbi)*s_bo + (b%nbi)*s_b + line(l) + elem(j) (see include/hdconv.h)."""
+    _fields_ = [("ptr", ctypes.c_void_p * HD_MAX_PAIRS), ("L", ctypes.c_int64),
+                ("nbi", ctypes.c_int64), ("s_bo", ctypes.c_int64), ("s_b", ctypes.c_int64),
+                ("tl", ctypes.c_int32), ("pad_", ctypes.c_int32), ("s_t", ctypes.c_int64),
+                ("s_l", ctypes.c_int64), ("jd", ctypes.c_int64), ("s_jt", ctypes.c_int64),
+                ("s_j", ctypes.c_int64)]
+
+    @staticmethod
+    def make(ptrs, L, s_l, s_j=1, jd=0, s_jt=0, s_b=0, nbi=0, s_bo=0, tl=40, s_t=0):
+        d = Lines()
+        for k, q in enumerate(ptrs):
+            d.ptr[k] = q
+        d.L, d.s_l, d.s_j, d.jd, d.s_jt = L, s_l, s_j, jd, s_jt
+        d.s_b, d.nbi, d.s_bo, d.tl, d.s_t = s_b, nbi, s_bo, tl, s_t
+        return d
+
+
+class PassDesc(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("npairs", ctypes.c_int32), ("nlines", ctypes.c_int64),
+                ("nbatch", ctypes.c_int64), ("M", ctypes.c_int64), ("axis", AxisPlan),
+                ("in_f", Lines), ("in_g", Lines), ("out", Lines), ("scale", ctypes.c_double),
+                ("batch_fastest", ctypes.c_int32), ("flags", ctypes.c_uint32)]
 
 
 class HDError(RuntimeError):
@@ -107,6 +134,7 @@ def _load():
         "hd_profile_read": ([P, I32, P, P, P], I32),
         "hd_profile_reset": ([P], ctypes.c_int),
         "hd_launch_count": ([P], I64),
+        "hd_pass": ([P, ctypes.c_int, ctypes.POINTER(PassDesc), P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -372,3 +400,7 @@ class Context:
 
     def launch_count(self):
         return int(_lib.hd_launch_count(self.h))
+
+    def hd_pass(self, dtype, desc, stream=None):
+        """One pass with explicit layouts (include/hdconv.h hd_pass)."""
+        self._chk(_lib.hd_pass(self.h, dtype, ctypes.byref(desc), _stream_ptr(stream)))

@@ -299,3 +299,21 @@ def test_w512_residues_match_generic(ctx, H, L, q):
             got = np.empty(512, complex)
             got[perm] = X[l, r * 512:(r + 1) * 512]
             assert oracle.rel_l2(got, full[l][r::q]) < 1e-12
+
+
+# ---------------------------------------------------------------- slab decomposition (hd_pass)
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("shape,m", [(((300, 260), (31, 17)), 64), (((1100, 700), (255, 60)), 512)])
+def test_slab_decomposition_emulated_ranks(ctx, H, world, shape, m):
+    """The multi-GPU slab path's kernels (hd_pass with the exchange layouts), with the
+    NCCL all-to-all replaced by device block copies between emulated ranks."""
+    from paper_2306_10016_b200.dist import GpuBackend, SlabConv2D, emulate_ranks
+    (Lf, Lg) = shape
+    f, g = synth.random_pair(400 + world, Lf, Lg)
+    plan = H.hd_plan_complete(H.HD_C128, list(Lf), list(Lg), H.Plan.make(2, [{"m": m}, {"m": m}]))
+    Kx = plan.axis[1].M1
+    be = GpuBackend(ctx, plan, H.HD_C128)
+    convs = [SlabConv2D(be, None, world, k, Lf, Lg, Kx) for k in range(world)]
+    parts = emulate_ranks(convs, dev(f), dev(g), be.empty)
+    h = np.concatenate([host(p) for p in parts], axis=0)
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
