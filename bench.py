@@ -260,8 +260,24 @@ def run_ours(args, rank, world, local_rank):
         plan = ctx.default_plan(dtc, Lf, Lg, npairs=N)
     plan = H.hd_plan_complete(dtc, Lf, Lg, plan, npairs=N)
 
+    slab = None
+    if args.mode == "slab":
+        if ndim != 2 or N != 1:
+            raise SystemExit("--mode slab: 2D single-pair configs only")
+        from paper_2306_10016_b200.dist import GpuBackend, SlabConv2D, torch_exchange
+
+        def local_exchange(send, recv, block):
+            recv[:block].copy_(send[:block])
+        be = GpuBackend(ctx, plan, dtc)
+        slab = SlabConv2D(be, torch_exchange() if dist else local_exchange, world, rank, Lf, Lg,
+                          plan.axis[1].M1)
+        r0, r1 = slab.plan.rows(rank)
+        f_local = fd[0][r0:r1].contiguous()
+
     def step():
-        if N > 1:
+        if slab is not None:
+            slab(f_local, gd[0])
+        elif N > 1:
             ctx.multiconv(fd, gd, plan=plan, h=hd_)
         else:
             ctx.conv(fd[0], gd[0], plan=plan, h=hd_, batch=(ndim == 1 and batch > 1))
@@ -302,7 +318,8 @@ def run_ours(args, rank, world, local_rank):
         ms = float(tt.item())
     clk = clocks.stop()
     samples_per_step = batch * int(np.prod(Lout))
-    value = world * samples_per_step * args.steps / (ms * 1e-3)
+    # weak: every rank convolves its own problem; strong (slab): one problem over all ranks
+    value = (1 if slab is not None else world) * samples_per_step * args.steps / (ms * 1e-3)
 
     # roofline of the dominant kernel (largest share of the step)
     peak, peak_src = peaks()
@@ -325,7 +342,7 @@ def run_ours(args, rank, world, local_rank):
 
     # end to end through the host-buffer C-ABI entry point (copies inside)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and slab is None:
         hh = torch.empty(out_shape, dtype=fd[0].dtype).pin_memory()
         k2 = max(2, min(args.steps, 10))
         ctx.hd_conv_host(fh, gh, hh, ndim=ndim, batch=batch, plan=plan)
@@ -345,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
 
     # explicit-padding GPU variant from the same kernels (context)
     explicit = None
-    if not args.no_explicit and ndim >= 2:
+    if not args.no_explicit and ndim >= 2 and slab is None:
         try:
             ctx.hd_conv_explicit(fd, gd, plan=plan, h=hd_)
             torch.cuda.synchronize()
@@ -372,11 +389,14 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if eb == 16 else "f32",
+            "scaling": "strong" if slab is not None else "weak", "vs_baseline": None,
+            "dtype": "f64" if eb == 16 else "f32",
             "data": "synthetic",
             "config": {"workload": name, "Lf": Lf, "Lg": Lg, "Lout": Lout, "pairs": N, "batch": batch,
                        "plan": [{k: v for k, v in a.items()} for a in plan.as_dict()["axis"]],
-                       "tune_seconds": tune_s, "parallelism": f"weak x{world} (independent problems)",
+                       "tune_seconds": tune_s,
+                       "parallelism": (f"slab x{world} (rows; NCCL all-to-all transposes)" if slab is not None
+                                       else f"weak x{world} (independent problems)"),
                        "l2": "inputs larger than L2 (image 268 MB > 126 MB L2); no flush needed"},
             "roofline": roof, "whole_step": whole, "cpu_baseline": cpu, "e2e": e2e,
             "explicit_variant": explicit, "gpu_launches": int(launches), "clocks": clk,
@@ -401,6 +421,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-explicit", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", default="independent", choices=["independent", "slab"],
+                    help="N>1: independent problems per rank (weak) or one slab-decomposed problem (strong)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))

@@ -34,6 +34,8 @@ struct hd_ctx {
   void* ws = nullptr;
   size_t ws_size = 0;
   void* io = nullptr;                   // device buffers for hd_conv_host
+  void* scratch = nullptr;              // warp-engine F-hat parking
+  size_t scratch_size = 0;
   size_t io_size = 0;
   std::map<std::string, hd_plan_t> plan_cache;
   std::vector<std::pair<hd_plan_t, double>> tune_log;
@@ -346,6 +348,21 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     threads = 32 * L.a.q;
     smem = 16 * (size_t)(round_slots(L.a.q, 16) + round_slots(hd::kQF * hd::kQF, 16) +
                          round_slots((int64_t)L.a.q * 512, 16));
+    if (L.mode == hd::MODE_CONV) {
+      // F-hat parking: one q*512 block per persistent CTA (<= 4 CTAs per SM)
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const size_t need = (size_t)sms * 4 * L.a.q * 512 * 16;
+      if (ctx->scratch_size < need) {
+        if (ctx->scratch) cudaFree(ctx->scratch);
+        ctx->scratch = nullptr; ctx->scratch_size = 0;
+        cudaError_t e = cudaMalloc(&ctx->scratch, need);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(scratch)");
+        ctx->scratch_size = need;
+      }
+      L.a.scratch = ctx->scratch;
+    }
     const void* tw1;
     hd_status_t s = get_w512_table(ctx, &tw1);
     if (s != HD_OK) return s;
@@ -763,6 +780,7 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   if (ctx->w512tw) cudaFree(ctx->w512tw);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
+  if (ctx->scratch) cudaFree(ctx->scratch);
   for (auto& p : ctx->prof)
     for (auto& ev : p.pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
   delete ctx;

@@ -282,6 +282,7 @@ struct PassArgs {
   const void* tw_m;        // zeta_m^k,  k < m
   const void* tw_M1;       // zeta_M1^k, k < M1
   const void* tw_st;       // stage twiddle table of m (see StageOff)
+  void* scratch;           // warp engine CONV: per-CTA F-hat parking (gridDim.x * q * m)
   int64_t nlines;          // lines per batch entry
   int64_t nbatch;
   int64_t ngroups;         // line groups per batch entry (work items = nbatch * ngroups)

@@ -27,7 +27,8 @@ static cudaError_t launch_w512_impl(const PassArgs& a, dim3 grid, int nt, size_t
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem) != cudaSuccess || nb < 1) nb = 1;
     occ_nt = nt; occ_smem = smem; occ_val = nb;
   }
-  const int64_t cap = (int64_t)sms * occ_val;
+  // CONV parks F-hat in a scratch sized for <= 4 CTAs per SM (hd_api.cu)
+  const int64_t cap = (int64_t)sms * (MODE == MODE_CONV ? (occ_val < 4 ? occ_val : 4) : occ_val);
   if ((int64_t)grid.x > cap) grid.x = (unsigned)cap;
   kern<<<grid, nt, smem, st>>>(a);
   return cudaGetLastError();

@@ -173,7 +173,7 @@ __device__ __forceinline__ void fft_inv(V* a, V* E, int lane, V w1l) {
 // exchange area; in CONV the F-hat spectrum stays in registers while G is transformed)
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(288, 2) w512_kernel(const __grid_constant__ PassArgs a) {
   constexpr int M = 512;
   constexpr int EPR = 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
   V* zq = smem;
   V* zt = zq + round_slots<EPR>(q);
   V* F = zt + round_slots<EPR>(kQF * kQF);
+  // CONV: per-CTA global scratch (L2-resident) where each warp parks its F-hat
+  V* Fh = MODE == MODE_CONV ? reinterpret_cast<V*>(a.scratch) + ((int64_t)blockIdx.x * q + (threadIdx.x >> 5)) * M
+                            : nullptr;
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
   const V w1l = ldg(twm + lane);  // zeta_512^{lane}: seeds this lane's L1 twiddles
@@ -256,16 +259,17 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
     } else {
       fold<V, M, 512>(F, a.in_f, 0, b, g, a.nlines, 1, 0, 0, q, q, zq, zt, twm, twM1);
       __syncthreads();
-      V fh[16];  // F-hat stays in registers
-#pragma unroll
-      for (int i = 0; i < 16; ++i) fh[i] = Fr[swz<V>(r * M + lane + 32 * i) - r * M];
-      fft_fwd(fh, Fr, lane, w1l);
-      // short input g: p_g == 1, fold in registers: w[s] = g[s] zeta_{M1}^{r s}, s = lane + 32 i
       V v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = Fr[swz<V>(r * M + lane + 32 * i) - r * M];
+      fft_fwd(v, Fr, lane, w1l);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) Fh[lane + 32 * k] = v[k];  // F-hat parked in L2 scratch
+      // short input g: p_g == 1, fold in registers: w[s] = g[s] zeta_{M1}^{r s}, s = lane + 32 i
       {
         const LineIn& in = a.in_g;
-        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b) +
-                     line_off(in, g);
+        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g);
         V wr = ldg(twM1 + (int64_t)r * lane);
         const V step = ldg(twM1 + (int64_t)r * 32);
 #pragma unroll
@@ -276,11 +280,11 @@ __global__ void __launch_bounds__(288, MODE == MODE_CONV ? 1 : 2) w512_kernel(co
           wr = cmul(wr, step);
         }
       }
-      fft_fwd(v, Fr, lane, w1l);  // F's exchange reads are complete (fft_fwd syncs the warp)
+      fft_fwd(v, Fr, lane, w1l);   // G's transform reuses this warp's SMEM row
       {
         const double sc = a.scale;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = cscale(cmul(fh[k], v[k]), sc);  // (1/prod M1) F-hat G-hat
+        for (int k = 0; k < 16; ++k) v[k] = cscale(cmul(Fh[lane + 32 * k], v[k]), sc);  // (1/prod M1) F-hat G-hat
       }
       fft_inv(v, Fr, lane, w1l);
       __syncwarp();
