@@ -15,8 +15,8 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhdconv.so")
 BUILD = os.path.join(HERE, "csrc", "build")
-SOURCES = ["hd_kernels.cu", "hd_api.cu", "hd_k_w512.cu"] + [f"hd_k_{d}_{n}.cu" for d in ("f64", "f32") for n in (256, 576, 1024)]
-HEADERS = ["hd_device.cuh", "hd_internal.h", "hd_kernels.cuh", "hd_w512.cuh"]
+SOURCES = ["hd_kernels.cu", "hd_api.cu", "hd_k_s512.cu"] + [f"hd_k_{d}_{n}.cu" for d in ("f64", "f32") for n in (256, 576, 1024)]
+HEADERS = ["hd_device.cuh", "hd_internal.h", "hd_kernels.cuh", "hd_w512.cuh", "hd_s512.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-I" + INCLUDE, "-I" + CSRC]
@@ -28,8 +28,27 @@ def _newest_input() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
+def _deps(path: str, seen: set | None = None) -> set:
+    """Transitive local #include "..." dependencies of a source file."""
+    seen = set() if seen is None else seen
+    for line in open(path):
+        line = line.strip()
+        if line.startswith("#include \""):
+            name = line.split("\"")[1]
+            for d in (CSRC, INCLUDE):
+                f = os.path.join(d, name)
+                if os.path.exists(f) and f not in seen:
+                    seen.add(f)
+                    _deps(f, seen)
+    return seen
+
+
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+    path = os.path.join(CSRC, src)
+    newest = max(os.path.getmtime(f) for f in _deps(path) | {path, os.path.abspath(__file__)})
+    if os.path.exists(obj) and os.path.getmtime(obj) >= newest:
+        return obj
     cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -6,6 +6,8 @@
 #include "hd_device.cuh"
 #include "hd_internal.h"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -30,12 +32,9 @@ struct hd_ctx {
   std::mutex mu;
   std::map<int64_t, void*> tw64, tw32;  // N -> device zeta_N^k tables
   std::map<int64_t, void*> st64, st32;  // m -> device stage twiddle tables
-  void* w512tw = nullptr;               // [15][32] zeta_512^{t j} for the warp engine
   void* ws = nullptr;
   size_t ws_size = 0;
   void* io = nullptr;                   // device buffers for hd_conv_host
-  void* scratch = nullptr;              // warp-engine F-hat parking
-  size_t scratch_size = 0;
   size_t io_size = 0;
   std::map<std::string, hd_plan_t> plan_cache;
   std::vector<std::pair<hd_plan_t, double>> tune_log;
@@ -149,28 +148,6 @@ hd_status_t get_stage_table(hd_ctx* ctx, int m, bool dbl, const void** out) {
   if (e != cudaSuccess) { cudaFree(d); return cuda_fail(ctx, e, "cudaMemcpy(stage twiddles)"); }
   cache[m] = d;
   *out = d;
-  return HD_OK;
-}
-
-// [15][32] table zeta_512^{t j}, j = 1..15, t < 32 (warp engine, hd_w512.cuh)
-hd_status_t get_w512_table(hd_ctx* ctx, const void** out) {
-  if (!ctx->w512tw) {
-    std::vector<double> full, tab;
-    host_twiddles(512, full);
-    for (int j = 1; j < 16; ++j)
-      for (int t = 0; t < 32; ++t) {
-        const int e = (t * j) % 512;
-        tab.push_back(full[2 * e]);
-        tab.push_back(full[2 * e + 1]);
-      }
-    void* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, tab.size() * sizeof(double));
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(w512 twiddles)");
-    e = cudaMemcpy(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) { cudaFree(d); return cuda_fail(ctx, e, "cudaMemcpy(w512 twiddles)"); }
-    ctx->w512tw = d;
-  }
-  *out = ctx->w512tw;
   return HD_OK;
 }
 
@@ -316,6 +293,7 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
 struct Launch {
   uint32_t flags;
   bool auto_engine;
+  bool s512_axis;   // the staged engine may run this pass (same engine for every pass of the axis)
   int mode;
   const char* name;
   PassArgs a;
@@ -326,13 +304,132 @@ struct Launch {
 void init_in(LineIn& in) { std::memset(&in, 0, sizeof(in)); in.nbi = 1; }
 void init_out(LineOut& o) { std::memset(&o, 0, sizeof(o)); o.nbi = 1; o.so_log2 = 0; }
 
-// The warp-level m = 512 engine applies to one line per CTA, all residues at once
-// (D = q <= 9), the fast fold (p <= 8) and, for the convolution pass, one pair with
-// a short input of a single block (p_g = 1).
-bool use_w512(hd_dtype_t dt, const Launch& L) {
+// ---------------------------------------------------------------------------
+// TMA descriptions of line families for the staged engine (hd_s512.cuh).
+// A line family is described by LineIn / LineOut; the kernel moves whole lines
+// in boxes of 256 elements (tensor maps) or one bulk copy (plain rows).
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// dims (innermost first, complex values as 2 doubles): {d0 doubles, d1, d2, nbi, nbo};
+// strides in elements of 16 B for dims 1..4 (0 = broadcast dimension of size 1)
+bool encode_lines(CUtensorMap* map, const void* base, const uint64_t dims[5], const int64_t strides[4],
+                  const uint32_t box[5]) {
+  auto enc = tensor_map_encoder();
+  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t gd[5];
+  cuuint64_t gs[4];
+  cuuint32_t bx[5], es[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) { gd[i] = dims[i] ? dims[i] : 1; bx[i] = box[i]; }
+  for (int i = 0; i < 4; ++i) {
+    if (strides[i] < 0) return false;
+    gs[i] = strides[i] > 0 ? (cuuint64_t)strides[i] * 16 : 16;
+    if (strides[i] == 0) gd[i + 1] = 1;
+    if (gs[i] >= (cuuint64_t(1) << 40)) return false;
+  }
+  for (int i = 0; i < 5; ++i) if (gd[i] > 0xffffffffull) return false;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), gd, gs, bx, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// input lines -> TMA_BULK (plain rows) or TMA_LINE_TILED (lines tiled by S, element stride s_j)
+bool tma_desc_in(const LineIn& in, int64_t nlines, int64_t nbatch, int narr, hd::TmaLine& t,
+                 CUtensorMap* maps) {
+  t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = in.nbi > 0 ? in.nbi : 1;
+  t.bcast = (in.s_b == 0 ? 1 : 0) | (in.s_bo == 0 ? 2 : 0);
+  if (in.jd > 0 || narr > hd::kTmaArrays) return false;
+  if (in.tl >= 30) {
+    if (in.s_j != 1) return false;
+    t.kind = hd::TMA_BULK;
+    return true;
+  }
+  if (in.s_l != 1) return false;
+  const int64_t S = int64_t(1) << in.tl;
+  const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)in.L, (uint64_t)ceil_div64(nlines, S), (uint64_t)t.nbi,
+                            (uint64_t)ceil_div64(nbatch, t.nbi)};
+  const int64_t str[4] = {in.s_j, in.s_t, in.s_b, in.s_bo};
+  const uint32_t box[5] = {2, 256, 1, 1, 1};
+  for (int k = 0; k < narr; ++k)
+    if (!encode_lines(&maps[k], in.ptr[k], dims, str, box)) return false;
+  t.kind = hd::TMA_LINE_TILED; t.slog = in.tl;
+  return true;
+}
+
+// output lines -> TMA_BULK (plain rows), TMA_ELEM_TILED (element axis tiled by S <= 16)
+// or TMA_LINE_TILED (lines tiled by S, element stride s_js)
+bool tma_desc_out(const LineOut& o, int64_t nlines, int64_t nbatch, int narr, hd::TmaLine& t,
+                  CUtensorMap* maps) {
+  t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = o.nbi > 0 ? o.nbi : 1;
+  t.bcast = (o.s_b == 0 ? 1 : 0) | (o.s_bo == 0 ? 2 : 0);
+  if (o.jd > 0 || narr > hd::kTmaArrays) return false;
+  const int64_t nbo = ceil_div64(nbatch, t.nbi);
+  if (o.tl >= 30 && o.so_log2 >= 30) {
+    if (o.s_js != 1) return false;
+    t.kind = hd::TMA_BULK;
+    return true;
+  }
+  if (o.tl >= 30) {
+    if (o.s_js != 1 || o.so_log2 > 4) return false;
+    const int64_t S = int64_t(1) << o.so_log2;
+    const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)nlines, (uint64_t)ceil_div64(o.L, S), (uint64_t)t.nbi,
+                              (uint64_t)nbo};
+    const int64_t str[4] = {o.s_l, o.s_jt, o.s_b, o.s_bo};
+    const uint32_t box[5] = {(uint32_t)(2 * S), 1, (uint32_t)(256 / S), 1, 1};
+    for (int k = 0; k < narr; ++k)
+      if (!encode_lines(&maps[k], o.ptr[k], dims, str, box)) return false;
+    t.kind = hd::TMA_ELEM_TILED; t.slog = o.so_log2;
+    return true;
+  }
+  if (o.so_log2 < 30 || o.s_l != 1) return false;
+  const int64_t S = int64_t(1) << o.tl;
+  const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)o.L, (uint64_t)ceil_div64(nlines, S), (uint64_t)t.nbi,
+                            (uint64_t)nbo};
+  const int64_t str[4] = {o.s_js, o.s_t, o.s_b, o.s_bo};
+  const uint32_t box[5] = {2, 256, 1, 1, 1};
+  for (int k = 0; k < narr; ++k)
+    if (!encode_lines(&maps[k], o.ptr[k], dims, str, box)) return false;
+  t.kind = hd::TMA_LINE_TILED; t.slog = o.tl;
+  return true;
+}
+
+// Fill the staged engine's TMA descriptions of a launch (falls back to per-thread
+// copies for anything a tensor map cannot express).
+void prepare_tma(Launch& L) {
+  PassArgs& a = L.a;
+  const int narr_in = L.mode == hd::MODE_FWD ? (int)L.narrays : 1;
+  const int narr_out = L.mode == hd::MODE_FWD ? (int)L.narrays : 1;
+  if (!tma_desc_in(a.in_f, a.nlines, a.nbatch, narr_in, a.tm_in, a.tm_in_map)) a.tm_in.kind = hd::TMA_NONE;
+  if (L.mode == hd::MODE_CONV) {
+    // both inputs of the convolution pass move by TMA or both by per-thread copies
+    if (!tma_desc_in(a.in_g, a.nlines, a.nbatch, 1, a.tm_in_g, &a.tm_in_g_map) || a.tm_in.kind == hd::TMA_NONE) {
+      a.tm_in.kind = hd::TMA_NONE; a.tm_in_g.kind = hd::TMA_NONE;
+    }
+  }
+  if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map)) a.tm_out.kind = hd::TMA_NONE;
+}
+
+// The staged warp engine (m = 512, hd_s512.cuh) applies to one line per CTA, all
+// residues at once (D = q <= 12), the fast fold (p <= 8) and, for the convolution
+// pass, one pair with a short input of a single block (p_g = 1).
+bool use_s512(hd_dtype_t dt, const Launch& L) {
   if (dt != HD_C128 || L.m != 512 || L.lines != 1 || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
-  if (!L.auto_engine) return false;
-  if (L.a.D != L.a.q || L.a.q > 9) return false;
+  if (!L.auto_engine || !L.s512_axis) return false;
+  if (L.a.D != L.a.q || L.a.q > hd::kS512QMax) return false;
   if (L.mode == hd::MODE_FWD) return L.a.in_f.p <= 8;
   if (L.mode == hd::MODE_CONV) return L.a.npairs == 1 && L.a.in_f.p <= 8 && L.a.in_g.p == 1;
   return true;
@@ -343,30 +440,11 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   hd::LaunchFn fn;
   size_t smem;
   int threads = L.threads;
-  if (use_w512(dt, L)) {
-    fn = hd::lookup_w512(L.mode);
+  if (use_s512(dt, L)) {
+    fn = hd::lookup_s512(L.mode, L.a.q);
     threads = 32 * L.a.q;
-    smem = 16 * (size_t)(round_slots(L.a.q, 16) + round_slots(hd::kQF * hd::kQF, 16) +
-                         round_slots((int64_t)L.a.q * 512, 16));
-    if (L.mode == hd::MODE_CONV) {
-      // F-hat parking: one q*512 block per persistent CTA (<= 4 CTAs per SM)
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const size_t need = (size_t)sms * 4 * L.a.q * 512 * 16;
-      if (ctx->scratch_size < need) {
-        if (ctx->scratch) cudaFree(ctx->scratch);
-        ctx->scratch = nullptr; ctx->scratch_size = 0;
-        cudaError_t e = cudaMalloc(&ctx->scratch, need);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(scratch)");
-        ctx->scratch_size = need;
-      }
-      L.a.scratch = ctx->scratch;
-    }
-    const void* tw1;
-    hd_status_t s = get_w512_table(ctx, &tw1);
-    if (s != HD_OK) return s;
-    L.a.tw_st = tw1;
+    smem = hd::s512_smem_bytes(L.a.q, L.mode);
+    prepare_tma(L);
   } else {
     fn = hd::lookup_launcher(dbl, L.m, L.mode, L.threads);
     smem = pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf);
@@ -412,8 +490,22 @@ struct Problem {
   const void* g[HD_MAX_PAIRS] = {};
   void* h = nullptr;
   AxisInfo ax[HD_MAX_DIM] = {};
+  bool s512[HD_MAX_DIM] = {};  // every pass along axis i may run on the staged m = 512 engine
   hd_plan_t plan{};
 };
+
+// One engine per axis: the staged engine's spectral order (lane-major) differs from
+// the generic engine's, so the forward and inverse passes of an axis must agree.
+// The convolution axis (0) has a single pass, so only that pass's conditions matter.
+void choose_engines(Problem& P) {
+  for (int i = 0; i < P.ndim; ++i) {
+    const AxisInfo& x = P.ax[i];
+    bool ok = P.dt == HD_C128 && x.m == 512 && x.lines == 1 && x.auto_engine && x.D == x.q &&
+              x.q <= hd::kS512QMax && !(P.plan.flags & HD_FLAG_GENERIC_FFT);
+    if (i > 0) ok = ok && x.pf <= 8 && x.pg <= 8;
+    P.s512[i] = ok;
+  }
+}
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
@@ -469,6 +561,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   L.lines = x.lines;
   L.threads = x.threads;
   L.auto_engine = x.auto_engine;
+  L.s512_axis = P.s512[axis];
   L.nbuf = (mode == hd::MODE_CONV) ? conv_nbuf(P.N) : 1;
   init_in(L.a.in_f);
   init_in(L.a.in_g);
@@ -743,6 +836,7 @@ hd_status_t setup(hd_ctx* ctx, Problem& P, hd_dtype_t dt, int ndim, int N, int64
   hd_status_t s = complete_plan(ctx, dt, ndim, N, Lf, Lg, M, &pl, P.ax);
   if (s != HD_OK) return s;
   P.plan = pl;
+  choose_engines(P);
   return HD_OK;
 }
 
@@ -777,10 +871,8 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   for (auto& kv : ctx->tw32) cudaFree(kv.second);
   for (auto& kv : ctx->st64) cudaFree(kv.second);
   for (auto& kv : ctx->st32) cudaFree(kv.second);
-  if (ctx->w512tw) cudaFree(ctx->w512tw);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
-  if (ctx->scratch) cudaFree(ctx->scratch);
   for (auto& p : ctx->prof)
     for (auto& ev : p.pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
   delete ctx;
@@ -1178,6 +1270,7 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   L.flags = d->flags;
   L.mode = d->mode;
   L.name = d->mode == HD_PASS_FWD ? "pass_fwd" : (d->mode == HD_PASS_INV ? "pass_inv" : "pass_conv");
+  L.s512_axis = d->mode == HD_PASS_CONV;  // fwd/inv keep the documented spectral order
   L.m = ap.m;
   L.lines = C;
   L.threads = ap.threads ? ap.threads : default_threads(C, D, ap.m);

@@ -17,6 +17,7 @@
 // Shared memory holds complex values in an XOR-swizzled layout so that both the
 // unit-stride and the radix-strided butterfly accesses are bank-conflict free.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -276,13 +277,27 @@ __device__ __forceinline__ int64_t line_off(const LineOut& o, int64_t l) {
   if (o.tl >= 30) return l * o.s_l;
   return (l >> o.tl) * o.s_t + (l & ((int64_t(1) << o.tl) - 1)) * o.s_l;
 }
+// TMA description of a family of lines (hd_s512.cuh; host side: hd_api.cu tma_desc_*)
+enum { TMA_NONE = 0, TMA_BULK = 1, TMA_LINE_TILED = 2, TMA_ELEM_TILED = 3 };
+struct TmaLine {
+  int32_t kind;            // TMA_NONE: per-thread copies; TMA_BULK: one 1-D bulk copy per line
+  int32_t slog;            // log2 of the tile width S (LINE_TILED: lines, ELEM_TILED: elements)
+  int32_t bcast;           // bit 0 / bit 1: batch dimension 3 / 4 has stride 0 (coordinate 0)
+  int32_t pad_;
+  int64_t nbi;             // two-level batch split (coordinates b % nbi, b / nbi)
+};
+constexpr int kTmaArrays = 6;  // arrays (multiconv pairs) with their own tensor maps
+
 struct PassArgs {
   LineIn in_f, in_g;
   LineOut out;
+  TmaLine tm_in, tm_in_g, tm_out;
+  CUtensorMap tm_in_map[kTmaArrays];
+  CUtensorMap tm_in_g_map;
+  CUtensorMap tm_out_map[kTmaArrays];
   const void* tw_m;        // zeta_m^k,  k < m
   const void* tw_M1;       // zeta_M1^k, k < M1
   const void* tw_st;       // stage twiddle table of m (see StageOff)
-  void* scratch;           // warp engine CONV: per-CTA F-hat parking (gridDim.x * q * m)
   int64_t nlines;          // lines per batch entry
   int64_t nbatch;
   int64_t ngroups;         // line groups per batch entry (work items = nbatch * ngroups)

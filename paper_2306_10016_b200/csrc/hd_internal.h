@@ -9,8 +9,10 @@ struct PassArgs;
 using LaunchFn = cudaError_t (*)(const PassArgs&, dim3, int, size_t, cudaStream_t);
 // nullptr if (m, mode) has no instantiation or threads exceeds every slice bound
 LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
-// warp-level m = 512 complex-double engine (hd_w512.cuh); blockDim = 32 q <= 288
-LaunchFn lookup_w512(int mode);
+// staged warp engine for m = 512 complex double (hd_s512.cuh); blockDim = 32 q <= 384
+LaunchFn lookup_s512(int mode, int q);
+constexpr int kS512QMax = 12;
+size_t s512_smem_bytes(int q, int mode);
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],

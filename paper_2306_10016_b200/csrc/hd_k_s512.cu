@@ -1,0 +1,51 @@
+// hd_k_s512.cu -- launchers of the staged m = 512 warp engine (hd_s512.cuh):
+// one persistent CTA per SM (two-stage cp.async ring, ~170 KB of shared memory),
+// blockDim = 32 q.
+#include "hd_internal.h"
+#include "hd_s512.cuh"
+
+namespace hd {
+
+template <int MODE, int NTMAX, int QC>
+static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
+  auto kern = s512::s512_kernel<MODE, NTMAX, QC>;
+  static size_t configured = 0;  // per instantiation
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (nt < 32 || nt > NTMAX || nt % 32) return cudaErrorInvalidConfiguration;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if ((int64_t)grid.x > sms) grid.x = (unsigned)sms;
+  kern<<<grid, nt, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// q = 9 (the BASELINE 2-D configs' axes) has a compile-time-q instantiation; other
+// q <= 9 get a 288-thread bound (up to 168 registers), q <= 12 a 384-thread bound.
+template <int MODE>
+static LaunchFn pick_s512(int q) {
+  if (q == 9) return launch_s512_impl<MODE, 288, 9>;
+  if (q < 9) return launch_s512_impl<MODE, 288, 0>;
+  return launch_s512_impl<MODE, 32 * s512::kQMax, 0>;
+}
+LaunchFn lookup_s512(int mode, int q) {
+  switch (mode) {
+    case MODE_FWD: return pick_s512<MODE_FWD>(q);
+    case MODE_INV: return pick_s512<MODE_INV>(q);
+    case MODE_CONV: return pick_s512<MODE_CONV>(q);
+    default: return nullptr;
+  }
+}
+
+size_t s512_smem_bytes(int q, int mode) {
+  return 128 + sizeof(double2) * (size_t)(kQF * kQF + 2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));
+}
+
+}  // namespace hd

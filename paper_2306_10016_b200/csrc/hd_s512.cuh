@@ -1,0 +1,456 @@
+// hd_s512.cuh -- staged warp engine for FFT size m = 512 (complex double).
+//
+// One persistent CTA per SM, one line per work item, q warps (warp r owns residue
+// r; blockDim = 32 q, q <= 12).  Lines move between HBM and a two-stage shared
+// memory ring by TMA: strided / tiled lines as 5-D tensor boxes of 256 elements
+// (cp.async.bulk.tensor, zero fill past the line end), plain rows as one 1-D bulk
+// copy; loads complete on an mbarrier, stores are bulk-async groups.  The next
+// item's loads are issued once the current item's first step is done, so they
+// overlap its FFTs and unfold.  Every step works in place on the stage:
+//
+//   stage [t][s] = x[t m + s]        (TMA load, rows t < p; the rest unread)
+//   fold     thread s:  w_r[s] = zeta_{qm}^{rs} sum_{t<p} zeta_q^{rt} x[tm+s]
+//            (Forward Eq. PAPER.md:528; Alg. Forward)   -> row r
+//   FFT      warp r: size-512 FFT of row r in registers (hd_w512.cuh)
+//   FWD      spectrum -> row r in lane-major order (position k2*32 + lane holds
+//            frequency freq_of(lane, k2)) -> TMA store of the line
+//   CONV     G's transform (short input, p_g = 1), product (1/prod M1) F G
+//            (PAPER.md:190-192), inverse FFT in registers -> row r
+//   INV      row r (lane-major spectrum) -> inverse FFT -> row r
+//   unfold   thread s: h[tm+s] = sum_r zeta_q^{-tr} zeta_{qm}^{-rs} V_r[s], t < T
+//            (Backward Eq. PAPER.md:531; Alg. Backward) -> stage
+//            [t][s] in place -> TMA store of the output line
+//
+// The lane-major spectral order is internal to the x (and 3-D y) passes of one
+// axis; hd_api.cu runs every pass of an axis on the same engine.
+#pragma once
+#include <cuda.h>
+
+#include "hd_internal.h"
+#include "hd_w512.cuh"
+#include "hd_zq_table.h"
+
+namespace hd {
+namespace s512 {
+
+using V = double2;
+constexpr int M = 512;
+constexpr int kQMax = kS512QMax;  // two stages of (q + 1) * 8 KB fit in 227 KB
+constexpr int kBox = 256;         // elements per TMA box
+
+// ---------------------------------------------------------------------------
+// TMA / mbarrier / bulk-copy primitives (PTX)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" :: "r"(su32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load(V* dst, const CUtensorMap* map, const int* c, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      :: "r"(su32(dst)), "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(V* dst, const V* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const int* c, const V* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+      :: "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(su32(src)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(V* dst, const V* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(dst), "r"(su32(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// per-thread fallback for layouts TMA cannot express (general element tiling)
+__device__ __forceinline__ void cp16(V* dst, const V* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// TMA coordinates of element j0 of line l, batch entry b (see TmaLine in hd_device.cuh)
+__device__ __forceinline__ void tma_coords(const TmaLine& t, int64_t b, int64_t l, int j0, int* c) {
+  const uint32_t ub = (uint32_t)b, un = (uint32_t)t.nbi;
+  const uint32_t bo = ub / un;
+  c[3] = (t.bcast & 1) ? 0 : (int)(ub - bo * un);
+  c[4] = (t.bcast & 2) ? 0 : (int)bo;
+  if (t.kind == TMA_LINE_TILED) {  // dims {2S (line in tile), j, line tile, b % nbi, b / nbi}
+    c[0] = 2 * (int)(l & ((1 << t.slog) - 1));
+    c[1] = j0;
+    c[2] = (int)(l >> t.slog);
+  } else {                          // TMA_ELEM_TILED: dims {2S (j in tile), line, j tile, ...}
+    c[0] = 0;
+    c[1] = (int)l;
+    c[2] = j0 >> t.slog;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Loads of one work item: in_f line (+ in_g line in CONV) -> stage slot j = element j
+// ---------------------------------------------------------------------------
+template <int MODE>
+__device__ __forceinline__ void issue_loads_tma(const PassArgs& a, int k_arr, int64_t b, int64_t g, V* buf,
+                                                uint64_t* bar) {
+  const bool live = g < a.nlines;
+  const LineIn& in = a.in_f;
+  const int L = (int)in.L;
+  uint32_t bytes = 0;
+  if (live) {
+    bytes += a.tm_in.kind == TMA_BULK ? (uint32_t)L * 16u : (uint32_t)((L + kBox - 1) / kBox) * kBox * 16u;
+    if (MODE == MODE_CONV)
+      bytes += a.tm_in_g.kind == TMA_BULK ? (uint32_t)a.in_g.L * 16u
+                                           : (uint32_t)((a.in_g.L + kBox - 1) / kBox) * kBox * 16u;
+  }
+  mbar_expect_tx(bar, bytes);
+  if (!live) return;
+  const int kk = MODE == MODE_FWD ? k_arr : 0;
+  if (a.tm_in.kind == TMA_BULK) {
+    const V* x = reinterpret_cast<const V*>(in.ptr[kk]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g);
+    bulk_load(buf, x, (uint32_t)L * 16u, bar);
+  } else {
+    const CUtensorMap* map = &a.tm_in_map[kk];
+    int c[5];
+    for (int j0 = 0; j0 < L; j0 += kBox) {
+      tma_coords(a.tm_in, b, g, j0, c);
+      tma_load(buf + j0, map, c, bar);
+    }
+  }
+  if constexpr (MODE == MODE_CONV) {
+    const LineIn& ig = a.in_g;
+    if (a.tm_in_g.kind == TMA_BULK) {
+      const V* xg = reinterpret_cast<const V*>(ig.ptr[0]) + boff(b, ig.nbi, ig.s_bo, ig.s_b) + line_off(ig, g);
+      bulk_load(buf + a.q * M, xg, (uint32_t)ig.L * 16u, bar);
+    } else {
+      int c[5];
+      for (int j0 = 0; j0 < (int)ig.L; j0 += kBox) {
+        tma_coords(a.tm_in_g, b, g, j0, c);
+        tma_load(buf + a.q * M + j0, &a.tm_in_g_map, c, bar);
+      }
+    }
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void issue_loads_cp(const PassArgs& a, int k_arr, int64_t b, int64_t g, V* buf,
+                                               int tid, int nth) {
+  if (g < a.nlines) {
+    const LineIn& in = a.in_f;
+    const V* x = reinterpret_cast<const V*>(in.ptr[MODE == MODE_FWD ? k_arr : 0]) +
+                 boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g);
+    for (int j = tid; j < (int)in.L; j += nth) cp16(buf + j, x + in_el(in, j));
+    if constexpr (MODE == MODE_CONV) {
+      const LineIn& ig = a.in_g;
+      const V* xg = reinterpret_cast<const V*>(ig.ptr[0]) + boff(b, ig.nbi, ig.s_bo, ig.s_b) + line_off(ig, g);
+      for (int j = tid; j < (int)ig.L; j += nth) cp16(buf + a.q * M + j, xg + in_el(ig, j));
+    }
+  }
+  cp_commit();
+}
+
+// ---------------------------------------------------------------------------
+// Stores of one work item: stage slots j < out.L -> output line
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void issue_stores_tma(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf) {
+  const LineOut& o = a.out;
+  const int L = (int)o.L;
+  if (a.tm_out.kind == TMA_BULK) {
+    V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
+    bulk_store(y, buf, (uint32_t)L * 16u);
+  } else {
+    const CUtensorMap* map = &a.tm_out_map[kk];
+    int c[5];
+    for (int j0 = 0; j0 < L; j0 += kBox) {
+      tma_coords(a.tm_out, b, g, j0, c);
+      tma_store(map, c, buf + j0);
+    }
+  }
+  bulk_commit();
+}
+
+__device__ __forceinline__ void stores_st(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf,
+                                          int tid, int nth) {
+  const LineOut& o = a.out;
+  V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
+  const int sl = out_sl(o);
+  for (int j = tid; j < (int)o.L; j += nth) y[jt_off(j, sl, o.s_jt, o.s_js)] = buf[j];
+}
+
+// ---------------------------------------------------------------------------
+// zeta_q^{rt}: compile-time q (QC > 0) from the constant table (constant-bank
+// operands), else the SMEM table zt[r*16 + t] = zeta_q^{(r t) mod q}
+// ---------------------------------------------------------------------------
+template <int QC>
+__device__ __forceinline__ V zq_rt(const V* zt, int r, int t) {
+  if constexpr (QC > 0) return c_zq[QC][(r * t) % QC];
+  else return zt[r * kQF + t];
+}
+
+// In-place fold of column s: rows t < p hold x[t m + s] (beyond the line: zero
+// by predicate), rows r < q receive w_r[s].  The q-point DFT over t is evaluated
+// in symmetric pairs (a_r, a_{q-r} share all real products).
+template <int QC, int P>
+__device__ __forceinline__ void fold_col(V* buf, int s, int rem, int qrt, const V* zt, V w1, V wq) {
+  const int q = QC > 0 ? QC : qrt;
+  V u[P];
+#pragma unroll
+  for (int t = 0; t < P; ++t) u[t] = (t * M < rem) ? buf[t * M + s] : cmk<V>(0, 0);
+  V a0 = u[0];
+#pragma unroll
+  for (int t = 1; t < P; ++t) a0 = cadd(a0, u[t]);
+  buf[s] = a0;
+  V wr = w1;
+#pragma unroll
+  for (int r = 1; r <= kQMax / 2; ++r) {
+    if (2 * r > q) break;
+    V A = u[0], B = cmk<V>(0, 0);
+#pragma unroll
+    for (int t = 1; t < P; ++t) {
+      const V z = zq_rt<QC>(zt, r, t);  // zeta_q^{r t}
+      A.x = fma(u[t].x, z.x, A.x); A.y = fma(u[t].y, z.x, A.y);
+      B.x = fma(u[t].x, z.y, B.x); B.y = fma(u[t].y, z.y, B.y);
+    }
+    buf[r * M + s] = cmul(cmk<V>(A.x - B.y, A.y + B.x), wr);  // a_r zeta^{rs}
+    if (2 * r < q) buf[(q - r) * M + s] = cmul(cmk<V>(A.x + B.y, A.y - B.x), cmulc(wq, wr));
+    wr = cmul(wr, w1);
+  }
+}
+
+template <int QC>
+__device__ __forceinline__ void fold_all(V* buf, int p, int L, bool live, int q, const V* zt, const V* twm,
+                                         const V* twM1, int tid, int nth) {
+  for (int s = tid; s < M; s += nth) {
+    const int rem = live ? L - s : 0;
+    const V w1 = ldg(twM1 + s), wq = ldg(twm + s);
+    if (p <= 1) fold_col<QC, 1>(buf, s, rem, q, zt, w1, wq);
+    else if (p <= 2) fold_col<QC, 2>(buf, s, rem, q, zt, w1, wq);
+    else if (p <= 4) fold_col<QC, 4>(buf, s, rem, q, zt, w1, wq);
+    else fold_col<QC, 8>(buf, s, rem, q, zt, w1, wq);
+  }
+}
+
+// In-place unfold of column s: rows r < q hold V_r[s]; rows t < T receive
+// h[tm+s] = sum_r zeta_q^{-tr} conj(zeta_{M1}^{rs}) V_r[s], in pairs (t, q-t).
+template <int QC, int QM>
+__device__ __forceinline__ void unfold_col(V* buf, int s, int qrt, int T, const V* zt, V w1) {
+  const int q = QC > 0 ? QC : qrt;
+  V v[QM];
+  v[0] = buf[s];
+  {
+    // conj twiddles zeta_{M1}^{-rs}: odd and even r by two interleaved recurrences
+    const V w2 = cmul(w1, w1);
+    V we = w2, wo = w1;
+#pragma unroll
+    for (int r = 1; r < QM; ++r) {
+      v[r] = cmk<V>(0, 0);
+      if (r < q) {
+        if (r & 1) { v[r] = cmulc(buf[r * M + s], wo); wo = cmul(wo, w2); }
+        else { v[r] = cmulc(buf[r * M + s], we); we = cmul(we, w2); }
+      }
+    }
+  }
+  V h0 = v[0];
+#pragma unroll
+  for (int r = 1; r < QM; ++r) h0 = cadd(h0, v[r]);
+  buf[s] = h0;
+#pragma unroll
+  for (int t = 1; t <= QM / 2; ++t) {
+    if (2 * t > q) break;
+    V A = cmk<V>(0, 0), B = cmk<V>(0, 0);
+#pragma unroll
+    for (int r = 0; r < QM; ++r) {
+      if (r < q) {
+        const V z = zq_rt<QC>(zt, t, r);  // zeta_q^{t r}
+        A.x = fma(v[r].x, z.x, A.x); A.y = fma(v[r].y, z.x, A.y);
+        B.x = fma(v[r].x, z.y, B.x); B.y = fma(v[r].y, z.y, B.y);
+      }
+    }
+    if (t < T) buf[t * M + s] = cmk<V>(A.x + B.y, A.y - B.x);
+    if (2 * t < q && q - t < T) buf[(q - t) * M + s] = cmk<V>(A.x - B.y, A.y + B.x);
+  }
+}
+
+template <int QC>
+__device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, const V* twM1, int tid, int nth) {
+  for (int s = tid; s < M; s += nth) {
+    const V w1 = ldg(twM1 + s);
+    if constexpr (QC > 0) unfold_col<QC, QC>(buf, s, q, T, zt, w1);
+    else if (q <= 4) unfold_col<0, 4>(buf, s, q, T, zt, w1);
+    else if (q <= 8) unfold_col<0, 8>(buf, s, q, T, zt, w1);
+    else unfold_col<0, kQMax>(buf, s, q, T, zt, w1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.  MODE_FWD: fold + FFT -> spectrum line (array blockIdx.z);
+// MODE_INV: spectrum line -> IFFT + unfold; MODE_CONV: fold + FFT of f, twiddle +
+// FFT of the short g (p_g = 1), product, IFFT, unfold (npairs == 1).
+// QC: compile-time q (0: runtime q, twiddles from the SMEM table).
+// Shared memory: [mbar x2 | pad][zt: 16x16][stage 0][stage 1], stage = q*512 (+512 CONV).
+// ---------------------------------------------------------------------------
+template <int MODE, int NTMAX, int QC>
+__global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ PassArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  V* zt = reinterpret_cast<V*>(smem_raw + 128);
+  V* stage0 = zt + kQF * kQF;
+  const int q = QC > 0 ? QC : a.q;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31;
+  const int r = tid >> 5;  // this warp's residue
+  const int k_arr = blockIdx.z;
+  const int SB = q * M + (MODE == MODE_CONV ? M : 0);
+  const bool tma_in = a.tm_in.kind != TMA_NONE;
+  const bool tma_out = a.tm_out.kind != TMA_NONE;
+  const V* twm = reinterpret_cast<const V*>(a.tw_m);
+  const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
+  if (QC == 0) {
+    for (int i = tid; i < kQF * kQF; i += nth) {
+      const int rr = i / kQF, t = i % kQF;
+      zt[i] = ldg(twM1 + (int64_t)((rr * t) % q) * M);
+    }
+  }
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const V w1l = ldg(twm + lane);  // zeta_512^{lane}: seeds this lane's L1 twiddles
+
+  const int64_t total = a.nbatch * a.ngroups;
+  int64_t w = blockIdx.x;
+  if (w < total) {
+    int64_t g0, b0;
+    split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b0, g0);
+    if (tma_in) { if (tid == 0) issue_loads_tma<MODE>(a, k_arr, b0, g0, stage0, &bars[0]); }
+    else issue_loads_cp<MODE>(a, k_arr, b0, g0, stage0, tid, nth);
+  }
+  for (int it = 0; w < total; w += gridDim.x, ++it) {
+    const int st = it & 1;
+    V* buf = stage0 + st * SB;
+    V* gbuf = buf + q * M;
+    int64_t g, b;
+    split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+    const bool live = g < a.nlines;
+    V* Fr = buf + r * M;  // this warp's residue row (also its FFT exchange area)
+    if (tma_in) mbar_wait(&bars[st], (uint32_t)(it >> 1) & 1u);
+    else { cp_wait0(); __syncthreads(); }
+
+    // step 1: fold (FWD, CONV) or the inverse FFT of the spectrum (INV)
+    if constexpr (MODE == MODE_INV) {
+      V v[16];
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fr[k2 * 32 + lane];
+      w512::fft_inv(v, Fr, lane, w1l);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
+    } else {
+      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twM1, tid, nth);
+    }
+    __syncthreads();
+
+    // the next item's loads go to the other stage (whose stores were issued one
+    // step earlier and have been read out of shared memory by now)
+    {
+      const int64_t wn = w + gridDim.x;
+      if (wn < total) {
+        int64_t gn, bn;
+        split_item(wn, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
+        V* nb = stage0 + (st ^ 1) * SB;
+        if (tma_in) {
+          if (tid == 0) {
+            if (tma_out) bulk_wait_read0();
+            issue_loads_tma<MODE>(a, k_arr, bn, gn, nb, &bars[st ^ 1]);
+          }
+        } else {
+          if (tma_out && tid == 0) bulk_wait_read0();
+          __syncthreads();
+          issue_loads_cp<MODE>(a, k_arr, bn, gn, nb, tid, nth);
+        }
+      }
+    }
+
+    if constexpr (MODE == MODE_FWD) {
+      V v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = Fr[lane + 32 * i];
+      w512::fft_fwd(v, Fr, lane, w1l);
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) Fr[k2 * 32 + lane] = v[k2];  // lane-major spectrum
+    } else if constexpr (MODE == MODE_CONV) {
+      V F[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) F[i] = Fr[lane + 32 * i];
+      w512::fft_fwd(F, Fr, lane, w1l);
+      // short input: p_g = 1, w[s] = (1/prod M1) zeta_{M1}^{r s} g[s], s = lane + 32 i;
+      // twiddles by four interleaved recurrences of step zeta_{M1}^{128 r}
+      V v[16];
+      {
+        const int Lg = live ? (int)a.in_g.L : 0;
+        const V st1 = ldg(twM1 + r * 32);
+        const V st4 = ldg(twM1 + r * 128);
+        V wc[4];
+        wc[0] = cscale(ldg(twM1 + r * lane), a.scale);
+        wc[1] = cmul(wc[0], st1);
+        wc[2] = cmul(wc[1], st1);
+        wc[3] = cmul(wc[2], st1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int s = lane + 32 * i;
+          v[i] = (s < Lg) ? cmul(gbuf[s], wc[i & 3]) : cmk<V>(0, 0);
+          if ((i & 3) == 3) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) wc[k] = cmul(wc[k], st4);
+          }
+        }
+      }
+      __syncwarp();
+      w512::fft_fwd(v, Fr, lane, w1l);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = cmul(F[k], v[k]);
+      w512::fft_inv(v, Fr, lane, w1l);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
+    }
+    if constexpr (MODE != MODE_FWD) {
+      __syncthreads();
+      unfold_all<QC>(buf, q, a.out.T, zt, twM1, tid, nth);
+    }
+    // results are in stage slots j < out.L: hand them to the async proxy and store
+    const int kk = MODE == MODE_FWD ? k_arr : 0;
+    if (tma_out) {
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0 && live) issue_stores_tma(a, kk, b, g, buf);
+    } else {
+      __syncthreads();
+      if (live) stores_st(a, kk, b, g, buf, tid, nth);
+      __syncthreads();
+    }
+  }
+  if (tid == 0 && tma_out) bulk_wait0();
+}
+
+}  // namespace s512
+}  // namespace hd

@@ -164,138 +164,5 @@ __device__ __forceinline__ void fft_inv(V* a, V* E, int lane, V w1l) {
   dft16<-1>(a);
 }
 
-// ---------------------------------------------------------------------------
-// Pass kernel on the warp engine: one line per CTA, one warp per residue
-// (blockDim = 32 q), D = q, fast fold/unfold (q <= 16, p <= 8).
-// MODE_FWD / MODE_INV / MODE_CONV as in pass_kernel; CONV needs npairs == 1 and
-// p_g == 1 (the short input's fold is done in registers, residue by residue).
-// Shared memory: [zq: q][zt: 16x16][F: q*512] (each warp's F row doubles as its
-// exchange area; in CONV the F-hat spectrum stays in registers while G is transformed)
-// ---------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(288, 2) w512_kernel(const __grid_constant__ PassArgs a) {
-  constexpr int M = 512;
-  constexpr int EPR = 8;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  V* smem = reinterpret_cast<V*>(smem_raw);
-  const int q = a.q;
-  const int k_arr = blockIdx.z;
-  const int lane = threadIdx.x & 31;
-  const int r = threadIdx.x >> 5;  // this warp's residue
-  V* zq = smem;
-  V* zt = zq + round_slots<EPR>(q);
-  V* F = zt + round_slots<EPR>(kQF * kQF);
-  // CONV: per-CTA global scratch (L2-resident) where each warp parks its F-hat
-  V* Fh = MODE == MODE_CONV ? reinterpret_cast<V*>(a.scratch) + ((int64_t)blockIdx.x * q + (threadIdx.x >> 5)) * M
-                            : nullptr;
-  const V* twm = reinterpret_cast<const V*>(a.tw_m);
-  const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
-  const V w1l = ldg(twm + lane);  // zeta_512^{lane}: seeds this lane's L1 twiddles
-  for (int i = threadIdx.x; i < q; i += (int)blockDim.x) zq[i] = ldg(twM1 + (int64_t)i * M);
-  for (int i = threadIdx.x; i < kQF * kQF; i += (int)blockDim.x) {
-    const int rr = i / kQF, t = i % kQF;
-    zt[i] = ldg(twM1 + (int64_t)((rr * t) % q) * M);
-  }
-  __syncthreads();
-
-  V* Fr = F + r * M;  // this warp's residue row (also its exchange region)
-  const int64_t total = a.nbatch * a.ngroups;
-  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    int64_t g, b;
-    split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
-    if (threadIdx.x == 0 && w + gridDim.x < total) {
-      int64_t gn, bn;
-      split_item(w + gridDim.x, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
-      prefetch_lines<V>(a.in_f, MODE == MODE_FWD ? k_arr : 0, bn, gn, 1, a.nlines);
-      if (MODE == MODE_CONV) prefetch_lines<V>(a.in_g, 0, bn, gn, 1, a.nlines);
-    }
-    const bool live = g < a.nlines;
-    if constexpr (MODE == MODE_FWD) {
-      fold<V, M, 512>(F, a.in_f, k_arr, b, g, a.nlines, 1, 0, 0, q, q, zq, zt, twm, twM1);
-      __syncthreads();
-      V v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = Fr[swz<V>(r * M + lane + 32 * i) - r * M];
-      fft_fwd(v, Fr, lane, w1l);
-      if (live) {
-        const LineOut& o = a.out;
-        V* y = reinterpret_cast<V*>(o.ptr[k_arr]) + boff(b, o.nbi, o.s_bo, o.s_b) +
-               line_off(o, g);
-        const int sl = out_sl(o);
-        const int64_t k0 = (int64_t)r * M;
-        if (sl >= 1 && sl < 30 && o.s_js == 1) {
-          // positions pos(f) and pos(f)+1 = pos(f+64): registers k2 and k2+4, k2 in {0..3, 8..11}
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const int k2 = (kk & 3) + ((kk >> 2) << 3);
-            const int p0 = pos_of_freq(freq_of(lane, k2));
-            st256(y + jt_off(k0 + p0, sl, o.s_jt, o.s_js), v[k2], v[k2 + 4]);
-          }
-        } else {
-#pragma unroll
-          for (int k2 = 0; k2 < 16; ++k2)
-            y[jt_off(k0 + pos_of_freq(freq_of(lane, k2)), sl, o.s_jt, o.s_js)] = v[k2];
-        }
-      }
-      __syncthreads();
-    } else if constexpr (MODE == MODE_INV) {
-      {
-        const LineIn& in = a.in_f;
-        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b) +
-                     line_off(in, g);
-        V v[16];
-        const int64_t k0 = (int64_t)r * M;
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2)
-          v[k2] = live ? x[in_el(in, k0 + pos_of_freq(freq_of(lane, k2)))] : cmk<V>(0, 0);
-        fft_inv(v, Fr, lane, w1l);
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) Fr[swz<V>(r * M + lane + 32 * i) - r * M] = v[i];
-      }
-      __syncthreads();
-      unfold<V, M, 512>(F, a.out, 0, b, g, a.nlines, 1, 0, 0, q, q, false, zq, zt, twm, twM1);
-      __syncthreads();
-    } else {
-      fold<V, M, 512>(F, a.in_f, 0, b, g, a.nlines, 1, 0, 0, q, q, zq, zt, twm, twM1);
-      __syncthreads();
-      V v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = Fr[swz<V>(r * M + lane + 32 * i) - r * M];
-      fft_fwd(v, Fr, lane, w1l);
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 16; ++k) Fh[lane + 32 * k] = v[k];  // F-hat parked in L2 scratch
-      // short input g: p_g == 1, fold in registers: w[s] = g[s] zeta_{M1}^{r s}, s = lane + 32 i
-      {
-        const LineIn& in = a.in_g;
-        const V* x = reinterpret_cast<const V*>(in.ptr[0]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g);
-        V wr = ldg(twM1 + (int64_t)r * lane);
-        const V step = ldg(twM1 + (int64_t)r * 32);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int s = lane + 32 * i;
-          const V u = (live && s < in.L) ? x[in_el(in, s)] : cmk<V>(0, 0);
-          v[i] = cmul(u, wr);
-          wr = cmul(wr, step);
-        }
-      }
-      fft_fwd(v, Fr, lane, w1l);   // G's transform reuses this warp's SMEM row
-      {
-        const double sc = a.scale;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = cscale(cmul(Fh[lane + 32 * k], v[k]), sc);  // (1/prod M1) F-hat G-hat
-      }
-      fft_inv(v, Fr, lane, w1l);
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) Fr[swz<V>(r * M + lane + 32 * i) - r * M] = v[i];
-      __syncthreads();
-      unfold<V, M, 512>(F, a.out, 0, b, g, a.nlines, 1, 0, 0, q, q, false, zq, zt, twm, twM1);
-      __syncthreads();
-    }
-  }
-}
-
 }  // namespace w512
 }  // namespace hd

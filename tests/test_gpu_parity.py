@@ -275,21 +275,47 @@ def test_tune_small(ctx, H):
     assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
 
 
-# ---------------------------------------------------------------- warp engine (m = 512)
-@pytest.mark.parametrize("shape", [((600, 700), (100, 90)), ((1000, 513), (255, 300))])
-def test_w512_engine_matches_oracle_and_generic(ctx, H, shape):
+# ---------------------------------------------------------------- staged warp engine (m = 512)
+# hd_s512.cuh runs every m = 512 complex-double pass with one line per CTA (C = 1)
+# and an automatic engine choice; HD_FLAG_GENERIC_FFT forces the generic engine.
+@pytest.mark.parametrize("shape,S", [(((600, 700), (100, 90)), 2), (((1000, 513), (255, 300)), 2),
+                                     (((1000, 513), (255, 300)), 1), (((700, 1200), (33, 511)), 4),
+                                     (((513, 2100), (512, 77)), 16)])
+def test_s512_engine_matches_oracle_and_generic(ctx, H, shape, S):
     (sf, sg) = shape
     f, g = synth.random_pair(90, sf, sg)
     ref = oracle.conv(f, g)
-    axes = [{"m": 512, "C": 1, "S": 2}, {"m": 512, "C": 1, "S": 2}]
+    axes = [{"m": 512, "C": 1, "S": S}, {"m": 512, "C": 1, "S": S}]
     hw = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes)))
     hg = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes, flags=H.HD_FLAG_GENERIC_FFT)))
     assert oracle.rel_l2(hw, ref) < 1e-11
     assert oracle.rel_l2(hg, ref) < 1e-11
 
 
+@pytest.mark.parametrize("shape", [((3000, 2500), (500, 300)), ((4000, 1700), (230, 4000))])
+def test_s512_engine_large_q_sampled(ctx, H, shape):
+    """q up to 12 along x (fwd/inv passes) and q = 7..9 along the convolution axis,
+    ragged last blocks; checked on a seeded sample of outputs with the direct sum."""
+    (sf, sg) = shape
+    f, g = synth.random_pair(91, sf, sg)
+    axes = [{"m": 512, "C": 1, "S": 2}, {"m": 512, "C": 1, "S": 2}]
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes)))
+    idx = synth.sample_indices(h.shape, n_random=1500)
+    ref = oracle.conv_sampled(f, g, idx)
+    assert oracle.rel_l2(h[tuple(idx.T)], ref) < 1e-11
+
+
+def test_s512_engine_batched_2d(ctx, H):
+    f = np.stack([synth.random_pair(92 + b, (300, 700), (40, 50))[0] for b in range(3)])
+    g = np.stack([synth.random_pair(95 + b, (300, 700), (40, 50))[1] for b in range(3)])
+    axes = [{"m": 512, "C": 1, "S": 2}, {"m": 512, "C": 1, "S": 2}]
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes), batch=True))
+    for b in range(3):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
+
+
 @pytest.mark.parametrize("L,q", [(512, 1), (1000, 2), (4000, 8), (4096, 9)])
-def test_w512_residues_match_generic(ctx, H, L, q):
+def test_s512_residues_match_dft(ctx, H, L, q):
     x = synth.random_pair(L, (3, L), (1,))[0]
     X = host(ctx.hd_forward_residues(dev(x), 512, q))
     perm = H.hd_spectral_permutation(512)
