@@ -421,6 +421,10 @@ void prepare_tma(Launch& L) {
     }
   }
   if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map)) a.tm_out.kind = hd::TMA_NONE;
+  // the kernel runs loads and stores both by TMA (producer warp) or both per thread
+  if (a.tm_in.kind == hd::TMA_NONE || a.tm_out.kind == hd::TMA_NONE) {
+    a.tm_in.kind = hd::TMA_NONE; a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE;
+  }
 }
 
 // The staged warp engine (m = 512, hd_s512.cuh) applies to one line per CTA, all
@@ -442,7 +446,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   int threads = L.threads;
   if (use_s512(dt, L)) {
     fn = hd::lookup_s512(L.mode, L.a.q);
-    threads = 32 * L.a.q;
+    threads = 32 * (L.a.q + 1);
     smem = hd::s512_smem_bytes(L.a.q, L.mode);
     prepare_tma(L);
   } else {
@@ -464,8 +468,28 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
   }
+  // debug: HD_PHASE_PROF=1 prints the staged engine's cycles per warp and work item
+  // for the phases 0 wait-load, 1 fold/step 1, 2 barrier, 3 issue next loads,
+  // 4 FFTs, 5 barrier, 6 unfold, 7 store + loop
+  static const bool phase_prof = getenv("HD_PHASE_PROF") != nullptr;
+  static unsigned long long* d_phase = nullptr;
+  L.a.phase_prof = nullptr;
+  if (phase_prof && use_s512(dt, L)) {
+    if (!d_phase) cudaMalloc(&d_phase, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_phase, 0, 8 * sizeof(unsigned long long), st);
+    L.a.phase_prof = d_phase;
+  }
   cudaError_t e = fn(L.a, grid, threads, smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, L.name);
+  if (L.a.phase_prof) {
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, d_phase, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double n = (double)total * (threads / 32 - 1);
+    fprintf(stderr, "[phase] %-8s", L.name);
+    for (int i = 0; i < 8; ++i) fprintf(stderr, " %7.0f", h[i] / n);
+    fprintf(stderr, "\n");
+  }
   ctx->launches += 1;
   if (ctx->profiling) {
     cudaEventRecord(e1, st);

@@ -295,6 +295,7 @@ struct PassArgs {
   CUtensorMap tm_in_map[kTmaArrays];
   CUtensorMap tm_in_g_map;
   CUtensorMap tm_out_map[kTmaArrays];
+  unsigned long long* phase_prof;  // debug (HD_PHASE_PROF=1): per-phase SM cycles, else null
   const void* tw_m;        // zeta_m^k,  k < m
   const void* tw_M1;       // zeta_M1^k, k < M1
   const void* tw_st;       // stage twiddle table of m (see StageOff)

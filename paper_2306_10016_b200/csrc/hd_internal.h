@@ -9,9 +9,9 @@ struct PassArgs;
 using LaunchFn = cudaError_t (*)(const PassArgs&, dim3, int, size_t, cudaStream_t);
 // nullptr if (m, mode) has no instantiation or threads exceeds every slice bound
 LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
-// staged warp engine for m = 512 complex double (hd_s512.cuh); blockDim = 32 q <= 384
+// staged warp engine for m = 512 complex double (hd_s512.cuh); blockDim = 32 (q + 1) <= 384
 LaunchFn lookup_s512(int mode, int q);
-constexpr int kS512QMax = 12;
+constexpr int kS512QMax = 11;
 size_t s512_smem_bytes(int q, int mode);
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);

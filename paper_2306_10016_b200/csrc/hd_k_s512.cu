@@ -28,12 +28,11 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
 }
 
 // q = 9 (the BASELINE 2-D configs' axes) has a compile-time-q instantiation; other
-// q <= 9 get a 288-thread bound (up to 168 registers), q <= 12 a 384-thread bound.
+// q get a runtime-q kernel.  blockDim = 32 (q + 1): q compute warps + the producer.
 template <int MODE>
 static LaunchFn pick_s512(int q) {
-  if (q == 9) return launch_s512_impl<MODE, 288, 9>;
-  if (q < 9) return launch_s512_impl<MODE, 288, 0>;
-  return launch_s512_impl<MODE, 32 * s512::kQMax, 0>;
+  if (q == 9) return launch_s512_impl<MODE, 320, 9>;
+  return launch_s512_impl<MODE, 32 * (s512::kQMax + 1), 0>;
 }
 LaunchFn lookup_s512(int mode, int q) {
   switch (mode) {
@@ -45,7 +44,8 @@ LaunchFn lookup_s512(int mode, int q) {
 }
 
 size_t s512_smem_bytes(int q, int mode) {
-  return 128 + sizeof(double2) * (size_t)(kQF * kQF + 2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));
+  return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 +
+                                          2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));
 }
 
 }  // namespace hd

@@ -1,7 +1,8 @@
 // hd_s512.cuh -- staged warp engine for FFT size m = 512 (complex double).
 //
-// One persistent CTA per SM, one line per work item, q warps (warp r owns residue
-// r; blockDim = 32 q, q <= 12).  Lines move between HBM and a two-stage shared
+// One persistent CTA per SM, one line per work item, q compute warps (warp r owns
+// residue r) plus one producer warp that issues every TMA copy and bulk wait, so
+// compute warps never stall on copy issue (blockDim = 32 (q + 1), q <= 11).  Lines move between HBM and a two-stage shared
 // memory ring by TMA: strided / tiled lines as 5-D tensor boxes of 256 elements
 // (cp.async.bulk.tensor, zero fill past the line end), plain rows as one 1-D bulk
 // copy; loads complete on an mbarrier, stores are bulk-async groups.  The next
@@ -35,7 +36,7 @@ namespace s512 {
 
 using V = double2;
 constexpr int M = 512;
-constexpr int kQMax = kS512QMax;  // two stages of (q + 1) * 8 KB fit in 227 KB
+constexpr int kQMax = kS512QMax;  // q + 1 warps at <= 3 per SM sub-partition (168 registers)
 constexpr int kBox = 256;         // elements per TMA box
 
 // ---------------------------------------------------------------------------
@@ -102,6 +103,29 @@ __device__ __forceinline__ void tma_coords(const TmaLine& t, int64_t b, int64_t 
     c[2] = j0 >> t.slog;
   }
 }
+
+// Debug phase timing (HD_PHASE_PROF=1 in the host driver): lane 0 of every warp
+// accumulates SM clock cycles per phase and adds them to a.phase_prof at exit.
+constexpr int kPhases = 8;
+struct PhaseClock {
+  unsigned long long acc[kPhases];
+  long long t0;
+  bool on;
+  __device__ __forceinline__ void start(bool enable) {
+    on = enable;
+#pragma unroll
+    for (int i = 0; i < kPhases; ++i) acc[i] = 0;
+    if (on) t0 = clock64();
+  }
+  __device__ __forceinline__ void mark(int ph) {
+    if (on) { const long long t = clock64(); acc[ph] += (unsigned long long)(t - t0); t0 = t; }
+  }
+  __device__ __forceinline__ void flush(unsigned long long* out) {
+    if (on && (threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int i = 0; i < kPhases; ++i) atomicAdd(out + i, acc[i]);
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Loads of one work item: in_f line (+ in_g line in CONV) -> stage slot j = element j
@@ -203,6 +227,84 @@ __device__ __forceinline__ V zq_rt(const V* zt, int r, int t) {
   else return zt[r * kQF + t];
 }
 
+// q = 9 codelets: the 9-point DFT y_r = sum_t zeta_9^{S r t} x_t as 3 x 3
+// (t = 3 t1 + t2, r = r1 + 3 r2: radix-3 over t1, twiddle zeta_9^{S r1 t2},
+// radix-3 over t2), 88 FP64 operations instead of the pair form's ~150.
+template <int S> __device__ __forceinline__ void dft3(V& x0, V& x1, V& x2) {
+  constexpr double h = 0.86602540378443864676;  // sin(2 pi / 3)
+  const V sm = cadd(x1, x2), df = csub(x1, x2);
+  const V mid = cmk<V>(fma(-0.5, sm.x, x0.x), fma(-0.5, sm.y, x0.y));
+  x0 = cadd(x0, sm);
+  // x1 = mid + S i h df, x2 = mid - S i h df
+  x1 = cmk<V>(fma(-S * h, df.y, mid.x), fma(S * h, df.x, mid.y));
+  x2 = cmk<V>(fma(S * h, df.y, mid.x), fma(-S * h, df.x, mid.y));
+}
+template <int S> __device__ __forceinline__ void dft9(V* x) {
+  dft3<S>(x[0], x[3], x[6]);
+  dft3<S>(x[1], x[4], x[7]);
+  dft3<S>(x[2], x[5], x[8]);
+  // twiddles zeta_9^{S r1 t2}: (r1, t2) = (1,1): 1, (2,1): 2, (1,2): 2, (2,2): 4
+  const V z1 = c_zq[9][1], z2 = c_zq[9][2], z4 = c_zq[9][4];
+  x[4] = S > 0 ? cmul(x[4], z1) : cmulc(x[4], z1);
+  x[7] = S > 0 ? cmul(x[7], z2) : cmulc(x[7], z2);
+  x[5] = S > 0 ? cmul(x[5], z2) : cmulc(x[5], z2);
+  x[8] = S > 0 ? cmul(x[8], z4) : cmulc(x[8], z4);
+  // radix-3 over t2 for each r1: inputs (x[3 r1'...]) -- element (r1, t2) sits at 3 t2' ...
+  dft3<S>(x[0], x[1], x[2]);  // r1 = 0 -> y_0, y_3, y_6
+  dft3<S>(x[3], x[4], x[5]);  // r1 = 1 -> y_1, y_4, y_7
+  dft3<S>(x[6], x[7], x[8]);  // r1 = 2 -> y_2, y_5, y_8
+}
+// After dft9, x[3 r1 + r2] holds y_{r1 + 3 r2}.
+__device__ __forceinline__ int dft9_slot(int r) { return 3 * (r % 3) + r / 3; }
+
+// NC columns per call (NC = 2: two independent columns interleaved for ILP)
+template <int P, int NC>
+__device__ __forceinline__ void fold_col9(V* buf, const int* s, const int* rem, const V* w1) {
+  V x[NC][9];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int t = 0; t < 9; ++t) x[c][t] = (t < P && t * M < rem[c]) ? buf[t * M + s[c]] : cmk<V>(0, 0);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) dft9<+1>(x[c]);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    buf[s[c]] = x[c][0];
+    // twiddles zeta_{M1}^{r s}: two interleaved recurrences (odd / even r)
+    const V w2 = cmul(w1[c], w1[c]);
+    V wo = w1[c], we = w2;
+#pragma unroll
+    for (int r = 1; r < 9; ++r) {
+      const V y = x[c][dft9_slot(r)];
+      if (r & 1) { buf[r * M + s[c]] = cmul(y, wo); wo = cmul(wo, w2); }
+      else { buf[r * M + s[c]] = cmul(y, we); we = cmul(we, w2); }
+    }
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ void unfold_col9(V* buf, const int* s, int T, const V* w1) {
+  V x[NC][9];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    x[c][0] = buf[s[c]];
+    const V w2 = cmul(w1[c], w1[c]);
+    V wo = w1[c], we = w2;
+#pragma unroll
+    for (int r = 1; r < 9; ++r) {
+      if (r & 1) { x[c][r] = cmulc(buf[r * M + s[c]], wo); wo = cmul(wo, w2); }
+      else { x[c][r] = cmulc(buf[r * M + s[c]], we); we = cmul(we, w2); }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) dft9<-1>(x[c]);
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int t = 0; t < 9; ++t)
+      if (t < T) buf[t * M + s[c]] = x[c][dft9_slot(t)];
+}
+
 // In-place fold of column s: rows t < p hold x[t m + s] (beyond the line: zero
 // by predicate), rows r < q receive w_r[s].  The q-point DFT over t is evaluated
 // in symmetric pairs (a_r, a_{q-r} share all real products).
@@ -235,14 +337,25 @@ __device__ __forceinline__ void fold_col(V* buf, int s, int rem, int qrt, const 
 
 template <int QC>
 __device__ __forceinline__ void fold_all(V* buf, int p, int L, bool live, int q, const V* zt, const V* twm,
-                                         const V* twM1, int tid, int nth) {
-  for (int s = tid; s < M; s += nth) {
-    const int rem = live ? L - s : 0;
-    const V w1 = ldg(twM1 + s), wq = ldg(twm + s);
-    if (p <= 1) fold_col<QC, 1>(buf, s, rem, q, zt, w1, wq);
-    else if (p <= 2) fold_col<QC, 2>(buf, s, rem, q, zt, w1, wq);
-    else if (p <= 4) fold_col<QC, 4>(buf, s, rem, q, zt, w1, wq);
-    else fold_col<QC, 8>(buf, s, rem, q, zt, w1, wq);
+                                         const V* twcol, int tid, int nth) {
+  if constexpr (QC == 9) {
+    // threads < 256 take columns s and s + 256 together (nth >= 256)
+    if (tid < M / 2) {
+      const int sc[2] = {tid, tid + M / 2};
+      const int rm[2] = {live ? L - sc[0] : 0, live ? L - sc[1] : 0};
+      const V w1[2] = {twcol[sc[0]], twcol[sc[1]]};
+      if (p <= 4) fold_col9<4, 2>(buf, sc, rm, w1);
+      else fold_col9<8, 2>(buf, sc, rm, w1);
+    }
+  } else {
+    for (int s = tid; s < M; s += nth) {
+      const int rem = live ? L - s : 0;
+      const V w1 = twcol[s], wq = ldg(twm + s);
+      if (p <= 1) fold_col<QC, 1>(buf, s, rem, q, zt, w1, wq);
+      else if (p <= 2) fold_col<QC, 2>(buf, s, rem, q, zt, w1, wq);
+      else if (p <= 4) fold_col<QC, 4>(buf, s, rem, q, zt, w1, wq);
+      else fold_col<QC, 8>(buf, s, rem, q, zt, w1, wq);
+    }
   }
 }
 
@@ -288,13 +401,21 @@ __device__ __forceinline__ void unfold_col(V* buf, int s, int qrt, int T, const 
 }
 
 template <int QC>
-__device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, const V* twM1, int tid, int nth) {
-  for (int s = tid; s < M; s += nth) {
-    const V w1 = ldg(twM1 + s);
-    if constexpr (QC > 0) unfold_col<QC, QC>(buf, s, q, T, zt, w1);
-    else if (q <= 4) unfold_col<0, 4>(buf, s, q, T, zt, w1);
-    else if (q <= 8) unfold_col<0, 8>(buf, s, q, T, zt, w1);
-    else unfold_col<0, kQMax>(buf, s, q, T, zt, w1);
+__device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, const V* twcol, int tid, int nth) {
+  if constexpr (QC == 9) {
+    if (tid < M / 2) {
+      const int sc[2] = {tid, tid + M / 2};
+      const V w1[2] = {twcol[sc[0]], twcol[sc[1]]};
+      unfold_col9<2>(buf, sc, T, w1);
+    }
+  } else {
+    for (int s = tid; s < M; s += nth) {
+      const V w1 = twcol[s];
+      if constexpr (QC > 0) unfold_col<QC, QC>(buf, s, q, T, zt, w1);
+      else if (q <= 4) unfold_col<0, 4>(buf, s, q, T, zt, w1);
+      else if (q <= 8) unfold_col<0, 8>(buf, s, q, T, zt, w1);
+      else unfold_col<0, kQMax>(buf, s, q, T, zt, w1);
+    }
   }
 }
 
@@ -303,47 +424,98 @@ __device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, co
 // MODE_INV: spectrum line -> IFFT + unfold; MODE_CONV: fold + FFT of f, twiddle +
 // FFT of the short g (p_g = 1), product, IFFT, unfold (npairs == 1).
 // QC: compile-time q (0: runtime q, twiddles from the SMEM table).
-// Shared memory: [mbar x2 | pad][zt: 16x16][stage 0][stage 1], stage = q*512 (+512 CONV).
+//
+// Roles (TMA mode): warp q is the producer.  It keeps two items in flight: loads
+// of item i land on full[i&1]; the compute warps (named barrier 1 among
+// themselves) process item i and arrive on done[i&1]; the producer then stores
+// item i from that stage, waits until the store has read the stage, and loads
+// item i + 2 into it.  Fallback mode (a layout TMA cannot express): the compute
+// warps copy with cp.async / plain stores and the producer warp idles.
+// Shared memory: [full x2, done x2 | pad][zt 16x16][tw 23x32][col 512]
+//                [stage 0][stage 1], stage = q*512 (+512 CONV).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void compute_sync(int n) { asm volatile("bar.sync 1, %0;" :: "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(su32(bar)) : "memory");
+}
+
 template <int MODE, int NTMAX, int QC>
 __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* done = full + 2;
   V* zt = reinterpret_cast<V*>(smem_raw + 128);
-  V* stage0 = zt + kQF * kQF;
+  V* twtab = zt + kQF * kQF;
+  V* twcol = twtab + w512::kTwRows * 32;   // zeta_{M1}^s, s < 512
+  V* stage0 = twcol + M;
   const int q = QC > 0 ? QC : a.q;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x;
+  const int nth = 32 * q;                  // compute threads; warp q is the producer
   const int lane = tid & 31;
-  const int r = tid >> 5;  // this warp's residue
+  const int r = tid >> 5;                  // this warp's residue (compute warps)
   const int k_arr = blockIdx.z;
   const int SB = q * M + (MODE == MODE_CONV ? M : 0);
-  const bool tma_in = a.tm_in.kind != TMA_NONE;
-  const bool tma_out = a.tm_out.kind != TMA_NONE;
+  const bool tma = a.tm_in.kind != TMA_NONE && a.tm_out.kind != TMA_NONE;
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
   if (QC == 0) {
-    for (int i = tid; i < kQF * kQF; i += nth) {
+    for (int i = tid; i < kQF * kQF; i += blockDim.x) {
       const int rr = i / kQF, t = i % kQF;
       zt[i] = ldg(twM1 + (int64_t)((rr * t) % q) * M);
     }
   }
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+  for (int i = tid; i < w512::kTwRows * 32; i += blockDim.x) twtab[i] = w512::tw_entry(twm, i >> 5, i & 31);
+  for (int i = tid; i < M; i += blockDim.x) twcol[i] = ldg(twM1 + i);
+  if (tid == nth) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&done[0], nth);
+    mbar_init(&done[1], nth);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const V w1l = ldg(twm + lane);  // zeta_512^{lane}: seeds this lane's L1 twiddles
-
   const int64_t total = a.nbatch * a.ngroups;
-  int64_t w = blockIdx.x;
-  if (w < total) {
-    int64_t g0, b0;
-    split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b0, g0);
-    if (tma_in) { if (tid == 0) issue_loads_tma<MODE>(a, k_arr, b0, g0, stage0, &bars[0]); }
-    else issue_loads_cp<MODE>(a, k_arr, b0, g0, stage0, tid, nth);
+  const int kk_out = MODE == MODE_FWD ? k_arr : 0;
+
+  // ------------------------------------------------------------ producer warp
+  if (tid >= nth) {
+    if (!tma || tid != nth) return;
+    int64_t wl = blockIdx.x;  // next item to load
+    for (int s2 = 0; s2 < 2 && wl < total; ++s2, wl += gridDim.x) {
+      int64_t g, b;
+      split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+      issue_loads_tma<MODE>(a, k_arr, b, g, stage0 + s2 * SB, &full[s2]);
+    }
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      const int st = it & 1;
+      V* buf = stage0 + st * SB;
+      mbar_wait(&done[st], (uint32_t)(it >> 1) & 1u);
+      int64_t g, b;
+      split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+      if (g < a.nlines) issue_stores_tma(a, kk_out, b, g, buf);
+      if (wl < total) {
+        bulk_wait_read0();  // this stage's results have left shared memory
+        split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+        issue_loads_tma<MODE>(a, k_arr, b, g, buf, &full[st]);
+        wl += gridDim.x;
+      }
+    }
+    bulk_wait0();
+    return;
   }
-  for (int it = 0; w < total; w += gridDim.x, ++it) {
+
+  // ------------------------------------------------------------ compute warps
+  const V* tw = twtab + lane;  // this lane's FFT twiddle column
+  PhaseClock pc;
+  pc.start(a.phase_prof != nullptr);
+  if (!tma && blockIdx.x < total) {
+    int64_t g0, b0;
+    split_item(blockIdx.x, a.nbatch, a.ngroups, a.batch_fastest, b0, g0);
+    issue_loads_cp<MODE>(a, k_arr, b0, g0, stage0, tid, nth);
+  }
+  int it = 0;
+  for (int64_t w = blockIdx.x; w < total; w += gridDim.x, ++it) {
     const int st = it & 1;
     V* buf = stage0 + st * SB;
     V* gbuf = buf + q * M;
@@ -351,49 +523,41 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
     split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
     const bool live = g < a.nlines;
     V* Fr = buf + r * M;  // this warp's residue row (also its FFT exchange area)
-    if (tma_in) mbar_wait(&bars[st], (uint32_t)(it >> 1) & 1u);
-    else { cp_wait0(); __syncthreads(); }
+    pc.mark(7);
+    if (tma) mbar_wait(&full[st], (uint32_t)(it >> 1) & 1u);
+    else { cp_wait0(); compute_sync(nth); }
+    pc.mark(0);
 
     // step 1: fold (FWD, CONV) or the inverse FFT of the spectrum (INV)
     if constexpr (MODE == MODE_INV) {
       V v[16];
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fr[k2 * 32 + lane];
-      w512::fft_inv(v, Fr, lane, w1l);
+      w512::fft_inv(v, Fr, lane, tw);
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
     } else {
-      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twM1, tid, nth);
+      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twcol, tid, nth);
     }
-    __syncthreads();
-
-    // the next item's loads go to the other stage (whose stores were issued one
-    // step earlier and have been read out of shared memory by now)
-    {
+    pc.mark(1);
+    compute_sync(nth);
+    pc.mark(2);
+    if (!tma) {  // fallback: the compute warps copy the next item into the other stage
       const int64_t wn = w + gridDim.x;
       if (wn < total) {
         int64_t gn, bn;
         split_item(wn, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
         V* nb = stage0 + (st ^ 1) * SB;
-        if (tma_in) {
-          if (tid == 0) {
-            if (tma_out) bulk_wait_read0();
-            issue_loads_tma<MODE>(a, k_arr, bn, gn, nb, &bars[st ^ 1]);
-          }
-        } else {
-          if (tma_out && tid == 0) bulk_wait_read0();
-          __syncthreads();
-          issue_loads_cp<MODE>(a, k_arr, bn, gn, nb, tid, nth);
-        }
+        issue_loads_cp<MODE>(a, k_arr, bn, gn, nb, tid, nth);
       }
     }
-
+    pc.mark(3);
     if constexpr (MODE == MODE_FWD) {
       V v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = Fr[lane + 32 * i];
-      w512::fft_fwd(v, Fr, lane, w1l);
+      w512::fft_fwd(v, Fr, lane, tw);
       __syncwarp();
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) Fr[k2 * 32 + lane] = v[k2];  // lane-major spectrum
@@ -401,7 +565,7 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
       V F[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) F[i] = Fr[lane + 32 * i];
-      w512::fft_fwd(F, Fr, lane, w1l);
+      w512::fft_fwd(F, Fr, lane, tw);
       // short input: p_g = 1, w[s] = (1/prod M1) zeta_{M1}^{r s} g[s], s = lane + 32 i;
       // twiddles by four interleaved recurrences of step zeta_{M1}^{128 r}
       V v[16];
@@ -425,31 +589,32 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
         }
       }
       __syncwarp();
-      w512::fft_fwd(v, Fr, lane, w1l);
+      w512::fft_fwd(v, Fr, lane, tw);
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = cmul(F[k], v[k]);
-      w512::fft_inv(v, Fr, lane, w1l);
+      w512::fft_inv(v, Fr, lane, tw);
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
     }
+    pc.mark(4);
     if constexpr (MODE != MODE_FWD) {
-      __syncthreads();
-      unfold_all<QC>(buf, q, a.out.T, zt, twM1, tid, nth);
+      compute_sync(nth);
+      pc.mark(5);
+      unfold_all<QC>(buf, q, a.out.T, zt, twcol, tid, nth);
     }
-    // results are in stage slots j < out.L: hand them to the async proxy and store
-    const int kk = MODE == MODE_FWD ? k_arr : 0;
-    if (tma_out) {
+    pc.mark(6);
+    // results are in stage slots j < out.L
+    if (tma) {
       fence_async_smem();
-      __syncthreads();
-      if (tid == 0 && live) issue_stores_tma(a, kk, b, g, buf);
+      mbar_arrive(&done[st]);  // the producer stores them
     } else {
-      __syncthreads();
-      if (live) stores_st(a, kk, b, g, buf, tid, nth);
-      __syncthreads();
+      compute_sync(nth);
+      if (live) stores_st(a, kk_out, b, g, buf, tid, nth);
+      compute_sync(nth);
     }
   }
-  if (tid == 0 && tma_out) bulk_wait0();
+  pc.flush(a.phase_prof);
 }
 
 }  // namespace s512

@@ -1,17 +1,15 @@
-// hd_w512.cuh -- warp-level engine for FFT size m = 512 (complex double).
+// hd_w512.cuh -- register FFT of size m = 512 (complex double) for one warp.
 //
 // One warp owns one residue r of one line: its size-512 FFT (PAPER.md:104,
 // "W <- m F(W)") runs in registers as 512 = 16 x 16 x 2:
 //   L1  radix-16 over x[lane + 32 i] (16 values per lane), twiddle zeta_512^{lane j}
 //   --  warp-local transpose through shared memory (no CTA barrier)
-//   L2  radix-16 over the stride-2 decimation of each 32-point sub-problem,
-//       twiddle zeta_32^{(lane&1) k2}
-//   L3  radix-2 between lane pairs (shuffle)
-// Lane u then holds frequency f = (u>>1) + 16 k2 + 256 (u&1) in register k2.  The
-// spectrum is stored in the SAME digit-reversed order as the generic radix-8 engine
-// (position = base-8 digit reversal of f), so the internal spectral layout does not
-// depend on which engine ran.  The inverse is the exact adjoint (negative exponent,
-// PAPER.md:121).  The multi-pass structure (fold, product, unfold) is unchanged.
+//   L2  radix-16 over the stride-2 decimation of each 32-point sub-problem
+//   L3  radix-2 between lane pairs: each lane of a pair takes half of the 16
+//       butterflies (one shuffle of 8 values each way), twiddle zeta_32^{k}
+// Lane u then holds frequency freq_of(u, k) in register k.  The twiddles come from a
+// per-lane shared-memory column (TwTab) filled once per CTA.  The inverse is the
+// exact adjoint (negative exponent).
 #pragma once
 #include "hd_device.cuh"
 
@@ -58,38 +56,15 @@ template <int S> __device__ __forceinline__ void dft16(V* v) {
 // exchange slot of element (row j < 16, column t < 32) inside a 512-slot region
 __device__ __forceinline__ int ex(int j, int t) { return j * 32 + (t ^ ((j & 3) << 1)); }
 
-// zeta_32^k, k < 16 (constant bank operands, no load instructions)
-__constant__ double2 c_w32[16] = {
-    {1.0, 0.0},
-    {0.98078528040323044913, 0.19509032201612826785},
-    {0.92387953251128675613, 0.38268343236508977173},
-    {0.83146961230254523708, 0.55557023301960222474},
-    {0.70710678118654752440, 0.70710678118654752440},
-    {0.55557023301960222474, 0.83146961230254523708},
-    {0.38268343236508977173, 0.92387953251128675613},
-    {0.19509032201612826785, 0.98078528040323044913},
-    {0.0, 1.0},
-    {-0.19509032201612826785, 0.98078528040323044913},
-    {-0.38268343236508977173, 0.92387953251128675613},
-    {-0.55557023301960222474, 0.83146961230254523708},
-    {-0.70710678118654752440, 0.70710678118654752440},
-    {-0.83146961230254523708, 0.55557023301960222474},
-    {-0.92387953251128675613, 0.38268343236508977173},
-    {-0.98078528040323044913, 0.19509032201612826785}};
 
-// L1 twiddles w[j] = zeta_512^{lane j}, j = 1..15, from w1 = zeta_512^{lane} by a
-// product tree of depth <= 4 (w[0] unused)
-__device__ __forceinline__ void l1_twiddles(V w1, V* w) {
-  w[1] = w1;
-  w[2] = cmul(w1, w1);
-  w[4] = cmul(w[2], w[2]);
-  w[8] = cmul(w[4], w[4]);
-  w[3] = cmul(w[2], w1);
-  w[5] = cmul(w[4], w1);
-  w[6] = cmul(w[4], w[2]);
-  w[7] = cmul(w[4], w[3]);
-#pragma unroll
-  for (int j = 9; j < 16; ++j) w[j] = cmul(w[8], w[j - 8]);
+// Per-lane twiddle column (shared memory, [kTwRows][32], read at tw[row * 32]):
+//   rows 0..14:  zeta_512^{lane (j+1)}                (L1)
+//   rows 15..22: zeta_32^{k + 8 (lane & 1)}, k < 8     (L3)
+constexpr int kTwRows = 23;
+__device__ __forceinline__ V tw_entry(const V* twm512, int row, int lane) {
+  if (row < 15) return ldg(twm512 + (lane * (row + 1)) % 512);
+  const int kk = (row - 15) + 8 * (lane & 1);
+  return ldg(twm512 + 16 * kk);
 }
 
 __device__ __forceinline__ V shfl_x1(V a) {
@@ -99,21 +74,17 @@ __device__ __forceinline__ V shfl_x1(V a) {
   return r;
 }
 
-// frequency held by (lane, k2) after the forward transform, and its position in the
-// generic engine's digit-reversed order
-__device__ __forceinline__ int freq_of(int lane, int k2) { return (lane >> 1) + 16 * k2 + 256 * (lane & 1); }
-__device__ __forceinline__ int pos_of_freq(int f) { return ((f & 7) << 6) | (f & 56) | (f >> 6); }
+// frequency held by register k of lane u after the forward transform
+__device__ __forceinline__ int freq_of(int u, int k) {
+  return (u >> 1) + 16 * ((k & 7) + 8 * (u & 1)) + 256 * (k >> 3);
+}
 
-// Forward FFT-512.  In: a[i] = x[lane + 32 i].  Out: a[k2] = X[freq_of(lane, k2)].
-// E: this warp's 512-slot exchange region (E[ex(j,t)]); w1l = zeta_512^{lane}.
-__device__ __forceinline__ void fft_fwd(V* a, V* E, int lane, V w1l) {
+// Forward FFT-512.  In: a[i] = x[lane + 32 i].  Out: a[k] = X[freq_of(lane, k)].
+// E: this warp's 512-slot exchange region (E[ex(j,t)]); tw: this lane's twiddle column.
+__device__ __forceinline__ void fft_fwd(V* a, V* E, int lane, const V* tw) {
   dft16<+1>(a);
-  {
-    V w[16];
-    l1_twiddles(w1l, w);
 #pragma unroll
-    for (int j = 1; j < 16; ++j) a[j] = cmul(a[j], w[j]);
-  }
+  for (int j = 1; j < 16; ++j) a[j] = cmul(a[j], tw[(j - 1) * 32]);
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 16; ++j) E[ex(j, lane)] = a[j];
@@ -122,32 +93,40 @@ __device__ __forceinline__ void fft_fwd(V* a, V* E, int lane, V w1l) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) a[i] = E[ex(jj, t2 + 2 * i)];
   dft16<+1>(a);
+  // even lane holds A[k], odd lane B[k] (k < 16); after the exchange lane t2 holds
+  // A[k + 8 t2] in a[k] and B[k + 8 t2] in a[k + 8], k < 8
 #pragma unroll
-  for (int k = 1; k < 16; ++k) {
-    const V aw = cmul(a[k], c_w32[k]);
-    a[k] = t2 ? aw : a[k];
+  for (int k = 0; k < 8; ++k) {
+    const V snd = t2 ? a[k] : a[k + 8];
+    const V rcv = shfl_x1(snd);
+    if (t2) a[k] = rcv; else a[k + 8] = rcv;
   }
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const V o = shfl_x1(a[k]);
-    a[k] = t2 ? csub(o, a[k]) : cadd(a[k], o);
+  for (int k = 0; k < 8; ++k) {
+    const V wb = cmul(a[k + 8], tw[(15 + k) * 32]);  // zeta_32^{k + 8 t2} B
+    const V A = a[k];
+    a[k] = cadd(A, wb);
+    a[k + 8] = csub(A, wb);
   }
 }
 
-// Inverse FFT-512 (adjoint of fft_fwd).  In: a[k2] = Y[freq_of(lane, k2)].
+// Inverse FFT-512 (adjoint of fft_fwd).  In: a[k] = Y[freq_of(lane, k)].
 // Out: a[i] = sum_f zeta_512^{-(lane + 32 i) f} Y[f].
-__device__ __forceinline__ void fft_inv(V* a, V* E, int lane, V w1l) {
+__device__ __forceinline__ void fft_inv(V* a, V* E, int lane, const V* tw) {
   const int jj = lane >> 1, t2 = lane & 1;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const V o = shfl_x1(a[k]);
-    a[k] = t2 ? csub(o, a[k]) : cadd(a[k], o);
+  for (int k = 0; k < 8; ++k) {
+    const V x0 = a[k], x1 = a[k + 8];
+    a[k] = cadd(x0, x1);                                  // A'[k + 8 t2]
+    a[k + 8] = cmulc(csub(x0, x1), tw[(15 + k) * 32]);    // B'[k + 8 t2]
   }
 #pragma unroll
-  for (int k = 1; k < 16; ++k) {
-    const V aw = cmulc(a[k], c_w32[k]);
-    a[k] = t2 ? aw : a[k];
+  for (int k = 0; k < 8; ++k) {
+    const V snd = t2 ? a[k] : a[k + 8];
+    const V rcv = shfl_x1(snd);
+    if (t2) a[k] = rcv; else a[k + 8] = rcv;
   }
+  // even lane: a = A'[0..15]; odd lane: a = B'[0..15]
   dft16<-1>(a);
   __syncwarp();
 #pragma unroll
@@ -155,12 +134,8 @@ __device__ __forceinline__ void fft_inv(V* a, V* E, int lane, V w1l) {
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 16; ++j) a[j] = E[ex(j, lane)];
-  {
-    V w[16];
-    l1_twiddles(w1l, w);
 #pragma unroll
-    for (int j = 1; j < 16; ++j) a[j] = cmulc(a[j], w[j]);
-  }
+  for (int j = 1; j < 16; ++j) a[j] = cmulc(a[j], tw[(j - 1) * 32]);
   dft16<-1>(a);
 }
 
