@@ -446,7 +446,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   int threads = L.threads;
   if (use_s512(dt, L)) {
     fn = hd::lookup_s512(L.mode, L.a.q);
-    threads = 32 * (L.a.q + 1);
+    threads = hd::s512_threads(L.a.q, L.mode);
     smem = hd::s512_smem_bytes(L.a.q, L.mode);
     prepare_tma(L);
   } else {
@@ -485,7 +485,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     unsigned long long h[8];
     cudaMemcpyAsync(h, d_phase, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    const double n = (double)total * (threads / 32 - 1);
+    const double n = (double)total * L.a.q;
     fprintf(stderr, "[phase] %-8s", L.name);
     for (int i = 0; i < 8; ++i) fprintf(stderr, " %7.0f", h[i] / n);
     fprintf(stderr, "\n");

@@ -13,6 +13,7 @@ LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
 LaunchFn lookup_s512(int mode, int q);
 constexpr int kS512QMax = 11;
 size_t s512_smem_bytes(int q, int mode);
+int s512_threads(int q, int mode);
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],

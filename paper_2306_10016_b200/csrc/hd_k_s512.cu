@@ -43,6 +43,8 @@ LaunchFn lookup_s512(int mode, int q) {
   }
 }
 
+int s512_threads(int q, int mode) { (void)mode; return 32 * (q + 1); }
+
 size_t s512_smem_bytes(int q, int mode) {
   return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 +
                                           2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));

@@ -67,6 +67,9 @@ __device__ __forceinline__ void bulk_load(V* dst, const V* src, uint32_t bytes, 
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const V* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_store(const CUtensorMap* map, const int* c, const V* src) {
   asm volatile(
       "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
@@ -170,6 +173,18 @@ __device__ __forceinline__ void issue_loads_tma(const PassArgs& a, int k_arr, in
       }
     }
   }
+}
+
+// L2 prefetch of a contiguous input line one item further ahead than the loads
+// (tensor-map lines are not prefetched: the strided prefetch competes with the
+// loads for the TMA unit and measured slower)
+template <int MODE>
+__device__ __forceinline__ void issue_prefetch(const PassArgs& a, int k_arr, int64_t b, int64_t g) {
+  if (g >= a.nlines || a.tm_in.kind != TMA_BULK) return;
+  const LineIn& in = a.in_f;
+  const int kk = MODE == MODE_FWD ? k_arr : 0;
+  bulk_prefetch_l2(reinterpret_cast<const V*>(in.ptr[kk]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g),
+                   (uint32_t)in.L * 16u);
 }
 
 template <int MODE>
@@ -434,6 +449,33 @@ __device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, co
 // Shared memory: [full x2, done x2 | pad][zt 16x16][tw 23x32][col 512]
 //                [stage 0][stage 1], stage = q*512 (+512 CONV).
 // ---------------------------------------------------------------------------
+// The short input's transform for residue r (p_g = 1): w[s] = (1/prod M1)
+// zeta_{M1}^{r s} g[s], s = lane + 32 i, then the size-512 FFT (E: exchange area).
+// LOWHALF (L_g <= 256): the upper half of w is zero.  Twiddles by four
+// interleaved recurrences of step zeta_{M1}^{128 r}.
+template <bool LOWHALF>
+__device__ __forceinline__ void g_transform(V* v, const V* gbuf, int Lg, int r, int lane, const V* twM1,
+                                            double scale, V* E, const V* tw) {
+  const V st1 = ldg(twM1 + r * 32);
+  const V st4 = ldg(twM1 + r * 128);
+  V wc[4];
+  wc[0] = cscale(ldg(twM1 + r * lane), scale);
+  wc[1] = cmul(wc[0], st1);
+  wc[2] = cmul(wc[1], st1);
+  wc[3] = cmul(wc[2], st1);
+#pragma unroll
+  for (int i = 0; i < (LOWHALF ? 8 : 16); ++i) {
+    const int s = lane + 32 * i;
+    v[i] = (s < Lg) ? cmul(gbuf[s], wc[i & 3]) : cmk<V>(0, 0);
+    if ((i & 3) == 3) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) wc[k] = cmul(wc[k], st4);
+    }
+  }
+  __syncwarp();
+  w512::fft_fwd<LOWHALF>(v, E, lane, tw);
+}
+
 __device__ __forceinline__ void compute_sync(int n) { asm volatile("bar.sync 1, %0;" :: "r"(n) : "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(su32(bar)) : "memory");
@@ -486,6 +528,11 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
       split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
       issue_loads_tma<MODE>(a, k_arr, b, g, stage0 + s2 * SB, &full[s2]);
     }
+    if (wl < total) {
+      int64_t g, b;
+      split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+      issue_prefetch<MODE>(a, k_arr, b, g);
+    }
     int it = 0;
     for (int64_t w = blockIdx.x; w < total; w += gridDim.x, ++it) {
       const int st = it & 1;
@@ -499,6 +546,10 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
         split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
         issue_loads_tma<MODE>(a, k_arr, b, g, buf, &full[st]);
         wl += gridDim.x;
+        if (wl < total) {  // and the item after it into L2
+          split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+          issue_prefetch<MODE>(a, k_arr, b, g);
+        }
       }
     }
     bulk_wait0();
@@ -566,30 +617,13 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
 #pragma unroll
       for (int i = 0; i < 16; ++i) F[i] = Fr[lane + 32 * i];
       w512::fft_fwd(F, Fr, lane, tw);
-      // short input: p_g = 1, w[s] = (1/prod M1) zeta_{M1}^{r s} g[s], s = lane + 32 i;
-      // twiddles by four interleaved recurrences of step zeta_{M1}^{128 r}
       V v[16];
       {
         const int Lg = live ? (int)a.in_g.L : 0;
-        const V st1 = ldg(twM1 + r * 32);
-        const V st4 = ldg(twM1 + r * 128);
-        V wc[4];
-        wc[0] = cscale(ldg(twM1 + r * lane), a.scale);
-        wc[1] = cmul(wc[0], st1);
-        wc[2] = cmul(wc[1], st1);
-        wc[3] = cmul(wc[2], st1);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int s = lane + 32 * i;
-          v[i] = (s < Lg) ? cmul(gbuf[s], wc[i & 3]) : cmk<V>(0, 0);
-          if ((i & 3) == 3) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) wc[k] = cmul(wc[k], st4);
-          }
-        }
+        __syncwarp();
+        if (Lg <= M / 2) g_transform<true>(v, gbuf, Lg, r, lane, twM1, a.scale, Fr, tw);
+        else g_transform<false>(v, gbuf, Lg, r, lane, twM1, a.scale, Fr, tw);
       }
-      __syncwarp();
-      w512::fft_fwd(v, Fr, lane, tw);
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = cmul(F[k], v[k]);
       w512::fft_inv(v, Fr, lane, tw);

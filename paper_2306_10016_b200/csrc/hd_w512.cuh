@@ -20,16 +20,28 @@ using V = double2;
 
 // 16-point DFT in registers, y_k = sum_n v_n zeta_16^{S n k}, natural order out.
 // 4 x 4 Cooley-Tukey: n = 4 n1 + n2, k = k1 + 4 k2.
-template <int S> __device__ __forceinline__ void dft16(V* v) {
+// LOWHALF: the input's upper half v[8..15] is zero (a short input padded to 512,
+// e.g. the kernel g with L_g <= 256); the first radix-4 layer then reduces to
+// 2-point sums (32 fewer FP64 operations).
+template <int S, bool LOWHALF = false> __device__ __forceinline__ void dft16(V* v) {
   const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
   const double h = 0.70710678118654752440;
   V A[4][4];
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) {
-    V t[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
-    dft4<V, S>(t);
+    if constexpr (LOWHALF) {
+      const V x0 = v[n2], x1 = v[4 + n2];
+      const V ix1 = cmul_si<V, S>(x1);
+      A[n2][0] = cadd(x0, x1);
+      A[n2][1] = cadd(x0, ix1);
+      A[n2][2] = csub(x0, x1);
+      A[n2][3] = csub(x0, ix1);
+    } else {
+      V t[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+      dft4<V, S>(t);
 #pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1) A[n2][k1] = t[k1];
+      for (int k1 = 0; k1 < 4; ++k1) A[n2][k1] = t[k1];
+    }
   }
   // twiddles zeta_16^{S n2 k1}
   auto rot = [&](V a, double c, double s) {  // a * (c + i S s)
@@ -79,10 +91,12 @@ __device__ __forceinline__ int freq_of(int u, int k) {
   return (u >> 1) + 16 * ((k & 7) + 8 * (u & 1)) + 256 * (k >> 3);
 }
 
-// Forward FFT-512.  In: a[i] = x[lane + 32 i].  Out: a[k] = X[freq_of(lane, k)].
+// Forward FFT-512.  In: a[i] = x[lane + 32 i] (LOWHALF: a[8..15] = 0, not read).
+// Out: a[k] = X[freq_of(lane, k)].
 // E: this warp's 512-slot exchange region (E[ex(j,t)]); tw: this lane's twiddle column.
+template <bool LOWHALF = false>
 __device__ __forceinline__ void fft_fwd(V* a, V* E, int lane, const V* tw) {
-  dft16<+1>(a);
+  dft16<+1, LOWHALF>(a);
 #pragma unroll
   for (int j = 1; j < 16; ++j) a[j] = cmul(a[j], tw[(j - 1) * 32]);
   __syncwarp();
