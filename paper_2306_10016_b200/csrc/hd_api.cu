@@ -23,7 +23,6 @@ using hd::PassArgs;
 
 namespace {
 thread_local std::string g_tls_error;
-constexpr int64_t kHugeTile = int64_t(1) << 30;
 }  // namespace
 
 struct hd_ctx {
@@ -276,7 +275,8 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
         if (c < best * 0.999) { best = c; bm = m; bD = D; bl = lines; }
       }
     }
-    const int lines = bl;
+    // one line per CTA where the staged m = 512 engine applies (hd_s512.cuh)
+    const int lines = (dt == HD_C128 && bm == 512 && bD == (int)cdiv(Mi, bm) && bD <= hd::kS512QMax) ? 1 : bl;
     p.axis[i].m = bm;
     p.axis[i].D = bD;
     p.axis[i].C = lines;
@@ -1353,7 +1353,7 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
   const int64_t Mi = (M && M[i] > 0) ? M[i] : Lout;
   const int m0 = base.axis[i].m;
   const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
-  std::vector<int> Ss = (ndim == 1) ? std::vector<int>{1} : std::vector<int>{1, 2, 4};
+  std::vector<int> Ss = (ndim == 1) ? std::vector<int>{1} : std::vector<int>{1, 2, 4, 8};
   for (int m = std::max(2, m0 / 2); m <= std::min(4096, m0 * 2); m *= 2) {
     const int q = (int)cdiv(Mi, m);
     for (int C : {1, 2}) {
@@ -1423,6 +1423,7 @@ hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int
     P.h = hp;
     if (complete_plan(ctx, dtype, ndim, N, Lf, Lg, M, &pl, P.ax) != HD_OK) return false;
     P.plan = pl;
+    choose_engines(P);
     for (int w = 0; w < 2; ++w)
       if (run_pipeline(ctx, P, nullptr, 0, st) != HD_OK) return false;
     std::vector<double> ts;

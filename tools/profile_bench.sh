@@ -14,6 +14,6 @@ NK=$(python -c "print({1:1,2:1,3:4,4:7,5:4}[$CFG])")
 python tools/run_config.py --config "$CFG" --steps 2 --plan "$PLAN" > gpurun_out/plain_${TAG}.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python tools/run_config.py --config "$CFG" --steps 2 --plan "$PLAN" > /dev/null 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"pass_kernel|w512" -s "$NK" -c "$NK" \
+ncu --set full --clock-control none --import-source on -k regex:"pass_kernel|s512" -s "$NK" -c "$NK" \
     -o gpurun_out/prof_${TAG} python tools/run_config.py --config "$CFG" --steps 2 --plan "$PLAN" > gpurun_out/ncu_${TAG}.log 2>&1
 echo "ncu rc=$?"
