@@ -124,9 +124,13 @@ struct PhaseClock {
     if (on) { const long long t = clock64(); acc[ph] += (unsigned long long)(t - t0); t0 = t; }
   }
   __device__ __forceinline__ void flush(unsigned long long* out) {
-    if (on && (threadIdx.x & 31) == 0)
+    if (on && (threadIdx.x & 31) == 0) {
 #pragma unroll
       for (int i = 0; i < kPhases; ++i) atomicAdd(out + i, acc[i]);
+      // per warp: transform phase (4) and its barrier (5)
+      atomicAdd(out + kPhases + 2 * (threadIdx.x >> 5), acc[4]);
+      atomicAdd(out + kPhases + 2 * (threadIdx.x >> 5) + 1, acc[5]);
+    }
   }
 };
 
