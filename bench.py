@@ -343,14 +343,17 @@ def run_ours(args, rank, world, local_rank):
     # end to end through the host-buffer C-ABI entry point (copies inside)
     e2e = None
     if not args.no_e2e and slab is None:
-        hh = torch.empty(out_shape, dtype=fd[0].dtype).pin_memory()
-        k2 = max(2, min(args.steps, 10))
-        ctx.hd_conv_host(fh, gh, hh, ndim=ndim, batch=batch, plan=plan)
+        # two result buffers: step k writes hh[k % 2] (asynchronous, double-buffered
+        # entry point: the copy-in of step k+1 overlaps the copy-out of step k)
+        hh = [torch.empty(out_shape, dtype=fd[0].dtype).pin_memory() for _ in range(2)]
+        k2 = max(4, min(args.steps, 20))
+        ctx.hd_conv_host(fh, gh, hh[0], ndim=ndim, batch=batch, plan=plan)
         if dist:
             dist.barrier()
         t = time.perf_counter()
-        for _ in range(k2):
-            ctx.hd_conv_host(fh, gh, hh, ndim=ndim, batch=batch, plan=plan)
+        for k in range(k2):
+            ctx.hd_conv_host_async(fh, gh, hh[k % 2], ndim=ndim, batch=batch, plan=plan)
+        ctx.host_sync()
         te = time.perf_counter() - t
         if dist:
             tt = torch.tensor([te], device=dev, dtype=torch.float64)

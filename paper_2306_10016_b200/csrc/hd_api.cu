@@ -35,6 +35,15 @@ struct hd_ctx {
   size_t ws_size = 0;
   void* io = nullptr;                   // device buffers for hd_conv_host
   size_t io_size = 0;
+  struct HostSlot {                     // hd_conv_host_async: double-buffered host I/O
+    void* io = nullptr;
+    size_t size = 0;
+    cudaStream_t st = nullptr;
+  };
+  HostSlot hslot[2];
+  int hnext = 0;
+  cudaEvent_t compute_done = nullptr;   // last enqueued convolution (shared workspace)
+  bool compute_pending = false;
   std::map<std::string, hd_plan_t> plan_cache;
   std::vector<std::pair<hd_plan_t, double>> tune_log;
   // profiling
@@ -901,6 +910,11 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   for (auto& kv : ctx->st32) cudaFree(kv.second);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
+  for (auto& sl : ctx->hslot) {
+    if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
+    if (sl.io) cudaFree(sl.io);
+  }
+  if (ctx->compute_done) cudaEventDestroy(ctx->compute_done);
   for (auto& p : ctx->prof)
     for (auto& ev : p.pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
   delete ctx;
@@ -1049,6 +1063,11 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
   const size_t need = (2 * N + 1) * inb + wsb;
   if (ctx->io_size < need) {
     if (ctx->io) cudaFree(ctx->io);
+  for (auto& sl : ctx->hslot) {
+    if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
+    if (sl.io) cudaFree(sl.io);
+  }
+  if (ctx->compute_done) cudaEventDestroy(ctx->compute_done);
     ctx->io = nullptr; ctx->io_size = 0;
     cudaError_t e = cudaMalloc(&ctx->io, need);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(explicit scratch)");
@@ -1099,6 +1118,11 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   const size_t need = N * (bf + bg) + bh;
   if (ctx->io_size < need) {
     if (ctx->io) cudaFree(ctx->io);
+  for (auto& sl : ctx->hslot) {
+    if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
+    if (sl.io) cudaFree(sl.io);
+  }
+  if (ctx->compute_done) cudaEventDestroy(ctx->compute_done);
     ctx->io = nullptr; ctx->io_size = 0;
     cudaError_t e = cudaMalloc(&ctx->io, need);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(host io)");
@@ -1123,6 +1147,73 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(h)");
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamSynchronize");
+  return HD_OK;
+}
+
+hd_status_t hd_conv_host_async(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
+                               const void* const* f, const int64_t* Lf, const void* const* g,
+                               const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan) {
+  Problem P;
+  hd_status_t s = setup(ctx, P, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan);
+  if (s != HD_OK) return s;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  hd_ctx::HostSlot& sl = ctx->hslot[ctx->hnext];
+  ctx->hnext ^= 1;
+  cudaError_t e;
+  if (!sl.st) {
+    e = cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamCreate");
+  }
+  if (!ctx->compute_done) {
+    e = cudaEventCreateWithFlags(&ctx->compute_done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaEventCreate");
+  }
+  const size_t eb = elem_bytes(dtype);
+  int64_t nf = batch, ng = P.shared_g ? 1 : batch, nh = batch;
+  for (int i = 0; i < ndim; ++i) { nf *= Lf[i]; ng *= Lg[i]; nh *= P.ax[i].O; }
+  const size_t bf = align256((size_t)nf * eb), bg = align256((size_t)ng * eb), bh = align256((size_t)nh * eb);
+  const size_t need = N * (bf + bg) + bh;
+  if (sl.size < need) {
+    cudaStreamSynchronize(sl.st);
+    if (sl.io) cudaFree(sl.io);
+    sl.io = nullptr; sl.size = 0;
+    e = cudaMalloc(&sl.io, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(host io slot)");
+    sl.size = need;
+  }
+  // copy-in on this slot's stream (after the slot's previous copy-out: same stream)
+  char* base = (char*)sl.io;
+  for (int k = 0; k < N; ++k) {
+    char* df = base + k * bf;
+    char* dg = base + N * bf + k * bg;
+    e = cudaMemcpyAsync(df, f[k], (size_t)nf * eb, cudaMemcpyHostToDevice, sl.st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(f)");
+    e = cudaMemcpyAsync(dg, g[k], (size_t)ng * eb, cudaMemcpyHostToDevice, sl.st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(g)");
+    P.f[k] = df;
+    P.g[k] = dg;
+  }
+  P.h = base + N * (bf + bg);
+  // the convolutions share the context workspace: run after the previous one
+  if (ctx->compute_pending) cudaStreamWaitEvent(sl.st, ctx->compute_done, 0);
+  s = run_pipeline(ctx, P, nullptr, 0, sl.st);
+  if (s != HD_OK) return s;
+  cudaEventRecord(ctx->compute_done, sl.st);
+  ctx->compute_pending = true;
+  e = cudaMemcpyAsync(h, P.h, (size_t)nh * eb, cudaMemcpyDeviceToHost, sl.st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(h)");
+  return HD_OK;
+}
+
+hd_status_t hd_host_sync(hd_ctx_t ctx) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  for (auto& sl : ctx->hslot) {
+    if (!sl.st) continue;
+    cudaError_t e = cudaStreamSynchronize(sl.st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamSynchronize(host slot)");
+  }
   return HD_OK;
 }
 

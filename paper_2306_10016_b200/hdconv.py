@@ -36,6 +36,7 @@ EXPORTED = [
     "hd_abi_version", "hd_create", "hd_destroy", "hd_last_error", "hd_plan_default",
     "hd_plan_complete", "hd_spectral_permutation", "hd_workspace_bytes", "hd_conv1d",
     "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host",
+    "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_log",
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_pass",
 ]
@@ -126,6 +127,8 @@ def _load():
         "hd_multiconv": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
         "hd_conv_explicit": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, PP, P], ctypes.c_int),
         "hd_conv_host": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, PP, P], ctypes.c_int),
+        "hd_conv_host_async": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, PP], ctypes.c_int),
+        "hd_host_sync": ([P], ctypes.c_int),
         "hd_forward_residues": ([P, ctypes.c_int, I64, P, I64, I32, I32, P, P], ctypes.c_int),
         "hd_backward_residues": ([P, ctypes.c_int, I64, P, I32, I32, P, I64, P], ctypes.c_int),
         "hd_tune": ([P, ctypes.c_int, I32, I32, I64, P, P, P, U32, I32, P, PP], ctypes.c_int),
@@ -335,6 +338,29 @@ class Context:
         self._chk(_lib.hd_conv_host(self.h, dt, nd, N, batch, fp, _i64arr(Lf), gp, _i64arr(Lg),
                                     ctypes.c_void_p(hp(h)), Mv, pp, _stream_ptr(stream)))
         return h
+
+    def hd_conv_host_async(self, fs, gs, h, ndim, batch=1, M=None, plan=None):
+        """Asynchronous hd_conv_host (double-buffered context streams): returns after
+        enqueueing; the buffers must stay alive and h unread until host_sync()."""
+        N = len(fs)
+        def hp(a):
+            return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+        nd = int(ndim)
+        Lf = list(fs[0].shape)[-nd:]
+        Lg = list(gs[0].shape)[-nd:]
+        is128 = (fs[0].dtype == np.complex128) if isinstance(fs[0], np.ndarray) else \
+            (str(fs[0].dtype) == "torch.complex128")
+        dt = HD_C128 if is128 else HD_C64
+        fp = (ctypes.c_void_p * N)(*[hp(t) for t in fs])
+        gp = (ctypes.c_void_p * N)(*[hp(t) for t in gs])
+        Mv = _i64arr(M) if M is not None else None
+        pp = ctypes.byref(plan) if plan is not None else None
+        self._chk(_lib.hd_conv_host_async(self.h, dt, nd, N, batch, fp, _i64arr(Lf), gp, _i64arr(Lg),
+                                          ctypes.c_void_p(hp(h)), Mv, pp))
+        return h
+
+    def host_sync(self):
+        self._chk(_lib.hd_host_sync(self.h))
 
     def hd_forward_residues(self, x, m, q, X=None, stream=None):
         """x: [nlines, L] -> X: [nlines, q*m] (internal residue order)."""

@@ -257,6 +257,25 @@ def test_host_entry_point(ctx):
     assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
 
 
+def test_host_async_pipeline(ctx):
+    """hd_conv_host_async: five calls in flight over the two context slots (copy-in
+    of call k+1 overlapping call k), different inputs, sizes and output buffers;
+    every result checked after one hd_host_sync."""
+    shapes = [((64, 50), (10, 12)), ((40, 33), (7, 9)), ((64, 50), (10, 12)), ((90, 20), (3, 31)),
+              ((64, 50), (10, 12))]
+    torch_ = pytest.importorskip("torch")
+    jobs = []
+    for i, (sf, sg) in enumerate(shapes):
+        f, g = synth.random_pair(700 + i, sf, sg)
+        ft, gt = torch_.from_numpy(f).pin_memory(), torch_.from_numpy(g).pin_memory()
+        h = torch_.zeros([a + b - 1 for a, b in zip(sf, sg)], dtype=torch_.complex128).pin_memory()
+        ctx.hd_conv_host_async([ft], [gt], h, ndim=2)
+        jobs.append((f, g, ft, gt, h))
+    ctx.host_sync()
+    for f, g, _, _, h in jobs:
+        assert oracle.rel_l2(h.numpy(), oracle.conv(f, g)) < 1e-11
+
+
 def test_alias_2d(ctx, H):
     f, g = synth.random_pair(71, (10, 12), (7, 5))
     p = H.Plan.make(2, [{"m": 4}, {"m": 4}], flags=H.HD_FLAG_ALLOW_ALIAS)
