@@ -49,12 +49,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(su32(bar)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase completes
+// (or ~1 ms passes) instead of re-issuing the probe, leaving issue slots to the
+// compute warps of its SM sub-partition
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = su32(bar);
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" :: "r"(su32(bar)), "r"(parity) : "memory");
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}" :: "r"(a), "r"(parity), "r"(1000000u) : "memory");
 }
 __device__ __forceinline__ void tma_load(V* dst, const CUtensorMap* map, const int* c, uint64_t* bar) {
   asm volatile(
@@ -378,6 +382,26 @@ __device__ __forceinline__ void fold_all(V* buf, int p, int L, bool live, int q,
   }
 }
 
+// q = 9 fold of one item by the 6 warps that do not share the SM sub-partition of
+// warps 0, 4, 8 (warp w runs on sub-partition (w + c) mod 4, so warps 0, 4, 8 always
+// share one and carry 3 of the 9 residues there): light thread lt < 192 folds the
+// columns lt, lt + 192 and (lt < 128) lt + 384.
+__device__ __forceinline__ void fold9_light(V* buf, int p, int L, bool live, const V* twcol, int lt) {
+  if (lt < 128) {
+    const int sc[3] = {lt, lt + 192, lt + 384};
+    const int rm[3] = {live ? L - sc[0] : 0, live ? L - sc[1] : 0, live ? L - sc[2] : 0};
+    const V w1[3] = {twcol[sc[0]], twcol[sc[1]], twcol[sc[2]]};
+    if (p <= 4) fold_col9<4, 3>(buf, sc, rm, w1);
+    else fold_col9<8, 3>(buf, sc, rm, w1);
+  } else {
+    const int sc[2] = {lt, lt + 192};
+    const int rm[2] = {live ? L - sc[0] : 0, live ? L - sc[1] : 0};
+    const V w1[2] = {twcol[sc[0]], twcol[sc[1]]};
+    if (p <= 4) fold_col9<4, 2>(buf, sc, rm, w1);
+    else fold_col9<8, 2>(buf, sc, rm, w1);
+  }
+}
+
 // In-place unfold of column s: rows r < q hold V_r[s]; rows t < T receive
 // h[tm+s] = sum_r zeta_q^{-tr} conj(zeta_{M1}^{rs}) V_r[s], in pairs (t, q-t).
 template <int QC, int QM>
@@ -502,6 +526,7 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
   const int k_arr = blockIdx.z;
   const int SB = q * M + (MODE == MODE_CONV ? M : 0);
   const bool tma = a.tm_in.kind != TMA_NONE && a.tm_out.kind != TMA_NONE;
+  constexpr bool kPipeFold = (MODE == MODE_CONV && QC == 9);
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
   if (QC == 0) {
@@ -579,12 +604,20 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
     const bool live = g < a.nlines;
     V* Fr = buf + r * M;  // this warp's residue row (also its FFT exchange area)
     pc.mark(7);
-    if (tma) mbar_wait(&full[st], (uint32_t)(it >> 1) & 1u);
-    else { cp_wait0(); compute_sync(nth); }
+    // CONV, q = 9, TMA: the fold of item it + 1 is done by the light warps during
+    // item it's transforms (kPipeFold); only the first item is folded up front.
+    const bool pipe_fold = kPipeFold && tma;
+    const bool folded = pipe_fold && it > 0;
+    if (!folded) {
+      if (tma) mbar_wait(&full[st], (uint32_t)(it >> 1) & 1u);
+      else { cp_wait0(); compute_sync(nth); }
+    }
     pc.mark(0);
 
     // step 1: fold (FWD, CONV) or the inverse FFT of the spectrum (INV)
-    if constexpr (MODE == MODE_INV) {
+    if (folded) {
+      // done during the previous item
+    } else if constexpr (MODE == MODE_INV) {
       V v[16];
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fr[k2 * 32 + lane];
@@ -634,6 +667,16 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
+    }
+    if (pipe_fold && (r & 3) != 0) {  // light warps: fold the next item now
+      const int64_t wn = w + gridDim.x;
+      if (wn < total) {
+        int64_t gn, bn;
+        split_item(wn, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
+        mbar_wait(&full[st ^ 1], (uint32_t)((it + 1) >> 1) & 1u);
+        const int lt = (r - 1 - (r > 4 ? 1 : 0)) * 32 + lane;
+        fold9_light(stage0 + (st ^ 1) * SB, a.in_f.p, (int)a.in_f.L, gn < a.nlines, twcol, lt);
+      }
     }
     pc.mark(4);
     if constexpr (MODE != MODE_FWD) {
