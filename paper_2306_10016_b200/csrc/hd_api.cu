@@ -1063,11 +1063,6 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
   const size_t need = (2 * N + 1) * inb + wsb;
   if (ctx->io_size < need) {
     if (ctx->io) cudaFree(ctx->io);
-  for (auto& sl : ctx->hslot) {
-    if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
-    if (sl.io) cudaFree(sl.io);
-  }
-  if (ctx->compute_done) cudaEventDestroy(ctx->compute_done);
     ctx->io = nullptr; ctx->io_size = 0;
     cudaError_t e = cudaMalloc(&ctx->io, need);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(explicit scratch)");
@@ -1118,11 +1113,6 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   const size_t need = N * (bf + bg) + bh;
   if (ctx->io_size < need) {
     if (ctx->io) cudaFree(ctx->io);
-  for (auto& sl : ctx->hslot) {
-    if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
-    if (sl.io) cudaFree(sl.io);
-  }
-  if (ctx->compute_done) cudaEventDestroy(ctx->compute_done);
     ctx->io = nullptr; ctx->io_size = 0;
     cudaError_t e = cudaMalloc(&ctx->io, need);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(host io)");

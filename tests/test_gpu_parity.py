@@ -276,6 +276,30 @@ def test_host_async_pipeline(ctx):
         assert oracle.rel_l2(h.numpy(), oracle.conv(f, g)) < 1e-11
 
 
+def test_host_async_mixed_with_other_entries(H):
+    """The async slots survive the other host/explicit entry points resizing their
+    buffers, and a context with live slots closes cleanly (own context)."""
+    torch_ = pytest.importorskip("torch")
+    c = H.Context(0)
+    f, g = synth.random_pair(720, (64, 50), (10, 12))
+    ft, gt = torch_.from_numpy(f).pin_memory(), torch_.from_numpy(g).pin_memory()
+    ref = oracle.conv(f, g)
+    h1 = torch_.zeros(ref.shape, dtype=torch_.complex128).pin_memory()
+    c.hd_conv_host_async([ft], [gt], h1, ndim=2)
+    c.host_sync()
+    fb, gb = synth.random_pair(721, (300, 200), (40, 30))
+    hb = c.hd_conv_explicit([dev(fb)], [dev(gb)])   # grows the context's scratch
+    hh = np.zeros((339, 229), complex)
+    c.hd_conv_host([fb], [gb], hh, ndim=2)
+    h2 = torch_.zeros(ref.shape, dtype=torch_.complex128).pin_memory()
+    c.hd_conv_host_async([ft], [gt], h2, ndim=2)
+    c.host_sync()
+    assert oracle.rel_l2(h1.numpy(), ref) < 1e-11 and oracle.rel_l2(h2.numpy(), ref) < 1e-11
+    refb = oracle.conv(fb, gb)
+    assert oracle.rel_l2(host(hb), refb) < 1e-11 and oracle.rel_l2(hh, refb) < 1e-11
+    c.close()
+
+
 def test_alias_2d(ctx, H):
     f, g = synth.random_pair(71, (10, 12), (7, 5))
     p = H.Plan.make(2, [{"m": 4}, {"m": 4}], flags=H.HD_FLAG_ALLOW_ALIAS)
