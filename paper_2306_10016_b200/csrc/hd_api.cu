@@ -420,12 +420,12 @@ bool tma_desc_out(const LineOut& o, int64_t nlines, int64_t nbatch, int narr, hd
 // copies for anything a tensor map cannot express).
 void prepare_tma(Launch& L) {
   PassArgs& a = L.a;
-  const int narr_in = L.mode == hd::MODE_FWD ? (int)L.narrays : 1;
+  const int narr_in = L.mode == hd::MODE_FWD ? (int)L.narrays : (L.mode == hd::MODE_CONV ? a.npairs : 1);
   const int narr_out = L.mode == hd::MODE_FWD ? (int)L.narrays : 1;
   if (!tma_desc_in(a.in_f, a.nlines, a.nbatch, narr_in, a.tm_in, a.tm_in_map)) a.tm_in.kind = hd::TMA_NONE;
   if (L.mode == hd::MODE_CONV) {
     // both inputs of the convolution pass move by TMA or both by per-thread copies
-    if (!tma_desc_in(a.in_g, a.nlines, a.nbatch, 1, a.tm_in_g, &a.tm_in_g_map) || a.tm_in.kind == hd::TMA_NONE) {
+    if (!tma_desc_in(a.in_g, a.nlines, a.nbatch, a.npairs, a.tm_in_g, a.tm_in_g_map) || a.tm_in.kind == hd::TMA_NONE) {
       a.tm_in.kind = hd::TMA_NONE; a.tm_in_g.kind = hd::TMA_NONE;
     }
   }
@@ -448,12 +448,31 @@ bool use_s512(hd_dtype_t dt, const Launch& L) {
   return true;
 }
 
+// The staged multi-pair convolution pass (MODE_MCONV): N <= 6 pairs or p_g > 1,
+// q <= 6, both inputs by TMA.
+bool use_s512_mconv(hd_dtype_t dt, const Launch& L) {
+  if (dt != HD_C128 || L.m != 512 || L.lines != 1 || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
+  if (!L.auto_engine || !L.s512_axis || L.mode != hd::MODE_CONV) return false;
+  if (L.a.D != L.a.q || L.a.q > hd::s512_mconv_qmax()) return false;
+  return L.a.npairs <= hd::kTmaArrays && L.a.in_f.p <= 8 && L.a.in_g.p <= 8;
+}
+
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
   hd::LaunchFn fn;
   size_t smem;
   int threads = L.threads;
-  if (use_s512(dt, L)) {
+  bool staged = use_s512(dt, L);
+  bool mconv = false;
+  if (!staged && use_s512_mconv(dt, L)) {
+    prepare_tma(L);
+    mconv = L.a.tm_in.kind == hd::TMA_LINE_TILED || L.a.tm_in.kind == hd::TMA_BULK;
+  }
+  if (mconv) {
+    fn = hd::lookup_s512_mconv();
+    threads = 32 * (L.a.q + 1);
+    smem = hd::s512_smem_bytes(L.a.q, hd::MODE_MCONV);
+  } else if (staged) {
     fn = hd::lookup_s512(L.mode, L.a.q);
     threads = hd::s512_threads(L.a.q, L.mode);
     smem = hd::s512_smem_bytes(L.a.q, L.mode);

@@ -293,7 +293,7 @@ struct PassArgs {
   LineOut out;
   TmaLine tm_in, tm_in_g, tm_out;
   CUtensorMap tm_in_map[kTmaArrays];
-  CUtensorMap tm_in_g_map;
+  CUtensorMap tm_in_g_map[kTmaArrays];
   CUtensorMap tm_out_map[kTmaArrays];
   unsigned long long* phase_prof;  // debug (HD_PHASE_PROF=1): per-phase SM cycles, else null
   const void* tw_m;        // zeta_m^k,  k < m
@@ -309,7 +309,7 @@ struct PassArgs {
   int32_t batch_fastest;
 };
 
-enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2 };
+enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2, MODE_MCONV = 3 /* staged engine only */ };
 
 constexpr int kQF = 16;    // fast q-point DFT paths: q <= 16
 constexpr int kPF = 8;     // fast fold path: p <= 8

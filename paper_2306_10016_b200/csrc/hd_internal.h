@@ -14,6 +14,9 @@ LaunchFn lookup_s512(int mode, int q);
 constexpr int kS512QMax = 11;
 size_t s512_smem_bytes(int q, int mode);
 int s512_threads(int q, int mode);
+// staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()
+LaunchFn lookup_s512_mconv();
+int s512_mconv_qmax();
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],

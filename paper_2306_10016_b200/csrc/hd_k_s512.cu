@@ -43,9 +43,36 @@ LaunchFn lookup_s512(int mode, int q) {
   }
 }
 
+static cudaError_t launch_s512_mconv(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
+  constexpr int NT = 32 * (s512::kMconvQMax + 1);
+  auto kern = s512::s512_mconv_kernel<NT>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (nt < 64 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if ((int64_t)grid.x > sms) grid.x = (unsigned)sms;
+  kern<<<grid, nt, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+LaunchFn lookup_s512_mconv() { return launch_s512_mconv; }
+int s512_mconv_qmax() { return s512::kMconvQMax; }
+
+// compute warps + the producer warp
 int s512_threads(int q, int mode) { (void)mode; return 32 * (q + 1); }
 
 size_t s512_smem_bytes(int q, int mode) {
+  if (mode == MODE_MCONV)
+    return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 + 2 * (2 * q * 512));
   return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 +
                                           2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));
 }

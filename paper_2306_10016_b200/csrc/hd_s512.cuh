@@ -177,7 +177,7 @@ __device__ __forceinline__ void issue_loads_tma(const PassArgs& a, int k_arr, in
       int c[5];
       for (int j0 = 0; j0 < (int)ig.L; j0 += kBox) {
         tma_coords(a.tm_in_g, b, g, j0, c);
-        tma_load(buf + a.q * M + j0, &a.tm_in_g_map, c, bar);
+        tma_load(buf + a.q * M + j0, &a.tm_in_g_map[0], c, bar);
       }
     }
   }
@@ -696,6 +696,157 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
     }
   }
   pc.flush(a.phase_prof);
+}
+
+// ---------------------------------------------------------------------------
+// MODE_MCONV: the convolution pass for N pairs (multi-convolution, PAPER.md:19;
+// h = sum_k f_k * g_k, BASELINE config 5) and short inputs of several blocks
+// (p_g <= 8).  One work item = one line; the producer streams its N pairs through
+// the two-stage ring (stage = 2q rows: f_k folded into rows 0..q-1, g_k into rows
+// q..2q-1).  Warp r keeps the running sum of F_k G_k of residue r in registers:
+//   fold f_k, g_k (thread per column) -> F-FFT in row r (spectrum parked there,
+//   lane-major) -> G-FFT in row q + r -> acc += F G;  after the last pair:
+//   inverse FFT of (1/prod M1) acc -> row r -> unfold -> the producer stores.
+// q <= 6 (two stages of 2q rows), blockDim = 32 (q + 1): at most two warps per
+// SM sub-partition, so acc and a transform fit in registers.
+// ---------------------------------------------------------------------------
+constexpr int kMconvQMax = 6;
+
+__device__ __forceinline__ void issue_loads_pair(const PassArgs& a, int64_t b, int64_t g, int k, V* buf,
+                                                 uint64_t* bar) {
+  const bool live = g < a.nlines;
+  const int Lf = (int)a.in_f.L, Lg = (int)a.in_g.L;
+  mbar_expect_tx(bar, live ? (uint32_t)(((Lf + kBox - 1) / kBox + (Lg + kBox - 1) / kBox) * kBox * 16) : 0u);
+  if (!live) return;
+  int c[5];
+  for (int j0 = 0; j0 < Lf; j0 += kBox) {
+    tma_coords(a.tm_in, b, g, j0, c);
+    tma_load(buf + j0, &a.tm_in_map[k], c, bar);
+  }
+  V* gb = buf + a.q * M;
+  for (int j0 = 0; j0 < Lg; j0 += kBox) {
+    tma_coords(a.tm_in_g, b, g, j0, c);
+    tma_load(gb + j0, &a.tm_in_g_map[k], c, bar);
+  }
+}
+
+template <int NTMAX>
+__global__ void __launch_bounds__(NTMAX, 1) s512_mconv_kernel(const __grid_constant__ PassArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* done = full + 2;
+  V* zt = reinterpret_cast<V*>(smem_raw + 128);
+  V* twtab = zt + kQF * kQF;
+  V* twcol = twtab + w512::kTwRows * 32;
+  V* stage0 = twcol + M;
+  const int q = a.q, N = a.npairs;
+  const int tid = threadIdx.x, lane = tid & 31, r = tid >> 5;
+  const int nth = 32 * q;
+  const int SB = 2 * q * M;
+  const V* twm = reinterpret_cast<const V*>(a.tw_m);
+  const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
+  for (int i = tid; i < kQF * kQF; i += blockDim.x) {
+    const int rr = i / kQF, t = i % kQF;
+    zt[i] = ldg(twM1 + (int64_t)((rr * t) % q) * M);
+  }
+  for (int i = tid; i < w512::kTwRows * 32; i += blockDim.x) twtab[i] = w512::tw_entry(twm, i >> 5, i & 31);
+  for (int i = tid; i < M; i += blockDim.x) twcol[i] = ldg(twM1 + i);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&done[0], nth);
+    mbar_init(&done[1], nth);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = a.nbatch * a.ngroups;
+  const int64_t nit = total > blockIdx.x ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nsteps = nit * N;  // (line, pair) steps of this CTA
+
+  if (tid >= nth) {  // producer warp (lane 0)
+    if (tid != nth) return;
+    auto step_item = [&](int64_t sg, int64_t& b, int64_t& g, int& k) {
+      const int64_t it = sg / N;
+      k = (int)(sg - it * N);
+      split_item(blockIdx.x + it * gridDim.x, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+    };
+    int64_t sl = 0;
+    for (; sl < 2 && sl < nsteps; ++sl) {
+      int64_t b, g; int k;
+      step_item(sl, b, g, k);
+      issue_loads_pair(a, b, g, k, stage0 + (sl & 1) * SB, &full[sl & 1]);
+    }
+    for (int64_t sg = 0; sg < nsteps; ++sg) {
+      const int st = (int)(sg & 1);
+      V* buf = stage0 + st * SB;
+      mbar_wait(&done[st], (uint32_t)(sg >> 1) & 1u);
+      int64_t b, g; int k;
+      step_item(sg, b, g, k);
+      if (k == N - 1 && g < a.nlines) issue_stores_tma(a, 0, b, g, buf);
+      if (sl < nsteps) {
+        bulk_wait_read0();
+        step_item(sl, b, g, k);
+        issue_loads_pair(a, b, g, k, buf, &full[st]);
+        ++sl;
+      }
+    }
+    bulk_wait0();
+    return;
+  }
+
+  const V* tw = twtab + lane;
+  const double scale = a.scale;
+  int64_t sg = 0;
+  for (int64_t it = 0; it < nit; ++it) {
+    int64_t g, b;
+    split_item(blockIdx.x + it * gridDim.x, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+    const bool live = g < a.nlines;
+    V acc[16];
+    for (int k = 0; k < N; ++k, ++sg) {
+      const int st = (int)(sg & 1);
+      V* buf = stage0 + st * SB;
+      V* Fr = buf + r * M;
+      V* Gr = buf + (q + r) * M;
+      mbar_wait(&full[st], (uint32_t)(sg >> 1) & 1u);
+      fold_all<0>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twcol, tid, nth);
+      fold_all<0>(buf + q * M, a.in_g.p, (int)a.in_g.L, live, q, zt, twm, twcol, tid, nth);
+      compute_sync(nth);
+      V v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = Fr[lane + 32 * i];
+      w512::fft_fwd(v, Fr, lane, tw);
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) Fr[k2 * 32 + lane] = v[k2];  // F-hat parked, lane-major
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = Gr[lane + 32 * i];
+      w512::fft_fwd(v, Gr, lane, tw);
+      __syncwarp();
+      if (k == 0) {
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cmul(Fr[k2 * 32 + lane], v[k2]);
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cfma(acc[k2], Fr[k2 * 32 + lane], v[k2]);
+      }
+      if (k < N - 1) {
+        mbar_arrive(&done[st]);  // stage free for the producer
+        continue;
+      }
+      // last pair: inverse transform of the scaled sum, unfold, store
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cscale(acc[k2], scale);
+      __syncwarp();
+      w512::fft_inv(acc, Fr, lane, tw);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = acc[i];
+      compute_sync(nth);
+      unfold_all<0>(buf, q, a.out.T, zt, twcol, tid, nth);
+      fence_async_smem();
+      mbar_arrive(&done[st]);
+    }
+  }
 }
 
 }  // namespace s512

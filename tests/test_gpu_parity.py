@@ -357,6 +357,20 @@ def test_s512_engine_batched_2d(ctx, H):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
 
 
+@pytest.mark.parametrize("N,sf,sg", [(3, (1200, 300), (700, 40)), (1, (900, 200), (600, 70)),
+                                     (6, (700, 130), (520, 20)), (2, (2048, 90), (1000, 33))])
+def test_s512_multipair_conv(ctx, H, N, sf, sg):
+    """Staged multi-pair convolution pass (MODE_MCONV: h = sum_k f_k * g_k, short
+    inputs of several blocks, q <= 6 along the convolution axis)."""
+    fs, gs = [], []
+    for k in range(N):
+        f, g = synth.random_pair(730 + 10 * N + k, sf, sg)
+        fs.append(f); gs.append(g)
+    axes = [{"m": 512, "C": 1, "S": 2}, {"m": 512, "C": 1, "S": 2}]
+    h = host(ctx.multiconv([dev(f) for f in fs], [dev(g) for g in gs], plan=H.Plan.make(2, axes)))
+    assert oracle.rel_l2(h, oracle.multiconv(fs, gs)) < 1e-11
+
+
 @pytest.mark.parametrize("L,q", [(512, 1), (1000, 2), (4000, 8), (4096, 9)])
 def test_s512_residues_match_dft(ctx, H, L, q):
     x = synth.random_pair(L, (3, L), (1,))[0]
