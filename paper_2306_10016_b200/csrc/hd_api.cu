@@ -1460,7 +1460,8 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
   std::vector<int> Ss = (ndim == 1) ? std::vector<int>{1} : std::vector<int>{1, 2, 4, 8};
   for (int m = std::max(2, m0 / 2); m <= std::min(4096, m0 * 2); m *= 2) {
     const int q = (int)cdiv(Mi, m);
-    for (int C : {1, 2}) {
+    for (int C : {1, 2, 4, 8}) {
+      if (C > 2 && m > 256) continue;  // wide line groups only pay for short lines
       std::vector<int> Ds = {q};
       if (q > 1) Ds.push_back((q + 1) / 2);
       for (int D : Ds) {
