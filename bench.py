@@ -92,6 +92,23 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12   # derived, see DESIGN.md section 6
+
+
+def conv_flops(ndim, N, Lf, Lg, Lout, plan, batch=1):
+    """Algorithmic flops of one launch of the convolution pass:
+    per line of the convolution axis (axis 0) with plan (m, q, p_f, p_g, T)."""
+    a = plan.axis[0]
+    m, q, pf, pg = a.m, a.q, a.p_f, a.p_g
+    T = -(-Lout[0] // m)
+    per_line = ((2 * N + 1) * q * 5 * m * np.log2(m) + 8 * m * q * (pf + pg) * N
+                + 8 * m * q * T + 6 * m * q * N)
+    lines = batch
+    for i in range(1, ndim):
+        lines *= plan.axis[i].M1
+    return float(per_line * lines)
+
+
 def ncu_traffic(kernel_name):
     """dram read+write bytes per launch of the kernel from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -334,6 +351,15 @@ def run_ours(args, rank, world, local_rank):
                 "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_src,
                 "alg_bytes_per_launch": ab.get(dom), "avg_launch_ms": avg,
                 "share_of_step": dms / sum(v[0] for v in prof.values())}
+        fl = conv_flops(ndim, N, Lf, Lg, Lout, plan, batch) if dom.startswith("conv") else None
+        if fl and eb == 16:
+            # the convolution pass is FP64-issue bound: its flops
+            # against the FP64 pipe, 64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz
+            ach = fl / (avg * 1e-3) / 1e12
+            roof["fp64"] = {"achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                            "frac": ach / FP64_PEAK_TFLOPS, "alg_flops_per_launch": fl,
+                            "flops": "nominal 5 m log2 m per residue FFT ((2N+1) q per line) + naive "
+                                     "fold 8 m q (p_f+p_g) N + unfold 8 m q T + product 6 m q N"}
     total_ab = sum(ab.values())
     whole = {"alg_bytes_per_step": total_ab,
              "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,
