@@ -430,10 +430,8 @@ void prepare_tma(Launch& L) {
     }
   }
   if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map)) a.tm_out.kind = hd::TMA_NONE;
-  // the kernel runs loads and stores both by TMA (producer warp) or both per thread
-  if (a.tm_in.kind == hd::TMA_NONE || a.tm_out.kind == hd::TMA_NONE) {
-    a.tm_in.kind = hd::TMA_NONE; a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE;
-  }
+  // loads by TMA need the producer warp; without them the stores go per thread too
+  if (a.tm_in.kind == hd::TMA_NONE) { a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE; }
 }
 
 // The staged warp engine (m = 512, hd_s512.cuh) applies to one line per CTA, all
@@ -720,7 +718,11 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       hd_status_t s = launch(ctx, P.dt, L, st);
       if (s != HD_OK) return s;
     }
-    // pass B: convolution along y for every spectral column (sum over pairs) -> Y[y/Sx][kx][y%Sx]
+    // Y: with the staged engine on x, plain rows Y[y][kx] (pass C loads each row with
+    // one bulk copy; pass B, compute-bound, stores its columns in 16-byte TMA pieces
+    // that L2 merges with the neighbouring columns'); otherwise Y[y/Sx][kx][y%Sx]
+    const bool yrows = P.s512[1] && y.lines == 1;
+    // pass B: convolution along y for every spectral column (sum over pairs) -> Y
     {
       Launch L = make_launch(ctx, P, hd::MODE_CONV, "conv_y", 0, twm[0], twM1[0], twst[0]);
       for (int k = 0; k < N; ++k) { L.a.in_f.ptr[k] = Xf[k]; L.a.in_g.ptr[k] = Xg[k]; }
@@ -729,7 +731,12 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_g.L = y.Lg; L.a.in_g.p = y.pg; L.a.in_g.nbi = B;
       L.a.in_g.s_b = P.shared_g ? 0 : Kxp * y.Lg; in_tiled(L.a.in_g, Sy, y.Lg * Sy);
       L.a.out.ptr[0] = Y; L.a.out.nbi = B; L.a.out.s_b = Oyp * Kxp;
-      out_elem_tiled(L.a.out, Sx, Sx, Kxp * Sx);
+      if (yrows) {  // lines kx (tile width 1), element y at stride Kxp
+        L.a.out.tl = 0; L.a.out.s_t = 1; L.a.out.s_l = 1; L.a.out.so_log2 = 40; L.a.out.s_jt = 0;
+        L.a.out.s_js = Kxp;
+      } else {
+        out_elem_tiled(L.a.out, Sx, Sx, Kxp * Sx);
+      }
       L.a.out.L = y.O; L.a.out.T = y.T;
       L.a.scale = scale;
       L.a.nlines = Kx; L.a.nbatch = B;
@@ -740,7 +747,9 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     // pass C: inverse along x for every output row
     {
       Launch L = make_launch(ctx, P, hd::MODE_INV, "inv_x", 1, twm[1], twM1[1], twst[1]);
-      L.a.in_f.ptr[0] = Y; L.a.in_f.nbi = B; L.a.in_f.s_b = Oyp * Kxp; in_tiled(L.a.in_f, Sx, Kxp * Sx);
+      L.a.in_f.ptr[0] = Y; L.a.in_f.nbi = B; L.a.in_f.s_b = Oyp * Kxp;
+      if (yrows) in_rows(L.a.in_f, Kxp);
+      else in_tiled(L.a.in_f, Sx, Kxp * Sx);
       L.a.in_f.L = Kx;
       L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; out_rows(L.a.out, x.O);
       L.a.out.L = x.O; L.a.out.T = x.T;

@@ -141,46 +141,63 @@ struct PhaseClock {
 // ---------------------------------------------------------------------------
 // Loads of one work item: in_f line (+ in_g line in CONV) -> stage slot j = element j
 // ---------------------------------------------------------------------------
+// Loads of one work item in the slot range [j0, j1) of the in_f line (the whole
+// short line g in CONV goes with the first range: it lands beyond the output slots).
+// issue_loads_arm sets the mbarrier's byte count for the whole item first.
 template <int MODE>
-__device__ __forceinline__ void issue_loads_tma(const PassArgs& a, int k_arr, int64_t b, int64_t g, V* buf,
-                                                uint64_t* bar) {
-  const bool live = g < a.nlines;
-  const LineIn& in = a.in_f;
-  const int L = (int)in.L;
+__device__ __forceinline__ void issue_loads_arm(const PassArgs& a, int64_t g, uint64_t* bar) {
   uint32_t bytes = 0;
-  if (live) {
+  if (g < a.nlines) {
+    const int L = (int)a.in_f.L;
     bytes += a.tm_in.kind == TMA_BULK ? (uint32_t)L * 16u : (uint32_t)((L + kBox - 1) / kBox) * kBox * 16u;
     if (MODE == MODE_CONV)
       bytes += a.tm_in_g.kind == TMA_BULK ? (uint32_t)a.in_g.L * 16u
                                            : (uint32_t)((a.in_g.L + kBox - 1) / kBox) * kBox * 16u;
   }
   mbar_expect_tx(bar, bytes);
-  if (!live) return;
+}
+
+template <int MODE>
+__device__ __forceinline__ void issue_loads_range(const PassArgs& a, int k_arr, int64_t b, int64_t g, V* buf,
+                                                  uint64_t* bar, int j0, int j1) {
+  if (g >= a.nlines) return;
+  const LineIn& in = a.in_f;
+  const int L = (int)in.L;
+  j1 = j1 < L ? j1 : L;
   const int kk = MODE == MODE_FWD ? k_arr : 0;
-  if (a.tm_in.kind == TMA_BULK) {
-    const V* x = reinterpret_cast<const V*>(in.ptr[kk]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g);
-    bulk_load(buf, x, (uint32_t)L * 16u, bar);
-  } else {
-    const CUtensorMap* map = &a.tm_in_map[kk];
-    int c[5];
-    for (int j0 = 0; j0 < L; j0 += kBox) {
-      tma_coords(a.tm_in, b, g, j0, c);
-      tma_load(buf + j0, map, c, bar);
+  if (j0 < j1) {
+    if (a.tm_in.kind == TMA_BULK) {
+      const V* x = reinterpret_cast<const V*>(in.ptr[kk]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g);
+      bulk_load(buf + j0, x + j0, (uint32_t)(j1 - j0) * 16u, bar);
+    } else {
+      const CUtensorMap* map = &a.tm_in_map[kk];
+      int c[5];
+      for (int jb = j0; jb < j1; jb += kBox) {
+        tma_coords(a.tm_in, b, g, jb, c);
+        tma_load(buf + jb, map, c, bar);
+      }
     }
   }
-  if constexpr (MODE == MODE_CONV) {
+  if (MODE == MODE_CONV && j0 == 0) {
     const LineIn& ig = a.in_g;
     if (a.tm_in_g.kind == TMA_BULK) {
       const V* xg = reinterpret_cast<const V*>(ig.ptr[0]) + boff(b, ig.nbi, ig.s_bo, ig.s_b) + line_off(ig, g);
       bulk_load(buf + a.q * M, xg, (uint32_t)ig.L * 16u, bar);
     } else {
       int c[5];
-      for (int j0 = 0; j0 < (int)ig.L; j0 += kBox) {
-        tma_coords(a.tm_in_g, b, g, j0, c);
-        tma_load(buf + a.q * M + j0, &a.tm_in_g_map[0], c, bar);
+      for (int jb = 0; jb < (int)ig.L; jb += kBox) {
+        tma_coords(a.tm_in_g, b, g, jb, c);
+        tma_load(buf + a.q * M + jb, &a.tm_in_g_map[0], c, bar);
       }
     }
   }
+}
+
+template <int MODE>
+__device__ __forceinline__ void issue_loads_tma(const PassArgs& a, int k_arr, int64_t b, int64_t g, V* buf,
+                                                uint64_t* bar) {
+  issue_loads_arm<MODE>(a, g, bar);
+  issue_loads_range<MODE>(a, k_arr, b, g, buf, bar, 0, 1 << 30);
 }
 
 // L2 prefetch of a contiguous input line one item further ahead than the loads
@@ -215,21 +232,62 @@ __device__ __forceinline__ void issue_loads_cp(const PassArgs& a, int k_arr, int
 // ---------------------------------------------------------------------------
 // Stores of one work item: stage slots j < out.L -> output line
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void issue_stores_tma(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf) {
+// Stores of the stage slots [j0, j1) of the output line as one bulk-async group.
+__device__ __forceinline__ void issue_stores_range(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf,
+                                                   int j0, int j1) {
   const LineOut& o = a.out;
   const int L = (int)o.L;
-  if (a.tm_out.kind == TMA_BULK) {
-    V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
-    bulk_store(y, buf, (uint32_t)L * 16u);
-  } else {
-    const CUtensorMap* map = &a.tm_out_map[kk];
-    int c[5];
-    for (int j0 = 0; j0 < L; j0 += kBox) {
-      tma_coords(a.tm_out, b, g, j0, c);
-      tma_store(map, c, buf + j0);
+  j1 = j1 < L ? j1 : L;
+  if (j0 < j1) {
+    if (a.tm_out.kind == TMA_BULK) {
+      V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
+      bulk_store(y + j0, buf + j0, (uint32_t)(j1 - j0) * 16u);
+    } else {
+      const CUtensorMap* map = &a.tm_out_map[kk];
+      int c[5];
+      for (int jb = j0; jb < j1; jb += kBox) {
+        tma_coords(a.tm_out, b, g, jb, c);
+        tma_store(map, c, buf + jb);
+      }
     }
   }
   bulk_commit();
+}
+
+__device__ __forceinline__ void issue_stores_tma(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf) {
+  issue_stores_range(a, kk, b, g, buf, 0, 1 << 30);
+}
+
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_n(int n) {
+  if (n >= 3) bulk_wait_read<3>();
+  else if (n == 2) bulk_wait_read<2>();
+  else if (n == 1) bulk_wait_read<1>();
+  else bulk_wait_read<0>();
+}
+
+// The producer's hand-over of one stage: the stores of the finished item go out in
+// kGroups slot ranges (bulk groups, in order), and the next item's loads into the
+// same stage follow range by range, each waiting only until the store groups that
+// overlap its slots have been read out of shared memory.
+constexpr int kGroups = 4;
+template <int MODE>
+__device__ __forceinline__ void handover(const PassArgs& a, int k_arr, int kk_out, bool store, int64_t bs,
+                                         int64_t gs, bool load, int64_t bl, int64_t gl, V* buf, uint64_t* bar) {
+  const int Ls = store ? (int)a.out.L : 0;
+  const int Ll = load ? (int)a.in_f.L : 0;
+  const int Lmax = Ls > Ll ? Ls : Ll;
+  const int chunk = ((Lmax + kGroups - 1) / kGroups + kBox - 1) / kBox * kBox;
+  if (store)
+    for (int k = 0; k < kGroups; ++k) issue_stores_range(a, kk_out, bs, gs, buf, k * chunk, (k + 1) * chunk);
+  if (!load) return;
+  issue_loads_arm<MODE>(a, gl, bar);
+  for (int k = 0; k < kGroups; ++k) {
+    if (store) bulk_wait_read_n(kGroups - 1 - k);
+    issue_loads_range<MODE>(a, k_arr, bl, gl, buf, bar, k * chunk, k == kGroups - 1 ? (1 << 30) : (k + 1) * chunk);
+  }
 }
 
 __device__ __forceinline__ void stores_st(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf,
@@ -525,7 +583,11 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
   const int r = tid >> 5;                  // this warp's residue (compute warps)
   const int k_arr = blockIdx.z;
   const int SB = q * M + (MODE == MODE_CONV ? M : 0);
-  const bool tma = a.tm_in.kind != TMA_NONE && a.tm_out.kind != TMA_NONE;
+  // loads by the producer's TMA (tma) or by every compute thread (cp.async);
+  // stores by the producer's TMA (tma_st) or by every compute thread (plain
+  // stores: lines TMA could only write in 16-byte pieces, see hd_api.cu)
+  const bool tma = a.tm_in.kind != TMA_NONE;
+  const bool tma_st = tma && a.tm_out.kind != TMA_NONE;
   constexpr bool kPipeFold = (MODE == MODE_CONV && QC == 9);
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
@@ -567,21 +629,21 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
       const int st = it & 1;
       V* buf = stage0 + st * SB;
       mbar_wait(&done[st], (uint32_t)(it >> 1) & 1u);
-      int64_t g, b;
-      split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
-      if (g < a.nlines) issue_stores_tma(a, kk_out, b, g, buf);
-      if (wl < total) {
-        bulk_wait_read0();  // this stage's results have left shared memory
-        split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
-        issue_loads_tma<MODE>(a, k_arr, b, g, buf, &full[st]);
+      int64_t gs, bs, gl = 0, bl = 0;
+      split_item(w, a.nbatch, a.ngroups, a.batch_fastest, bs, gs);
+      const bool load = wl < total;
+      if (load) split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, bl, gl);
+      handover<MODE>(a, k_arr, kk_out, tma_st && gs < a.nlines, bs, gs, load, bl, gl, buf, &full[st]);
+      if (load) {
         wl += gridDim.x;
         if (wl < total) {  // and the item after it into L2
+          int64_t g, b;
           split_item(wl, a.nbatch, a.ngroups, a.batch_fastest, b, g);
           issue_prefetch<MODE>(a, k_arr, b, g);
         }
       }
     }
-    bulk_wait0();
+    if (tma_st) bulk_wait0();
     return;
   }
 
@@ -686,9 +748,13 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
     }
     pc.mark(6);
     // results are in stage slots j < out.L
-    if (tma) {
+    if (tma_st) {
       fence_async_smem();
       mbar_arrive(&done[st]);  // the producer stores them
+    } else if (tma) {
+      compute_sync(nth);
+      if (live) stores_st(a, kk_out, b, g, buf, tid, nth);
+      mbar_arrive(&done[st]);  // stage free once every thread's stores have read it
     } else {
       compute_sync(nth);
       if (live) stores_st(a, kk_out, b, g, buf, tid, nth);
