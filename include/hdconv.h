@@ -160,6 +160,18 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
                              const void* const* g, const int64_t* Lg,
                              void* h, const hd_plan_t* plan, void* stream);
 
+/* Output window (PAPER.md:1482-1489 modes full / same_big / same_small / valid
+ * are windows): h = (sum_k f[k] * g[k])[win_lo + w] for
+ * 0 <= w_i < win_n[i], h an array of extents [batch] x win_n (device pointer).
+ * Only the window is written; the last pass of every axis skips the rest.
+ * Requires 0 <= win_lo[i] and win_lo[i] + win_n[i] <= L_f,i + L_g,i - 1.
+ * Other arguments as hd_multiconv (N = 1 for a plain convolution) with batch. */
+hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                           int64_t batch, const void* const* f, const int64_t* Lf,
+                           const void* const* g, const int64_t* Lg, void* h,
+                           const int64_t* M, const int64_t* win_lo, const int64_t* win_n,
+                           const hd_plan_t* plan, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- end-to-end with HOST buffers ------------------------------------------ */
 /* Same as hd_multiconv with batch (N = 1 for plain conv) but f, g, h are HOST
  * pointers (pinned for best speed).  Copies in, convolves, copies out and

@@ -163,7 +163,8 @@ hd_status_t get_stage_table(hd_ctx* ctx, int m, bool dbl, const void** out) {
 // plans
 // ---------------------------------------------------------------------------
 struct AxisInfo {
-  int64_t Lf, Lg, Lout, M, M1, O;  // O: output extent (Lout, or M1 if aliased)
+  int64_t Lf, Lg, Lout, M, M1, O;  // O: output extent (Lout, or M1 if aliased; the window size)
+  int64_t o0;                      // output window start (0: from the first output)
   int m, q, pf, pg, T, C, S, D, lines, threads;
   bool auto_engine;                // plan threads == 0: warp engine where it applies
 };
@@ -221,6 +222,7 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     if (x.M1 < x.Lout && !(plan->flags & HD_FLAG_ALLOW_ALIAS))
       return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": M < L_f + L_g - 1 would alias (PAPER.md:592)");
     x.O = std::min(x.Lout, x.M1);
+    x.o0 = 0;
     x.pf = (int)cdiv(x.Lf, a.m);
     x.pg = (int)cdiv(x.Lg, a.m);
     x.T = (int)cdiv(x.O, a.m);
@@ -241,6 +243,21 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     if (pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
       return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": lines*D*m too large for shared memory");
     a.p_f = x.pf; a.p_g = x.pg; a.q = x.q; a.M1 = x.M1;
+  }
+  return HD_OK;
+}
+
+// Output window: keep outputs
+// [lo[i], lo[i] + n[i]) of each axis; the last pass of every axis writes only those.
+hd_status_t apply_window(hd_ctx* ctx, int ndim, const int64_t* lo, const int64_t* n, AxisInfo* ax) {
+  if (!lo || !n) return HD_OK;
+  for (int i = 0; i < ndim; ++i) {
+    AxisInfo& x = ax[i];
+    if (lo[i] < 0 || n[i] < 1 || lo[i] + n[i] > x.O)
+      return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": window outside the output");
+    x.o0 = lo[i];
+    x.O = n[i];
+    x.T = (int)cdiv(x.o0 + x.O, x.m);
   }
   return HD_OK;
 }
@@ -430,6 +447,8 @@ void prepare_tma(Launch& L) {
     }
   }
   if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map)) a.tm_out.kind = hd::TMA_NONE;
+  // a window start that is not tile-aligned cannot be expressed by element-tiled boxes
+  if (a.out.j0 != 0 && a.tm_out.kind == hd::TMA_ELEM_TILED) a.tm_out.kind = hd::TMA_NONE;
   // loads by TMA need the producer warp; without them the stores go per thread too
   if (a.tm_in.kind == hd::TMA_NONE) { a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE; }
 }
@@ -685,6 +704,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; in_rows(L.a.in_f, x.Lf);
     L.a.in_g.L = x.Lg; L.a.in_g.p = x.pg; in_rows(L.a.in_g, P.shared_g ? 0 : x.Lg);
     L.a.out.ptr[0] = P.h; L.a.out.L = x.O; L.a.out.T = x.T; out_rows(L.a.out, x.O);
+    L.a.out.j0 = x.o0;
     L.a.scale = scale;
     L.a.nlines = B; L.a.nbatch = 1;
     L.ngroups = cdiv(B, x.lines); L.nbatch = 1;
@@ -737,7 +757,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       } else {
         out_elem_tiled(L.a.out, Sx, Sx, Kxp * Sx);
       }
-      L.a.out.L = y.O; L.a.out.T = y.T;
+      L.a.out.L = y.O; L.a.out.T = y.T; L.a.out.j0 = y.o0;
       L.a.scale = scale;
       L.a.nlines = Kx; L.a.nbatch = B;
       L.ngroups = cdiv(Kx, Cy); L.nbatch = B;
@@ -752,7 +772,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       else in_tiled(L.a.in_f, Sx, Kxp * Sx);
       L.a.in_f.L = Kx;
       L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; out_rows(L.a.out, x.O);
-      L.a.out.L = x.O; L.a.out.T = x.T;
+      L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.j0 = x.o0;
       L.a.nlines = y.O; L.a.nbatch = B;
       L.ngroups = cdiv(y.O, Cx); L.nbatch = B;
       return launch(ctx, P.dt, L, st);
@@ -820,7 +840,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_g.s_b = Kxp * z.Lg; in_tiled(L.a.in_g, S0, z.Lg * S0);
     L.a.out.ptr[0] = Zl; L.a.out.nbi = Ky; L.a.out.s_bo = z.O * Kxp * Ky; L.a.out.s_b = S1;
     out_line_tiled(L.a.out, S1, Ky * S1, Kxp * Ky);
-    L.a.out.L = z.O; L.a.out.T = z.T;
+    L.a.out.L = z.O; L.a.out.T = z.T; L.a.out.j0 = z.o0;
     L.a.scale = scale;
     L.a.batch_fastest = 1;
     L.a.nlines = Kx; L.a.nbatch = B * Ky;
@@ -834,7 +854,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_f.ptr[0] = Zl; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Kxp * Ky; in_tiled(L.a.in_f, S1, Ky * S1);
     L.a.in_f.L = Ky;
     L.a.out.ptr[0] = W; L.a.out.nbi = B * z.O; L.a.out.s_b = Oyp * Kxp; out_elem_tiled(L.a.out, Sx, Sx, Kxp * Sx);
-    L.a.out.L = y.O; L.a.out.T = y.T;
+    L.a.out.L = y.O; L.a.out.T = y.T; L.a.out.j0 = y.o0;
     L.a.nlines = Kx; L.a.nbatch = B * z.O;
     L.ngroups = cdiv(Kx, Cy); L.nbatch = B * z.O;
     hd_status_t s = launch(ctx, P.dt, L, st);
@@ -846,7 +866,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.in_f.ptr[0] = W; L.a.in_f.nbi = B * z.O; L.a.in_f.s_b = Oyp * Kxp; in_tiled(L.a.in_f, Sx, Kxp * Sx);
     L.a.in_f.L = Kx;
     L.a.out.ptr[0] = P.h; L.a.out.nbi = B * z.O; L.a.out.s_b = y.O * x.O; out_rows(L.a.out, x.O);
-    L.a.out.L = x.O; L.a.out.T = x.T;
+    L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.j0 = x.o0;
     L.a.nlines = y.O; L.a.nbatch = B * z.O;
     L.ngroups = cdiv(y.O, Cx); L.nbatch = B * z.O;
     return launch(ctx, P.dt, L, st);
@@ -866,7 +886,8 @@ std::string problem_key(hd_dtype_t dt, int ndim, int N, int64_t batch, const int
 // Build a Problem from the public arguments (plan: explicit, cached or default).
 hd_status_t setup(hd_ctx* ctx, Problem& P, hd_dtype_t dt, int ndim, int N, int64_t batch,
                   const void* const* f, const int64_t* Lf, const void* const* g, const int64_t* Lg,
-                  void* h, const int64_t* M, const hd_plan_t* plan, bool need_ptrs = true) {
+                  void* h, const int64_t* M, const hd_plan_t* plan, bool need_ptrs = true,
+                  const int64_t* win_lo = nullptr, const int64_t* win_n = nullptr) {
   if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
   if (dt != HD_C64 && dt != HD_C128) return fail(ctx, HD_ERR_INVALID, "dtype must be HD_C64 or HD_C128");
   if (ndim < 1 || ndim > HD_MAX_DIM) return fail(ctx, HD_ERR_INVALID, "ndim must be 1, 2 or 3");
@@ -899,6 +920,8 @@ hd_status_t setup(hd_ctx* ctx, Problem& P, hd_dtype_t dt, int ndim, int N, int64
   }
   P.shared_g = (pl.flags & HD_FLAG_SHARED_G) != 0;
   hd_status_t s = complete_plan(ctx, dt, ndim, N, Lf, Lg, M, &pl, P.ax);
+  if (s != HD_OK) return s;
+  s = apply_window(ctx, ndim, win_lo, win_n, P.ax);
   if (s != HD_OK) return s;
   P.plan = pl;
   choose_engines(P);
@@ -1007,13 +1030,23 @@ size_t hd_workspace_bytes(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t 
 static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64_t batch,
                              const void* const* f, const int64_t* Lf, const void* const* g,
                              const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan,
-                             void* ws, size_t ws_bytes, void* stream) {
+                             void* ws, size_t ws_bytes, void* stream, const int64_t* win_lo = nullptr,
+                             const int64_t* win_n = nullptr) {
   Problem P;
-  hd_status_t s = setup(ctx, P, dt, ndim, N, batch, f, Lf, g, Lg, h, M, plan);
+  hd_status_t s = setup(ctx, P, dt, ndim, N, batch, f, Lf, g, Lg, h, M, plan, true, win_lo, win_n);
   if (s != HD_OK) return s;
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   return run_pipeline(ctx, P, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
+                          const void* const* f, const int64_t* Lf, const void* const* g,
+                          const int64_t* Lg, void* h, const int64_t* M, const int64_t* win_lo,
+                          const int64_t* win_n, const hd_plan_t* plan, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (!win_lo || !win_n) return fail(ctx, HD_ERR_INVALID, "null window");
+  return run_entry(ctx, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan, ws, ws_bytes, stream, win_lo, win_n);
 }
 
 hd_status_t hd_conv1d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,

@@ -270,6 +270,8 @@ struct LineOut {           // element j of line l = g*C + c: ptr[k] + (b/nbi)*s_
   int32_t tl;              // log2 line-tile width (>= 30: untiled)
   int32_t pad_;
   int64_t jd;              // > 0: element j -> (j / jd)*s_jt + (j % jd)*s_js (overrides so_log2)
+  int64_t j0;              // output window: element j of the full line is written to
+                           // position j - j0, kept when 0 <= j - j0 < L
 };
 // element-axis tile code for jt_off: log2 tile (0..29), plain (>= 30), or -width (general)
 __device__ __forceinline__ int out_sl(const LineOut& o) { return o.jd > 0 ? -(int)o.jd : o.so_log2; }
@@ -473,7 +475,8 @@ __device__ __forceinline__ void unfold_fast(const V* buf, V* y, const LineOut& o
       V h0 = v[0];
 #pragma unroll
       for (int r = 1; r < QM; ++r) h0 = cadd(h0, v[r]);
-      if (s < L) yl[jt_off(s, sl, out.s_jt, out.s_js)] = h0;
+      const int64_t p0 = s - out.j0;
+      if (p0 >= 0 && p0 < L) yl[jt_off(p0, sl, out.s_jt, out.s_js)] = h0;
     }
 #pragma unroll
     for (int t = 1; t <= QM / 2; ++t) {
@@ -486,11 +489,11 @@ __device__ __forceinline__ void unfold_fast(const V* buf, V* y, const LineOut& o
         B.x = fma(v[r].x, z.y, B.x); B.y = fma(v[r].y, z.y, B.y);
       }
       // h_t = sum v_r conj(z) = A - iB ; h_{q-t} = A + iB
-      const int64_t j1 = (int64_t)t * M + s;
-      if (t < T && j1 < L) yl[jt_off(j1, sl, out.s_jt, out.s_js)] = cmk<V>(A.x + B.y, A.y - B.x);
+      const int64_t p1 = (int64_t)t * M + s - out.j0;
+      if (t < T && p1 >= 0 && p1 < L) yl[jt_off(p1, sl, out.s_jt, out.s_js)] = cmk<V>(A.x + B.y, A.y - B.x);
       if (2 * t < q) {
-        const int64_t j2 = (int64_t)(q - t) * M + s;
-        if (q - t < T && j2 < L) yl[jt_off(j2, sl, out.s_jt, out.s_js)] = cmk<V>(A.x - B.y, A.y + B.x);
+        const int64_t p2 = (int64_t)(q - t) * M + s - out.j0;
+        if (q - t < T && p2 >= 0 && p2 < L) yl[jt_off(p2, sl, out.s_jt, out.s_js)] = cmk<V>(A.x - B.y, A.y + B.x);
       }
     }
   }
@@ -538,7 +541,7 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
       for (int d = 0; d < kFoldChunk; ++d) e[d] = 0;
       const bool add = accumulate || d0 > 0;
       for (int t = 0; t < T; ++t) {
-        const int64_t j = (int64_t)t * M + s;
+        const int64_t j = (int64_t)t * M + s - out.j0;  // position in the output window
         if (j >= L) break;
         V val = cmk<V>(0, 0);
 #pragma unroll
@@ -549,6 +552,7 @@ __device__ __forceinline__ void unfold(const V* buf, const LineOut& out, int k, 
             if (e[d] >= q) e[d] -= q;
           }
         }
+        if (j < 0) continue;
         V* dst = yl + jt_off(j, sl, out.s_jt, out.s_js);
         if (add) { V o = *dst; val = cadd(o, val); }
         *dst = val;

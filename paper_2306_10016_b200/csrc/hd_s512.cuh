@@ -232,22 +232,37 @@ __device__ __forceinline__ void issue_loads_cp(const PassArgs& a, int k_arr, int
 // ---------------------------------------------------------------------------
 // Stores of one work item: stage slots j < out.L -> output line
 // ---------------------------------------------------------------------------
-// Stores of the stage slots [j0, j1) of the output line as one bulk-async group.
+// Stores of the output positions [p0, p1) (stage slots p + out.j0: the output
+// window) as one bulk-async group.  Tensor boxes start at 8-aligned slots (128-byte
+// shared-memory alignment); positions before the window are clipped by TMA.
 __device__ __forceinline__ void issue_stores_range(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf,
-                                                   int j0, int j1) {
+                                                   int p0, int p1) {
   const LineOut& o = a.out;
   const int L = (int)o.L;
-  j1 = j1 < L ? j1 : L;
-  if (j0 < j1) {
+  const int j0 = (int)o.j0;
+  p1 = p1 < L ? p1 : L;
+  if (p0 < p1) {
     if (a.tm_out.kind == TMA_BULK) {
       V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
-      bulk_store(y + j0, buf + j0, (uint32_t)(j1 - j0) * 16u);
+      bulk_store(y + p0, buf + j0 + p0, (uint32_t)(p1 - p0) * 16u);
     } else {
       const CUtensorMap* map = &a.tm_out_map[kk];
+      // boxes start at 8-aligned slots: positions p0 - sh + 256 k (the first group's
+      // head before the first aligned slot goes by plain stores; later groups rewrite
+      // sh positions of the group before with the same values).  Element-tiled lines with a window
+      // go through per-thread stores instead (hd_api.cu prepare_tma).
+      const int sh = j0 & 7;
+      int pb = p0 - sh;
+      if (pb < 0) {  // positions before the first 8-aligned slot: plain stores
+        V* yl = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
+        const int hp = (8 - sh) < p1 ? (8 - sh) : p1;
+        for (int p = 0; p < hp; ++p) yl[jt_off(p, out_sl(o), o.s_jt, o.s_js)] = buf[j0 + p];
+        pb += 8;
+      }
       int c[5];
-      for (int jb = j0; jb < j1; jb += kBox) {
-        tma_coords(a.tm_out, b, g, jb, c);
-        tma_store(map, c, buf + jb);
+      for (; pb < p1; pb += kBox) {
+        tma_coords(a.tm_out, b, g, pb, c);
+        tma_store(map, c, buf + j0 + pb);
       }
     }
   }
@@ -295,7 +310,7 @@ __device__ __forceinline__ void stores_st(const PassArgs& a, int kk, int64_t b, 
   const LineOut& o = a.out;
   V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
   const int sl = out_sl(o);
-  for (int j = tid; j < (int)o.L; j += nth) y[jt_off(j, sl, o.s_jt, o.s_js)] = buf[j];
+  for (int j = tid; j < (int)o.L; j += nth) y[jt_off(j, sl, o.s_jt, o.s_js)] = buf[j + o.j0];
 }
 
 // ---------------------------------------------------------------------------

@@ -35,7 +35,7 @@ STATUS_NAMES = {0: "HD_OK", 1: "HD_ERR_INVALID", 2: "HD_ERR_UNSUPPORTED", 3: "HD
 EXPORTED = [
     "hd_abi_version", "hd_create", "hd_destroy", "hd_last_error", "hd_plan_default",
     "hd_plan_complete", "hd_spectral_permutation", "hd_workspace_bytes", "hd_conv1d",
-    "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host",
+    "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host", "hd_conv_window",
     "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_log",
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_pass",
@@ -126,6 +126,8 @@ def _load():
         "hd_conv3d": ([P, ctypes.c_int, I64, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
         "hd_multiconv": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
         "hd_conv_explicit": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, PP, P], ctypes.c_int),
+        "hd_conv_window": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, P, P, PP, P, ctypes.c_size_t, P],
+                           ctypes.c_int),
         "hd_conv_host": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, PP, P], ctypes.c_int),
         "hd_conv_host_async": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, PP], ctypes.c_int),
         "hd_host_sync": ([P], ctypes.c_int),
@@ -217,6 +219,34 @@ def hd_abi_version():
 # ---------------------------------------------------------------------------
 # context
 # ---------------------------------------------------------------------------
+def window_for_mode(mode, Lf, Lg):
+    """(lo, n) per axis for the output modes of the paper's 2-D listing
+    (N = L1 + L2 - 1 with L1 = L_f, L2 = L_g as in its call
+    mainconvolve(f, g, ...)): full [0, N); same_big [0, L2); same_small [1, 1 + L1);
+    valid [ceil(N/L2) - 1, ceil(N/L1) + 1) -- the listing's formula as written
+    (SPEC.md flags it as differing from the conventional valid size), clipped to
+    the output."""
+    lo, n = [], []
+    for a, b in zip(Lf, Lg):
+        N = a + b - 1
+        if mode == "full":
+            v, v1 = 0, N
+        elif mode == "same_big":
+            v, v1 = 0, b
+        elif mode == "same_small":
+            v, v1 = 1, 1 + a
+        elif mode == "valid":
+            v, v1 = -(-N // b) - 1, -(-N // a) + 1
+        else:
+            raise ValueError(f"unknown mode {mode!r}: full, same_big, same_small, valid")
+        v, v1 = max(0, v), min(N, v1)
+        if v1 <= v:
+            raise ValueError(f"empty {mode} window for extents {a}, {b}")
+        lo.append(v)
+        n.append(v1 - v)
+    return lo, n
+
+
 class Context:
     """One hd_ctx_t bound to a CUDA device (owns twiddle tables, plan cache, scratch)."""
 
@@ -305,6 +335,25 @@ class Context:
         return h
 
     multiconv = hd_multiconv
+
+    def hd_conv_window(self, fs, gs, lo, n, batch=False, M=None, plan=None, h=None, stream=None):
+        """Window [lo, lo + n) (per axis) of sum_k fs[k] * gs[k]; fs/gs lists of tensors
+        (leading batch axis when batch=True).  See window_for_mode for the paper's modes."""
+        N = len(fs)
+        nd = fs[0].dim() - (1 if batch else 0)
+        B = fs[0].shape[0] if batch else 1
+        Lf, Lg = list(fs[0].shape[-nd:]), list(gs[0].shape[-nd:])
+        if h is None:
+            h = self._out(fs[0], ([B] if batch else []) + [int(v) for v in n])
+        fp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in fs])
+        gp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in gs])
+        Mv = _i64arr(M) if M is not None else None
+        pp = ctypes.byref(plan) if plan is not None else None
+        self._chk(_lib.hd_conv_window(self.h, _dtype_code(fs[0]), nd, N, B, fp, _i64arr(Lf), gp, _i64arr(Lg),
+                                      _ptr(h), Mv, _i64arr(lo), _i64arr(n), pp, None, 0, _stream_ptr(stream)))
+        return h
+
+    conv_window = hd_conv_window
 
     def hd_conv_explicit(self, fs, gs, plan=None, h=None, stream=None):
         N = len(fs)

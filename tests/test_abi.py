@@ -96,3 +96,17 @@ def test_no_cpu_fallback(H):
     with pytest.raises(H.HDError) as e:
         H.Context(0)
     assert e.value.status == H.HD_ERR_CUDA
+
+
+def test_window_modes_match_the_paper_formulas(H):
+    """Output windows of the paper's 2-D listing (worked values
+    SPEC.md:269-274): for L1 = 3, L2 = 5 (N = 7): full (0, 7), same_big (0, 5),
+    same_small (1, 4), valid (ceil(7/5) - 1, ceil(7/3) + 1) = (1, 4)."""
+    cases = {"full": (0, 7), "same_big": (0, 5), "same_small": (1, 4), "valid": (1, 4)}
+    for mode, (v, v1) in cases.items():
+        lo, n = H.window_for_mode(mode, [3, 3], [5, 5])
+        assert lo == [v, v] and n == [v1 - v, v1 - v], mode
+    # a 3-tap kernel over a 100-sample line: same_big keeps the first 100 outputs
+    assert H.window_for_mode("same_big", [3], [100]) == ([0], [100])
+    with pytest.raises(ValueError):
+        H.window_for_mode("nope", [3], [5])

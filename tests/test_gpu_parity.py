@@ -300,6 +300,52 @@ def test_host_async_mixed_with_other_entries(H):
     c.close()
 
 
+# ---------------------------------------------------------------- output windows (f3)
+@pytest.mark.parametrize("case", [
+    ("1d", (300,), (70,), (5,), (300,), None),
+    ("2d-staged", (900, 700), (200, 90), (13, 77), (850, 600), None),
+    ("2d-staged-mode", (600, 520), (31, 17), None, None, "same_big"),
+    ("2d-generic", (300, 260), (31, 17), (3, 1), (320, 250), "generic"),
+    ("2d-small-mode", (64, 50), (10, 12), None, None, "same_small"),
+])
+def test_output_window(ctx, H, case):
+    """hd_conv_window: every output inside the window equals the oracle's full
+    convolution at the same index (PAPER.md:1482-1489 modes are windows)."""
+    name, sf, sg, lo, n, mode = case
+    f, g = synth.random_pair(750 + len(name), sf, sg)
+    if mode in ("same_big", "same_small"):
+        lo, n = H.window_for_mode(mode, list(sf), list(sg))
+    nd = len(sf)
+    flags = H.HD_FLAG_GENERIC_FFT if mode == "generic" else 0
+    m = 512 if "staged" in name else 64
+    plan = H.Plan.make(nd, [{"m": m, "C": 1, "S": 2}] * nd, flags=flags)
+    h = host(ctx.conv_window([dev(f)], [dev(g)], lo, n, plan=plan))
+    full = oracle.conv(f, g)
+    ref = full[tuple(slice(a, a + b) for a, b in zip(lo, n))]
+    assert h.shape == ref.shape and oracle.rel_l2(h, ref) < 1e-11
+
+
+def test_output_window_3d_c64_and_multiconv(ctx, H):
+    f, g = synth.random_pair(760, (20, 18, 30), (5, 7, 4), dtype=np.complex64)
+    lo, n = [2, 0, 9], [15, 20, 20]
+    h = host(ctx.conv_window([dev(f)], [dev(g)], lo, n))
+    full = oracle.conv(f, g)
+    ref = full[2:17, 0:20, 9:29]
+    assert oracle.rel_l2(h, ref) < 1e-5
+    fs, gs = zip(*[synth.random_pair(770 + k, (700, 130), (520, 20)) for k in range(3)])
+    lo, n = [100, 7], [1000, 120]
+    plan = H.Plan.make(2, [{"m": 512, "C": 1, "S": 2}] * 2)
+    h = host(ctx.conv_window([dev(x) for x in fs], [dev(x) for x in gs], lo, n, plan=plan))
+    ref = oracle.multiconv(list(fs), list(gs))[100:1100, 7:127]
+    assert oracle.rel_l2(h, ref) < 1e-11
+
+
+def test_output_window_rejects_outside(ctx, H):
+    f, g = synth.random_pair(780, (30, 20), (5, 5))
+    with pytest.raises(H.HDError):
+        ctx.conv_window([dev(f)], [dev(g)], [0, 0], [35, 25])
+
+
 def test_alias_2d(ctx, H):
     f, g = synth.random_pair(71, (10, 12), (7, 5))
     p = H.Plan.make(2, [{"m": 4}, {"m": 4}], flags=H.HD_FLAG_ALLOW_ALIAS)
