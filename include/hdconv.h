@@ -260,6 +260,29 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* desc, 
 hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
                     int64_t batch, const int64_t* Lf, const int64_t* Lg, const int64_t* M,
                     uint32_t flags, int32_t reps, void* stream, hd_plan_t* out);
+/* Extended tuning.  flags:
+ *   HD_TUNE_PER_AXIS / HD_TUNE_EXHAUSTIVE as hd_tune;
+ *   HD_TUNE_RANDOM: A1 random search: n1 plans sampled uniformly
+ *     without replacement from the cross product (all of it when n1 >= its size),
+ *     deterministic for a seed (splitmix64); argmin, lexicographic tie-break.
+ * proxy_rows > 0 (per-axis search, ndim >= 2): the axes other than 0 are timed on
+ *   the skinny proxy problem with min(L, proxy_rows) lines along axis 0 and the
+ *   winners reused for the full problem (the L_y = 32 heuristic).
+ * fake_cost (testing hook, no device work): 1 = the cost of a plan is a fixed hash
+ *   of it (and of seed), 2 = every plan costs the same.
+ * The result is cached like hd_tune's; hd_tune_log lists every evaluated plan. */
+#define HD_TUNE_RANDOM 0x2u
+typedef struct {
+  uint32_t flags;
+  int32_t reps;          /* timed runs per candidate (median); 0 = 5 */
+  int32_t n1;            /* HD_TUNE_RANDOM: sample size (>= 1) */
+  int32_t fake_cost;     /* 0: time on the device */
+  uint64_t seed;
+  int64_t proxy_rows;    /* 0: no proxy */
+} hd_tune_opts_t;
+hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
+                       int64_t batch, const int64_t* Lf, const int64_t* Lg, const int64_t* M,
+                       const hd_tune_opts_t* opts, void* stream, hd_plan_t* out);
 /* Number of candidates evaluated by the last hd_tune and their (plan, seconds). */
 int32_t     hd_tune_log(hd_ctx_t ctx, int32_t max, hd_plan_t* plans, double* seconds);
 

@@ -1529,17 +1529,25 @@ void apply_cand(hd_plan_t& p, int i, int ndim, const AxisCand& c) {
 
 extern "C" {
 
-hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
-                    const int64_t* Lf, const int64_t* Lg, const int64_t* M, uint32_t flags,
-                    int32_t reps, void* stream, hd_plan_t* out) {
-  if (!ctx || !out) return fail(ctx, HD_ERR_INVALID, "null argument");
+// The paper's tuning "experience": A0 grid search over the cross
+// product, per-axis search (separability), A1 random search
+// and the skinny-rectangle proxy heuristic.
+hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
+                       const int64_t* Lf, const int64_t* Lg, const int64_t* M, const hd_tune_opts_t* opts,
+                       void* stream, hd_plan_t* out) {
+  if (!ctx || !out || !opts) return fail(ctx, HD_ERR_INVALID, "null argument");
+  const uint32_t flags = opts->flags;
+  const bool random = (flags & HD_TUNE_RANDOM) != 0;
+  if (random && opts->n1 < 1) return fail(ctx, HD_ERR_INVALID, "HD_TUNE_RANDOM needs n1 >= 1");
+  if (opts->proxy_rows < 0) return fail(ctx, HD_ERR_INVALID, "proxy_rows must be >= 0");
   Problem P0;
   hd_status_t s = setup(ctx, P0, dtype, ndim, N, batch, nullptr, Lf, nullptr, Lg, nullptr, M, nullptr, false);
   if (s != HD_OK) return s;
   hd_plan_t base;
   s = default_plan(ctx, dtype, ndim, N, Lf, Lg, M, &base);
   if (s != HD_OK) return s;
-  if (reps <= 0) reps = 5;
+  const int reps = opts->reps > 0 ? opts->reps : 5;
+  const bool fake = opts->fake_cost != 0;
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
@@ -1549,28 +1557,62 @@ hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int
   for (int i = 0; i < ndim; ++i) { nf *= Lf[i]; ng *= Lg[i]; nh *= Lf[i] + Lg[i] - 1; }
   const size_t bf = align256((size_t)nf * eb), bg = align256((size_t)ng * eb), bh = align256((size_t)nh * eb);
   char* scratch = nullptr;
-  cudaError_t e = cudaMalloc(&scratch, N * (bf + bg) + bh);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(tune scratch)");
-  cudaMemsetAsync(scratch, 0, N * (bf + bg) + bh, st);
+  if (!fake) {
+    cudaError_t e = cudaMalloc(&scratch, N * (bf + bg) + bh);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(tune scratch)");
+    cudaMemsetAsync(scratch, 0, N * (bf + bg) + bh, st);
+  }
   const void* fp[HD_MAX_PAIRS];
   const void* gp[HD_MAX_PAIRS];
   for (int k = 0; k < N; ++k) { fp[k] = scratch + k * bf; gp[k] = scratch + N * bf + k * bg; }
   void* hp = scratch + N * (bf + bg);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (!fake) { cudaEventCreate(&e0); cudaEventCreate(&e1); }
   ctx->tune_log.clear();
   const bool prof_was = ctx->profiling;
   ctx->profiling = false;
 
-  auto time_plan = [&](hd_plan_t pl, double* secs) -> bool {
+  // skinny proxy: the same problem with at most proxy_rows lines along axis 0
+  int64_t Lfp[HD_MAX_DIM], Lgp[HD_MAX_DIM], Mp[HD_MAX_DIM];
+  const bool proxy = opts->proxy_rows > 0 && ndim >= 2;
+  for (int i = 0; i < ndim; ++i) {
+    Lfp[i] = Lf[i]; Lgp[i] = Lg[i]; Mp[i] = M ? M[i] : 0;
+  }
+  if (proxy) {
+    Lfp[0] = std::min<int64_t>(Lf[0], opts->proxy_rows);
+    Lgp[0] = std::min<int64_t>(Lg[0], opts->proxy_rows);
+    Mp[0] = 0;
+  }
+
+  // testing hook: a deterministic cost of the candidate instead of a timing
+  auto fake_cost = [&](const hd_plan_t& pl) -> double {
+    if (opts->fake_cost == 2) return 1.0;  // every candidate ties
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ (uint64_t)opts->seed;
+    for (int i = 0; i < ndim; ++i) {
+      const hd_axis_plan_t& a = pl.axis[i];
+      for (int64_t v : {(int64_t)a.m, (int64_t)a.C, (int64_t)a.S, (int64_t)a.D, (int64_t)a.threads}) {
+        h ^= (uint64_t)v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 31;
+      }
+    }
+    return 1.0 + (double)(h >> 11) * (1.0 / 9007199254740992.0);
+  };
+
+  auto time_plan_on = [&](hd_plan_t pl, const int64_t* lf, const int64_t* lg, const int64_t* mm,
+                          double* secs) -> bool {
     Problem P;
     P.dt = dtype; P.ndim = ndim; P.N = N; P.batch = batch; P.shared_g = false;
     for (int k = 0; k < N; ++k) { P.f[k] = fp[k]; P.g[k] = gp[k]; }
     P.h = hp;
-    if (complete_plan(ctx, dtype, ndim, N, Lf, Lg, M, &pl, P.ax) != HD_OK) return false;
+    if (complete_plan(ctx, dtype, ndim, N, lf, lg, mm, &pl, P.ax) != HD_OK) return false;
     P.plan = pl;
     choose_engines(P);
+    if (fake) {
+      *secs = fake_cost(pl);
+      ctx->tune_log.push_back({pl, *secs});
+      return true;
+    }
     for (int w = 0; w < 2; ++w)
       if (run_pipeline(ctx, P, nullptr, 0, st) != HD_OK) return false;
     std::vector<double> ts;
@@ -1588,11 +1630,21 @@ hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int
     ctx->tune_log.push_back({pl, *secs});
     return true;
   };
+  auto time_plan = [&](hd_plan_t pl, double* secs) { return time_plan_on(pl, Lf, Lg, M, secs); };
+  // lexicographic order of whole plans (axis by axis on (m, C, S, D, threads))
+  auto plan_less = [&](const hd_plan_t& x, const hd_plan_t& y) {
+    for (int i = 0; i < ndim; ++i) {
+      const AxisCand a{x.axis[i].m, x.axis[i].C, x.axis[i].S, x.axis[i].D, x.axis[i].threads};
+      const AxisCand b{y.axis[i].m, y.axis[i].C, y.axis[i].S, y.axis[i].D, y.axis[i].threads};
+      if (cand_less(a, b)) return true;
+      if (cand_less(b, a)) return false;
+    }
+    return false;
+  };
 
   hd_plan_t best = base;
   double best_t = 1e300;
-  if (!time_plan(best, &best_t)) best_t = 1e300;
-  if (flags & HD_TUNE_EXHAUSTIVE) {
+  if (flags & (HD_TUNE_EXHAUSTIVE | HD_TUNE_RANDOM)) {
     std::vector<std::vector<AxisCand>> lists;
     size_t combos = 1;
     for (int i = 0; i < ndim; ++i) {
@@ -1600,36 +1652,64 @@ hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int
       combos *= std::max<size_t>(1, lists.back().size());
     }
     combos = std::min<size_t>(combos, 4096);
-    for (size_t c = 0; c < combos; ++c) {
+    std::vector<size_t> order(combos);
+    for (size_t c = 0; c < combos; ++c) order[c] = c;
+    size_t count = combos;
+    if (random && (size_t)opts->n1 < combos) {
+      // partial Fisher-Yates with splitmix64: n1 candidates uniformly without replacement
+      uint64_t x = opts->seed;
+      auto next = [&]() {
+        uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+      };
+      count = (size_t)opts->n1;
+      for (size_t k = 0; k < count; ++k) {
+        const size_t j = k + (size_t)(next() % (uint64_t)(combos - k));
+        std::swap(order[k], order[j]);
+      }
+    }
+    for (size_t k = 0; k < count; ++k) {
       hd_plan_t pl = base;
-      size_t r = c;
+      size_t r = order[k];
       for (int i = 0; i < ndim; ++i) {
         if (lists[i].empty()) continue;
         apply_cand(pl, i, ndim, lists[i][r % lists[i].size()]);
         r /= lists[i].size();
       }
       double t;
-      if (time_plan(pl, &t) && t < best_t) { best_t = t; best = pl; }
+      if (!time_plan(pl, &t)) continue;
+      const bool tie = std::fabs(t - best_t) <= 1e-12 * best_t;
+      if ((t < best_t && !tie) || (tie && plan_less(pl, best))) { best_t = t; best = pl; }
     }
   } else {
+    if (!time_plan(best, &best_t)) best_t = 1e300;
     for (int i = 0; i < ndim; ++i) {
-      std::vector<AxisCand> cands = axis_candidates(best, i, ndim, N, Lf, Lg, M, eb);
+      const bool on_proxy = proxy && i > 0;
+      std::vector<AxisCand> cands = axis_candidates(best, i, ndim, N, on_proxy ? Lfp : Lf, on_proxy ? Lgp : Lg,
+                                                    on_proxy ? Mp : M, eb);
       AxisCand bc{best.axis[i].m, best.axis[i].C, best.axis[i].S, best.axis[i].D, best.axis[i].threads};
+      double ref_t = best_t;
+      if (on_proxy && !time_plan_on(best, Lfp, Lgp, Mp, &ref_t)) ref_t = 1e300;
       for (const AxisCand& c : cands) {
         hd_plan_t pl = best;
         apply_cand(pl, i, ndim, c);
         double t;
-        if (!time_plan(pl, &t)) continue;
-        const bool tie = std::fabs(t - best_t) <= 1e-12 * best_t;
-        if (t < best_t && !tie) { best_t = t; best = pl; bc = c; }
+        if (!(on_proxy ? time_plan_on(pl, Lfp, Lgp, Mp, &t) : time_plan(pl, &t))) continue;
+        const bool tie = std::fabs(t - ref_t) <= 1e-12 * ref_t;
+        if (t < ref_t && !tie) { ref_t = t; best = pl; bc = c; }
         else if (tie && cand_less(c, bc)) { best = pl; bc = c; }
       }
+      if (on_proxy) best_t = 1e300;  // the full problem's time of the final plan is taken below
+      else best_t = ref_t;
     }
+    if (best_t >= 1e300) time_plan(best, &best_t);
   }
   ctx->profiling = prof_was;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaFree(scratch);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (scratch) cudaFree(scratch);
   AxisInfo ax[HD_MAX_DIM];
   s = complete_plan(ctx, dtype, ndim, N, Lf, Lg, M, &best, ax);
   if (s != HD_OK) return s;
@@ -1637,6 +1717,16 @@ hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int
   ctx->plan_cache[problem_key(dtype, ndim, N, batch, Lf, Lg, M, 0)] = best;
   *out = best;
   return HD_OK;
+}
+
+hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
+                    const int64_t* Lf, const int64_t* Lg, const int64_t* M, uint32_t flags,
+                    int32_t reps, void* stream, hd_plan_t* out) {
+  hd_tune_opts_t o;
+  std::memset(&o, 0, sizeof(o));
+  o.flags = flags & HD_TUNE_EXHAUSTIVE;
+  o.reps = reps;
+  return hd_tune_ex(ctx, dtype, ndim, N, batch, Lf, Lg, M, &o, stream, out);
 }
 
 int32_t hd_tune_log(hd_ctx_t ctx, int32_t max, hd_plan_t* plans, double* seconds) {

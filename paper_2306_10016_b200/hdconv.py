@@ -37,7 +37,7 @@ EXPORTED = [
     "hd_plan_complete", "hd_spectral_permutation", "hd_workspace_bytes", "hd_conv1d",
     "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host", "hd_conv_window",
     "hd_conv_host_async", "hd_host_sync",
-    "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_log",
+    "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_ex", "hd_tune_log",
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_pass",
 ]
 HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
@@ -71,6 +71,15 @@ class Plan(ctypes.Structure):
             p.axis[i].D = int(a.get("D", 0))
             p.axis[i].threads = int(a.get("threads", 0))
         return p
+
+
+HD_TUNE_RANDOM = 0x2
+
+
+class TuneOpts(ctypes.Structure):
+    """hd_tune_opts_t (include/hdconv.h)."""
+    _fields_ = [("flags", ctypes.c_uint32), ("reps", ctypes.c_int32), ("n1", ctypes.c_int32),
+                ("fake_cost", ctypes.c_int32), ("seed", ctypes.c_uint64), ("proxy_rows", ctypes.c_int64)]
 
 
 class Lines(ctypes.Structure):
@@ -134,6 +143,7 @@ def _load():
         "hd_forward_residues": ([P, ctypes.c_int, I64, P, I64, I32, I32, P, P], ctypes.c_int),
         "hd_backward_residues": ([P, ctypes.c_int, I64, P, I32, I32, P, I64, P], ctypes.c_int),
         "hd_tune": ([P, ctypes.c_int, I32, I32, I64, P, P, P, U32, I32, P, PP], ctypes.c_int),
+        "hd_tune_ex": ([P, ctypes.c_int, I32, I32, I64, P, P, P, ctypes.POINTER(TuneOpts), P, PP], ctypes.c_int),
         "hd_tune_log": ([P, I32, PP, P], I32),
         "hd_profile_enable": ([P, I32], ctypes.c_int),
         "hd_profile_read": ([P, I32, P, P, P], I32),
@@ -219,6 +229,63 @@ def hd_abi_version():
 # ---------------------------------------------------------------------------
 # context
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+# Tuning-record analysis of the paper's heuristics (host logic, no device work)
+def sort_lists_topk(A, B, k):
+    """Pairs (A_i, B_i) sorted ascending by B (stable); the first k of each and their
+    original indices (the appendix optimisation code's sort-and-take-k helper)."""
+    if len(A) != len(B):
+        raise ValueError("length mismatch")
+    idx = sorted(range(len(B)), key=lambda i: B[i])[:max(0, k)]
+    return [A[i] for i in idx], [B[i] for i in idx], idx
+
+
+def sort_lists_eps(A, B, eps):
+    """Algorithm 'Sort lists by threshold': with t_best = min B,
+    t_worst = max B and T = t_best + eps (t_worst - t_best), the a_i with b_i <= T,
+    ascending in b, paired with (b_i - t_best) / (t_worst - t_best) (0 when all equal)."""
+    if len(A) != len(B) or not A:
+        raise ValueError("need equal, non-empty lists")
+    tb, tw = min(B), max(B)
+    T = tb + eps * (tw - tb)
+    out_a, out_b = [], []
+    for i in sorted(range(len(B)), key=lambda i: B[i]):
+        if B[i] <= T:
+            out_a.append(A[i])
+            out_b.append(0.0 if tw == tb else (B[i] - tb) / (tw - tb))
+    return out_a, out_b
+
+
+def epsilon_smallest_rectangle(square, rects, eps):
+    """Smallest rectangle height whose eps-filtered m list contains the square's best
+    m (the algorithm's gamma = t_best + eps (t_worst - t_best)).
+    square = (m_values, times); rects = {L_y: (m_values, times)}; None if none does."""
+    ms, ts = square
+    if not ms:
+        raise ValueError("empty square record")
+    m_star = ms[min(range(len(ts)), key=lambda i: ts[i])]
+    for ly in sorted(rects):
+        a, b = rects[ly]
+        if m_star in sort_lists_eps(list(a), list(b), eps)[0]:
+            return ly
+    return None
+
+
+def skinny_estimate(square, rect):
+    """The L_y = 32 heuristic: the rectangle's best m, the square's
+    time at that m, and the square's own optimum; transfer miss if the square never
+    timed that m.  Returns (m_transfer, time_at_transfer, m_best, time_best) or
+    ('miss', m_transfer, m_best, time_best)."""
+    (ms, ts), (mr, tr) = square, rect
+    if not ms or not mr:
+        raise ValueError("empty record")
+    m_t = mr[min(range(len(tr)), key=lambda i: tr[i])]
+    ib = min(range(len(ts)), key=lambda i: ts[i])
+    if m_t not in ms:
+        return ("miss", m_t, ms[ib], ts[ib])
+    return (m_t, ts[ms.index(m_t)], ms[ib], ts[ib])
+
+
 def window_for_mode(mode, Lf, Lg):
     """(lo, n) per axis for the output modes of the paper's 2-D listing
     (N = L1 + L2 - 1 with L1 = L_f, L2 = L_g as in its call
@@ -440,6 +507,18 @@ class Context:
         return p
 
     tune = hd_tune
+
+    def hd_tune_ex(self, dtype, Lf, Lg, M=None, N=1, batch=1, mode="per_axis", n1=16, seed=0,
+                   proxy_rows=0, reps=5, fake_cost=0, stream=None):
+        """Extended tuner: mode per_axis | exhaustive | random (A1, n1 samples, seed);
+        proxy_rows > 0 tunes the axes other than 0 on the skinny proxy problem."""
+        flags = {"per_axis": HD_TUNE_PER_AXIS, "exhaustive": HD_TUNE_EXHAUSTIVE, "random": HD_TUNE_RANDOM}[mode]
+        o = TuneOpts(flags=flags, reps=reps, n1=n1, fake_cost=fake_cost, seed=seed, proxy_rows=proxy_rows)
+        p = Plan()
+        Mv = _i64arr(M) if M is not None else None
+        self._chk(_lib.hd_tune_ex(self.h, dtype, len(Lf), N, batch, _i64arr(Lf), _i64arr(Lg), Mv,
+                                  ctypes.byref(o), _stream_ptr(stream), ctypes.byref(p)))
+        return p
 
     def hd_tune_log(self):
         n = _lib.hd_tune_log(self.h, 0, None, None)
