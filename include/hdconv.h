@@ -172,6 +172,19 @@ hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t
                            const int64_t* M, const int64_t* win_lo, const int64_t* win_n,
                            const hd_plan_t* plan, void* ws, size_t ws_bytes, void* stream);
 
+/* Real inputs: f, g, h REAL arrays of the complex dtype's
+ * component type (HD_C128: double, HD_C64: float), device pointers, batch pairs,
+ * h = f * g (full, extent L_f + L_g - 1 per axis).  The two halves of f along
+ * axis 0 (rows [0, A) and [A, L_f,0), A = ceil(L_f,0 / 2)) are packed as the real
+ * and imaginary parts of one complex array z; because g is real, w = z * g (the
+ * complex pipeline, hd_conv1d/2d/3d's kernels) holds both half convolutions, and
+ * h[y] = Re w[y] + Im w[y - A] (overlap-add of the two halves).  About half the
+ * transform work and half the input/output bytes of the complex path.  `plan`
+ * is for the packed problem (extents A, L_f,1.. and L_g); NULL = cached/default. */
+hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch,
+                         const void* f, const int64_t* Lf, const void* g, const int64_t* Lg,
+                         void* h, const hd_plan_t* plan, void* stream);
+
 /* ---- end-to-end with HOST buffers ------------------------------------------ */
 /* Same as hd_multiconv with batch (N = 1 for plain conv) but f, g, h are HOST
  * pointers (pinned for best speed).  Copies in, convolves, copies out and

@@ -35,6 +35,8 @@ struct hd_ctx {
   size_t ws_size = 0;
   void* io = nullptr;                   // device buffers for hd_conv_host
   size_t io_size = 0;
+  void* rio = nullptr;                  // hd_conv_real: packed input, complex g, complex result
+  size_t rio_size = 0;
   struct HostSlot {                     // hd_conv_host_async: double-buffered host I/O
     void* io = nullptr;
     size_t size = 0;
@@ -961,6 +963,7 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   for (auto& kv : ctx->st32) cudaFree(kv.second);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
+  if (ctx->rio) cudaFree(ctx->rio);
   for (auto& sl : ctx->hslot) {
     if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
     if (sl.io) cudaFree(sl.io);
@@ -1047,6 +1050,56 @@ hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t
                           void* stream) {
   if (!win_lo || !win_n) return fail(ctx, HD_ERR_INVALID, "null window");
   return run_entry(ctx, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan, ws, ws_bytes, stream, win_lo, win_n);
+}
+
+hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch, const void* f,
+                         const int64_t* Lf, const void* g, const int64_t* Lg, void* h, const hd_plan_t* plan,
+                         void* stream) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (!f || !g || !h || !Lf || !Lg) return fail(ctx, HD_ERR_INVALID, "null argument");
+  if (dtype != HD_C64 && dtype != HD_C128) return fail(ctx, HD_ERR_INVALID, "dtype must be HD_C64 or HD_C128");
+  if (ndim < 1 || ndim > HD_MAX_DIM || batch < 1) return fail(ctx, HD_ERR_INVALID, "bad ndim or batch");
+  for (int i = 0; i < ndim; ++i)
+    if (Lf[i] < 1 || Lg[i] < 1) return fail(ctx, HD_ERR_INVALID, "extents must be >= 1");
+  const bool dbl = dtype == HD_C128;
+  const size_t rb = dbl ? 8 : 4, cb = 2 * rb;
+  // z: the two halves of f along axis 0 (A = ceil(Lf0 / 2) rows each, zero-padded)
+  const int64_t A = (Lf[0] + 1) / 2;
+  int64_t Lz[HD_MAX_DIM];
+  int64_t rest_f = 1, rest_g = 1, rest_o = 1;
+  for (int i = 0; i < ndim; ++i) Lz[i] = Lf[i];
+  Lz[0] = A;
+  for (int i = 1; i < ndim; ++i) { rest_f *= Lf[i]; rest_g *= Lg[i]; rest_o *= Lf[i] + Lg[i] - 1; }
+  const int64_t Ow0 = A + Lg[0] - 1, Lout0 = Lf[0] + Lg[0] - 1;
+  const size_t bz = align256((size_t)(batch * A * rest_f) * cb);
+  const size_t bgc = align256((size_t)(batch * Lg[0] * rest_g) * cb);
+  const size_t bw = align256((size_t)(batch * Ow0 * rest_o) * cb);
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (ctx->rio_size < bz + bgc + bw) {
+      if (ctx->rio) cudaFree(ctx->rio);
+      ctx->rio = nullptr; ctx->rio_size = 0;
+      cudaError_t e = cudaMalloc(&ctx->rio, bz + bgc + bw);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(real path)");
+      ctx->rio_size = bz + bgc + bw;
+    }
+  }
+  char* z = (char*)ctx->rio;
+  char* gc = z + bz;
+  char* w = gc + bgc;
+  cudaError_t e = hd::launch_real_pack(dbl, f, z, Lf[0], A, rest_f, batch, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "real pack");
+  e = hd::launch_real_to_complex(dbl, g, gc, batch * Lg[0] * rest_g, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "real to complex");
+  const void* fa[1] = {z};
+  const void* ga[1] = {gc};
+  hd_status_t s = run_entry(ctx, dtype, ndim, 1, batch, fa, Lz, ga, Lg, w, nullptr, plan, nullptr, 0, stream);
+  if (s != HD_OK) return s;
+  e = hd::launch_real_unpack(dbl, w, h, Lout0, Ow0, A, rest_o, batch, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "real unpack");
+  return HD_OK;
 }
 
 hd_status_t hd_conv1d(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,

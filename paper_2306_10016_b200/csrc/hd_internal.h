@@ -21,5 +21,11 @@ cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],
                         const int64_t P[3], int64_t nb, cudaStream_t st);
+// real-input path (hd_conv_real): pack / promote / unpack kernels (hd_kernels.cu)
+cudaError_t launch_real_pack(bool is_double, const void* f, void* z, int64_t Lf0, int64_t A, int64_t rest,
+                             int64_t nb, cudaStream_t st);
+cudaError_t launch_real_to_complex(bool is_double, const void* g, void* gc, int64_t n, cudaStream_t st);
+cudaError_t launch_real_unpack(bool is_double, const void* w, void* h, int64_t Lout0, int64_t Ow0, int64_t A,
+                               int64_t rest, int64_t nb, cudaStream_t st);
 constexpr size_t kMaxSmem = 227 * 1024;
 }  // namespace hd

@@ -55,4 +55,82 @@ cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_
                    : launch_crop_impl<float2>(src, dst, O, P, nb, st);
 }
 
+// ---------------------------------------------------------------------------
+// Real-input path (hd_conv_real): pack the two halves of a real f along axis 0 as
+// the real and imaginary parts of one complex array, and unpack the complex result
+//   z[b][y][r] = f[b][y][r] + i f[b][y + A][r]            (y < A, 0 beyond Lf0)
+//   h[b][y][r] = Re w[b][y][r] + Im w[b][y - A][r]         (each term where defined)
+// R rows of `rest` elements each; memory-bound grid-stride loops.
+// one CTA per (b, y) row at a time, threads along the contiguous rest: no per-element
+// division, coalesced rows
+template <typename R>
+__global__ void real_pack_kernel(const R* __restrict__ f, typename cplx_of<R>::type* __restrict__ z,
+                                 int64_t Lf0, int64_t A, int64_t rest, int64_t nb) {
+  using V = typename cplx_of<R>::type;
+  for (int64_t row = blockIdx.x; row < nb * A; row += gridDim.x) {
+    const int64_t b = row / A, y = row - b * A;
+    const R* fa = f + (b * Lf0 + y) * rest;
+    const R* fb = (y + A < Lf0) ? fa + A * rest : nullptr;
+    V* zr = z + row * rest;
+    for (int64_t r = threadIdx.x; r < rest; r += blockDim.x) {
+      V v;
+      v.x = fa[r];
+      v.y = fb ? fb[r] : (R)0;
+      zr[r] = v;
+    }
+  }
+}
+template <typename R>
+__global__ void real_to_complex_kernel(const R* __restrict__ g, typename cplx_of<R>::type* __restrict__ gc,
+                                       int64_t n) {
+  using V = typename cplx_of<R>::type;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    V v; v.x = g[i]; v.y = (R)0;
+    gc[i] = v;
+  }
+}
+template <typename R>
+__global__ void real_unpack_kernel(const typename cplx_of<R>::type* __restrict__ w, R* __restrict__ h,
+                                   int64_t Lout0, int64_t Ow0, int64_t A, int64_t rest, int64_t nb) {
+  using V = typename cplx_of<R>::type;
+  for (int64_t row = blockIdx.x; row < nb * Lout0; row += gridDim.x) {
+    const int64_t b = row / Lout0, y = row - b * Lout0;
+    const V* wa = (y < Ow0) ? w + (b * Ow0 + y) * rest : nullptr;
+    const V* wb = (y >= A && y - A < Ow0) ? w + (b * Ow0 + y - A) * rest : nullptr;
+    R* hr = h + row * rest;
+    for (int64_t r = threadIdx.x; r < rest; r += blockDim.x) {
+      R acc = wa ? wa[r].x : (R)0;
+      if (wb) acc += wb[r].y;
+      hr[r] = acc;
+    }
+  }
+}
+
+static unsigned grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (unsigned)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+cudaError_t launch_real_pack(bool is_double, const void* f, void* z, int64_t Lf0, int64_t A, int64_t rest,
+                             int64_t nb, cudaStream_t st) {
+  const unsigned g = grid_for(nb * A * 256);
+  if (is_double) real_pack_kernel<double><<<g, 256, 0, st>>>((const double*)f, (double2*)z, Lf0, A, rest, nb);
+  else real_pack_kernel<float><<<g, 256, 0, st>>>((const float*)f, (float2*)z, Lf0, A, rest, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_real_to_complex(bool is_double, const void* g, void* gc, int64_t n, cudaStream_t st) {
+  const unsigned gr = grid_for(n);
+  if (is_double) real_to_complex_kernel<double><<<gr, 256, 0, st>>>((const double*)g, (double2*)gc, n);
+  else real_to_complex_kernel<float><<<gr, 256, 0, st>>>((const float*)g, (float2*)gc, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_real_unpack(bool is_double, const void* w, void* h, int64_t Lout0, int64_t Ow0, int64_t A,
+                               int64_t rest, int64_t nb, cudaStream_t st) {
+  const unsigned g = grid_for(nb * Lout0 * 256);
+  if (is_double)
+    real_unpack_kernel<double><<<g, 256, 0, st>>>((const double2*)w, (double*)h, Lout0, Ow0, A, rest, nb);
+  else real_unpack_kernel<float><<<g, 256, 0, st>>>((const float2*)w, (float*)h, Lout0, Ow0, A, rest, nb);
+  return cudaGetLastError();
+}
+
 }  // namespace hd

@@ -36,6 +36,7 @@ EXPORTED = [
     "hd_abi_version", "hd_create", "hd_destroy", "hd_last_error", "hd_plan_default",
     "hd_plan_complete", "hd_spectral_permutation", "hd_workspace_bytes", "hd_conv1d",
     "hd_conv2d", "hd_conv3d", "hd_multiconv", "hd_conv_explicit", "hd_conv_host", "hd_conv_window",
+    "hd_conv_real",
     "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_ex", "hd_tune_log",
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_pass",
@@ -135,6 +136,7 @@ def _load():
         "hd_conv3d": ([P, ctypes.c_int, I64, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
         "hd_multiconv": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, P, PP, P, SZ, P], ctypes.c_int),
         "hd_conv_explicit": ([P, ctypes.c_int, I32, I32, P, P, P, P, P, PP, P], ctypes.c_int),
+        "hd_conv_real": ([P, ctypes.c_int, I32, I64, P, P, P, P, P, PP, P], ctypes.c_int),
         "hd_conv_window": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, P, P, PP, P, ctypes.c_size_t, P],
                            ctypes.c_int),
         "hd_conv_host": ([P, ctypes.c_int, I32, I32, I64, P, P, P, P, P, P, PP, P], ctypes.c_int),
@@ -421,6 +423,31 @@ class Context:
         return h
 
     conv_window = hd_conv_window
+
+    def hd_conv_real(self, f, g, plan=None, h=None, batch=False, stream=None):
+        """Full linear convolution of REAL torch tensors (float64 -> complex128
+        machinery, float32 -> complex64); leading batch axis when batch=True."""
+        import torch
+        nd = f.dim() - (1 if batch else 0)
+        B = f.shape[0] if batch else 1
+        Lf, Lg = list(f.shape[-nd:]), list(g.shape[-nd:])
+        if f.dtype == torch.float64:
+            dt = HD_C128
+        elif f.dtype == torch.float32:
+            dt = HD_C64
+        else:
+            raise TypeError(f"unsupported dtype {f.dtype} (float32 / float64 only)")
+        if g.dtype != f.dtype or not f.is_contiguous() or not g.is_contiguous():
+            raise TypeError("f and g must be contiguous tensors of the same real dtype")
+        if h is None:
+            h = torch.empty(([B] if batch else []) + [a + b - 1 for a, b in zip(Lf, Lg)], dtype=f.dtype,
+                            device=f.device)
+        pp = ctypes.byref(plan) if plan is not None else None
+        self._chk(_lib.hd_conv_real(self.h, dt, nd, B, _ptr(f), _i64arr(Lf), _ptr(g), _i64arr(Lg), _ptr(h), pp,
+                                    _stream_ptr(stream)))
+        return h
+
+    conv_real = hd_conv_real
 
     def hd_conv_explicit(self, fs, gs, plan=None, h=None, stream=None):
         N = len(fs)
