@@ -279,16 +279,21 @@ def run_ours(args, rank, world, local_rank):
 
     slab = None
     if args.mode == "slab":
-        if ndim != 2 or N != 1:
-            raise SystemExit("--mode slab: 2D single-pair configs only")
-        from paper_2306_10016_b200.dist import GpuBackend, SlabConv2D, torch_exchange
+        if ndim < 2 or N != 1 or batch != 1:
+            raise SystemExit("--mode slab: 2D/3D single-pair configs only")
+        from paper_2306_10016_b200.dist import (GpuBackend, GpuBackend3D, SlabConv2D, SlabConv3D,
+                                                torch_exchange)
 
         def local_exchange(send, recv, block):
             recv[:block].copy_(send[:block])
-        be = GpuBackend(ctx, plan, dtc)
-        slab = SlabConv2D(be, torch_exchange() if dist else local_exchange, world, rank, Lf, Lg,
-                          plan.axis[1].M1)
-        r0, r1 = slab.plan.rows(rank)
+        exch = torch_exchange() if dist else local_exchange
+        if ndim == 2:
+            slab = SlabConv2D(GpuBackend(ctx, plan, dtc), exch, world, rank, Lf, Lg, plan.axis[1].M1)
+            r0, r1 = slab.plan.rows(rank)
+        else:
+            slab = SlabConv3D(GpuBackend3D(ctx, plan, dtc), exch, world, rank, Lf, Lg, plan.axis[1].M1,
+                              plan.axis[2].M1)
+            r0, r1 = slab.plan.planes(rank)
         f_local = fd[0][r0:r1].contiguous()
 
     def step():
@@ -449,7 +454,8 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": name, "Lf": Lf, "Lg": Lg, "Lout": Lout, "pairs": N, "batch": batch,
                        "plan": [{k: v for k, v in a.items()} for a in plan.as_dict()["axis"]],
                        "tune_seconds": tune_s,
-                       "parallelism": (f"slab x{world} (rows; NCCL all-to-all transposes)" if slab is not None
+                       "parallelism": (f"slab x{world} ({'rows' if ndim == 2 else 'z-planes'}; NCCL all-to-all "
+                                       "transposes)" if slab is not None
                                        else f"weak x{world} (independent problems)"),
                        "l2": "inputs larger than L2 (image 268 MB > 126 MB L2); no flush needed"},
             "roofline": roof, "whole_step": whole, "cpu_baseline": cpu, "e2e": e2e,

@@ -200,6 +200,204 @@ class GpuBackend:
         return h
 
 
+# ---------------------------------------------------------------------------
+# 3-D: z-slabs: rank k holds f planes [k Rz, (k+1) Rz) (g replicated)
+#   1. forward along x, then y, of the local planes       -> send1[dest][kyl][kx][zl]
+#   2. all-to-all: rank k' receives the spectral rows ky of its slab for every z
+#   3. convolution along z of its (ky, kx) lines            -> send2[dest][kyl][kx][zol]
+#   4. all-to-all: rank k receives its output planes for every (ky, kx)
+#   5. inverse along y, then x, of the local output planes  -> h planes
+@dataclass
+class SlabPlan3D:
+    """Partition of a 3-D problem f [Lf0][Lf1][Lf2] * g over `world` ranks; Ky, Kx the
+    spectral extents (M1) along y and x."""
+    world: int
+    Lf: tuple
+    Lg: tuple
+    Ky: int
+    Kx: int
+
+    def __post_init__(self):
+        self.O = tuple(a + b - 1 for a, b in zip(self.Lf, self.Lg))
+        self.Rz = cdiv(self.Lf[0], self.world)      # f planes per rank
+        self.Roz = cdiv(self.O[0], self.world)      # output planes per rank
+        self.Kys = cdiv(self.Ky, self.world)        # spectral y rows per rank
+
+    def planes(self, k):
+        return min(k * self.Rz, self.Lf[0]), min((k + 1) * self.Rz, self.Lf[0])
+
+    def out_planes(self, k):
+        return min(k * self.Roz, self.O[0]), min((k + 1) * self.Roz, self.O[0])
+
+    def kys(self, k):
+        return min(k * self.Kys, self.Ky), min((k + 1) * self.Kys, self.Ky)
+
+    @property
+    def block1(self):
+        return self.Kys * self.Kx * self.Rz
+
+    @property
+    def block2(self):
+        return self.Kys * self.Kx * self.Roz
+
+    def bytes_sent_per_rank(self, elem_bytes):
+        return (self.world - 1) * (self.block1 + self.block2) * elem_bytes
+
+
+class SlabConv3D:
+    """Slab-decomposed 3-D convolution on one rank of `world`.
+
+    backend: fwd_planes(f_planes, nz, send1, P)     passes 1 (x, then y) of the local planes
+             fwd_g(g, xyg, P)                        the replicated g's x and y transforms
+             conv_lines(recv1, xyg, ky0, nky, send2, P)  convolution along z
+             inv_planes(recv2, nzo, P) -> h planes   passes 5 (y, then x)
+             empty(n)
+    exchange(send, recv, block) as for SlabConv2D."""
+
+    def __init__(self, backend, exchange, world, rank, Lf, Lg, Ky, Kx):
+        self.b = backend
+        self.exchange = exchange
+        self.rank = rank
+        self.plan = SlabPlan3D(world, tuple(Lf), tuple(Lg), Ky, Kx)
+
+    def stage1(self, f_planes, g):
+        P, k, b = self.plan, self.rank, self.b
+        z0, z1 = P.planes(k)
+        send = b.empty(P.world * P.block1)
+        b.fwd_planes(f_planes, z1 - z0, send, P)
+        xyg = b.empty(P.Ky * P.Kx * P.Lg[0])
+        b.fwd_g(g, xyg, P)
+        return send, xyg
+
+    def stage2(self, recv1, xyg):
+        P, k, b = self.plan, self.rank, self.b
+        y0, y1 = P.kys(k)
+        send = b.empty(P.world * P.block2)
+        b.conv_lines(recv1, xyg, y0, y1 - y0, send, P)
+        return send
+
+    def stage3(self, recv2):
+        P, k = self.plan, self.rank
+        o0, o1 = P.out_planes(k)
+        return self.b.inv_planes(recv2, o1 - o0, P)
+
+    def __call__(self, f_planes, g):
+        P, b = self.plan, self.b
+        s1, xyg = self.stage1(f_planes, g)
+        r1 = b.empty(P.world * P.block1)
+        self.exchange(s1, r1, P.block1)
+        s2 = self.stage2(r1, xyg)
+        r2 = b.empty(P.world * P.block2)
+        self.exchange(s2, r2, P.block2)
+        return self.stage3(r2)
+
+
+def emulate_ranks_3d(convs, f, g, empty):
+    """SlabConv3D on `world` emulated ranks in one process (block copies for the
+    all-to-alls)."""
+    world = len(convs)
+    P = convs[0].plan
+    st1 = []
+    for k, c in enumerate(convs):
+        z0, z1 = P.planes(k)
+        st1.append(c.stage1(f[z0:z1], g))
+
+    def a2a(sends, block):
+        recvs = [empty(world * block) for _ in range(world)]
+        for src in range(world):
+            for dst in range(world):
+                recvs[dst][src * block:(src + 1) * block] = sends[src][dst * block:(dst + 1) * block]
+        return recvs
+    r1 = a2a([s for s, _ in st1], P.block1)
+    s2 = [c.stage2(r1[k], st1[k][1]) for k, c in enumerate(convs)]
+    r2 = a2a(s2, P.block2)
+    return [c.stage3(r2[k]) for k, c in enumerate(convs)]
+
+
+class GpuBackend3D:
+    """3-D slab passes on libhdconv.so (hd_pass descriptors, device tensors)."""
+
+    def __init__(self, ctx, plan, dtype):
+        import torch
+        from . import hdconv as H
+        self.H, self.torch, self.ctx = H, torch, ctx
+        self.dt = dtype
+        self.tdt = torch.complex128 if dtype == H.HD_C128 else torch.complex64
+        self.ax = plan.as_dict()["axis"]     # [z, y, x]
+        self.scale = 1.0 / (self.ax[0]["M1"] * self.ax[1]["M1"] * self.ax[2]["M1"])
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, n):
+        return self.torch.empty(max(1, n), dtype=self.tdt, device=self.dev)
+
+    def _desc(self, mode, axis, nlines, nbatch):
+        d = self.H.PassDesc()
+        a = self.ax[axis]
+        d.mode, d.npairs, d.nlines, d.nbatch, d.M = mode, 1, nlines, nbatch, a["M1"]
+        d.axis.m, d.axis.C, d.axis.D, d.axis.threads = a["m"], 1, 0, 0
+        return d
+
+    def _xy(self, src, nz, Ly, Lx, out_ptr, s_ky, s_kx, s_z, jd=0, s_jt=0):
+        """x then y forward transforms of nz planes [z][y][x]; spectral element (z, ky, kx)
+        -> out + (ky tiling) + kx * s_kx + z * s_z."""
+        H, P = self.H, None
+        x1 = self.empty(nz * self.ax[2]["M1"] * Ly)                   # X1[z][kx][y]
+        Kx = self.ax[2]["M1"]
+        d = self._desc(H.HD_PASS_FWD, 2, Ly, nz)
+        d.in_f = H.Lines.make([src.data_ptr()], Lx, s_l=Lx, s_b=Ly * Lx, nbi=nz)
+        d.out = H.Lines.make([x1.data_ptr()], Kx, s_l=1, s_j=Ly, s_b=Kx * Ly, nbi=nz)
+        self.ctx.hd_pass(self.dt, d)
+        d = self._desc(H.HD_PASS_FWD, 1, Kx, nz)
+        d.in_f = H.Lines.make([x1.data_ptr()], Ly, s_l=Ly, s_b=Kx * Ly, nbi=nz)
+        d.out = H.Lines.make([out_ptr], self.ax[1]["M1"], s_l=s_kx, s_j=s_ky, jd=jd, s_jt=s_jt, s_b=s_z, nbi=nz)
+        self.ctx.hd_pass(self.dt, d)
+
+    def fwd_planes(self, f_planes, nz, send, P):
+        if nz <= 0:
+            return
+        # element (zl, ky, kx) -> [ky / Kys][ky % Kys][kx][zl] of the send buffer
+        self._xy(f_planes, nz, P.Lf[1], P.Lf[2], send.data_ptr(), s_ky=P.Kx * P.Rz, s_kx=P.Rz, s_z=1,
+                 jd=P.Kys, s_jt=P.Kys * P.Kx * P.Rz)
+
+    def fwd_g(self, g, xyg, P):
+        # XYg[ky][kx][z]
+        self._xy(g, P.Lg[0], P.Lg[1], P.Lg[2], xyg.data_ptr(), s_ky=P.Kx * P.Lg[0], s_kx=P.Lg[0], s_z=1)
+
+    def conv_lines(self, recv1, xyg, ky0, nky, send2, P):
+        if nky <= 0:
+            return
+        H = self.H
+        eb = xyg.element_size()
+        d = self._desc(H.HD_PASS_CONV, 0, P.Kx, nky)
+        # element z = src * Rz + zl of line (kyl, kx): [src][kyl][kx][zl]
+        d.in_f = H.Lines.make([recv1.data_ptr()], P.Lf[0], s_l=P.Rz, s_j=1, jd=P.Rz, s_jt=P.block1,
+                              s_b=P.Kx * P.Rz, nbi=nky)
+        d.in_g = H.Lines.make([xyg.data_ptr() + ky0 * P.Kx * P.Lg[0] * eb], P.Lg[0], s_l=P.Lg[0],
+                              s_b=P.Kx * P.Lg[0], nbi=nky)
+        d.out = H.Lines.make([send2.data_ptr()], P.O[0], s_l=P.Roz, s_j=1, jd=P.Roz, s_jt=P.block2,
+                             s_b=P.Kx * P.Roz, nbi=nky)
+        d.scale = self.scale
+        self.ctx.hd_pass(self.dt, d)
+
+    def inv_planes(self, recv2, nzo, P):
+        h = self.torch.empty((max(nzo, 0), P.O[1], P.O[2]), dtype=self.tdt, device=self.dev)
+        if nzo <= 0:
+            return h
+        H = self.H
+        w = self.empty(nzo * P.O[1] * P.Kx)                           # W[zol][y][kx]
+        d = self._desc(H.HD_PASS_INV, 1, P.Kx, nzo)
+        # element ky = src * Kys + kyl of line (zol, kx): [src][kyl][kx][zol]
+        d.in_f = H.Lines.make([recv2.data_ptr()], P.Ky, s_l=P.Roz, s_j=P.Kx * P.Roz, jd=P.Kys, s_jt=P.block2,
+                              s_b=1, nbi=nzo)
+        d.out = H.Lines.make([w.data_ptr()], P.O[1], s_l=1, s_j=P.Kx, s_b=P.O[1] * P.Kx, nbi=nzo)
+        self.ctx.hd_pass(self.dt, d)
+        d = self._desc(H.HD_PASS_INV, 2, P.O[1], nzo)
+        d.in_f = H.Lines.make([w.data_ptr()], P.Kx, s_l=P.Kx, s_b=P.O[1] * P.Kx, nbi=nzo)
+        d.out = H.Lines.make([h.data_ptr()], P.O[2], s_l=P.O[2], s_b=P.O[1] * P.O[2], nbi=nzo)
+        self.ctx.hd_pass(self.dt, d)
+        return h
+
+
 def torch_exchange(group=None):
     """all-to-all of equal contiguous blocks with torch.distributed (NCCL on GPU)."""
     import torch.distributed as dist

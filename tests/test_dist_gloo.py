@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2306_10016_b200.dist import SlabConv2D, SlabPlan2D
+from paper_2306_10016_b200.dist import SlabConv2D, SlabConv3D, SlabPlan2D, SlabPlan3D
 
 
 class NumpyBackend:
@@ -119,3 +119,100 @@ def test_slab_plan_partitions():
         cols = [P.cols(k) for k in range(world)]
         assert sum(b - a for a, b in cols) == 4608
         assert P.bytes_sent_per_rank(16) == (world - 1) * (P.x_block + P.y_block) * 16
+
+
+# ---------------------------------------------------------------- 3-D z-slabs
+class NumpyBackend3D:
+    """Test stand-in for GpuBackend3D: same exchange layouts, numpy transforms."""
+
+    def __init__(self, Kz):
+        self.Kz = Kz
+
+    def empty(self, n):
+        return np.zeros(max(1, n), dtype=np.complex128)
+
+    @staticmethod
+    def _xy(planes, Ky, Kx):
+        X = np.fft.ifft(planes, n=Kx, axis=2) * Kx                # + exponent, unnormalised
+        return np.fft.ifft(X, n=Ky, axis=1) * Ky                  # [z][ky][kx]
+
+    def fwd_planes(self, f_planes, nz, send, P):
+        S = self._xy(f_planes, P.Ky, P.Kx)
+        for zl in range(nz):
+            for ky in range(P.Ky):
+                base = (ky // P.Kys) * P.block1 + (ky % P.Kys) * P.Kx * P.Rz + zl
+                send[base + np.arange(P.Kx) * P.Rz] = S[zl, ky]
+
+    def fwd_g(self, g, xyg, P):
+        S = self._xy(g, P.Ky, P.Kx)                               # [z][ky][kx]
+        xyg[: P.Ky * P.Kx * P.Lg[0]] = np.transpose(S, (1, 2, 0)).reshape(-1)
+
+    def conv_lines(self, recv1, xyg, ky0, nky, send2, P):
+        zs, zo = np.arange(P.Lf[0]), np.arange(P.O[0])
+        for kyl in range(nky):
+            for kx in range(P.Kx):
+                fcol = recv1[(zs // P.Rz) * P.block1 + kyl * P.Kx * P.Rz + kx * P.Rz + zs % P.Rz]
+                gcol = xyg[((ky0 + kyl) * P.Kx + kx) * P.Lg[0] + np.arange(P.Lg[0])]
+                F = np.fft.ifft(fcol, n=self.Kz) * self.Kz
+                G = np.fft.ifft(gcol, n=self.Kz) * self.Kz
+                V = np.fft.fft(F * G) / (self.Kz * P.Ky * P.Kx)
+                send2[(zo // P.Roz) * P.block2 + kyl * P.Kx * P.Roz + kx * P.Roz + zo % P.Roz] = V[: P.O[0]]
+
+    def inv_planes(self, recv2, nzo, P):
+        h = np.zeros((nzo, P.O[1], P.O[2]), dtype=np.complex128)
+        ky = np.arange(P.Ky)
+        for zol in range(nzo):
+            W = np.zeros((P.O[1], P.Kx), dtype=np.complex128)
+            for kx in range(P.Kx):
+                row = recv2[(ky // P.Kys) * P.block2 + (ky % P.Kys) * P.Kx * P.Roz + kx * P.Roz + zol]
+                W[:, kx] = np.fft.fft(row)[: P.O[1]]
+            h[zol] = np.fft.fft(W, axis=1)[:, : P.O[2]]
+        return h
+
+
+def _worker3d(rank, world, port, Lf, Lg, Kz, Ky, Kx, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        f, g = synth.random_pair(322, Lf, Lg)
+        P = SlabPlan3D(world, Lf, Lg, Ky, Kx)
+        z0, z1 = P.planes(rank)
+        conv = SlabConv3D(NumpyBackend3D(Kz), gloo_exchange, world, rank, Lf, Lg, Ky, Kx)
+        h = conv(np.ascontiguousarray(f[z0:z1]), g)
+        parts = [None] * world
+        dist.all_gather_object(parts, h)
+        if rank == 0:
+            q.put(np.concatenate(parts, axis=0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Lf,Lg,K", [((7, 6, 5), (3, 4, 2), (10, 12, 8)), ((4, 9, 6), (5, 2, 3), (9, 11, 9))])
+def test_slab3d_two_ranks(Lf, Lg, K):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker3d, args=(r, world, port, Lf, Lg, K[0], K[1], K[2], q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    h = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    f, g = synth.random_pair(322, Lf, Lg)
+    ref = oracle.conv(f, g)
+    assert h.shape == ref.shape
+    assert oracle.rel_l2(h, ref) < 1e-12
+
+
+def test_slab3d_plan_partitions():
+    for world in (1, 2, 3, 8):
+        P = SlabPlan3D(world, (512, 512, 512), (129, 129, 129), 640, 640)
+        pl = [P.planes(k) for k in range(world)]
+        assert pl[0][0] == 0 and pl[-1][1] == 512 and all(pl[i][1] == pl[i + 1][0] for i in range(world - 1))
+        assert sum(b - a for a, b in (P.out_planes(k) for k in range(world))) == 640
+        assert sum(b - a for a, b in (P.kys(k) for k in range(world))) == 640
+        assert P.bytes_sent_per_rank(8) == (world - 1) * (P.block1 + P.block2) * 8
