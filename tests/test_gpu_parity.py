@@ -411,6 +411,26 @@ def test_s512_engine_matches_oracle_and_generic(ctx, H, shape, S):
     assert oracle.rel_l2(hg, ref) < 1e-11
 
 
+@pytest.mark.parametrize("shape", [
+    ((1, 1), (1, 1)),            # single element: q = 1, p = 1, one output
+    ((300, 200), (100, 100)),    # q = 1 on both axes
+    ((17, 3), (512, 2)),         # short input of exactly m = 512 rows (p_g = 1, not pruned)
+    ((600, 513), (257, 40)),     # L_g = 257 (just past the pruned half), x: p = 2 from 513
+    ((1100, 90), (40, 5000)),    # x: the long input is g (swapped roles), q = 10
+    ((2, 5000), (1, 600)),       # x: q = 11 (largest staged q), p_f = 10 > 8 -> generic fwd
+])
+def test_s512_engine_edge_cases(ctx, H, shape):
+    """Degenerate and boundary shapes through the staged m = 512 plans (automatic
+    engine choice falls back to the generic engine where the staged one does not
+    apply; both must agree with the oracle)."""
+    sf, sg = shape
+    f, g = synth.random_pair(840 + sf[0], sf, sg)
+    axes = [{"m": 512, "C": 1, "S": 2}, {"m": 512, "C": 1, "S": 2}]
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(2, axes)))
+    ref = oracle.conv(f, g)
+    assert h.shape == ref.shape and oracle.rel_l2(h, ref) < 1e-11
+
+
 @pytest.mark.parametrize("shape", [((3000, 2500), (500, 300)), ((4000, 1700), (230, 4000))])
 def test_s512_engine_large_q_sampled(ctx, H, shape):
     """q up to 12 along x (fwd/inv passes) and q = 7..9 along the convolution axis,
