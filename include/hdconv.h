@@ -309,6 +309,14 @@ int32_t     hd_profile_read(hd_ctx_t ctx, int32_t max, double* ms, int64_t* laun
 hd_status_t hd_profile_reset(hd_ctx_t ctx);
 /* Total kernel launches issued by this context since creation. */
 int64_t     hd_launch_count(hd_ctx_t ctx);
+/* Pass launches issued by this context since creation on one engine (HD_ENGINE_*),
+ * or -1 for a null context / unknown engine.  The engine of each pass is chosen
+ * automatically per axis (plan threads = 0); this reports which ones ran. */
+#define HD_ENGINE_GENERIC 0     /* shared-memory radix-8 engine, any m and dtype */
+#define HD_ENGINE_S512 1        /* staged warp engine, m = 512 complex double (C = 1) */
+#define HD_ENGINE_S512_MCONV 2  /* its multi-pair convolution pass */
+#define HD_ENGINE_S128 3        /* staged engine, m = 128 complex float (C = 4) */
+int64_t     hd_engine_launches(hd_ctx_t ctx, int32_t engine);
 
 #ifdef __cplusplus
 }

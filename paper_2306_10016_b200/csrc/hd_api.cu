@@ -58,6 +58,7 @@ struct hd_ctx {
   };
   std::vector<ProfEntry> prof;
   int64_t launches = 0;
+  int64_t engine_launches[4] = {0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
 };
 
 namespace {
@@ -322,6 +323,7 @@ struct Launch {
   uint32_t flags;
   bool auto_engine;
   bool s512_axis;   // the staged engine may run this pass (same engine for every pass of the axis)
+  bool s128_axis;   // likewise for the m = 128 complex-float staged engine
   int mode;
   const char* name;
   PassArgs a;
@@ -351,10 +353,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// dims (innermost first, complex values as 2 doubles): {d0 doubles, d1, d2, nbi, nbo};
-// strides in elements of 16 B for dims 1..4 (0 = broadcast dimension of size 1)
+// dims (innermost first, complex values as 2 scalars): {d0 scalars, d1, d2, nbi, nbo};
+// strides in complex elements (16 B, or 8 B when f32) for dims 1..4 (0 = broadcast
+// dimension of size 1)
 bool encode_lines(CUtensorMap* map, const void* base, const uint64_t dims[5], const int64_t strides[4],
-                  const uint32_t box[5]) {
+                  const uint32_t box[5], bool f32 = false) {
+  const cuuint64_t eb = f32 ? 8 : 16;
   auto enc = tensor_map_encoder();
   if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
   cuuint64_t gd[5];
@@ -363,37 +367,48 @@ bool encode_lines(CUtensorMap* map, const void* base, const uint64_t dims[5], co
   for (int i = 0; i < 5; ++i) { gd[i] = dims[i] ? dims[i] : 1; bx[i] = box[i]; }
   for (int i = 0; i < 4; ++i) {
     if (strides[i] < 0) return false;
-    gs[i] = strides[i] > 0 ? (cuuint64_t)strides[i] * 16 : 16;
+    gs[i] = strides[i] > 0 ? (cuuint64_t)strides[i] * eb : 16;
+    if (gs[i] % 16) return false;
     if (strides[i] == 0) gd[i + 1] = 1;
     if (gs[i] >= (cuuint64_t(1) << 40)) return false;
   }
   for (int i = 0; i < 5; ++i) if (gd[i] > 0xffffffffull) return false;
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), gd, gs, bx, es,
+  return enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), gd, gs, bx, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// input lines -> TMA_BULK (plain rows) or TMA_LINE_TILED (lines tiled by S, element stride s_j)
+// 1-D bulk copies of complex-float rows need 16-byte aligned starts and lengths
+bool bulk_ok_f32(const void* const* ptr, int narr, std::initializer_list<int64_t> v) {
+  for (int k = 0; k < narr; ++k)
+    if (reinterpret_cast<uintptr_t>(ptr[k]) & 15) return false;
+  for (int64_t x : v) if (x & 1) return false;
+  return true;
+}
+
+// input lines -> TMA_BULK (plain rows) or TMA_LINE_TILED (lines tiled by S, element stride s_j).
+// c64 (the m = 128 engine, 4 lines per item): boxes of 128 elements x 4 lines (S >= 4).
 bool tma_desc_in(const LineIn& in, int64_t nlines, int64_t nbatch, int narr, hd::TmaLine& t,
-                 CUtensorMap* maps) {
+                 CUtensorMap* maps, bool c64 = false) {
   t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = in.nbi > 0 ? in.nbi : 1;
   t.bcast = (in.s_b == 0 ? 1 : 0) | (in.s_bo == 0 ? 2 : 0);
   if (in.jd > 0 || narr > hd::kTmaArrays) return false;
   if (in.tl >= 30) {
     if (in.s_j != 1) return false;
+    if (c64 && !bulk_ok_f32(in.ptr, narr, {in.L, in.s_l, in.s_b, in.s_bo})) return false;
     t.kind = hd::TMA_BULK;
     return true;
   }
-  if (in.s_l != 1) return false;
+  if (in.s_l != 1 || (c64 && in.tl < 2)) return false;
   const int64_t S = int64_t(1) << in.tl;
   const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)in.L, (uint64_t)ceil_div64(nlines, S), (uint64_t)t.nbi,
                             (uint64_t)ceil_div64(nbatch, t.nbi)};
   const int64_t str[4] = {in.s_j, in.s_t, in.s_b, in.s_bo};
-  const uint32_t box[5] = {2, 256, 1, 1, 1};
+  const uint32_t box[5] = {c64 ? 8u : 2u, c64 ? 128u : 256u, 1, 1, 1};
   for (int k = 0; k < narr; ++k)
-    if (!encode_lines(&maps[k], in.ptr[k], dims, str, box)) return false;
+    if (!encode_lines(&maps[k], in.ptr[k], dims, str, box, c64)) return false;
   t.kind = hd::TMA_LINE_TILED; t.slog = in.tl;
   return true;
 }
@@ -401,13 +416,15 @@ bool tma_desc_in(const LineIn& in, int64_t nlines, int64_t nbatch, int narr, hd:
 // output lines -> TMA_BULK (plain rows), TMA_ELEM_TILED (element axis tiled by S <= 16)
 // or TMA_LINE_TILED (lines tiled by S, element stride s_js)
 bool tma_desc_out(const LineOut& o, int64_t nlines, int64_t nbatch, int narr, hd::TmaLine& t,
-                  CUtensorMap* maps) {
+                  CUtensorMap* maps, bool c64 = false) {
   t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = o.nbi > 0 ? o.nbi : 1;
   t.bcast = (o.s_b == 0 ? 1 : 0) | (o.s_bo == 0 ? 2 : 0);
   if (o.jd > 0 || narr > hd::kTmaArrays) return false;
   const int64_t nbo = ceil_div64(nbatch, t.nbi);
   if (o.tl >= 30 && o.so_log2 >= 30) {
     if (o.s_js != 1) return false;
+    if (c64 && !bulk_ok_f32(const_cast<const void* const*>(o.ptr), narr, {o.L, o.s_l, o.s_b, o.s_bo}))
+      return false;
     t.kind = hd::TMA_BULK;
     return true;
   }
@@ -417,40 +434,42 @@ bool tma_desc_out(const LineOut& o, int64_t nlines, int64_t nbatch, int narr, hd
     const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)nlines, (uint64_t)ceil_div64(o.L, S), (uint64_t)t.nbi,
                               (uint64_t)nbo};
     const int64_t str[4] = {o.s_l, o.s_jt, o.s_b, o.s_bo};
-    const uint32_t box[5] = {(uint32_t)(2 * S), 1, (uint32_t)(256 / S), 1, 1};
+    const uint32_t box[5] = {(uint32_t)(2 * S), c64 ? 4u : 1u, (uint32_t)((c64 ? 128 : 256) / S), 1, 1};
     for (int k = 0; k < narr; ++k)
-      if (!encode_lines(&maps[k], o.ptr[k], dims, str, box)) return false;
+      if (!encode_lines(&maps[k], o.ptr[k], dims, str, box, c64)) return false;
     t.kind = hd::TMA_ELEM_TILED; t.slog = o.so_log2;
     return true;
   }
-  if (o.so_log2 < 30 || o.s_l != 1) return false;
+  if (o.so_log2 < 30 || o.s_l != 1 || (c64 && o.tl < 2)) return false;
   const int64_t S = int64_t(1) << o.tl;
   const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)o.L, (uint64_t)ceil_div64(nlines, S), (uint64_t)t.nbi,
                             (uint64_t)nbo};
   const int64_t str[4] = {o.s_js, o.s_t, o.s_b, o.s_bo};
-  const uint32_t box[5] = {2, 256, 1, 1, 1};
+  const uint32_t box[5] = {c64 ? 8u : 2u, c64 ? 128u : 256u, 1, 1, 1};
   for (int k = 0; k < narr; ++k)
-    if (!encode_lines(&maps[k], o.ptr[k], dims, str, box)) return false;
+    if (!encode_lines(&maps[k], o.ptr[k], dims, str, box, c64)) return false;
   t.kind = hd::TMA_LINE_TILED; t.slog = o.tl;
   return true;
 }
 
 // Fill the staged engine's TMA descriptions of a launch (falls back to per-thread
 // copies for anything a tensor map cannot express).
-void prepare_tma(Launch& L) {
+void prepare_tma(Launch& L, bool c64 = false) {
   PassArgs& a = L.a;
   const int narr_in = L.mode == hd::MODE_FWD ? (int)L.narrays : (L.mode == hd::MODE_CONV ? a.npairs : 1);
   const int narr_out = L.mode == hd::MODE_FWD ? (int)L.narrays : 1;
-  if (!tma_desc_in(a.in_f, a.nlines, a.nbatch, narr_in, a.tm_in, a.tm_in_map)) a.tm_in.kind = hd::TMA_NONE;
+  if (!tma_desc_in(a.in_f, a.nlines, a.nbatch, narr_in, a.tm_in, a.tm_in_map, c64)) a.tm_in.kind = hd::TMA_NONE;
   if (L.mode == hd::MODE_CONV) {
     // both inputs of the convolution pass move by TMA or both by per-thread copies
-    if (!tma_desc_in(a.in_g, a.nlines, a.nbatch, a.npairs, a.tm_in_g, a.tm_in_g_map) || a.tm_in.kind == hd::TMA_NONE) {
+    if (!tma_desc_in(a.in_g, a.nlines, a.nbatch, a.npairs, a.tm_in_g, a.tm_in_g_map, c64) ||
+        a.tm_in.kind == hd::TMA_NONE) {
       a.tm_in.kind = hd::TMA_NONE; a.tm_in_g.kind = hd::TMA_NONE;
     }
   }
-  if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map)) a.tm_out.kind = hd::TMA_NONE;
+  if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map, c64)) a.tm_out.kind = hd::TMA_NONE;
   // a window start that is not tile-aligned cannot be expressed by element-tiled boxes
-  if (a.out.j0 != 0 && a.tm_out.kind == hd::TMA_ELEM_TILED) a.tm_out.kind = hd::TMA_NONE;
+  // (the m = 128 engine stores every window by plain stores)
+  if (a.out.j0 != 0 && (c64 || a.tm_out.kind == hd::TMA_ELEM_TILED)) a.tm_out.kind = hd::TMA_NONE;
   // loads by TMA need the producer warp; without them the stores go per thread too
   if (a.tm_in.kind == hd::TMA_NONE) { a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE; }
 }
@@ -476,18 +495,36 @@ bool use_s512_mconv(hd_dtype_t dt, const Launch& L) {
   return L.a.npairs <= hd::kTmaArrays && L.a.in_f.p <= 8 && L.a.in_g.p <= 8;
 }
 
+// The staged m = 128 complex-float engine (hd_s128.cuh): four lines per CTA item
+// (C = 4), all residues at once (D = q <= 8), p <= 8, one pair in the convolution pass.
+bool use_s128(hd_dtype_t dt, const Launch& L) {
+  if (dt != HD_C64 || L.m != 128 || L.lines != 4 || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
+  if (!L.auto_engine || !L.s128_axis) return false;
+  if (L.a.D != L.a.q || L.a.q > hd::kS128QMax || L.a.in_f.p > 8) return false;
+  if (L.mode == hd::MODE_CONV) return L.a.npairs == 1 && L.a.in_g.p <= 8;
+  return true;
+}
+
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
-  hd::LaunchFn fn;
-  size_t smem;
+  hd::LaunchFn fn = nullptr;
+  size_t smem = 0;
   int threads = L.threads;
   bool staged = use_s512(dt, L);
   bool mconv = false;
-  if (!staged && use_s512_mconv(dt, L)) {
+  const bool s128 = use_s128(dt, L);
+  if (s128) {
+    prepare_tma(L, true);
+    fn = hd::lookup_s128(L.mode, L.a.q);
+    threads = 32 * (L.a.q + 1);
+    smem = hd::s128_smem_bytes(L.a.q, L.mode, L.a.M1, L.a.tm_in.kind, L.a.tm_out.kind);
+  } else if (!staged && use_s512_mconv(dt, L)) {
     prepare_tma(L);
     mconv = L.a.tm_in.kind == hd::TMA_LINE_TILED || L.a.tm_in.kind == hd::TMA_BULK;
   }
-  if (mconv) {
+  if (s128) {
+    // set above
+  } else if (mconv) {
     fn = hd::lookup_s512_mconv();
     threads = 32 * (L.a.q + 1);
     smem = hd::s512_smem_bytes(L.a.q, hd::MODE_MCONV);
@@ -542,6 +579,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     fprintf(stderr, "\n");
   }
   ctx->launches += 1;
+  ctx->engine_launches[s128 ? HD_ENGINE_S128 : mconv ? HD_ENGINE_S512_MCONV : staged ? HD_ENGINE_S512
+                                                                              : HD_ENGINE_GENERIC] += 1;
   if (ctx->profiling) {
     cudaEventRecord(e1, st);
     hd_ctx::ProfEntry* pe = nullptr;
@@ -566,6 +605,7 @@ struct Problem {
   void* h = nullptr;
   AxisInfo ax[HD_MAX_DIM] = {};
   bool s512[HD_MAX_DIM] = {};  // every pass along axis i may run on the staged m = 512 engine
+  bool s128[HD_MAX_DIM] = {};  // ... on the staged m = 128 complex-float engine
   hd_plan_t plan{};
 };
 
@@ -579,6 +619,10 @@ void choose_engines(Problem& P) {
               x.q <= hd::kS512QMax && !(P.plan.flags & HD_FLAG_GENERIC_FFT);
     if (i > 0) ok = ok && x.pf <= 8 && x.pg <= 8;
     P.s512[i] = ok;
+    bool ok128 = P.dt == HD_C64 && x.m == 128 && x.lines == 4 && x.auto_engine && x.D == x.q &&
+                 x.q <= hd::kS128QMax && x.pf <= 8 && !(P.plan.flags & HD_FLAG_GENERIC_FFT);
+    if (i > 0) ok128 = ok128 && x.pg <= 8;
+    P.s128[i] = ok128;
   }
 }
 
@@ -637,6 +681,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   L.threads = x.threads;
   L.auto_engine = x.auto_engine;
   L.s512_axis = P.s512[axis];
+  L.s128_axis = P.s128[axis];
   L.nbuf = (mode == hd::MODE_CONV) ? conv_nbuf(P.N) : 1;
   init_in(L.a.in_f);
   init_in(L.a.in_g);
@@ -1428,6 +1473,11 @@ hd_status_t hd_profile_reset(hd_ctx_t ctx) {
 
 int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
+int64_t hd_engine_launches(hd_ctx_t ctx, int32_t engine) {
+  if (!ctx || engine < 0 || engine > HD_ENGINE_S128) return -1;
+  return ctx->engine_launches[engine];
+}
+
 static bool conv_lines_in(const hd_lines_t& d, LineIn& in, int64_t nbatch, int n, bool need_ptr) {
   for (int k = 0; k < n; ++k) {
     if (need_ptr && !d.ptr[k]) return false;
@@ -1494,6 +1544,7 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   L.mode = d->mode;
   L.name = d->mode == HD_PASS_FWD ? "pass_fwd" : (d->mode == HD_PASS_INV ? "pass_inv" : "pass_conv");
   L.s512_axis = d->mode == HD_PASS_CONV;  // fwd/inv keep the documented spectral order
+  L.s128_axis = d->mode == HD_PASS_CONV;
   L.m = ap.m;
   L.lines = C;
   L.threads = ap.threads ? ap.threads : default_threads(C, D, ap.m);

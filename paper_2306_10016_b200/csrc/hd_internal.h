@@ -17,6 +17,11 @@ int s512_threads(int q, int mode);
 // staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()
 LaunchFn lookup_s512_mconv();
 int s512_mconv_qmax();
+// staged engine for m = 128 complex float, 4 lines per item (hd_s128.cuh);
+// blockDim = 32 (q + 1), q <= kS128QMax
+LaunchFn lookup_s128(int mode, int q);
+constexpr int kS128QMax = 8;
+size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind);
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],

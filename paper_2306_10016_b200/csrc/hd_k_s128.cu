@@ -1,0 +1,56 @@
+// hd_k_s128.cu -- launchers of the staged m = 128 complex-float engine (hd_s128.cuh):
+// persistent CTAs (as many per SM as shared memory allows), blockDim = 32 (q + 1).
+#include "hd_internal.h"
+#include "hd_s128.cuh"
+
+namespace hd {
+
+template <int MODE, int NT, int QC>
+static cudaError_t launch_s128_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
+  auto kern = s128::s128_kernel<MODE, NT, QC>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (nt < 64 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const int64_t cap = (int64_t)sms * occ;
+  if ((int64_t)grid.x > cap) grid.x = (unsigned)cap;
+  kern<<<grid, nt, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// q = 5 (BASELINE config 4: M1 = 640 on every axis) has a compile-time-q kernel;
+// blockDim bound 192 (q <= 5: two CTAs per SM at <= 168 registers) or 288 (q <= 8)
+template <int MODE>
+static LaunchFn pick_s128(int q) {
+  if (q == 5) return launch_s128_impl<MODE, 192, 5>;
+  if (q < 5) return launch_s128_impl<MODE, 192, 0>;
+  return launch_s128_impl<MODE, 32 * (s128::kQMax + 1), 0>;
+}
+LaunchFn lookup_s128(int mode, int q) {
+  if (q < 1 || q > s128::kQMax) return nullptr;
+  switch (mode) {
+    case MODE_FWD: return pick_s128<MODE_FWD>(q);
+    case MODE_INV: return pick_s128<MODE_INV>(q);
+    case MODE_CONV: return pick_s128<MODE_CONV>(q);
+    default: return nullptr;
+  }
+}
+
+size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind) {
+  return s128::smem_bytes(q, mode, (int)M1, s128::inplace_of(in_kind, out_kind));
+}
+
+}  // namespace hd

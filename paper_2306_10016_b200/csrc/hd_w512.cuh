@@ -23,9 +23,11 @@ using V = double2;
 // LOWHALF: the input's upper half v[8..15] is zero (a short input padded to 512,
 // e.g. the kernel g with L_g <= 256); the first radix-4 layer then reduces to
 // 2-point sums (32 fewer FP64 operations).
-template <int S, bool LOWHALF = false> __device__ __forceinline__ void dft16(V* v) {
-  const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
-  const double h = 0.70710678118654752440;
+template <int S, bool LOWHALF = false, typename VT = V> __device__ __forceinline__ void dft16(VT* v) {
+  using R = decltype(VT::x);
+  using V = VT;  // complex double (FFT-512) or complex float (hd_s128.cuh)
+  const R c1 = (R)0.92387953251128675613, s1 = (R)0.38268343236508977173;
+  const R h = (R)0.70710678118654752440;
   V A[4][4];
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) {
@@ -44,7 +46,7 @@ template <int S, bool LOWHALF = false> __device__ __forceinline__ void dft16(V* 
     }
   }
   // twiddles zeta_16^{S n2 k1}
-  auto rot = [&](V a, double c, double s) {  // a * (c + i S s)
+  auto rot = [&](V a, R c, R s) {  // a * (c + i S s)
     return cmk<V>(fma(a.x, c, -S * a.y * s), fma(a.y, c, S * a.x * s));
   };
   A[1][1] = rot(A[1][1], c1, s1);                                   // 1

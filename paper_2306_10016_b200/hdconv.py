@@ -24,6 +24,7 @@ HD_OK, HD_ERR_INVALID, HD_ERR_UNSUPPORTED, HD_ERR_CUDA, HD_ERR_NCCL, HD_ERR_WORK
 HD_FLAG_ALLOW_ALIAS = 0x1
 HD_FLAG_SHARED_G = 0x2
 HD_FLAG_GENERIC_FFT = 0x4
+HD_ENGINE_GENERIC, HD_ENGINE_S512, HD_ENGINE_S512_MCONV, HD_ENGINE_S128 = 0, 1, 2, 3
 HD_TUNE_PER_AXIS = 0x0
 HD_TUNE_EXHAUSTIVE = 0x1
 HD_MAX_DIM = 3
@@ -39,7 +40,7 @@ EXPORTED = [
     "hd_conv_real",
     "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_ex", "hd_tune_log",
-    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_pass",
+    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_pass",
 ]
 HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
 
@@ -151,6 +152,7 @@ def _load():
         "hd_profile_read": ([P, I32, P, P, P], I32),
         "hd_profile_reset": ([P], ctypes.c_int),
         "hd_launch_count": ([P], I64),
+        "hd_engine_launches": ([P, I32], I64),
         "hd_pass": ([P, ctypes.c_int, ctypes.POINTER(PassDesc), P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -581,6 +583,10 @@ class Context:
 
     def launch_count(self):
         return int(_lib.hd_launch_count(self.h))
+
+    def engine_launches(self, engine):
+        """Pass launches on one engine (HD_ENGINE_*) since the context was created."""
+        return int(_lib.hd_engine_launches(self.h, engine))
 
     def hd_pass(self, dtype, desc, stream=None):
         """One pass with explicit layouts (include/hdconv.h hd_pass)."""

@@ -515,3 +515,51 @@ def test_slab3d_emulated_ranks(ctx, H, world, dtype, m):
     h = np.concatenate([host(p) for p in parts], axis=0)
     tol = 1e-11 if dtype == np.complex128 else 1e-5
     assert oracle.rel_l2(h, oracle.conv(f, g)) < tol
+
+
+# ---------------------------------------------------------------- staged engine (m = 128, complex64)
+# hd_s128.cuh runs every pass of a complex64 axis with m = 128, C = 4 lines per item
+# and D = q <= 8 (automatic engine choice); HD_ENGINE_S128 counts its launches.
+S128_AXES = [{"m": 128, "C": 4, "S": 4}] * 3
+
+
+@pytest.mark.parametrize("sf,sg,S", [
+    ((9, 130, 260), (4, 10, 9), 4),      # q = 1, 2, 3; plain rows by bulk copies, p_f = 3 along x
+    ((40, 33, 129), (100, 7, 129), 4),   # odd rows (per-thread loads), 33 lines (ragged group)
+    ((3, 5, 900), (2, 3, 120), 4),       # x: q = 8, p_f = 8 (largest staged q / p)
+    ((30, 64, 200), (9, 64, 57), 8),     # tiles of 8 lines: a 4-line group is half a tile
+    ((30, 64, 200), (9, 64, 57), 2),     # tiles of 2 lines: no tensor boxes (per-thread copies)
+    ((300, 4, 4), (250, 2, 3), 4),       # q = 5 (compile-time-q kernel) along z, p_f = 3, p_g = 2
+    ((4, 300, 6), (2, 250, 3), 4),       # ... along y
+    ((4, 6, 512), (2, 3, 129), 4),       # ... along x: the config-4 row lengths (p_f = 4, p_g = 2)
+])
+def test_s128_engine_3d(ctx, H, sf, sg, S):
+    f, g = synth.random_pair(1280 + sf[2] + S, sf, sg, dtype=np.complex64)
+    ref = oracle.conv(f, g)
+    axes = [{"m": 128, "C": 4, "S": S}] * 3
+    n0 = ctx.engine_launches(H.HD_ENGINE_S128)
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(3, axes)))
+    assert ctx.engine_launches(H.HD_ENGINE_S128) - n0 == 7
+    hg = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(3, axes, flags=H.HD_FLAG_GENERIC_FFT)))
+    assert oracle.rel_l2(h, ref) < 1e-5
+    assert oracle.rel_l2(hg, ref) < 1e-5
+
+
+def test_s128_engine_batched_multipair_window(ctx, H):
+    """Batched 3-D, N = 2 pairs (forward passes with two arrays; the convolution pass
+    of several pairs runs on the generic engine), and an output window (plain stores)."""
+    fs, gs = zip(*[synth.random_pair(1300 + k, (12, 40, 150), (5, 9, 20), dtype=np.complex64)
+                   for k in range(2)])
+    h = host(ctx.multiconv([dev(x) for x in fs], [dev(x) for x in gs], plan=H.Plan.make(3, S128_AXES)))
+    assert oracle.rel_l2(h, oracle.multiconv(list(fs), list(gs))) < 1e-5
+    f = np.stack([synth.random_pair(1310 + b, (10, 20, 300), (3, 6, 30), dtype=np.complex64)[0] for b in range(3)])
+    g = np.stack([synth.random_pair(1320 + b, (10, 20, 300), (3, 6, 30), dtype=np.complex64)[1] for b in range(3)])
+    n0 = ctx.engine_launches(H.HD_ENGINE_S128)
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(3, S128_AXES), batch=True))
+    assert ctx.engine_launches(H.HD_ENGINE_S128) - n0 == 7
+    for b in range(3):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-5
+    lo, n = [1, 3, 17], [10, 20, 250]
+    h = host(ctx.conv_window([dev(f[0])], [dev(g[0])], lo, n, plan=H.Plan.make(3, S128_AXES)))
+    ref = oracle.conv(f[0], g[0])[1:11, 3:23, 17:267]
+    assert oracle.rel_l2(h, ref) < 1e-5
