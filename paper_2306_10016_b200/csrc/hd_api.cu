@@ -470,6 +470,8 @@ void prepare_tma(Launch& L, bool c64 = false) {
   // a window start that is not tile-aligned cannot be expressed by element-tiled boxes
   // (the m = 128 engine stores every window by plain stores)
   if (a.out.j0 != 0 && (c64 || a.tm_out.kind == hd::TMA_ELEM_TILED)) a.tm_out.kind = hd::TMA_NONE;
+  static const bool st_lt = getenv("HD_EXP_ST_LINE_TILED") != nullptr;  // experiment
+  if (c64 && st_lt && a.tm_out.kind == hd::TMA_LINE_TILED) a.tm_out.kind = hd::TMA_NONE;
   // loads by TMA need the producer warp; without them the stores go per thread too
   if (a.tm_in.kind == hd::TMA_NONE) { a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE; }
 }
@@ -563,6 +565,12 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     cudaMemsetAsync(d_phase, 0, 40 * sizeof(unsigned long long), st);
     L.a.phase_prof = d_phase;
   }
+  // debug: HD_DEBUG_LAUNCH=1 prints each pass's engine, TMA kinds and shape
+  static const bool dbg_launch = getenv("HD_DEBUG_LAUNCH") != nullptr;
+  if (dbg_launch)
+    fprintf(stderr, "[launch] %-8s engine=%s m=%d C=%d q=%d D=%d items=%lld threads=%d smem=%zu tma in=%d g=%d out=%d\n",
+            L.name, s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m, L.lines, L.a.q, L.a.D,
+            (long long)total, threads, smem, L.a.tm_in.kind, L.a.tm_in_g.kind, L.a.tm_out.kind);
   cudaError_t e = fn(L.a, grid, threads, smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, L.name);
   if (L.a.phase_prof) {

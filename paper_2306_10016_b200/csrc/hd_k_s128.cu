@@ -50,7 +50,7 @@ LaunchFn lookup_s128(int mode, int q) {
 }
 
 size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind) {
-  return s128::smem_bytes(q, mode, (int)M1, s128::inplace_of(in_kind, out_kind));
+  return s128::smem_bytes(q, mode, (int)M1, s128::inplace_of(mode, in_kind, out_kind));
 }
 
 }  // namespace hd

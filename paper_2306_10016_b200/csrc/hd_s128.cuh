@@ -121,6 +121,13 @@ __device__ __forceinline__ void store_st(const PassArgs& a, int kk, int64_t b, i
   const int L = (int)o.L, j0 = (int)o.j0;
   V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b);
   const int sl = out_sl(o);
+  if (o.tl < 30 && o.s_l == 1) {  // lines interleaved in memory: line index fastest (coalesced)
+    for (int i = tid; i < C * L; i += nth) {
+      const int c = i & 3, j = i >> 2;
+      if (c < nlive) y[line_off(o, 4 * g + c) + jt_off(j, sl, o.s_jt, o.s_js)] = ob[lo.at(c, j + j0)];
+    }
+    return;
+  }
   for (int i = tid; i < nlive * L; i += nth) {
     const int c = i / L, j = i - c * L;
     y[line_off(o, 4 * g + c) + jt_off(j, sl, o.s_jt, o.s_js)] = ob[lo.at(c, j + j0)];
@@ -357,8 +364,11 @@ __host__ __device__ inline size_t smem_bytes(int q, int mode, int M1, bool inpla
   return 128 + sizeof(float2) * (size_t)(M + m1_slots(M1) +
                                          2 * (in_floats2(q, mode) + (inplace ? 0 : out_floats2(q))));
 }
-// in place when the output family's stage layout equals the input's
-__host__ __device__ inline bool inplace_of(int in_kind, int out_kind) {
+// The convolution pass (2q input rows) works in place when the output family's stage
+// layout equals the input's; the forward / inverse passes always use a separate
+// output region, so the next item's loads need not wait for the stores to drain.
+__host__ __device__ inline bool inplace_of(int mode, int in_kind, int out_kind) {
+  if (mode != MODE_CONV) return false;
   const bool il_in = in_kind == TMA_LINE_TILED;
   if (out_kind == TMA_ELEM_TILED) return false;
   return il_in == (out_kind == TMA_LINE_TILED);
@@ -385,7 +395,7 @@ __global__ void __launch_bounds__(NT, 2) s128_kernel(const __grid_constant__ Pas
   const bool tma = a.tm_in.kind != TMA_NONE;
   const bool tma_st = tma && a.tm_out.kind != TMA_NONE;
   const bool il = a.tm_in.kind == TMA_LINE_TILED;
-  const bool inplace = inplace_of(a.tm_in.kind, a.tm_out.kind);
+  const bool inplace = inplace_of(MODE, a.tm_in.kind, a.tm_out.kind);
   const int IN = in_floats2(q, MODE);
   const int SB = IN + (inplace ? 0 : out_floats2(q));
   const Lay li = il ? lay_interleaved() : lay_rows(IN / C);
