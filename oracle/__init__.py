@@ -145,6 +145,46 @@ def residue_block(x, m: int, q: int, r: int) -> np.ndarray:
     return dft(x, q * m, +1)[r::q]
 
 
+def lambda_conv(f, g, m: int, Lam: int, M: int | None = None) -> np.ndarray:
+    """Linear convolution of a short f and a long g by the Lambda > 1 residue
+    matching of PAPER.md:680-702 (Final Algorithm For One Dimension), written out
+    step by step in the paper's notation with naive DFTs (slow; small sizes only):
+
+      p_f = ceil(L_f / m), p_g = ceil(L_g / (Lam m)), q_g = ceil(M / (Lam m)),
+      q_f = Lam q_g  (PAPER.md:684-687); M1 = q_g Lam m = q_f m;
+      F_{r_f}[l_f] = F_{q_f l_f + r_f} (size-m residues of f),
+      G_{r_g}[l_g] = G_{q_g l_g + r_g} (size-Lam m residues of g);
+      for l_g < Lam m: l_f = floor(l_g / Lam), lambda = l_g mod Lam,
+      r_f = q_g lambda + r_g, so q_g l_g + r_g = q_f l_f + r_f (PAPER.md:692-699);
+      H_{r_g}[l_g] = F_{r_f}[l_f] G_{r_g}[l_g] (the product of matching
+      residues), h_k = (1/M1) sum_{r_g, l_g} zeta_{M1}^{-k (q_g l_g + r_g)} H_{r_g}[l_g]
+      (Backward Eq. PAPER.md:531 with q_g, Lam m), k < L_f + L_g - 1.
+
+    Requires L_f <= L_g (the larger array is called g)."""
+    f = _c128(f).ravel()
+    g = _c128(g).ravel()
+    Lf, Lg = f.size, g.size
+    if Lf > Lg:
+        raise ValueError("lambda_conv needs L_f <= L_g (PAPER.md:682)")
+    Lout = Lf + Lg - 1
+    M = Lout if M is None else int(M)
+    qg = -(-M // (Lam * m))
+    qf = Lam * qg
+    M1 = qg * Lam * m
+    if -(-Lf // m) > qf or -(-Lg // (Lam * m)) > qg:
+        raise ValueError("inputs longer than M1")
+    F = [residue_block(f, m, qf, rf) for rf in range(qf)]          # F_{r_f}[l_f]
+    G = [residue_block(g, Lam * m, qg, rg) for rg in range(qg)]    # G_{r_g}[l_g]
+    S = np.zeros(M1, dtype=np.complex128)                          # spectrum at q_g l_g + r_g
+    for rg in range(qg):
+        for lg in range(Lam * m):
+            lf, lam = lg // Lam, lg % Lam
+            rf = qg * lam + rg
+            S[qg * lg + rg] = F[rf][lf] * G[rg][lg]
+    h = dft(S, M1, -1) / M1
+    return h[:Lout]
+
+
 def poly_eval(a, z) -> np.ndarray:
     """P_a(z) = sum_o a[o] prod_i z_i^{o_i} at points z[p, :] (nested Horner)."""
     a = _c128(a)

@@ -304,12 +304,17 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
         if (c < best * 0.999) { best = c; bm = m; bD = D; bl = lines; }
       }
     }
-    // one line per CTA where the staged m = 512 engine applies (hd_s512.cuh)
-    const int lines = (dt == HD_C128 && bm == 512 && bD == (int)cdiv(Mi, bm) && bD <= hd::kS512QMax) ? 1 : bl;
+    // one line per CTA where the staged m = 512 engine applies (hd_s512.cuh); four
+    // lines per item and tiles of four for the staged complex-float m = 128 engine
+    // (hd_s128.cuh) in 2-D / 3-D
+    const int qb = (int)cdiv(Mi, bm);
+    const bool s128 = dt == HD_C64 && ndim > 1 && bm == 128 && bD == qb && qb <= hd::kS128QMax &&
+                      cdiv(Lf[i], bm) <= 8 && cdiv(Lg[i], bm) <= 8;
+    const int lines = (dt == HD_C128 && bm == 512 && bD == qb && bD <= hd::kS512QMax) ? 1 : s128 ? 4 : bl;
     p.axis[i].m = bm;
     p.axis[i].D = bD;
     p.axis[i].C = lines;
-    p.axis[i].S = (ndim == 1) ? 1 : 2;
+    p.axis[i].S = (ndim == 1) ? 1 : s128 ? 4 : 2;
     p.axis[i].threads = 0;  // automatic engine choice
   }
   *out = p;
@@ -470,8 +475,6 @@ void prepare_tma(Launch& L, bool c64 = false) {
   // a window start that is not tile-aligned cannot be expressed by element-tiled boxes
   // (the m = 128 engine stores every window by plain stores)
   if (a.out.j0 != 0 && (c64 || a.tm_out.kind == hd::TMA_ELEM_TILED)) a.tm_out.kind = hd::TMA_NONE;
-  static const bool st_lt = getenv("HD_EXP_ST_LINE_TILED") != nullptr;  // experiment
-  if (c64 && st_lt && a.tm_out.kind == hd::TMA_LINE_TILED) a.tm_out.kind = hd::TMA_NONE;
   // loads by TMA need the producer warp; without them the stores go per thread too
   if (a.tm_in.kind == hd::TMA_NONE) { a.tm_in_g.kind = hd::TMA_NONE; a.tm_out.kind = hd::TMA_NONE; }
 }

@@ -245,3 +245,38 @@ def test_config_inputs_recipe():
     assert g[0] == complex(-1 + 2 * u[0], -1 + 2 * u[1])
     d3 = synth.config_inputs(3, scale=16)
     assert np.all(d3["f"][0].imag == 0)
+
+
+@pytest.mark.parametrize("Lf,Lg,m,Lam,M", [(7, 30, 4, 2, None), (13, 50, 4, 4, None), (5, 21, 2, 8, 40),
+                                           (16, 16, 4, 2, None), (1, 9, 2, 2, None), (30, 100, 8, 2, 160)])
+def test_lambda_conv_matches_numpy(Lf, Lg, m, Lam, M):
+    # f1: the Lambda > 1 residue matching reaches the linear
+    # convolution: compare with numpy's direct convolution (not the oracle's C code)
+    f, g = synth.random_pair(60 + Lf, (Lf,), (Lg,))
+    h = oracle.lambda_conv(f, g, m, Lam, M)
+    assert oracle.rel_l2(h, np.convolve(f, g)) < 1e-12
+
+
+def test_lambda_index_map_is_a_bijection():
+    # q_g l_g + r_g = q_f l_f + r_f with l_f = floor(l_g / Lam),
+    # lambda = l_g mod Lam, r_f = q_g lambda + r_g covers every frequency of M1 once
+    for qg, Lam, m in [(3, 2, 4), (5, 4, 8), (1, 8, 2), (9, 2, 16)]:
+        qf = Lam * qg
+        seen = set()
+        for rg in range(qg):
+            for lg in range(Lam * m):
+                lf, lam = lg // Lam, lg % Lam
+                rf = qg * lam + rg
+                assert 0 <= rf < qf and 0 <= lf < m
+                assert qg * lg + rg == qf * lf + rf
+                seen.add(qf * lf + rf)
+        assert seen == set(range(qg * Lam * m))
+
+
+def test_lambda_conv_integer_exact_and_rejects_swapped():
+    f, g = synth.integer_pair(62, (9,), (40,))
+    re, im = _int_conv(f, g)
+    h = oracle.lambda_conv(f, g, 4, 2)
+    assert np.abs(h.real - re).max() < 1e-9 and np.abs(h.imag - im).max() < 1e-9
+    with pytest.raises(ValueError):
+        oracle.lambda_conv(g, f, 4, 2)
