@@ -299,6 +299,26 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
 /* Number of candidates evaluated by the last hd_tune and their (plan, seconds). */
 int32_t     hd_tune_log(hd_ctx_t ctx, int32_t max, hd_plan_t* plans, double* seconds);
 
+/* ---- row f1: Lambda > 1 residue matching (1-D) ------------------------------- */
+/* Linear convolution of a short input f (L_f) with a long input g (L_g >= L_f) by
+ * the unequal-size construction of PAPER.md:680-702 ("Final Algorithm For One
+ * Dimension"): p_f = ceil(L_f/m), p_g = ceil(L_g/(Lambda m)), q_g = ceil(M/(Lambda m)),
+ * q_f = Lambda q_g.  f is transformed into q_f residues of FFT size
+ * m, g into q_g residues of FFT size Lambda m; residue r_g of g meets residues
+ * r_f = q_g lambda + r_g of f at l_f = floor(l_g / Lambda), lambda = l_g mod Lambda
+ * (q_g l_g + r_g = q_f l_f + r_f); the matched product is inverted
+ * with size Lambda m and accumulated over the q_g residues.
+ *   f : [batch][L_f], g : [batch][L_g], h : [batch][L_f + L_g - 1], device pointers,
+ *       contiguous rows, interleaved complex (HD_C64 / HD_C128), h not aliasing f, g;
+ *   M : padded length (0: L_f + L_g - 1; M < L_f + L_g - 1 is rejected);
+ *   m, Lambda : powers of two, Lambda m <= 4096 (Lambda = 1: the Lambda = 1 method).
+ * Runs as four launches on `stream` (two forward residue passes, the matched product,
+ * one backward pass) with a context-owned workspace of 2 batch q_g Lambda m elements.
+ * Errors: HD_ERR_INVALID for L_f > L_g, bad m / Lambda, M too small, null pointers. */
+hd_status_t hd_conv1d_lambda(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
+                             const void* g, int64_t Lg, void* h, int64_t M, int32_t m, int32_t Lambda,
+                             void* stream);
+
 /* ---- measurement hooks ------------------------------------------------------ */
 /* When enabled, each kernel launch of the compute entry points is bracketed by
  * CUDA events on its stream; hd_profile_read returns (after a stream sync by the

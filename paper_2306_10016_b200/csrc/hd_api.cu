@@ -31,6 +31,7 @@ struct hd_ctx {
   std::mutex mu;
   std::map<int64_t, void*> tw64, tw32;  // N -> device zeta_N^k tables
   std::map<int64_t, void*> st64, st32;  // m -> device stage twiddle tables
+  std::map<int64_t, int32_t*> perm;     // 2n (+1: inverse) -> device spectral permutation
   void* ws = nullptr;
   size_t ws_size = 0;
   void* io = nullptr;                   // device buffers for hd_conv_host
@@ -202,6 +203,12 @@ int default_threads(int lines, int D, int m) {
   return best;
 }
 bool valid_threads(int t) { return t >= 32 && t <= 1024 && t % 32 == 0; }
+// automatic CTA size: passes whose shared memory leaves room for one CTA per SM
+// get 1024 threads (latency hiding by width; config 2: 3.0 -> 2.5 ms at m = 1024)
+int auto_threads(int lines, int D, int m, size_t smem) {
+  if (smem > hd::kMaxSmem / 2 && (int64_t)lines * D * (m / 8) >= 512) return 1024;
+  return default_threads(lines, D, m);
+}
 
 hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const int64_t* Lf,
                           const int64_t* Lg, const int64_t* M, hd_plan_t* plan, AxisInfo* ax) {
@@ -238,7 +245,10 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     x.D = a.D;
     if (a.D == 0) a.D = x.q;
     x.auto_engine = (a.threads == 0);
-    x.threads = a.threads ? a.threads : default_threads(lines_for(a, i, ndim), a.D, a.m);
+    x.threads = a.threads ? a.threads
+                          : auto_threads(lines_for(a, i, ndim), a.D, a.m,
+                                         pass_smem(eb, x.q, lines_for(a, i, ndim), a.D, a.m,
+                                                   (i == 0) ? conv_nbuf(npairs) : 1));
     if (!valid_threads(x.threads))
       return fail(ctx, HD_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 1024]");
     x.lines = lines_for(a, i, ndim);
@@ -1016,6 +1026,7 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   for (auto& kv : ctx->tw64) cudaFree(kv.second);
   for (auto& kv : ctx->tw32) cudaFree(kv.second);
   for (auto& kv : ctx->st64) cudaFree(kv.second);
+  for (auto& kv : ctx->perm) cudaFree(kv.second);
   for (auto& kv : ctx->st32) cudaFree(kv.second);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
@@ -1377,14 +1388,13 @@ hd_status_t hd_host_sync(hd_ctx_t ctx) {
   return HD_OK;
 }
 
-hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* x,
-                                int64_t L, int32_t m, int32_t q, void* X, void* stream) {
-  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
-  if (!x || !X || nlines < 1 || L < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
-  if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < L)
-    return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= L");
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  cudaSetDevice(ctx->device);
+}  // extern "C"
+
+namespace {
+// forward / backward residue passes of nlines plain rows (generic engine, spectral
+// order of hd_spectral_permutation); the caller holds ctx->mu
+hd_status_t forward_residues_locked(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* x, int64_t L,
+                                    int32_t m, int32_t q, void* X, cudaStream_t stream) {
   const bool dbl = dtype == HD_C128;
   const size_t eb = elem_bytes(dtype);
   Problem P;
@@ -1394,7 +1404,7 @@ hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, 
   a.lines = 1;
   a.D = q;
   while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
-  a.threads = default_threads(1, a.D, m);
+  a.threads = auto_threads(1, a.D, m, pass_smem(eb, q, 1, a.D, m, 1));
   a.auto_engine = true;
   const void *twm, *twM1;
   hd_status_t s = get_table(ctx, m, dbl, &twm);
@@ -1409,17 +1419,11 @@ hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, 
   Lh.a.out.ptr[0] = X; out_rows(Lh.a.out, a.M1); Lh.a.out.L = a.M1;
   Lh.a.nlines = nlines; Lh.a.nbatch = 1;
   Lh.ngroups = nlines; Lh.nbatch = 1;
-  return launch(ctx, dtype, Lh, (cudaStream_t)stream);
+  return launch(ctx, dtype, Lh, stream);
 }
 
-hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* X,
-                                 int32_t m, int32_t q, void* x, int64_t Lout, void* stream) {
-  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
-  if (!x || !X || nlines < 1 || Lout < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
-  if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < Lout)
-    return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= Lout");
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  cudaSetDevice(ctx->device);
+hd_status_t backward_residues_locked(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* X, int32_t m,
+                                     int32_t q, void* x, int64_t Lout, cudaStream_t stream) {
   const bool dbl = dtype == HD_C128;
   const size_t eb = elem_bytes(dtype);
   Problem P;
@@ -1429,7 +1433,7 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
   a.lines = 1;
   a.D = q;
   while (a.D > 1 && pass_smem(eb, q, 1, a.D, m, 1) > hd::kMaxSmem) --a.D;
-  a.threads = default_threads(1, a.D, m);
+  a.threads = auto_threads(1, a.D, m, pass_smem(eb, q, 1, a.D, m, 1));
   a.auto_engine = true;
   const void *twm, *twM1;
   hd_status_t s = get_table(ctx, m, dbl, &twm);
@@ -1444,7 +1448,100 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
   Lh.a.out.ptr[0] = x; out_rows(Lh.a.out, Lout); Lh.a.out.L = Lout; Lh.a.out.T = a.T;
   Lh.a.nlines = nlines; Lh.a.nbatch = 1;
   Lh.ngroups = nlines; Lh.nbatch = 1;
-  return launch(ctx, dtype, Lh, (cudaStream_t)stream);
+  return launch(ctx, dtype, Lh, stream);
+}
+
+// device copy of the spectral permutation of size n (pos -> frequency) or its inverse
+hd_status_t get_perm(hd_ctx* ctx, int32_t n, bool inverse, const int32_t** out) {
+  const int64_t key = 2 * (int64_t)n + (inverse ? 1 : 0);
+  auto it = ctx->perm.find(key);
+  if (it != ctx->perm.end()) { *out = it->second; return HD_OK; }
+  std::vector<int32_t> p(n), v(n);
+  hd_status_t s = hd_spectral_permutation(n, p.data());
+  if (s != HD_OK) return s;
+  for (int32_t i = 0; i < n; ++i) v[inverse ? p[i] : i] = inverse ? i : p[i];
+  int32_t* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(int32_t) * n);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(permutation)");
+  e = cudaMemcpy(d, v.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(d); return cuda_fail(ctx, e, "cudaMemcpy(permutation)"); }
+  ctx->perm[key] = d;
+  *out = d;
+  return HD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* x,
+                                int64_t L, int32_t m, int32_t q, void* X, void* stream) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (!x || !X || nlines < 1 || L < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
+  if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < L)
+    return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= L");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  return forward_residues_locked(ctx, dtype, nlines, x, L, m, q, X, (cudaStream_t)stream);
+}
+
+hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, const void* X,
+                                 int32_t m, int32_t q, void* x, int64_t Lout, void* stream) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (!x || !X || nlines < 1 || Lout < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
+  if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < Lout)
+    return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= Lout");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  return backward_residues_locked(ctx, dtype, nlines, X, m, q, x, Lout, (cudaStream_t)stream);
+}
+
+// Row f1: short f with size-m residues (q_f = Lambda q_g), long g
+// with size-(Lambda m) residues (q_g), matched product, size-(Lambda m) inverse.
+hd_status_t hd_conv1d_lambda(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
+                             const void* g, int64_t Lg, void* h, int64_t M, int32_t m, int32_t Lambda,
+                             void* stream) {
+  if (!ctx) return fail(nullptr, HD_ERR_INVALID, "null context");
+  if (dtype != HD_C64 && dtype != HD_C128) return fail(ctx, HD_ERR_INVALID, "dtype must be HD_C64 or HD_C128");
+  if (!f || !g || !h || batch < 1 || Lf < 1 || Lg < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
+  if (Lf > Lg) return fail(ctx, HD_ERR_INVALID, "hd_conv1d_lambda needs L_f <= L_g (PAPER.md:682)");
+  if (!is_pow2(m) || m < 2 || !is_pow2(Lambda) || Lambda < 1 || (int64_t)m * Lambda > 4096)
+    return fail(ctx, HD_ERR_INVALID, "m and Lambda must be powers of two with Lambda*m <= 4096");
+  const int64_t Lout = Lf + Lg - 1;
+  if (M <= 0) M = Lout;
+  if (M < Lout) return fail(ctx, HD_ERR_INVALID, "M < L_f + L_g - 1 would alias (PAPER.md:592)");
+  const int32_t Lm = m * Lambda;
+  const int64_t qg64 = cdiv(M, Lm);
+  if (qg64 * Lambda > (1 << 20)) return fail(ctx, HD_ERR_UNSUPPORTED, "too many residues");
+  const int32_t qg = (int32_t)qg64, qf = Lambda * qg;
+  const int64_t M1 = (int64_t)qg * Lm;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const size_t eb = elem_bytes(dtype);
+  const size_t need = 2 * align256((size_t)batch * M1 * eb);
+  if (ctx->ws_size < need) {
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr; ctx->ws_size = 0;
+    cudaError_t e = cudaMalloc(&ctx->ws, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(workspace)");
+    ctx->ws_size = need;
+  }
+  char* Xf = (char*)ctx->ws;
+  char* Xg = Xf + align256((size_t)batch * M1 * eb);
+  const int32_t *perm_g = nullptr, *iperm_f = nullptr;
+  hd_status_t s = get_perm(ctx, Lm, false, &perm_g);
+  if (s != HD_OK) return s;
+  s = get_perm(ctx, m, true, &iperm_f);
+  if (s != HD_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  s = forward_residues_locked(ctx, dtype, batch, f, Lf, m, qf, Xf, st);
+  if (s != HD_OK) return s;
+  s = forward_residues_locked(ctx, dtype, batch, g, Lg, Lm, qg, Xg, st);
+  if (s != HD_OK) return s;
+  cudaError_t e = hd::launch_lambda_product(dtype == HD_C128, Xf, Xg, perm_g, iperm_f, batch, m, Lambda, qg,
+                                            1.0 / (double)M1, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "lambda_product");
+  ctx->launches += 1;
+  return backward_residues_locked(ctx, dtype, batch, Xg, Lm, qg, h, Lout, st);
 }
 
 hd_status_t hd_profile_enable(hd_ctx_t ctx, int32_t enable) {
@@ -1626,6 +1723,10 @@ std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, in
         const int dt = default_threads(C, D, m);
         std::vector<int> ths = {0, dt};  // 0: automatic engine (warp engine where it applies)
         if (dt != 256) ths.push_back(256);
+        // wide CTAs for passes whose shared memory allows one CTA per SM (latency hiding)
+        const int64_t bflies = (int64_t)C * D * (m / 8);
+        if (bflies >= 512 && pass_smem(eb, q, C, D, m, nbuf) > hd::kMaxSmem / 2)
+          for (int t : {768, 1024}) if (t != dt) ths.push_back(t);
         for (int S : Ss)
           for (int th : ths) out.push_back(AxisCand{m, C, S, D, th});
       }

@@ -133,4 +133,44 @@ cudaError_t launch_real_unpack(bool is_double, const void* w, void* h, int64_t L
   return cudaGetLastError();
 }
 
+// Row f1 matched product: H_{r_g}[l_g] = F_{q_g lambda + r_g}[l_f]
+// G_{r_g}[l_g] * scale, l_f = l_g / Lambda, lambda = l_g mod Lambda; residue rows in
+// the engine's spectral order (perm_g: position -> frequency of size Lambda m;
+// iperm_f: frequency -> position of size m).  H overwrites G.
+template <typename V>
+__global__ void lambda_product_kernel(const V* __restrict__ Xf, V* Xg, const int32_t* __restrict__ perm_g,
+                                      const int32_t* __restrict__ iperm_f, int64_t n, int m, int Lam, int qg,
+                                      decltype(V::x) scale) {
+  const int Lm = m * Lam;
+  const int64_t M1 = (int64_t)qg * Lm;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = i / M1;
+    const int64_t P = i - l * M1;
+    const int rg = (int)(P / Lm), pos = (int)(P - (int64_t)rg * Lm);
+    const int lg = __ldg(perm_g + pos);
+    const int lam = lg % Lam, lf = lg / Lam;
+    const int rf = qg * lam + rg;
+    const V a = Xf[l * M1 + (int64_t)rf * m + __ldg(iperm_f + lf)];
+    const V b = Xg[i];
+    V c;
+    c.x = (a.x * b.x - a.y * b.y) * scale;
+    c.y = (a.x * b.y + a.y * b.x) * scale;
+    Xg[i] = c;
+  }
+}
+
+cudaError_t launch_lambda_product(bool is_double, const void* Xf, void* Xg, const int32_t* perm_g,
+                                  const int32_t* iperm_f, int64_t nlines, int m, int Lam, int qg, double scale,
+                                  cudaStream_t st) {
+  const int64_t n = nlines * (int64_t)qg * m * Lam;
+  const unsigned g = grid_for(n);
+  if (is_double)
+    lambda_product_kernel<double2><<<g, 256, 0, st>>>((const double2*)Xf, (double2*)Xg, perm_g, iperm_f, n, m,
+                                                      Lam, qg, scale);
+  else
+    lambda_product_kernel<float2><<<g, 256, 0, st>>>((const float2*)Xf, (float2*)Xg, perm_g, iperm_f, n, m, Lam,
+                                                     qg, (float)scale);
+  return cudaGetLastError();
+}
+
 }  // namespace hd

@@ -40,7 +40,7 @@ EXPORTED = [
     "hd_conv_real",
     "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_ex", "hd_tune_log",
-    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_pass",
+    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_pass", "hd_conv1d_lambda",
 ]
 HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
 
@@ -153,6 +153,7 @@ def _load():
         "hd_profile_reset": ([P], ctypes.c_int),
         "hd_launch_count": ([P], I64),
         "hd_engine_launches": ([P, I32], I64),
+        "hd_conv1d_lambda": ([P, ctypes.c_int, I64, P, I64, P, I64, P, I64, I32, I32, P], ctypes.c_int),
         "hd_pass": ([P, ctypes.c_int, ctypes.POINTER(PassDesc), P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -523,6 +524,24 @@ class Context:
         self._chk(_lib.hd_backward_residues(self.h, _dtype_code(X), nl, _ptr(X), m, q, _ptr(x),
                                             Lout, _stream_ptr(stream)))
         return x
+
+    def hd_conv1d_lambda(self, f, g, m, Lambda, M=None, h=None, stream=None):
+        """Row f1 (include/hdconv.h): short f [batch, L_f] (* ) long g [batch, L_g] by the
+        Lambda > 1 residue matching; returns h [batch, L_f + L_g - 1]."""
+        if f.dim() == 1:
+            f, g = f.unsqueeze(0), g.unsqueeze(0)
+            squeeze = True
+        else:
+            squeeze = False
+        nb, Lf = f.shape
+        Lg = g.shape[1]
+        if h is None:
+            h = self._out(f, [nb, Lf + Lg - 1])
+        self._chk(_lib.hd_conv1d_lambda(self.h, _dtype_code(f), nb, _ptr(f), Lf, _ptr(g), Lg, _ptr(h),
+                                        0 if M is None else int(M), int(m), int(Lambda), _stream_ptr(stream)))
+        return h[0] if squeeze else h
+
+    conv1d_lambda = hd_conv1d_lambda
 
     def default_plan(self, dtype, Lf, Lg, M=None, npairs=1):
         return hd_plan_default(dtype, Lf, Lg, M, npairs)

@@ -563,3 +563,32 @@ def test_s128_engine_batched_multipair_window(ctx, H):
     h = host(ctx.conv_window([dev(f[0])], [dev(g[0])], lo, n, plan=H.Plan.make(3, S128_AXES)))
     ref = oracle.conv(f[0], g[0])[1:11, 3:23, 17:267]
     assert oracle.rel_l2(h, ref) < 1e-5
+
+
+# ---------------------------------------------------------------- row f1: Lambda > 1 (1-D)
+@pytest.mark.parametrize("Lf,Lg,m,Lam,dtype", [
+    (7, 30, 4, 2, np.complex128), (13, 50, 4, 4, np.complex128), (100, 1000, 32, 4, np.complex128),
+    (255, 4096, 256, 2, np.complex128), (1, 9, 2, 2, np.complex128), (64, 64, 16, 1, np.complex128),
+    (300, 5000, 64, 8, np.complex64), (129, 512, 64, 2, np.complex64)])
+def test_lambda_conv_matches_oracle(ctx, H, Lf, Lg, m, Lam, dtype):
+    f, g = synth.random_pair(1400 + Lf, (3, Lf), (3, Lg), dtype=dtype)
+    h = host(ctx.conv1d_lambda(dev(f), dev(g), m, Lam))
+    for b in range(3):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < TOL[dtype]
+    if Lg <= 200:  # the step-by-step oracle of the construction itself (slow)
+        assert oracle.rel_l2(h[0], oracle.lambda_conv(f[0], g[0], m, Lam)) < TOL[dtype]
+
+
+def test_lambda_conv_config2_shape_and_padding(ctx, H):
+    """The config-2 pair (3000 (*) 8192, batch 8 here) with Lambda = 4, m = 256, and an
+    explicit M above L_out; sampled lines against the direct sum."""
+    f, g = synth.random_pair(1450, (8, 3000), (8, 8192))
+    h = host(ctx.conv1d_lambda(dev(f), dev(g), 256, 4))
+    h2 = host(ctx.conv1d_lambda(dev(f), dev(g), 256, 4, M=12288))
+    for b in (0, 7):
+        ref = oracle.conv(f[b], g[b])
+        assert oracle.rel_l2(h[b], ref) < 1e-11 and oracle.rel_l2(h2[b], ref) < 1e-11
+    with pytest.raises(H.HDError):
+        ctx.conv1d_lambda(dev(g), dev(f), 256, 4)  # L_f > L_g
+    with pytest.raises(H.HDError):
+        ctx.conv1d_lambda(dev(f), dev(g), 256, 4, M=100)

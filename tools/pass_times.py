@@ -40,8 +40,12 @@ for axes in json.loads(a.plans):
         flags = axes.get("flags", 0)
         axes = axes["axes"]
     plan = H.Plan.make(nd, axes, flags=flags)
-    for _ in range(3):
-        step(plan)
+    try:
+        for _ in range(3):
+            step(plan)
+    except H.HDError as e:
+        print(json.dumps({"plan": axes, "error": str(e)}), flush=True)
+        continue
     torch.cuda.synchronize()
     ctx.profile_reset()
     e0 = [ctx.engine_launches(e) for e in range(4)]
