@@ -361,10 +361,22 @@ def run_ours(args, rank, world, local_rank):
             # the convolution pass is FP64-issue bound: its flops
             # against the FP64 pipe, 64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz
             ach = fl / (avg * 1e-3) / 1e12
-            roof["fp64"] = {"achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                            "frac": ach / FP64_PEAK_TFLOPS, "alg_flops_per_launch": fl,
-                            "flops": "nominal 5 m log2 m per residue FFT ((2N+1) q per line) + naive "
-                                     "fold 8 m q (p_f+p_g) N + unfold 8 m q T + product 6 m q N"}
+            fp64 = {"achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP64_PEAK_TFLOPS, "alg_flops_per_launch": fl,
+                    "flops": "nominal 5 m log2 m per residue FFT ((2N+1) q per line) + naive "
+                             "fold 8 m q (p_f+p_g) N + unfold 8 m q T + product 6 m q N"}
+            if fp64["frac"] > roof["frac"]:
+                # the binding roof is the FP64 pipe (plain ALU arithmetic): report it
+                # as the kernel's roofline, with the HBM figures alongside
+                hbm = {k: roof[k] for k in ("achieved", "peak", "unit", "frac", "peak_source",
+                                            "alg_bytes_per_launch")}
+                roof.update({"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                             "unit": "TFLOP/s", "frac": fp64["frac"],
+                             "peak_source": "derived: 64 FP64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz "
+                                            "(DESIGN.md section 6)",
+                             "alg_flops_per_launch": fl, "flops": fp64["flops"], "hbm": hbm})
+            else:
+                roof["fp64"] = fp64
     total_ab = sum(ab.values())
     whole = {"alg_bytes_per_step": total_ab,
              "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,

@@ -18,6 +18,18 @@ __global__ void k_write(float4* buf) {  // buf[ky][g][z][2 x float4]
     }
   }
 }
+// pieces of 32 * W bytes: one item = W consecutive z (the same bytes in total)
+template <int W>
+__global__ void k_write_w(float4* buf) {
+  const int items = NG * NZ / W;
+  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    const int z0 = (w % (NZ / W)) * W, g = w / (NZ / W);
+    for (int i = threadIdx.x; i < KY * 2 * W; i += blockDim.x) {
+      const int ky = i / (2 * W), o = i % (2 * W);
+      buf[(((size_t)ky * NG + g) * NZ + z0) * 2 + o] = make_float4(w, ky, o, 0);
+    }
+  }
+}
 __global__ void k_read(const float4* buf, float* out) {
   const int items = NG * NZ;
   float acc = 0;
@@ -68,6 +80,16 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
     }
     printf("CTAs/SM %d contiguous write: %.3f ms %.2f TB/s\n", bpsm, ms, bytes / ms / 1e9);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a); k_write_w<2><<<grid, 128>>>(buf); cudaEventRecord(b); cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+    }
+    printf("CTAs/SM %d 64-byte pieces write: %.3f ms %.2f TB/s\n", bpsm, ms, bytes / ms / 1e9);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a); k_write_w<4><<<grid, 128>>>(buf); cudaEventRecord(b); cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+    }
+    printf("CTAs/SM %d 128-byte pieces write: %.3f ms %.2f TB/s\n", bpsm, ms, bytes / ms / 1e9);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
