@@ -520,6 +520,23 @@ bool use_s128(hd_dtype_t dt, const Launch& L) {
   return true;
 }
 
+// The batch-grouped forward pass of the m = 128 engine (hd_s128.cuh
+// s128_bg_fwd_kernel): four consecutive batch entries x four lines per item, where
+// the output keeps the line tile (4) innermost and the batch entries adjacent
+// (stride 4 elements), so each output element of an item is 128 contiguous bytes
+// (the 3-D fwd_y pass).  Needs tensor-box input loads (prepare_tma first).
+bool use_s128_bg(const Launch& L) {
+  const PassArgs& a = L.a;
+  const LineOut& o = a.out;
+  if (L.mode != hd::MODE_FWD || a.q != 5 || a.tm_in.kind != hd::TMA_LINE_TILED) return false;
+  if (o.tl != 2 || o.s_l != 1 || o.so_log2 < 30 || o.jd > 0 || o.j0 != 0 || o.s_b != 4) return false;
+  if (o.nbi % 4 || a.nbatch % 4 || !a.batch_fastest || L.narrays > hd::kTmaArrays) return false;
+  if ((o.s_t | o.s_bo | o.s_js) & 1) return false;
+  for (int k = 0; k < (int)L.narrays; ++k)
+    if (reinterpret_cast<uintptr_t>(o.ptr[k]) & 15) return false;
+  return true;
+}
+
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
   hd::LaunchFn fn = nullptr;
@@ -530,9 +547,15 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool s128 = use_s128(dt, L);
   if (s128) {
     prepare_tma(L, true);
-    fn = hd::lookup_s128(L.mode, L.a.q);
-    threads = 32 * (L.a.q + 1);
-    smem = hd::s128_smem_bytes(L.a.q, L.mode, L.a.M1, L.a.tm_in.kind, L.a.tm_out.kind);
+    if (use_s128_bg(L)) {
+      fn = hd::lookup_s128_bg(L.mode, L.a.q);
+      threads = hd::s128_bg_threads(L.a.q);
+      smem = hd::s128_bg_smem_bytes(L.a.q, L.a.M1);
+    } else {
+      fn = hd::lookup_s128(L.mode, L.a.q);
+      threads = 32 * (L.a.q + 1);
+      smem = hd::s128_smem_bytes(L.a.q, L.mode, L.a.M1, L.a.tm_in.kind, L.a.tm_out.kind, L.a.in_g.p);
+    }
   } else if (!staged && use_s512_mconv(dt, L)) {
     prepare_tma(L);
     mconv = L.a.tm_in.kind == hd::TMA_LINE_TILED || L.a.tm_in.kind == hd::TMA_BULK;

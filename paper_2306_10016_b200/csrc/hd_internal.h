@@ -21,7 +21,11 @@ int s512_mconv_qmax();
 // blockDim = 32 (q + 1), q <= kS128QMax
 LaunchFn lookup_s128(int mode, int q);
 constexpr int kS128QMax = 8;
-size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind);
+size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind, int pg);
+// its batch-grouped forward pass (4 batch entries x 4 lines per item), q = 5
+LaunchFn lookup_s128_bg(int mode, int q);
+int s128_bg_threads(int q);
+size_t s128_bg_smem_bytes(int q, int64_t M1);
 cudaError_t launch_pad(bool is_double, const void* src, void* dst, const int64_t L[3],
                        const int64_t P[3], int64_t nb, cudaStream_t st);
 cudaError_t launch_crop(bool is_double, const void* src, void* dst, const int64_t O[3],

@@ -1,13 +1,15 @@
 // hd_k_s128.cu -- launchers of the staged m = 128 complex-float engine (hd_s128.cuh):
 // persistent CTAs (as many per SM as shared memory allows), blockDim = 32 (q + 1).
+#include <cstdlib>
+
 #include "hd_internal.h"
 #include "hd_s128.cuh"
 
 namespace hd {
 
-template <int MODE, int NT, int QC>
+template <int MODE, int NT, int QC, int MINB = 2>
 static cudaError_t launch_s128_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
-  auto kern = s128::s128_kernel<MODE, NT, QC>;
+  auto kern = s128::s128_kernel<MODE, NT, QC, MINB>;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -35,7 +37,7 @@ static cudaError_t launch_s128_impl(const PassArgs& a, dim3 grid, int nt, size_t
 // blockDim bound 192 (q <= 5: two CTAs per SM at <= 168 registers) or 288 (q <= 8)
 template <int MODE>
 static LaunchFn pick_s128(int q) {
-  if (q == 5) return launch_s128_impl<MODE, 192, 5>;
+  if (q == 5) return launch_s128_impl<MODE, 192, 5, 2>;
   if (q < 5) return launch_s128_impl<MODE, 192, 0>;
   return launch_s128_impl<MODE, 32 * (s128::kQMax + 1), 0>;
 }
@@ -49,8 +51,41 @@ LaunchFn lookup_s128(int mode, int q) {
   }
 }
 
-size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind) {
-  return s128::smem_bytes(q, mode, (int)M1, s128::inplace_of(mode, in_kind, out_kind));
+static cudaError_t launch_s128_bg_fwd(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
+  constexpr int NT = 32 * (s128::kBG * 5 + 1);
+  auto kern = s128::s128_bg_fwd_kernel<5>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (nt != NT) return cudaErrorInvalidConfiguration;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const int64_t cap = (int64_t)sms * occ;
+  if ((int64_t)grid.x > cap) grid.x = (unsigned)cap;
+  kern<<<grid, nt, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// batch-grouped forward pass (four batch entries x four lines per item): q = 5 only
+LaunchFn lookup_s128_bg(int mode, int q) {
+  return (mode == MODE_FWD && q == 5) ? launch_s128_bg_fwd : nullptr;
+}
+int s128_bg_threads(int q) { return 32 * (s128::kBG * q + 1); }
+size_t s128_bg_smem_bytes(int q, int64_t M1) { return s128::bg_smem_bytes(q, (int)M1); }
+
+size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind, int pg) {
+  return s128::smem_bytes(q, mode, (int)M1, s128::inplace_of(mode, in_kind, out_kind), pg);
 }
 
 }  // namespace hd

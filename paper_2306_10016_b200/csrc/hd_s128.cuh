@@ -355,15 +355,20 @@ __device__ __forceinline__ void load_spec(V* a, const V* buf, const Lay& ly, int
 
 // shared memory: barriers (128 B) | zeta_128 table | zeta_{M1} table | 2 stages
 // stage = input rows (R_in = q, CONV: 2q) [+ output region of q rows unless in place]
-__host__ __device__ inline int in_floats2(int q, int mode) {
+// (measured: folding g on the fly per residue warp from its p_g raw rows saves
+// shared memory but not time -- 2.30 vs 2.27 ms on config 4's conv_z, 2.58 ms
+// when the saving is spent on a third CTA per SM at 96 registers)
+__host__ __device__ inline int in_floats2(int q, int mode, int pg = 0) {
+  (void)pg;
   return C * ((mode == MODE_CONV ? 2 * q : q) * M + kPad);
 }
 __host__ __device__ inline int out_floats2(int q) { return C * (q * M + kPad); }
 __host__ __device__ inline int m1_slots(int M1) { return (M1 + 15) / 16 * 16; }
-__host__ __device__ inline size_t smem_bytes(int q, int mode, int M1, bool inplace) {
+__host__ __device__ inline size_t smem_bytes(int q, int mode, int M1, bool inplace, int pg) {
   return 128 + sizeof(float2) * (size_t)(M + m1_slots(M1) +
-                                         2 * (in_floats2(q, mode) + (inplace ? 0 : out_floats2(q))));
+                                         2 * (in_floats2(q, mode, pg) + (inplace ? 0 : out_floats2(q))));
 }
+
 // The convolution pass (2q input rows) works in place when the output family's stage
 // layout equals the input's; the forward / inverse passes always use a separate
 // output region, so the next item's loads need not wait for the stores to drain.
@@ -374,8 +379,8 @@ __host__ __device__ inline bool inplace_of(int mode, int in_kind, int out_kind) 
   return il_in == (out_kind == TMA_LINE_TILED);
 }
 
-template <int MODE, int NT, int QC>
-__global__ void __launch_bounds__(NT, 2) s128_kernel(const __grid_constant__ PassArgs a) {
+template <int MODE, int NT, int QC, int MINB = 2>
+__global__ void __launch_bounds__(NT, MINB) s128_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* done = full + 2;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(NT, 2) s128_kernel(const __grid_constant__ Pas
   const bool tma_st = tma && a.tm_out.kind != TMA_NONE;
   const bool il = a.tm_in.kind == TMA_LINE_TILED;
   const bool inplace = inplace_of(MODE, a.tm_in.kind, a.tm_out.kind);
-  const int IN = in_floats2(q, MODE);
+  const int IN = in_floats2(q, MODE, MODE == MODE_CONV ? a.in_g.p : 0);
   const int SB = IN + (inplace ? 0 : out_floats2(q));
   const Lay li = il ? lay_interleaved() : lay_rows(IN / C);
   const Lay lo = inplace ? li
@@ -540,6 +545,122 @@ __global__ void __launch_bounds__(NT, 2) s128_kernel(const __grid_constant__ Pas
       if (tma) { fence_async_smem(); mbar_arrive(&done[st]); }
       else compute_sync(nth);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batch-grouped forward pass (BG = 4): one work item = four consecutive batch
+// entries b = 4 b4 + k of one group of four tiled lines, i.e. 16 lines, for the
+// y -> z transpose of the 3-D pipeline (fwd_y: batch = z with stride 4 elements =
+// the line tile), where four batch entries x four lines of one output element are
+// 128 contiguous bytes.  Loads: TMA tensor boxes per sub-item (as s128_kernel);
+// transform in place per sub-item (warp (k, r): residue r of sub-item k); stores:
+// plain 16-byte stores from every thread, eight threads per 128-byte piece
+// (tools/micro/scatter32.cu: 128-byte pieces at 5.0 TB/s vs 1.1 TB/s for the 32-byte
+// pieces of one 4-line item).  Host conditions: hd_api.cu use_s128_bg.
+// ---------------------------------------------------------------------------
+constexpr int kBG = 4;
+__host__ __device__ inline size_t bg_smem_bytes(int q, int M1) {
+  return 128 + sizeof(float2) * (size_t)(M + m1_slots(M1) + 2 * kBG * in_floats2(q, MODE_FWD));
+}
+
+template <int QC>
+__global__ void __launch_bounds__(32 * (kBG * QC + 1), 1) s128_bg_fwd_kernel(const __grid_constant__ PassArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* done = full + 2;
+  V* t128 = reinterpret_cast<V*>(smem_raw + 128);
+  V* tM1 = t128 + M;
+  constexpr int q = QC;
+  const int M1 = (int)a.M1;
+  V* stage0 = tM1 + m1_slots(M1);
+  const int tid = threadIdx.x;
+  constexpr int nth1 = 32 * q, nth = kBG * nth1;
+  const int lane = tid & 31;
+  const int wi = tid >> 5;
+  const int k = wi / q, r = wi - k * q;  // sub-item, residue (compute warps)
+  const int k_arr = blockIdx.z;
+  const int IN = in_floats2(q, MODE_FWD);
+  const int SB = kBG * IN;
+  const Lay li = lay_interleaved();
+  for (int i = tid; i < M; i += blockDim.x) t128[i] = ldg(reinterpret_cast<const V*>(a.tw_m) + i);
+  for (int i = tid; i < M1; i += blockDim.x) tM1[i] = ldg(reinterpret_cast<const V*>(a.tw_M1) + i);
+  if (tid == 0) {
+    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    mbar_init(&done[0], nth); mbar_init(&done[1], nth);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nb4 = a.nbatch / kBG;
+  const int64_t total = nb4 * a.ngroups;
+
+  if (tid >= nth) {  // producer
+    if (tid != nth) return;
+    auto load_item = [&](int64_t w, int s2) {
+      int64_t g, b4;
+      split_item(w, nb4, a.ngroups, 1, b4, g);
+      const int nlive = (int)(a.nlines - 4 * g < C ? a.nlines - 4 * g : C);
+      V* buf = stage0 + s2 * SB;
+      mbar_expect_tx(&full[s2], kBG * item_bytes(a.tm_in, a.in_f, nlive));
+      for (int kk = 0; kk < kBG; ++kk)
+        load_family(a.tm_in, &a.tm_in_map[k_arr], a.in_f, k_arr, 4 * b4 + kk, g, nlive, buf + kk * IN, li, 0,
+                    &full[s2]);
+    };
+    int64_t wl = blockIdx.x;
+    for (int s2 = 0; s2 < 2 && wl < total; ++s2, wl += gridDim.x) load_item(wl, s2);
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      const int st = it & 1;
+      mbar_wait(&done[st], (uint32_t)(it >> 1) & 1u);
+      if (wl < total) { load_item(wl, st); wl += gridDim.x; }
+    }
+    return;
+  }
+
+  const int c = lane >> 3, u = lane & 7;
+  const int tl = tid - k * nth1;
+  const LineOut& o = a.out;
+  const int Lout = (int)o.L;
+  int it = 0;
+  for (int64_t w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+    const int st = it & 1;
+    V* buf = stage0 + st * SB;
+    V* bk = buf + k * IN;
+    int64_t g, b4;
+    split_item(w, nb4, a.ngroups, 1, b4, g);
+    const int nlive = (int)(a.nlines - 4 * g < C ? a.nlines - 4 * g : C);
+    mbar_wait(&full[st], (uint32_t)(it >> 1) & 1u);
+    {
+      const int rstep = (M >> li.sl) * li.sjt;
+      for (int i = tl; i < C * M; i += nth1) {
+        const int cc = i & 3, s = i >> 2;
+        fold_dispatch<QC>(bk, li.at(cc, s), rstep, (int)a.in_f.L - s, a.in_f.p, tM1[s]);
+      }
+    }
+    compute_sync(nth);
+    {
+      V v[16];
+      load_time(v, bk, li, c, u, r);
+      fft_fwd(v, bk, ex_of(li, true, r), c, u, t128);
+      __syncwarp();
+      store_spec(v, bk, li, c, u, r);
+    }
+    compute_sync(nth);
+    // 16-byte stores: thread i -> element j = i >> 3, sub-item (i >> 1) & 3, line pair i & 1
+    V* y = reinterpret_cast<V*>(o.ptr[k_arr]);
+    const int64_t l0 = 4 * g;
+    for (int i = tid; i < Lout * 8; i += nth) {
+      const int j = i >> 3, kk = (i >> 1) & 3, cp = i & 1;
+      const V* src = buf + kk * IN + li.at(2 * cp, j);
+      V* dst = y + boff(4 * b4 + kk, o.nbi, o.s_bo, o.s_b) + line_off(o, l0 + 2 * cp) + (int64_t)j * o.s_js;
+      if (2 * cp + 1 < nlive) {
+        *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
+      } else if (2 * cp < nlive) {
+        *dst = *src;
+      }
+    }
+    fence_async_smem();
+    mbar_arrive(&done[st]);
   }
 }
 
