@@ -552,7 +552,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
       threads = hd::s128_bg_threads(L.a.q);
       smem = hd::s128_bg_smem_bytes(L.a.q, L.a.M1);
     } else {
-      fn = hd::lookup_s128(L.mode, L.a.q);
+      fn = hd::lookup_s128(L.mode, L.a.q, L.a.tm_in.kind, L.a.tm_out.kind, L.a.tm_out.slog);
       threads = 32 * (L.a.q + 1);
       smem = hd::s128_smem_bytes(L.a.q, L.mode, L.a.M1, L.a.tm_in.kind, L.a.tm_out.kind, L.a.in_g.p);
     }

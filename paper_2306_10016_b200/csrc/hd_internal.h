@@ -19,7 +19,8 @@ LaunchFn lookup_s512_mconv();
 int s512_mconv_qmax();
 // staged engine for m = 128 complex float, 4 lines per item (hd_s128.cuh);
 // blockDim = 32 (q + 1), q <= kS128QMax
-LaunchFn lookup_s128(int mode, int q);
+// in_kind / out_kind / out_slog: the launch's TMA descriptions (compile-time layouts)
+LaunchFn lookup_s128(int mode, int q, int in_kind, int out_kind, int out_slog);
 constexpr int kS128QMax = 8;
 size_t s128_smem_bytes(int q, int mode, int64_t M1, int in_kind, int out_kind, int pg);
 // its batch-grouped forward pass (4 batch entries x 4 lines per item), q = 5

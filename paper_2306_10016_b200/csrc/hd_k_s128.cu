@@ -7,9 +7,9 @@
 
 namespace hd {
 
-template <int MODE, int NT, int QC, int MINB = 2>
+template <int MODE, int NT, int QC, int MINB = 2, int ILK = 0, int OUTK = 0>
 static cudaError_t launch_s128_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
-  auto kern = s128::s128_kernel<MODE, NT, QC, MINB>;
+  auto kern = s128::s128_kernel<MODE, NT, QC, MINB, ILK, OUTK>;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -35,18 +35,34 @@ static cudaError_t launch_s128_impl(const PassArgs& a, dim3 grid, int nt, size_t
 
 // q = 5 (BASELINE config 4: M1 = 640 on every axis) has a compile-time-q kernel;
 // blockDim bound 192 (q <= 5: two CTAs per SM at <= 168 registers) or 288 (q <= 8)
+// q = 5 with line-tiled input: the layouts of the 3-D pipeline's passes at compile
+// time (conv_z in place; inv_y -> element tiles of 4; inv_x -> rows; fwd_y_g ->
+// interleaved)
 template <int MODE>
-static LaunchFn pick_s128(int q) {
+static LaunchFn pick_s128(int q, int in_kind, int out_kind, int out_slog) {
+  const bool il = in_kind == TMA_LINE_TILED;
+  if (q == 5 && il) {
+    const bool ip = s128::inplace_of(MODE, in_kind, out_kind);
+    if constexpr (MODE == MODE_CONV) {
+      if (ip) return launch_s128_impl<MODE, 192, 5, 2, 1, 1>;
+    } else if constexpr (MODE == MODE_INV) {
+      if (out_kind == TMA_ELEM_TILED && out_slog == 2) return launch_s128_impl<MODE, 192, 5, 2, 1, 2>;
+      if (out_kind == TMA_BULK) return launch_s128_impl<MODE, 192, 5, 2, 1, 3>;
+    } else {
+      if (out_kind == TMA_LINE_TILED) return launch_s128_impl<MODE, 192, 5, 2, 1, 4>;
+    }
+    return launch_s128_impl<MODE, 192, 5, 2, 1>;
+  }
   if (q == 5) return launch_s128_impl<MODE, 192, 5, 2>;
   if (q < 5) return launch_s128_impl<MODE, 192, 0>;
   return launch_s128_impl<MODE, 32 * (s128::kQMax + 1), 0>;
 }
-LaunchFn lookup_s128(int mode, int q) {
+LaunchFn lookup_s128(int mode, int q, int in_kind, int out_kind, int out_slog) {
   if (q < 1 || q > s128::kQMax) return nullptr;
   switch (mode) {
-    case MODE_FWD: return pick_s128<MODE_FWD>(q);
-    case MODE_INV: return pick_s128<MODE_INV>(q);
-    case MODE_CONV: return pick_s128<MODE_CONV>(q);
+    case MODE_FWD: return pick_s128<MODE_FWD>(q, in_kind, out_kind, out_slog);
+    case MODE_INV: return pick_s128<MODE_INV>(q, in_kind, out_kind, out_slog);
+    case MODE_CONV: return pick_s128<MODE_CONV>(q, in_kind, out_kind, out_slog);
     default: return nullptr;
   }
 }

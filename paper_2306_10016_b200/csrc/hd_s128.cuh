@@ -379,7 +379,11 @@ __host__ __device__ inline bool inplace_of(int mode, int in_kind, int out_kind) 
   return il_in == (out_kind == TMA_LINE_TILED);
 }
 
-template <int MODE, int NT, int QC, int MINB = 2>
+// ILK = 1: the input family is line-tiled (interleaved stage layout) at compile
+// time, so every stage address is an immediate offset from a per-lane base.
+// OUTK: the output stage layout at compile time (0: from the launch's TMA kinds;
+// 1: in place; 2: element-tiled by 4, 3: plain rows, 4: interleaved -- separate region)
+template <int MODE, int NT, int QC, int MINB = 2, int ILK = 0, int OUTK = 0>
 __global__ void __launch_bounds__(NT, MINB) s128_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -399,12 +403,13 @@ __global__ void __launch_bounds__(NT, MINB) s128_kernel(const __grid_constant__ 
   const int kk_in = MODE == MODE_FWD ? k_arr : 0;
   const bool tma = a.tm_in.kind != TMA_NONE;
   const bool tma_st = tma && a.tm_out.kind != TMA_NONE;
-  const bool il = a.tm_in.kind == TMA_LINE_TILED;
-  const bool inplace = inplace_of(MODE, a.tm_in.kind, a.tm_out.kind);
+  const bool il = ILK == 1 ? true : a.tm_in.kind == TMA_LINE_TILED;
+  const bool inplace = OUTK == 1 ? true : OUTK > 1 ? false : inplace_of(MODE, a.tm_in.kind, a.tm_out.kind);
   const int IN = in_floats2(q, MODE, MODE == MODE_CONV ? a.in_g.p : 0);
   const int SB = IN + (inplace ? 0 : out_floats2(q));
   const Lay li = il ? lay_interleaved() : lay_rows(IN / C);
-  const Lay lo = inplace ? li
+  const Lay lo = OUTK == 2 ? lay_elem(2) : OUTK == 3 ? lay_rows(q * M + kPad) : OUTK == 4 ? lay_interleaved()
+                 : inplace ? li
                  : a.tm_out.kind == TMA_ELEM_TILED ? lay_elem(a.tm_out.slog)
                  : a.tm_out.kind == TMA_LINE_TILED ? lay_interleaved()
                                                    : lay_rows(q * M + kPad);
