@@ -47,15 +47,22 @@ __device__ __forceinline__ void cp16(V* dst, const V* src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Debug phase timing (HD_PHASE_PROF=1 in the host driver): lane 0 of every warp
-// accumulates SM clock cycles per phase and adds them to a.phase_prof at exit.
+// Debug phase timing (library built with NVCC_APPEND_FLAGS=-DHD_PHASE_PROF_BUILD and
+// run with HD_PHASE_PROF=1): lane 0 of every warp accumulates SM clock cycles per
+// phase and adds them to a.phase_prof at exit.  Compiled out otherwise (the
+// disabled probes cost ~2 % of the convolution pass's instructions).
 constexpr int kPhases = 8;
+#ifdef HD_PHASE_PROF_BUILD
+constexpr bool kPhaseProf = true;
+#else
+constexpr bool kPhaseProf = false;
+#endif
 struct PhaseClock {
   unsigned long long acc[kPhases];
   long long t0;
   bool on;
   __device__ __forceinline__ void start(bool enable) {
-    on = enable;
+    on = kPhaseProf && enable;
 #pragma unroll
     for (int i = 0; i < kPhases; ++i) acc[i] = 0;
     if (on) t0 = clock64();
