@@ -12,6 +12,7 @@ LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
 // staged warp engine for m = 512 complex double (hd_s512.cuh); blockDim = 32 (q + 1) <= 384
 LaunchFn lookup_s512(int mode, int q);
 constexpr int kS512QMax = 11;
+constexpr int kS512LeanQ = 5;  // q <= 5: two CTAs per SM (zeta_{M1}^s from global memory)
 size_t s512_smem_bytes(int q, int mode);
 int s512_threads(int q, int mode);
 // staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()

@@ -6,9 +6,9 @@
 
 namespace hd {
 
-template <int MODE, int NTMAX, int QC>
+template <int MODE, int NTMAX, int QC, int LEAN = 0>
 static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
-  auto kern = s512::s512_kernel<MODE, NTMAX, QC>;
+  auto kern = s512::s512_kernel<MODE, NTMAX, QC, LEAN>;
   static size_t configured = 0;  // per instantiation
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -22,7 +22,13 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  if ((int64_t)grid.x > sms) grid.x = (unsigned)sms;
+  int occ = 1;
+  if (LEAN) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  if ((int64_t)grid.x > (int64_t)sms * occ) grid.x = (unsigned)(sms * occ);
   kern<<<grid, nt, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -32,6 +38,7 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
 template <int MODE>
 static LaunchFn pick_s512(int q) {
   if (q == 9) return launch_s512_impl<MODE, 320, 9>;
+  if (q <= kS512LeanQ) return launch_s512_impl<MODE, 32 * (kS512LeanQ + 1), 0, 1>;
   return launch_s512_impl<MODE, 32 * (s512::kQMax + 1), 0>;
 }
 LaunchFn lookup_s512(int mode, int q) {
@@ -73,7 +80,8 @@ int s512_threads(int q, int mode) { (void)mode; return 32 * (q + 1); }
 size_t s512_smem_bytes(int q, int mode) {
   if (mode == MODE_MCONV)
     return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 + 2 * (2 * q * 512));
-  return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 +
+  const bool lean = q <= kS512LeanQ && q != 9;
+  return 128 + sizeof(double2) * (size_t)(q * kQF + w512::kTwRows * 32 + (lean ? 0 : 512) +
                                           2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));
 }
 

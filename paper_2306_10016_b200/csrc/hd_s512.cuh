@@ -490,7 +490,7 @@ __device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, co
 // item i from that stage, waits until the store has read the stage, and loads
 // item i + 2 into it.  Fallback mode (a layout TMA cannot express): the compute
 // warps copy with cp.async / plain stores and the producer warp idles.
-// Shared memory: [full x2, done x2 | pad][zt 16x16][tw 23x32][col 512]
+// Shared memory: [full x2, done x2 | pad][zt q x 16][tw 23x32][col 512 (not LEAN)]
 //                [stage 0][stage 1], stage = q*512 (+512 CONV).
 // ---------------------------------------------------------------------------
 // The short input's transform for residue r (p_g = 1): w[s] = (1/prod M1)
@@ -521,16 +521,20 @@ __device__ __forceinline__ void g_transform(V* v, const V* gbuf, int Lg, int r, 
 }
 
 
-template <int MODE, int NTMAX, int QC>
-__global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ PassArgs a) {
+// LEAN (q <= 5): zeta_{M1}^s is read from global memory instead of a shared-memory
+// column, so that two CTAs fit one SM (q + 1 <= 6 warps each at <= 168 registers):
+// the small-q passes (the real-input path's packed convolution axis, q = 5) then
+// run 12 warps per SM instead of 6.
+template <int MODE, int NTMAX, int QC, int LEAN = 0>
+__global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* done = full + 2;
-  V* zt = reinterpret_cast<V*>(smem_raw + 128);
-  V* twtab = zt + kQF * kQF;
-  V* twcol = twtab + w512::kTwRows * 32;   // zeta_{M1}^s, s < 512
-  V* stage0 = twcol + M;
   const int q = QC > 0 ? QC : a.q;
+  V* zt = reinterpret_cast<V*>(smem_raw + 128);  // zt[r * kQF + t], r < q
+  V* twtab = zt + q * kQF;
+  V* twcol = twtab + w512::kTwRows * 32;   // zeta_{M1}^s, s < 512 (not LEAN)
+  V* stage0 = LEAN ? twcol : twcol + M;
   const int tid = threadIdx.x;
   const int nth = 32 * q;                  // compute threads; warp q is the producer
   const int lane = tid & 31;
@@ -546,13 +550,15 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
   if (QC == 0) {
-    for (int i = tid; i < kQF * kQF; i += blockDim.x) {
+    for (int i = tid; i < q * kQF; i += blockDim.x) {
       const int rr = i / kQF, t = i % kQF;
       zt[i] = ldg(twM1 + (int64_t)((rr * t) % q) * M);
     }
   }
   for (int i = tid; i < w512::kTwRows * 32; i += blockDim.x) twtab[i] = w512::tw_entry(twm, i >> 5, i & 31);
-  for (int i = tid; i < M; i += blockDim.x) twcol[i] = ldg(twM1 + i);
+  if (!LEAN)
+    for (int i = tid; i < M; i += blockDim.x) twcol[i] = ldg(twM1 + i);
+  const V* twc = LEAN ? twM1 : twcol;
   if (tid == nth) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -642,7 +648,7 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
     } else {
-      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twcol, tid, nth);
+      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twc, tid, nth);
     }
     pc.mark(1);
     compute_sync(nth);
@@ -691,14 +697,14 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_kernel(const __grid_constant__ 
         split_item(wn, a.nbatch, a.ngroups, a.batch_fastest, bn, gn);
         mbar_wait(&full[st ^ 1], (uint32_t)((it + 1) >> 1) & 1u);
         const int lt = (r - 1 - (r > 4 ? 1 : 0)) * 32 + lane;
-        fold9_light(stage0 + (st ^ 1) * SB, a.in_f.p, (int)a.in_f.L, gn < a.nlines, twcol, lt);
+        fold9_light(stage0 + (st ^ 1) * SB, a.in_f.p, (int)a.in_f.L, gn < a.nlines, twc, lt);
       }
     }
     pc.mark(4);
     if constexpr (MODE != MODE_FWD) {
       compute_sync(nth);
       pc.mark(5);
-      unfold_all<QC>(buf, q, a.out.T, zt, twcol, tid, nth);
+      unfold_all<QC>(buf, q, a.out.T, zt, twc, tid, nth);
     }
     pc.mark(6);
     // results are in stage slots j < out.L
