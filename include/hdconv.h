@@ -336,6 +336,7 @@ int64_t     hd_launch_count(hd_ctx_t ctx);
 #define HD_ENGINE_S512 1        /* staged warp engine, m = 512 complex double (C = 1) */
 #define HD_ENGINE_S512_MCONV 2  /* its multi-pair convolution pass */
 #define HD_ENGINE_S128 3        /* staged engine, m = 128 complex float (C = 4) */
+#define HD_ENGINE_S512C 4       /* 1-D pass of long lines, m = 512 complex double, two-CTA clusters */
 int64_t     hd_engine_launches(hd_ctx_t ctx, int32_t engine);
 
 #ifdef __cplusplus

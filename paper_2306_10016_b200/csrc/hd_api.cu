@@ -59,7 +59,7 @@ struct hd_ctx {
   };
   std::vector<ProfEntry> prof;
   int64_t launches = 0;
-  int64_t engine_launches[4] = {0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
+  int64_t engine_launches[5] = {0, 0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
 };
 
 namespace {
@@ -253,7 +253,11 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
       return fail(ctx, HD_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 1024]");
     x.lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
-    if (pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
+    // the 1-D two-CTA cluster pass (hd_s512c.cuh) holds at most 11 residue rows per CTA
+    const bool cluster_1d = dt == HD_C128 && ndim == 1 && npairs == 1 && x.m == 512 && x.D == x.q &&
+                            x.q >= hd::kS512cQMin && x.q <= hd::kS512cQMax && x.lines == 1 && x.auto_engine &&
+                            !(plan->flags & HD_FLAG_GENERIC_FFT);
+    if (!cluster_1d && pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
       return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": lines*D*m too large for shared memory");
     a.p_f = x.pf; a.p_g = x.pg; a.q = x.q; a.M1 = x.M1;
   }
@@ -339,6 +343,7 @@ struct Launch {
   bool auto_engine;
   bool s512_axis;   // the staged engine may run this pass (same engine for every pass of the axis)
   bool s128_axis;   // likewise for the m = 128 complex-float staged engine
+  bool s512c_axis;  // the 1-D two-CTA cluster pass may run (automatic engine on a 1-D problem)
   int mode;
   const char* name;
   PassArgs a;
@@ -537,6 +542,19 @@ bool use_s128_bg(const Launch& L) {
   return true;
 }
 
+// The 1-D convolution pass of long lines on two-CTA clusters (hd_s512c.cuh): m = 512,
+// complex double, all residues (D = q), 12 <= q <= 22, one pair, plain rows.
+bool use_s512c(hd_dtype_t dt, const Launch& L) {
+  if (dt != HD_C128 || L.m != 512 || L.lines != 1 || L.mode != hd::MODE_CONV || (L.flags & HD_FLAG_GENERIC_FFT))
+    return false;
+  if (!L.auto_engine || !L.s512c_axis || L.a.D != L.a.q || L.a.q < hd::kS512cQMin || L.a.q > hd::kS512cQMax)
+    return false;
+  const PassArgs& a = L.a;
+  return a.npairs == 1 && a.nbatch == 1 && a.in_f.p <= 32 && a.in_g.p <= 32 && a.out.T <= 32 && a.in_f.tl >= 30 && a.in_f.s_j == 1 && a.in_g.tl >= 30 &&
+         a.in_g.s_j == 1 && a.out.tl >= 30 && a.out.so_log2 >= 30 && a.out.s_js == 1 && a.in_f.jd <= 0 &&
+         a.in_g.jd <= 0 && a.out.jd <= 0;
+}
+
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
   hd::LaunchFn fn = nullptr;
@@ -545,7 +563,12 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   bool staged = use_s512(dt, L);
   bool mconv = false;
   const bool s128 = use_s128(dt, L);
-  if (s128) {
+  const bool s512c = !staged && use_s512c(dt, L);
+  if (s512c) {
+    fn = hd::lookup_s512c();
+    threads = hd::s512c_threads(L.a.q);
+    smem = hd::s512c_smem_bytes();
+  } else if (s128) {
     prepare_tma(L, true);
     if (use_s128_bg(L)) {
       fn = hd::lookup_s128_bg(L.mode, L.a.q);
@@ -560,7 +583,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     prepare_tma(L);
     mconv = L.a.tm_in.kind == hd::TMA_LINE_TILED || L.a.tm_in.kind == hd::TMA_BULK;
   }
-  if (s128) {
+  if (s128 || s512c) {
     // set above
   } else if (mconv) {
     fn = hd::lookup_s512_mconv();
@@ -605,7 +628,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   static const bool dbg_launch = getenv("HD_DEBUG_LAUNCH") != nullptr;
   if (dbg_launch)
     fprintf(stderr, "[launch] %-8s engine=%s m=%d C=%d q=%d D=%d items=%lld threads=%d smem=%zu tma in=%d g=%d out=%d\n",
-            L.name, s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m, L.lines, L.a.q, L.a.D,
+            L.name, s512c ? "s512c" : s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m,
+            L.lines, L.a.q, L.a.D,
             (long long)total, threads, smem, L.a.tm_in.kind, L.a.tm_in_g.kind, L.a.tm_out.kind);
   cudaError_t e = fn(L.a, grid, threads, smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, L.name);
@@ -623,8 +647,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     fprintf(stderr, "\n");
   }
   ctx->launches += 1;
-  ctx->engine_launches[s128 ? HD_ENGINE_S128 : mconv ? HD_ENGINE_S512_MCONV : staged ? HD_ENGINE_S512
-                                                                              : HD_ENGINE_GENERIC] += 1;
+  ctx->engine_launches[s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128 : mconv ? HD_ENGINE_S512_MCONV
+                       : staged ? HD_ENGINE_S512 : HD_ENGINE_GENERIC] += 1;
   if (ctx->profiling) {
     cudaEventRecord(e1, st);
     hd_ctx::ProfEntry* pe = nullptr;
@@ -726,6 +750,7 @@ Launch make_launch(hd_ctx* ctx, const Problem& P, int mode, const char* name, in
   L.auto_engine = x.auto_engine;
   L.s512_axis = P.s512[axis];
   L.s128_axis = P.s128[axis];
+  L.s512c_axis = P.ndim == 1;
   L.nbuf = (mode == hd::MODE_CONV) ? conv_nbuf(P.N) : 1;
   init_in(L.a.in_f);
   init_in(L.a.in_g);
@@ -1605,7 +1630,7 @@ hd_status_t hd_profile_reset(hd_ctx_t ctx) {
 int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
 int64_t hd_engine_launches(hd_ctx_t ctx, int32_t engine) {
-  if (!ctx || engine < 0 || engine > HD_ENGINE_S128) return -1;
+  if (!ctx || engine < 0 || engine > HD_ENGINE_S512C) return -1;
   return ctx->engine_launches[engine];
 }
 

@@ -13,6 +13,12 @@ LaunchFn lookup_launcher(bool is_double, int m, int mode, int threads);
 LaunchFn lookup_s512(int mode, int q);
 constexpr int kS512QMax = 11;
 constexpr int kS512LeanQ = 5;  // q <= 5: two CTAs per SM (zeta_{M1}^s from global memory)
+// 1-D convolution pass of long lines (hd_s512c.cuh): m = 512, a two-CTA cluster
+// per line, 12 <= q <= 22
+constexpr int kS512cQMin = 12, kS512cQMax = 22;
+LaunchFn lookup_s512c();
+int s512c_threads(int q);
+size_t s512c_smem_bytes();
 size_t s512_smem_bytes(int q, int mode);
 int s512_threads(int q, int mode);
 // staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()

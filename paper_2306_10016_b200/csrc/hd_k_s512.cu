@@ -86,3 +86,42 @@ size_t s512_smem_bytes(int q, int mode) {
 }
 
 }  // namespace hd
+
+// ---------------------------------------------------------------------------
+// 1-D long lines: two-CTA clusters (hd_s512c.cuh), 12 <= q <= 22
+// ---------------------------------------------------------------------------
+#include "hd_s512c.cuh"
+namespace hd {
+static cudaError_t launch_s512c(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
+  constexpr int NT = 32 * s512c::kRMax;
+  auto kern = s512c::s512c_kernel<NT>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (nt < 32 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // one cluster of two CTAs per line, persistent: at most one CTA per SM
+  int64_t ncl = (int64_t)a.nlines;
+  if (ncl > sms / 2) ncl = sms / 2;
+  grid.x = (unsigned)(2 * ncl);
+  grid.y = 1;
+  grid.z = 1;
+  kern<<<grid, nt, smem, st>>>(a);
+  return cudaGetLastError();
+}
+LaunchFn lookup_s512c() { return launch_s512c; }
+int s512c_threads(int q) {
+  const int P = (q - 1) / 2, K0 = (q & 1) ? (P + 1) / 2 : P / 2;
+  const int n0 = 1 + 2 * K0, n1 = 2 * (P - K0) + ((q & 1) ? 0 : 1);
+  return 32 * (n0 > n1 ? n0 : n1);
+}
+size_t s512c_smem_bytes() { return s512c::smem_bytes(); }
+}  // namespace hd

@@ -592,3 +592,33 @@ def test_lambda_conv_config2_shape_and_padding(ctx, H):
         ctx.conv1d_lambda(dev(g), dev(f), 256, 4)  # L_f > L_g
     with pytest.raises(H.HDError):
         ctx.conv1d_lambda(dev(f), dev(g), 256, 4, M=100)
+
+
+# ---------------------------------------------------------------- 1-D long lines: two-CTA clusters
+# hd_s512c.cuh: m = 512, 12 <= q <= 22, residues split over a cluster of two CTAs,
+# partial unfolds exchanged through distributed shared memory.
+@pytest.mark.parametrize("B,Lf,Lg", [(4, 8192, 3000),   # config 2's pair: q = 22
+                                      (3, 6000, 200),    # q = 13 (odd: 7 / 6 residues)
+                                      (2, 6000, 145),    # L_out = 12 x 512 exactly: q = 12
+                                      (5, 300, 9000),    # the long input is g
+                                      (1, 5000, 4000)])  # p_f = 10, p_g = 8
+def test_s512c_cluster_conv1d(ctx, H, B, Lf, Lg):
+    f, g = synth.random_pair(1500 + Lf, (B, Lf), (B, Lg))
+    plan = H.Plan.make(1, [{"m": 512, "C": 1}])
+    n0 = ctx.engine_launches(H.HD_ENGINE_S512C)
+    h = host(ctx.conv(dev(f), dev(g), plan=plan, batch=True))
+    assert ctx.engine_launches(H.HD_ENGINE_S512C) - n0 == 1
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
+
+
+def test_s512c_shared_g_and_window(ctx, H):
+    f = np.stack([synth.random_pair(1520 + b, (7000,), (1,))[0] for b in range(3)])
+    g = synth.random_pair(1530, (1,), (2500,))[1]
+    plan = H.Plan.make(1, [{"m": 512, "C": 1}])
+    h = host(ctx.conv(dev(f), dev(g), plan=plan, batch=True, shared_g=True))
+    for b in range(3):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g)) < 1e-11
+    lo, n = [1234], [5000]
+    hw = host(ctx.conv_window([dev(f[0])], [dev(g)], lo, n, plan=plan))
+    assert oracle.rel_l2(hw, oracle.conv(f[0], g)[1234:6234]) < 1e-11

@@ -48,7 +48,7 @@ for axes in json.loads(a.plans):
         continue
     torch.cuda.synchronize()
     ctx.profile_reset()
-    e0 = [ctx.engine_launches(e) for e in range(4)]
+    e0 = [ctx.engine_launches(e) for e in range(5)]
     ctx.profile_enable(True)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
@@ -58,8 +58,8 @@ for axes in json.loads(a.plans):
     torch.cuda.synchronize()
     ctx.profile_enable(False)
     prof = ctx.profile_read()
-    eng = [(ctx.engine_launches(e) - e0[e]) // a.steps for e in range(4)]
+    eng = [(ctx.engine_launches(e) - e0[e]) // a.steps for e in range(5)]
     out = {"plan": axes, "flags": flags, "step_ms": s0.elapsed_time(s1) / a.steps,
-           "engines": dict(zip(["generic", "s512", "s512_mconv", "s128"], eng)),
+           "engines": dict(zip(["generic", "s512", "s512_mconv", "s128", "s512c"], eng)),
            "passes": {k: round(v[0] / max(v[1], 1), 4) for k, v in prof.items()}}
     print(json.dumps(out), flush=True)
