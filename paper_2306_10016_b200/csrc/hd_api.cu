@@ -318,6 +318,16 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
         if (c < best * 0.999) { best = c; bm = m; bD = D; bl = lines; }
       }
     }
+    // multi-D complex double: prefer m = 512 where the staged engine runs every pass
+    // of the axis (q <= 11, p <= 8; the convolution axis with several pairs: the
+    // multi-pair pass, q <= 6) -- measured faster than the cost model's pick (config
+    // 5's y axis: 0.92 ms staged vs 1.98 ms at m = 1024 generic)
+    if (dt == HD_C128 && ndim > 1 && bm != 512) {
+      const int64_t q5 = cdiv(Mi, 512);
+      const bool p_ok = cdiv(Lf[i], 512) <= 8 && cdiv(Lg[i], 512) <= 8;
+      const bool q_ok = (conv && npairs > 1) ? q5 <= 6 : q5 <= hd::kS512QMax;
+      if (p_ok && q_ok) { bm = 512; bD = (int)q5; }
+    }
     // one line per CTA where the staged m = 512 engine applies (hd_s512.cuh); four
     // lines per item and tiles of four for the staged complex-float m = 128 engine
     // (hd_s128.cuh) in 2-D / 3-D
