@@ -499,15 +499,16 @@ def test_slab_decomposition_emulated_ranks(ctx, H, world, shape, m):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3])
-@pytest.mark.parametrize("dtype,m", [(np.complex128, 16), (np.complex64, 16), (np.complex128, 32)])
-def test_slab3d_emulated_ranks(ctx, H, world, dtype, m):
+@pytest.mark.parametrize("dtype,m,C", [(np.complex128, 16, 1), (np.complex64, 16, 1), (np.complex128, 32, 1),
+                                       (np.complex64, 128, 4)])  # last: the c64 staged conv pass in hd_pass
+def test_slab3d_emulated_ranks(ctx, H, world, dtype, m, C):
     """3-D z-slab path (dist.SlabConv3D on hd_pass) with the all-to-alls replaced by
     block copies between emulated ranks."""
     from paper_2306_10016_b200.dist import GpuBackend3D, SlabConv3D, emulate_ranks_3d
-    Lf, Lg = (21, 18, 24), (5, 7, 4)
+    Lf, Lg = (21, 18, 24) if m < 128 else (150, 18, 24), (5, 7, 4)
     f, g = synth.random_pair(820 + world, Lf, Lg, dtype=dtype)
     dt = H.HD_C128 if dtype == np.complex128 else H.HD_C64
-    plan = H.hd_plan_complete(dt, list(Lf), list(Lg), H.Plan.make(3, [{"m": m}] * 3))
+    plan = H.hd_plan_complete(dt, list(Lf), list(Lg), H.Plan.make(3, [{"m": m, "C": C}] * 3))
     Ky, Kx = plan.axis[1].M1, plan.axis[2].M1
     be = GpuBackend3D(ctx, plan, dt)
     convs = [SlabConv3D(be, None, world, k, Lf, Lg, Ky, Kx) for k in range(world)]
