@@ -685,6 +685,16 @@ struct Problem {
   bool s512[HD_MAX_DIM] = {};  // every pass along axis i may run on the staged m = 512 engine
   bool s128[HD_MAX_DIM] = {};  // ... on the staged m = 128 complex-float engine
   hd_plan_t plan{};
+  // hd_conv_real fused into the 2-D x passes (fwd_x_f reads the real row pairs, inv_x
+  // writes the real split; see PassArgs rp / rs): f real [Lf0][Lf1], h real
+  // [Lout0][Lout1], side buffer of Lg0 - 1 rows
+  struct RealFuse {
+    bool on = false;
+    const void* f = nullptr;
+    void* h = nullptr;
+    void* side = nullptr;
+    int64_t Lf0 = 0, A = 0, Lg0 = 0, Lout0 = 0;
+  } rf;
 };
 
 // One engine per axis: the staged engine's spectral order (lane-major) differs from
@@ -857,6 +867,12 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       }
       L.a.in_f.L = len; L.a.in_f.p = which == 0 ? x.pf : x.pg;
       L.a.in_f.nbi = nb; L.a.in_f.s_b = rows * len; in_rows(L.a.in_f, len);
+      if (which == 0 && P.rf.on) {  // rows y and y + A of the real f (doubles)
+        L.a.rp = 1;
+        L.a.in_f.ptr[0] = P.rf.f;
+        L.a.rp_off = P.rf.A * len;
+        L.a.rp_rows = P.rf.Lf0 - P.rf.A;
+      }
       L.a.out.nbi = nb; L.a.out.s_b = Kxp * rows; out_elem_tiled(L.a.out, Sy, Sy, rows * Sy);
       L.a.out.L = Kx;
       L.a.nlines = rows; L.a.nbatch = nb;
@@ -899,6 +915,14 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.in_f.L = Kx;
       L.a.out.ptr[0] = P.h; L.a.out.nbi = B; L.a.out.s_b = y.O * x.O; out_rows(L.a.out, x.O);
       L.a.out.L = x.O; L.a.out.T = x.T; L.a.out.j0 = x.o0;
+      if (P.rf.on) {  // real split into h (doubles) and the side buffer
+        L.a.rs = 1;
+        L.a.out.ptr[0] = P.rf.h;
+        L.a.rs_A = P.rf.A;
+        L.a.rs_side_rows = P.rf.Lg0 - 1;
+        L.a.rs_rows = P.rf.Lout0;
+        L.a.rs_side = P.rf.side;
+      }
       L.a.nlines = y.O; L.a.nbatch = B;
       L.ngroups = cdiv(y.O, Cx); L.nbatch = B;
       return launch(ctx, P.dt, L, st);
@@ -1159,10 +1183,11 @@ static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64
                              const void* const* f, const int64_t* Lf, const void* const* g,
                              const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan,
                              void* ws, size_t ws_bytes, void* stream, const int64_t* win_lo = nullptr,
-                             const int64_t* win_n = nullptr) {
+                             const int64_t* win_n = nullptr, const Problem::RealFuse* rf = nullptr) {
   Problem P;
   hd_status_t s = setup(ctx, P, dt, ndim, N, batch, f, Lf, g, Lg, h, M, plan, true, win_lo, win_n);
   if (s != HD_OK) return s;
+  if (rf) P.rf = *rf;
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   return run_pipeline(ctx, P, ws, ws_bytes, (cudaStream_t)stream);
@@ -1175,6 +1200,25 @@ hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t
                           void* stream) {
   if (!win_lo || !win_n) return fail(ctx, HD_ERR_INVALID, "null window");
   return run_entry(ctx, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan, ws, ws_bytes, stream, win_lo, win_n);
+}
+
+// The real path's pack / unpack fuse into the x passes when the packed 2-D problem
+// runs its x axis on the staged engine with q = 9 (the compile-time-q kernel that
+// has the real-pair / real-split modes) and every real row moves by 16-byte bulk copies.
+static bool real_fusable(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, int64_t batch, const void* f, const int64_t* Lz,
+                         const int64_t* Lf, const int64_t* Lg, const void* h, const hd_plan_t* plan) {
+  if (dtype != HD_C128 || ndim != 2 || batch != 1) return false;
+  static const bool off = getenv("HD_NO_REAL_FUSE") != nullptr;  // A/B switch
+  if (off) return false;
+  const int64_t Lout1 = Lf[1] + Lg[1] - 1;
+  if ((Lf[1] & 1) || (Lout1 & 1) || (reinterpret_cast<uintptr_t>(f) & 15) || (reinterpret_cast<uintptr_t>(h) & 15))
+    return false;
+  Problem P;
+  const void* fa[1] = {f};
+  const void* ga[1] = {f};
+  if (setup(ctx, P, dtype, 2, 1, 1, fa, Lz, ga, Lg, nullptr, nullptr, plan, false) != HD_OK) return false;
+  const AxisInfo& x = P.ax[1];
+  return P.s512[1] && x.q == 9 && x.lines == 1 && x.D == 9 && x.pf <= 8 && x.o0 == 0 && x.O == Lout1;
 }
 
 hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch, const void* f,
@@ -1214,6 +1258,23 @@ hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t b
   char* z = (char*)ctx->rio;
   char* gc = z + bz;
   char* w = gc + bgc;
+  if (real_fusable(ctx, dtype, ndim, batch, f, Lz, Lf, Lg, h, plan)) {
+    // pack / unpack inside the x passes: only g is promoted; the Im rows of w that
+    // overlap Re rows (Lg0 - 1 of them) go to a side buffer (w's space) and are added
+    cudaError_t e = hd::launch_real_to_complex(dbl, g, gc, Lg[0] * rest_g, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "real to complex");
+    Problem::RealFuse rf;
+    rf.on = true; rf.f = f; rf.h = h; rf.side = w;
+    rf.Lf0 = Lf[0]; rf.A = A; rf.Lg0 = Lg[0]; rf.Lout0 = Lout0;
+    const void* fa[1] = {f};
+    const void* ga[1] = {gc};
+    hd_status_t s = run_entry(ctx, dtype, ndim, 1, 1, fa, Lz, ga, Lg, h, nullptr, plan, nullptr, 0, stream,
+                              nullptr, nullptr, &rf);
+    if (s != HD_OK) return s;
+    e = hd::launch_real_fixup(w, h, Lg[0] - 1, A, Lout0, rest_o, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "real fix-up");
+    return HD_OK;
+  }
   cudaError_t e = hd::launch_real_pack(dbl, f, z, Lf[0], A, rest_f, batch, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "real pack");
   e = hd::launch_real_to_complex(dbl, g, gc, batch * Lg[0] * rest_g, st);

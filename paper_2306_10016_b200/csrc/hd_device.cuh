@@ -309,6 +309,16 @@ struct PassArgs {
   int32_t q, D, C, c_log2; // residues, residues per group, lines per CTA (power of two)
   int32_t npairs;
   int32_t batch_fastest;
+  // hd_conv_real fused into the staged m = 512 x passes (hd_s512.cuh, q = 9):
+  // rp (forward): line y is two real rows, re = (double*)in_f.ptr[0] + y * in_f.s_l and
+  //   im = re + rp_off (zero for y >= rp_rows): the packed z = f[y] + i f[y + A];
+  // rs (inverse): output line y (of w) is split: Re -> (double*)out.ptr[0] + y * out.s_l,
+  //   Im -> row y + rs_A of the same array when y >= rs_side_rows (rows >= rs_rows
+  //   dropped), else row y of rs_side (added by a fix-up kernel afterwards).
+  int32_t rp, rs;
+  int64_t rp_off, rp_rows;
+  int64_t rs_A, rs_side_rows, rs_rows;
+  void* rs_side;
 };
 
 enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2, MODE_MCONV = 3 /* staged engine only */ };

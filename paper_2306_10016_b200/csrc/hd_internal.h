@@ -44,6 +44,9 @@ cudaError_t launch_real_pack(bool is_double, const void* f, void* z, int64_t Lf0
 cudaError_t launch_real_to_complex(bool is_double, const void* g, void* gc, int64_t n, cudaStream_t st);
 cudaError_t launch_real_unpack(bool is_double, const void* w, void* h, int64_t Lout0, int64_t Ow0, int64_t A,
                                int64_t rest, int64_t nb, cudaStream_t st);
+// fused real path: h[y + A] += side[y] for y < rows (rows of `rest` doubles, y + A < Lout0)
+cudaError_t launch_real_fixup(const void* side, void* h, int64_t rows, int64_t A, int64_t Lout0, int64_t rest,
+                              cudaStream_t st);
 // row f1 (hd_conv1d_lambda): matched product of the Lambda > 1 residue construction
 cudaError_t launch_lambda_product(bool is_double, const void* Xf, void* Xg, const int32_t* perm_g,
                                   const int32_t* iperm_f, int64_t nlines, int m, int Lam, int qg, double scale,

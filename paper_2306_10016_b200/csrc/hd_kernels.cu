@@ -133,6 +133,22 @@ cudaError_t launch_real_unpack(bool is_double, const void* w, void* h, int64_t L
   return cudaGetLastError();
 }
 
+// fused real path (hd_conv_real): the Im parts of the w rows that overlap Re rows
+__global__ void real_fixup_kernel(const double* __restrict__ side, double* h, int64_t rows, int64_t A,
+                                  int64_t Lout0, int64_t rest) {
+  const int64_t n = rows * rest;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / rest;
+    if (y + A < Lout0) h[i + A * rest] += side[i];
+  }
+}
+cudaError_t launch_real_fixup(const void* side, void* h, int64_t rows, int64_t A, int64_t Lout0, int64_t rest,
+                              cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  real_fixup_kernel<<<grid_for(rows * rest), 256, 0, st>>>((const double*)side, (double*)h, rows, A, Lout0, rest);
+  return cudaGetLastError();
+}
+
 // Row f1 matched product: H_{r_g}[l_g] = F_{q_g lambda + r_g}[l_f]
 // G_{r_g}[l_g] * scale, l_f = l_g / Lambda, lambda = l_g mod Lambda; residue rows in
 // the engine's spectral order (perm_g: position -> frequency of size Lambda m;

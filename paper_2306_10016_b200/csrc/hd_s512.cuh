@@ -87,9 +87,17 @@ struct PhaseClock {
 // Loads of one work item in the slot range [j0, j1) of the in_f line (the whole
 // short line g in CONV goes with the first range: it lands beyond the output slots).
 // issue_loads_arm sets the mbarrier's byte count for the whole item first.
+// real-pair input (a.rp): the re row at the stage start, the im row from double rp_im_slot
+__device__ __forceinline__ int rp_im_slot(const PassArgs& a) { return (int)((a.in_f.L + 1) / 2 * 2); }
+
 template <int MODE>
 __device__ __forceinline__ void issue_loads_arm(const PassArgs& a, int64_t g, uint64_t* bar) {
   uint32_t bytes = 0;
+  if (MODE == MODE_FWD && a.rp) {
+    if (g < a.nlines) bytes = (uint32_t)a.in_f.L * 8u * (g < a.rp_rows ? 2u : 1u);
+    mbar_expect_tx(bar, bytes);
+    return;
+  }
   if (g < a.nlines) {
     const int L = (int)a.in_f.L;
     bytes += a.tm_in.kind == TMA_BULK ? (uint32_t)L * 16u : (uint32_t)((L + kBox - 1) / kBox) * kBox * 16u;
@@ -106,6 +114,14 @@ __device__ __forceinline__ void issue_loads_range(const PassArgs& a, int k_arr, 
   if (g >= a.nlines) return;
   const LineIn& in = a.in_f;
   const int L = (int)in.L;
+  if (MODE == MODE_FWD && a.rp) {  // both real rows with the first range
+    if (j0 != 0) return;
+    const double* re = reinterpret_cast<const double*>(in.ptr[0]) + line_off(in, g);
+    double* sb = reinterpret_cast<double*>(buf);
+    bulk_load(sb, re, (uint32_t)L * 8u, bar);
+    if (g < a.rp_rows) bulk_load(sb + rp_im_slot(a), re + a.rp_off, (uint32_t)L * 8u, bar);
+    return;
+  }
   j1 = j1 < L ? j1 : L;
   const int kk = MODE == MODE_FWD ? k_arr : 0;
   if (j0 < j1) {
@@ -148,7 +164,7 @@ __device__ __forceinline__ void issue_loads_tma(const PassArgs& a, int k_arr, in
 // loads for the TMA unit and measured slower)
 template <int MODE>
 __device__ __forceinline__ void issue_prefetch(const PassArgs& a, int k_arr, int64_t b, int64_t g) {
-  if (g >= a.nlines || a.tm_in.kind != TMA_BULK) return;
+  if (g >= a.nlines || a.tm_in.kind != TMA_BULK || (MODE == MODE_FWD && a.rp)) return;
   const LineIn& in = a.in_f;
   const int kk = MODE == MODE_FWD ? k_arr : 0;
   bulk_prefetch_l2(reinterpret_cast<const V*>(in.ptr[kk]) + boff(b, in.nbi, in.s_bo, in.s_b) + line_off(in, g),
@@ -231,9 +247,32 @@ __device__ __forceinline__ void bulk_wait_read_n(int n) {
 // same stage follow range by range, each waiting only until the store groups that
 // overlap its slots have been read out of shared memory.
 constexpr int kGroups = 4;
+constexpr int T9SLOTS = 9 * M;  // real split: the Im array starts at double 9 m of the stage
 template <int MODE>
 __device__ __forceinline__ void handover(const PassArgs& a, int k_arr, int kk_out, bool store, int64_t bs,
                                          int64_t gs, bool load, int64_t bl, int64_t gl, V* buf, uint64_t* bar) {
+  if ((MODE == MODE_INV && a.rs) || (MODE == MODE_FWD && a.rp)) {
+    if (store) {
+      if (MODE == MODE_INV && a.rs) {  // Re row and Im row of the output line (real split)
+        const LineOut& o = a.out;
+        const uint32_t nb = (uint32_t)o.L * 8u;
+        const double* sb = reinterpret_cast<const double*>(buf);
+        double* h = reinterpret_cast<double*>(o.ptr[0]);
+        bulk_store(h + gs * o.s_l, sb, nb);
+        const int64_t yi = gs + a.rs_A;
+        if (gs < a.rs_side_rows) bulk_store(reinterpret_cast<double*>(a.rs_side) + gs * o.s_l, sb + T9SLOTS, nb);
+        else if (yi < a.rs_rows) bulk_store(h + yi * o.s_l, sb + T9SLOTS, nb);
+        bulk_commit();
+      } else {
+        issue_stores_range(a, kk_out, bs, gs, buf, 0, 1 << 30);
+      }
+    }
+    if (!load) return;
+    issue_loads_arm<MODE>(a, gl, bar);
+    if (store) bulk_wait_read_n(0);
+    issue_loads_range<MODE>(a, k_arr, bl, gl, buf, bar, 0, 1 << 30);
+    return;
+  }
   const int Ls = store ? (int)a.out.L : 0;
   const int Ll = load ? (int)a.in_f.L : 0;
   const int Lmax = Ls > Ll ? Ls : Ll;
@@ -318,6 +357,83 @@ __device__ __forceinline__ void fold_col9(V* buf, const int* s, const int* rem, 
       if (r & 1) { buf[r * M + s[c]] = cmul(y, wo); wo = cmul(wo, w2); }
       else { buf[r * M + s[c]] = cmul(y, we); we = cmul(we, w2); }
     }
+  }
+}
+
+// fold_col9 for the real-pair input (a.rp): x[t m + s] = (re[t m + s], im[t m + s]) from
+// the two real rows at the stage start; every compute thread joins the barrier that
+// separates the loads (columns of other threads) from the in-place residue stores.
+template <int P>
+__device__ __forceinline__ void fold9_rp(V* buf, int L, bool live, bool im_ok, int im_slot, const V* twcol,
+                                         int tid, int nth) {
+  constexpr int NC = 2;
+  const bool act = tid < M / 2;
+  const int s[NC] = {tid, tid + M / 2};
+  V x[NC][9];
+  const double* re = reinterpret_cast<const double*>(buf);
+  const double* im = re + im_slot;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const bool ok = act && live && t < P && t * M + s[c] < L;
+      x[c][t] = cmk<V>(ok ? re[t * M + s[c]] : 0.0, (ok && im_ok) ? im[t * M + s[c]] : 0.0);
+    }
+  compute_sync(nth);
+  if (!act) return;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) dft9<+1>(x[c]);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const V w1 = twcol[s[c]];
+    buf[s[c]] = x[c][0];
+    const V w2 = cmul(w1, w1);
+    V wo = w1, we = w2;
+#pragma unroll
+    for (int r = 1; r < 9; ++r) {
+      const V y = x[c][dft9_slot(r)];
+      if (r & 1) { buf[r * M + s[c]] = cmul(y, wo); wo = cmul(wo, w2); }
+      else { buf[r * M + s[c]] = cmul(y, we); we = cmul(we, w2); }
+    }
+  }
+}
+
+// unfold_col9 with the real-split output (a.rs): Re of h[t m + s] -> double t m + s of
+// the stage, Im -> double T9SLOTS + t m + s, after a barrier (the doubles overlap
+// other columns' residues)
+__device__ __forceinline__ void unfold9_rs(V* buf, int T, const V* twcol, int tid, int nth) {
+  constexpr int NC = 2;
+  const bool act = tid < M / 2;
+  const int s[NC] = {tid, tid + M / 2};
+  V x[NC][9];
+  if (act) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const V w1 = twcol[s[c]];
+      x[c][0] = buf[s[c]];
+      const V w2 = cmul(w1, w1);
+      V wo = w1, we = w2;
+#pragma unroll
+      for (int r = 1; r < 9; ++r) {
+        if (r & 1) { x[c][r] = cmulc(buf[r * M + s[c]], wo); wo = cmul(wo, w2); }
+        else { x[c][r] = cmulc(buf[r * M + s[c]], we); we = cmul(we, w2); }
+      }
+    }
+  }
+  compute_sync(nth);
+  if (!act) return;
+  double* dre = reinterpret_cast<double*>(buf);
+  double* dim = dre + T9SLOTS;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    dft9<-1>(x[c]);
+#pragma unroll
+    for (int t = 0; t < 9; ++t)
+      if (t < T) {
+        const V v = x[c][dft9_slot(t)];
+        dre[t * M + s[c]] = v.x;
+        dim[t * M + s[c]] = v.y;
+      }
   }
 }
 
@@ -648,7 +764,12 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
     } else {
-      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twc, tid, nth);
+      if (QC == 9 && MODE == MODE_FWD && a.rp) {
+        if (a.in_f.p <= 4) fold9_rp<4>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
+        else fold9_rp<8>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
+      } else {
+        fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twc, tid, nth);
+      }
     }
     pc.mark(1);
     compute_sync(nth);
@@ -704,7 +825,8 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     if constexpr (MODE != MODE_FWD) {
       compute_sync(nth);
       pc.mark(5);
-      unfold_all<QC>(buf, q, a.out.T, zt, twc, tid, nth);
+      if (QC == 9 && MODE == MODE_INV && a.rs) unfold9_rs(buf, a.out.T, twc, tid, nth);
+      else unfold_all<QC>(buf, q, a.out.T, zt, twc, tid, nth);
     }
     pc.mark(6);
     // results are in stage slots j < out.L

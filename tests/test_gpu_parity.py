@@ -363,6 +363,22 @@ def test_real_path_matches_oracle(ctx, H, sf, sg, m):
     assert h.shape == ref.shape and oracle.rel_l2(h, ref.real) < 1e-11
 
 
+@pytest.mark.parametrize("sf,sg", [((300, 4000), (20, 300)),    # x: q = 9 -> pack / unpack fused
+                                   ((301, 4000), (31, 300)),    # odd rows: the last pair has no im row
+                                   ((40, 4096), (255, 255)),    # g taller than f's half: A < L_g
+                                   ((7, 4600), (2, 9))])        # x: p_f = 9 > 8 -> unfused fallback
+def test_real_path_fused_x_passes(ctx, H, sf, sg):
+    """hd_conv_real with the real-pair input / real-split output modes of the staged
+    q = 9 x passes (and the fix-up of the rows where two halves overlap)."""
+    torch_ = pytest.importorskip("torch")
+    rng = np.random.default_rng(820 + sf[0])
+    f = rng.uniform(-1, 1, sf)
+    g = rng.uniform(-1, 1, sg)
+    h = ctx.conv_real(torch_.from_numpy(f).cuda(), torch_.from_numpy(g).cuda()).cpu().numpy()
+    ref = oracle.conv(f.astype(complex), g.astype(complex)).real
+    assert h.shape == ref.shape and oracle.rel_l2(h, ref) < 1e-11
+
+
 def test_real_path_batched_and_c64(ctx, H):
     torch_ = pytest.importorskip("torch")
     rng = np.random.default_rng(811)
