@@ -639,3 +639,16 @@ def test_s512c_shared_g_and_window(ctx, H):
     lo, n = [1234], [5000]
     hw = host(ctx.conv_window([dev(f[0])], [dev(g)], lo, n, plan=plan))
     assert oracle.rel_l2(hw, oracle.conv(f[0], g)[1234:6234]) < 1e-11
+
+
+@pytest.mark.parametrize("sf,sg", [((300, 500), (40, 90)),     # x: q = 5 (compile-time kernels), y: q = 3
+                                   ((129, 640), (3, 1)),       # x: L_out = 640 exactly
+                                   ((1000, 77), (25, 51))])    # y: q = 9 (runtime-q kernel, 288 threads)
+def test_s128_engine_2d(ctx, H, sf, sg):
+    """The staged complex-float engine on both axes of a 2-D problem."""
+    f, g = synth.random_pair(1600 + sf[0], sf, sg, dtype=np.complex64)
+    plan = H.Plan.make(2, [{"m": 128, "C": 4, "S": 4}] * 2)
+    n0 = ctx.engine_launches(H.HD_ENGINE_S128)
+    h = host(ctx.conv(dev(f), dev(g), plan=plan))
+    assert ctx.engine_launches(H.HD_ENGINE_S128) - n0 >= 3
+    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-5
