@@ -254,9 +254,10 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     x.lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
     // the 1-D two-CTA cluster pass (hd_s512c.cuh) holds at most 11 residue rows per CTA
-    const bool cluster_1d = dt == HD_C128 && ndim == 1 && npairs == 1 && x.m == 512 && x.D == x.q &&
-                            x.q >= hd::kS512cQMin && x.q <= hd::kS512cQMax && x.lines == 1 && x.auto_engine &&
-                            !(plan->flags & HD_FLAG_GENERIC_FFT);
+    const bool cluster_q = (x.m == 512 && x.q >= hd::kS512cQMin && x.q <= hd::kS512cQMax) ||
+                           (x.m == 2048 && x.q >= hd::kS2048cQMin && x.q <= hd::kS2048cQMax);
+    const bool cluster_1d = dt == HD_C128 && ndim == 1 && npairs == 1 && cluster_q && x.D == x.q &&
+                            x.lines == 1 && x.auto_engine && !(plan->flags & HD_FLAG_GENERIC_FFT);
     if (!cluster_1d && pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
       return fail(ctx, HD_ERR_INVALID, "axis " + std::to_string(i) + ": lines*D*m too large for shared memory");
     a.p_f = x.pf; a.p_g = x.pg; a.q = x.q; a.M1 = x.M1;
@@ -555,10 +556,12 @@ bool use_s128_bg(const Launch& L) {
 // The 1-D convolution pass of long lines on two-CTA clusters (hd_s512c.cuh): m = 512,
 // complex double, all residues (D = q), 12 <= q <= 22, one pair, plain rows.
 bool use_s512c(hd_dtype_t dt, const Launch& L) {
-  if (dt != HD_C128 || L.m != 512 || L.lines != 1 || L.mode != hd::MODE_CONV || (L.flags & HD_FLAG_GENERIC_FFT))
+  if (dt != HD_C128 || (L.m != 512 && L.m != 2048) || L.lines != 1 || L.mode != hd::MODE_CONV ||
+      (L.flags & HD_FLAG_GENERIC_FFT))
     return false;
-  if (!L.auto_engine || !L.s512c_axis || L.a.D != L.a.q || L.a.q < hd::kS512cQMin || L.a.q > hd::kS512cQMax)
-    return false;
+  if (!L.auto_engine || !L.s512c_axis || L.a.D != L.a.q) return false;
+  if (L.m == 512 && (L.a.q < hd::kS512cQMin || L.a.q > hd::kS512cQMax)) return false;
+  if (L.m == 2048 && (L.a.q < hd::kS2048cQMin || L.a.q > hd::kS2048cQMax)) return false;
   const PassArgs& a = L.a;
   return a.npairs == 1 && a.nbatch == 1 && a.in_f.p <= 32 && a.in_g.p <= 32 && a.out.T <= 32 && a.in_f.tl >= 30 && a.in_f.s_j == 1 && a.in_g.tl >= 30 &&
          a.in_g.s_j == 1 && a.out.tl >= 30 && a.out.so_log2 >= 30 && a.out.s_js == 1 && a.in_f.jd <= 0 &&
@@ -574,7 +577,11 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   bool mconv = false;
   const bool s128 = use_s128(dt, L);
   const bool s512c = !staged && use_s512c(dt, L);
-  if (s512c) {
+  if (s512c && L.m == 2048) {
+    fn = hd::lookup_s2048c();
+    threads = hd::s2048c_threads(L.a.q);
+    smem = hd::s2048c_smem_bytes();
+  } else if (s512c) {
     fn = hd::lookup_s512c();
     threads = hd::s512c_threads(L.a.q);
     smem = hd::s512c_smem_bytes();

@@ -19,6 +19,11 @@ constexpr int kS512cQMin = 12, kS512cQMax = 22;
 LaunchFn lookup_s512c();
 int s512c_threads(int q);
 size_t s512c_smem_bytes();
+// the same at m = 2048 with four warps per residue (hd_s2048c.cuh), 4 <= q <= 6
+constexpr int kS2048cQMin = 4, kS2048cQMax = 6;
+LaunchFn lookup_s2048c();
+int s2048c_threads(int q);
+size_t s2048c_smem_bytes();
 size_t s512_smem_bytes(int q, int mode);
 int s512_threads(int q, int mode);
 // staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()

@@ -614,14 +614,18 @@ def test_lambda_conv_config2_shape_and_padding(ctx, H):
 # ---------------------------------------------------------------- 1-D long lines: two-CTA clusters
 # hd_s512c.cuh: m = 512, 12 <= q <= 22, residues split over a cluster of two CTAs,
 # partial unfolds exchanged through distributed shared memory.
-@pytest.mark.parametrize("B,Lf,Lg", [(4, 8192, 3000),   # config 2's pair: q = 22
-                                      (3, 6000, 200),    # q = 13 (odd: 7 / 6 residues)
-                                      (2, 6000, 145),    # L_out = 12 x 512 exactly: q = 12
-                                      (5, 300, 9000),    # the long input is g
-                                      (1, 5000, 4000)])  # p_f = 10, p_g = 8
-def test_s512c_cluster_conv1d(ctx, H, B, Lf, Lg):
-    f, g = synth.random_pair(1500 + Lf, (B, Lf), (B, Lg))
-    plan = H.Plan.make(1, [{"m": 512, "C": 1}])
+@pytest.mark.parametrize("B,Lf,Lg,m", [(4, 8192, 3000, 512),   # config 2's pair: q = 22
+                                        (3, 6000, 200, 512),    # q = 13 (odd: 7 / 6 residues)
+                                        (2, 6000, 145, 512),    # L_out = 12 x 512 exactly: q = 12
+                                        (5, 300, 9000, 512),    # the long input is g
+                                        (1, 5000, 4000, 512),   # p_f = 10, p_g = 8
+                                        (4, 8192, 3000, 2048),  # m = 2048 (four warps per residue): q = 6
+                                        (3, 9000, 500, 2048),   # q = 5 (3 / 2 residues)
+                                        (2, 6000, 200, 2048),   # q = 4 (1 / 3 residues)
+                                        (2, 300, 11000, 2048)]) # swapped roles, p_g = 6
+def test_s512c_cluster_conv1d(ctx, H, B, Lf, Lg, m):
+    f, g = synth.random_pair(1500 + Lf + m, (B, Lf), (B, Lg))
+    plan = H.Plan.make(1, [{"m": m, "C": 1}])
     n0 = ctx.engine_launches(H.HD_ENGINE_S512C)
     h = host(ctx.conv(dev(f), dev(g), plan=plan, batch=True))
     assert ctx.engine_launches(H.HD_ENGINE_S512C) - n0 == 1
