@@ -317,8 +317,6 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    ctx.profile_reset()
-    ctx.profile_enable(True)
     l0 = ctx.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -330,9 +328,20 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks.mark(1)
     launches = ctx.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    # per-pass device times for the roofline: the same K steps again with CUDA events
+    # around every launch on the launch stream (hd_profile_*).  The events cost ~20 us
+    # per step, so they stay out of the headline timing above.
+    ctx.profile_reset()
+    ctx.profile_enable(True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
     ctx.profile_enable(False)
     prof = ctx.profile_read()
-    ms = e0.elapsed_time(e1)
+    ms_profiled = e0.elapsed_time(e1)
     if dist:
         dist.barrier()
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -381,7 +390,8 @@ def run_ours(args, rank, world, local_rank):
     whole = {"alg_bytes_per_step": total_ab,
              "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,
              "frac_of_hbm": total_ab / (ms * 1e-3 / args.steps) / 1e9 / peak,
-             "per_kernel_ms": {k: v[0] / v[1] for k, v in prof.items()}}
+             "per_kernel_ms": {k: v[0] / v[1] for k, v in prof.items()},
+             "profiled_ms_per_step": ms_profiled / args.steps}
 
     # end to end through the host-buffer C-ABI entry point (copies inside)
     e2e = None
