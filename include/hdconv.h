@@ -180,7 +180,11 @@ hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t
  * complex pipeline, hd_conv1d/2d/3d's kernels) holds both half convolutions, and
  * h[y] = Re w[y] + Im w[y - A] (overlap-add of the two halves).  About half the
  * transform work and half the input/output bytes of the complex path.  `plan`
- * is for the packed problem (extents A, L_f,1.. and L_g); NULL = cached/default. */
+ * is for the packed problem (extents A, L_f,1.. and L_g); NULL = cached/default.
+ * 2-D HD_C128 with batch 1, even row lengths and the x axis on the staged q = 9
+ * kernel: the pack and the unpack run inside the first and last passes (no z or
+ * w array; a fix-up kernel adds the L_g,0 - 1 overlapping rows).  Results are the
+ * same either way; the context's real-path buffers are reused across calls. */
 hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch,
                          const void* f, const int64_t* Lf, const void* g, const int64_t* Lg,
                          void* h, const hd_plan_t* plan, void* stream);
@@ -336,7 +340,8 @@ int64_t     hd_launch_count(hd_ctx_t ctx);
 #define HD_ENGINE_S512 1        /* staged warp engine, m = 512 complex double (C = 1) */
 #define HD_ENGINE_S512_MCONV 2  /* its multi-pair convolution pass */
 #define HD_ENGINE_S128 3        /* staged engine, m = 128 complex float (C = 4) */
-#define HD_ENGINE_S512C 4       /* 1-D pass of long lines, m = 512 complex double, two-CTA clusters */
+#define HD_ENGINE_S512C 4       /* 1-D pass of long lines on two-CTA clusters, complex double,
+                                   m = 512 (12 <= q <= 22) or m = 2048 (4 <= q <= 6) */
 int64_t     hd_engine_launches(hd_ctx_t ctx, int32_t engine);
 
 #ifdef __cplusplus
