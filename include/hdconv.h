@@ -71,6 +71,12 @@ typedef enum {
 #define HD_FLAG_SHARED_G    0x2u   /* batch > 1: one g shared by every batch entry */
 #define HD_FLAG_GENERIC_FFT 0x4u   /* force the generic radix-8 shared-memory FFT engine
                                       (default: the warp-level engine where it applies) */
+#define HD_FLAG_GRAPH       0x8u   /* hd_conv1d/2d/3d, hd_multiconv, hd_conv_window: the first
+                                      call also captures its kernel launches into a CUDA graph;
+                                      later calls with identical arguments (pointers, extents,
+                                      plan, window, stream) replay it with one graph launch.
+                                      Dropped when the context reallocates its workspace or is
+                                      destroyed.  Not with profiling enabled. */
 
 /* Per-axis parameters (L, M, C, m, D per dimension).
  *  m  : FFT size, a power of two in [2, 4096]
@@ -343,6 +349,9 @@ int64_t     hd_launch_count(hd_ctx_t ctx);
 #define HD_ENGINE_S512C 4       /* 1-D pass of long lines on two-CTA clusters, complex double,
                                    m = 512 (12 <= q <= 22) or m = 2048 (4 <= q <= 6) */
 int64_t     hd_engine_launches(hd_ctx_t ctx, int32_t engine);
+/* Calls served by replaying a captured CUDA graph (HD_FLAG_GRAPH) since creation;
+ * -1 for a null context.  Replays do not add to hd_launch_count. */
+int64_t     hd_graph_replays(hd_ctx_t ctx);
 
 #ifdef __cplusplus
 }

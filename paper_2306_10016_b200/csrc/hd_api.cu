@@ -60,6 +60,11 @@ struct hd_ctx {
   std::vector<ProfEntry> prof;
   int64_t launches = 0;
   int64_t engine_launches[5] = {0, 0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
+  // HD_FLAG_GRAPH: captured pass sequences keyed by their full argument list
+  std::map<std::string, cudaGraphExec_t> graphs;
+  cudaStream_t capture_stream = nullptr;
+  bool capturing = false;
+  int64_t graph_replays = 0;
 };
 
 namespace {
@@ -663,8 +668,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
       fprintf(stderr, " %d:%.0f/%.0f", w, h[8 + 2 * w] / (double)total, h[9 + 2 * w] / (double)total);
     fprintf(stderr, "\n");
   }
-  ctx->launches += 1;
-  ctx->engine_launches[s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128 : mconv ? HD_ENGINE_S512_MCONV
+  if (!ctx->capturing) ctx->launches += 1;
+  if (!ctx->capturing) ctx->engine_launches[s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128 : mconv ? HD_ENGINE_S512_MCONV
                        : staged ? HD_ENGINE_S512 : HD_ENGINE_GENERIC] += 1;
   if (ctx->profiling) {
     cudaEventRecord(e1, st);
@@ -820,6 +825,8 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
   if (need > 0) {
     if (!ws) {
       if (ctx->ws_size < need) {
+        for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);  // they address the old workspace
+        ctx->graphs.clear();
         if (ctx->ws) cudaFree(ctx->ws);
         ctx->ws = nullptr; ctx->ws_size = 0;
         cudaError_t e = cudaMalloc(&ctx->ws, need);
@@ -1116,6 +1123,8 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
   for (auto& kv : ctx->tw32) cudaFree(kv.second);
   for (auto& kv : ctx->st64) cudaFree(kv.second);
   for (auto& kv : ctx->perm) cudaFree(kv.second);
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
   for (auto& kv : ctx->st32) cudaFree(kv.second);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
@@ -1197,7 +1206,49 @@ static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64
   if (rf) P.rf = *rf;
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
-  return run_pipeline(ctx, P, ws, ws_bytes, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(P.plan.flags & HD_FLAG_GRAPH) || rf || ctx->profiling) return run_pipeline(ctx, P, ws, ws_bytes, st);
+  // HD_FLAG_GRAPH: replay the captured launches of an identical earlier call
+  std::string key = problem_key(dt, ndim, N, batch, Lf, Lg, M, P.plan.flags);
+  char buf[64];
+  auto add = [&](const void* p) { snprintf(buf, sizeof(buf), "|%p", p); key += buf; };
+  for (int k = 0; k < N; ++k) { add(P.f[k]); add(P.g[k]); }
+  add(h); add(ws); add(stream);
+  key += "|" + std::to_string(ws_bytes);
+  for (int i = 0; i < ndim; ++i) {
+    const AxisInfo& x = P.ax[i];
+    key += "|" + std::to_string(x.m) + "," + std::to_string(x.lines) + "," + std::to_string(x.S) + "," +
+           std::to_string(x.D) + "," + std::to_string(x.threads) + "," + std::to_string(x.auto_engine) + "," +
+           std::to_string(x.o0) + "," + std::to_string(x.O);
+  }
+  auto it = ctx->graphs.find(key);
+  if (it != ctx->graphs.end()) {
+    cudaError_t e = cudaGraphLaunch(it->second, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphLaunch");
+    ctx->graph_replays += 1;
+    return HD_OK;
+  }
+  s = run_pipeline(ctx, P, ws, ws_bytes, st);  // this call's result
+  if (s != HD_OK) return s;
+  if (!ctx->capture_stream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamCreate(capture)");
+  }
+  cudaError_t e = cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamBeginCapture");
+  ctx->capturing = true;
+  hd_status_t sc = run_pipeline(ctx, P, ws, ws_bytes, ctx->capture_stream);
+  ctx->capturing = false;
+  cudaGraph_t gr = nullptr;
+  e = cudaStreamEndCapture(ctx->capture_stream, &gr);
+  if (sc != HD_OK) { if (gr) cudaGraphDestroy(gr); return sc; }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiate(&ex, gr, 0);
+  cudaGraphDestroy(gr);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+  ctx->graphs[key] = ex;
+  return HD_OK;
 }
 
 hd_status_t hd_conv_window(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, int64_t batch,
@@ -1706,6 +1757,8 @@ hd_status_t hd_profile_reset(hd_ctx_t ctx) {
 }
 
 int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
+int64_t hd_graph_replays(hd_ctx_t ctx) { return ctx ? ctx->graph_replays : -1; }
 
 int64_t hd_engine_launches(hd_ctx_t ctx, int32_t engine) {
   if (!ctx || engine < 0 || engine > HD_ENGINE_S512C) return -1;

@@ -24,6 +24,7 @@ HD_OK, HD_ERR_INVALID, HD_ERR_UNSUPPORTED, HD_ERR_CUDA, HD_ERR_NCCL, HD_ERR_WORK
 HD_FLAG_ALLOW_ALIAS = 0x1
 HD_FLAG_SHARED_G = 0x2
 HD_FLAG_GENERIC_FFT = 0x4
+HD_FLAG_GRAPH = 0x8
 HD_ENGINE_GENERIC, HD_ENGINE_S512, HD_ENGINE_S512_MCONV, HD_ENGINE_S128, HD_ENGINE_S512C = 0, 1, 2, 3, 4
 HD_TUNE_PER_AXIS = 0x0
 HD_TUNE_EXHAUSTIVE = 0x1
@@ -40,7 +41,7 @@ EXPORTED = [
     "hd_conv_real",
     "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_ex", "hd_tune_log",
-    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_pass", "hd_conv1d_lambda",
+    "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_graph_replays", "hd_pass", "hd_conv1d_lambda",
 ]
 HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
 
@@ -153,6 +154,7 @@ def _load():
         "hd_profile_reset": ([P], ctypes.c_int),
         "hd_launch_count": ([P], I64),
         "hd_engine_launches": ([P, I32], I64),
+        "hd_graph_replays": ([P], I64),
         "hd_conv1d_lambda": ([P, ctypes.c_int, I64, P, I64, P, I64, P, I64, I32, I32, P], ctypes.c_int),
         "hd_pass": ([P, ctypes.c_int, ctypes.POINTER(PassDesc), P], ctypes.c_int),
     }
@@ -602,6 +604,10 @@ class Context:
 
     def launch_count(self):
         return int(_lib.hd_launch_count(self.h))
+
+    def graph_replays(self):
+        """Calls served by a captured CUDA graph (HD_FLAG_GRAPH)."""
+        return int(_lib.hd_graph_replays(self.h))
 
     def engine_launches(self, engine):
         """Pass launches on one engine (HD_ENGINE_*) since the context was created."""

@@ -656,3 +656,26 @@ def test_s128_engine_2d(ctx, H, sf, sg):
     h = host(ctx.conv(dev(f), dev(g), plan=plan))
     assert ctx.engine_launches(H.HD_ENGINE_S128) - n0 >= 3
     assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-5
+
+
+# ---------------------------------------------------------------- HD_FLAG_GRAPH (CUDA-graph replay)
+@pytest.mark.parametrize("sf,sg,axes", [((64,), (40,), [{"m": 32}]),
+                                        ((300, 700), (40, 50), [{"m": 512, "C": 1, "S": 2}] * 2),
+                                        ((20, 30, 40), (5, 6, 7), [{"m": 16, "C": 2, "S": 2}] * 3)])
+def test_graph_replay_matches_and_tracks_inputs(ctx, H, sf, sg, axes):
+    """The second identical call replays the graph captured on the first; the graph
+    reads the buffers at replay time (new contents, same pointers -> new result)."""
+    f, g = synth.random_pair(1700 + len(sf), sf, sg)
+    plan = H.Plan.make(len(sf), axes, flags=H.HD_FLAG_GRAPH)
+    fd, gd = dev(f), dev(g)
+    h = ctx.conv(fd, gd, plan=plan)
+    r0 = ctx.graph_replays()
+    ctx.conv(fd, gd, plan=plan, h=h)
+    assert ctx.graph_replays() == r0 + 1
+    assert oracle.rel_l2(host(h), oracle.conv(f, g)) < 1e-11
+    f2, g2 = synth.random_pair(1710 + len(sf), sf, sg)
+    fd.copy_(torch.from_numpy(f2).cuda())
+    gd.copy_(torch.from_numpy(g2).cuda())
+    ctx.conv(fd, gd, plan=plan, h=h)
+    assert ctx.graph_replays() == r0 + 2
+    assert oracle.rel_l2(host(h), oracle.conv(f2, g2)) < 1e-11
