@@ -679,3 +679,25 @@ def test_graph_replay_matches_and_tracks_inputs(ctx, H, sf, sg, axes):
     ctx.conv(fd, gd, plan=plan, h=h)
     assert ctx.graph_replays() == r0 + 2
     assert oracle.rel_l2(host(h), oracle.conv(f2, g2)) < 1e-11
+
+
+def test_graph_dropped_when_workspace_grows(H):
+    """A larger problem reallocates the context workspace: the captured graphs (which
+    address the old workspace) are dropped and the next identical call re-captures."""
+    c = H.Context(0)
+    try:
+        f, g = synth.random_pair(1720, (40, 50), (9, 7))
+        plan = H.Plan.make(2, [{"m": 32, "C": 2, "S": 2}] * 2, flags=H.HD_FLAG_GRAPH)
+        fd, gd = dev(f), dev(g)
+        h = c.conv(fd, gd, plan=plan)
+        c.conv(fd, gd, plan=plan, h=h)
+        assert c.graph_replays() == 1
+        F, G = synth.random_pair(1721, (600, 700), (50, 40))
+        c.conv(dev(F), dev(G))                      # grows the workspace
+        c.conv(fd, gd, plan=plan, h=h)              # re-captured, not replayed
+        assert c.graph_replays() == 1
+        c.conv(fd, gd, plan=plan, h=h)
+        assert c.graph_replays() == 2
+        assert oracle.rel_l2(host(h), oracle.conv(f, g)) < 1e-11
+    finally:
+        c.close()
