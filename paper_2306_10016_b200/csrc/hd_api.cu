@@ -503,6 +503,10 @@ void prepare_tma(Launch& L, bool c64 = false) {
     }
   }
   if (!tma_desc_out(a.out, a.nlines, a.nbatch, narr_out, a.tm_out, a.tm_out_map, c64)) a.tm_out.kind = hd::TMA_NONE;
+  if (a.fam2) {  // the second line family of a merged forward launch (see PassArgs fam2)
+    if (!tma_desc_in(a.in_g, a.nlines2, 1, 1, a.tm_in_g, a.tm_in_g_map)) a.tm_in_g.kind = hd::TMA_NONE;
+    if (!tma_desc_out(a.out2, a.nlines2, 1, 1, a.tm_out2, &a.tm_out_map[1])) a.tm_out2.kind = hd::TMA_NONE;
+  }
   // a window start that is not tile-aligned cannot be expressed by element-tiled boxes
   // (the m = 128 engine stores every window by plain stores)
   if (a.out.j0 != 0 && (c64 || a.tm_out.kind == hd::TMA_ELEM_TILED)) a.tm_out.kind = hd::TMA_NONE;
@@ -582,6 +586,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   bool mconv = false;
   const bool s128 = use_s128(dt, L);
   const bool s512c = !staged && use_s512c(dt, L);
+  if (L.a.fam2 && (!staged || s128 || s512c)) return HD_ERR_UNSUPPORTED;
   if (s512c && L.m == 2048) {
     fn = hd::lookup_s2048c();
     threads = hd::s2048c_threads(L.a.q);
@@ -616,7 +621,13 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     threads = hd::s512_threads(L.a.q, L.mode);
     smem = hd::s512_smem_bytes(L.a.q, L.mode);
     prepare_tma(L);
+    if (L.a.fam2 && !(L.mode == hd::MODE_FWD && L.a.q == 9 && L.narrays == 1 && L.a.nbatch == 1 &&
+                      L.a.tm_in.kind == hd::TMA_BULK && L.a.tm_in_g.kind == hd::TMA_BULK &&
+                      L.a.tm_out.kind != hd::TMA_NONE && L.a.tm_out2.kind != hd::TMA_NONE && L.a.out.j0 == 0 &&
+                      L.a.out2.j0 == 0))
+      return HD_ERR_UNSUPPORTED;  // silently: the caller falls back to one launch per family
   } else {
+    if (L.a.fam2) return HD_ERR_UNSUPPORTED;
     fn = hd::lookup_launcher(dbl, L.m, L.mode, L.threads);
     smem = pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf);
   }
@@ -870,7 +881,28 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     char** Xg = &reg[N];
     char* Y = reg[2 * N];
     // pass A: forward along x for the rows of every f_k, then every g_k -> X[kx/Sy][y][kx%Sy]
-    for (int which = 0; which < 2; ++which) {
+    // (one pair, one batch entry, staged q = 9 x axis: both families in one launch,
+    // so the g rows fill the f rows' last wave instead of a launch of their own)
+    bool merged = false;
+    if (P.s512[1] && x.q == 9 && x.lines == 1 && N == 1 && B == 1 && Bg == 1 && !P.rf.on) {
+      Launch L = make_launch(ctx, P, hd::MODE_FWD, "fwd_x", 1, twm[1], twM1[1], twst[1]);
+      L.a.in_f.ptr[0] = P.f[0]; L.a.out.ptr[0] = Xf[0];
+      L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; in_rows(L.a.in_f, x.Lf);
+      L.a.out.s_b = Kxp * y.Lf; out_elem_tiled(L.a.out, Sy, Sy, y.Lf * Sy);
+      L.a.out.L = Kx;
+      L.a.nlines = y.Lf; L.a.nbatch = 1;
+      L.ngroups = y.Lf; L.nbatch = 1; L.narrays = 1;
+      L.a.fam2 = 1;
+      L.a.in_g.ptr[0] = P.g[0]; L.a.in_g.L = x.Lg; L.a.in_g.p = x.pg; in_rows(L.a.in_g, x.Lg);
+      init_out(L.a.out2);
+      L.a.out2.ptr[0] = Xg[0]; L.a.out2.s_b = Kxp * y.Lg; out_elem_tiled(L.a.out2, Sy, Sy, y.Lg * Sy);
+      L.a.out2.L = Kx;
+      L.a.nlines2 = y.Lg;
+      hd_status_t s = launch(ctx, P.dt, L, st);
+      if (s == HD_OK) merged = true;
+      else if (s != HD_ERR_UNSUPPORTED) return s;
+    }
+    for (int which = 0; which < 2 && !merged; ++which) {
       const int64_t rows = which == 0 ? y.Lf : y.Lg;
       const int64_t len = which == 0 ? x.Lf : x.Lg;
       const int64_t nb = which == 0 ? B : Bg;

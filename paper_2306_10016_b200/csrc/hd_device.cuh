@@ -316,6 +316,14 @@ struct PassArgs {
   //   Im -> row y + rs_A of the same array when y >= rs_side_rows (rows >= rs_rows
   //   dropped), else row y of rs_side (added by a fix-up kernel afterwards).
   int32_t rp, rs;
+  // fam2 (forward, q = 9): a second family of plain-row lines after the first (the
+  // 2-D g rows in the same launch as the f rows): items >= nbatch * ngroups are lines
+  // of in_g (nlines2 of them, one batch entry), stored through out2 / tm_out2 /
+  // tm_out_map[1]; both families move by bulk loads and element-tiled TMA stores
+  int32_t fam2, pad_f2;
+  int64_t nlines2;
+  LineOut out2;
+  TmaLine tm_out2;
   int64_t rp_off, rp_rows;
   int64_t rs_A, rs_side_rows, rs_rows;
   void* rs_side;

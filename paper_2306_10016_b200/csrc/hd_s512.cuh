@@ -194,18 +194,16 @@ __device__ __forceinline__ void issue_loads_cp(const PassArgs& a, int k_arr, int
 // Stores of the output positions [p0, p1) (stage slots p + out.j0: the output
 // window) as one bulk-async group.  Tensor boxes start at 8-aligned slots (128-byte
 // shared-memory alignment); positions before the window are clipped by TMA.
-__device__ __forceinline__ void issue_stores_range(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf,
-                                                   int p0, int p1) {
-  const LineOut& o = a.out;
+__device__ __forceinline__ void issue_stores_range_o(const LineOut& o, const TmaLine& tmo, const CUtensorMap* map,
+                                                     int kk, int64_t b, int64_t g, const V* buf, int p0, int p1) {
   const int L = (int)o.L;
   const int j0 = (int)o.j0;
   p1 = p1 < L ? p1 : L;
   if (p0 < p1) {
-    if (a.tm_out.kind == TMA_BULK) {
+    if (tmo.kind == TMA_BULK) {
       V* y = reinterpret_cast<V*>(o.ptr[kk]) + boff(b, o.nbi, o.s_bo, o.s_b) + line_off(o, g);
       bulk_store(y + p0, buf + j0 + p0, (uint32_t)(p1 - p0) * 16u);
     } else {
-      const CUtensorMap* map = &a.tm_out_map[kk];
       // boxes start at 8-aligned slots: positions p0 - sh + 256 k (the first group's
       // head before the first aligned slot goes by plain stores; later groups rewrite
       // sh positions of the group before with the same values).  Element-tiled lines with a window
@@ -220,12 +218,16 @@ __device__ __forceinline__ void issue_stores_range(const PassArgs& a, int kk, in
       }
       int c[5];
       for (; pb < p1; pb += kBox) {
-        tma_coords(a.tm_out, b, g, pb, c);
+        tma_coords(tmo, b, g, pb, c);
         tma_store(map, c, buf + j0 + pb);
       }
     }
   }
   bulk_commit();
+}
+__device__ __forceinline__ void issue_stores_range(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf,
+                                                   int p0, int p1) {
+  issue_stores_range_o(a.out, a.tm_out, &a.tm_out_map[kk], kk, b, g, buf, p0, p1);
 }
 
 __device__ __forceinline__ void issue_stores_tma(const PassArgs& a, int kk, int64_t b, int64_t g, const V* buf) {
@@ -248,6 +250,21 @@ __device__ __forceinline__ void bulk_wait_read_n(int n) {
 // overlap its slots have been read out of shared memory.
 constexpr int kGroups = 4;
 constexpr int T9SLOTS = 9 * M;  // real split: the Im array starts at double 9 m of the stage
+// second-family (a.fam2) item: the stores of line gs of out2, the bulk load of line
+// gl of in_g (whole, after every store group has been read)
+__device__ __forceinline__ void handover_fam2(const PassArgs& a, bool store, int st_fam, int64_t gs, bool load,
+                                              int ld_fam, int64_t gl, V* buf, uint64_t* bar) {
+  if (store) {
+    if (st_fam == 2) issue_stores_range_o(a.out2, a.tm_out2, &a.tm_out_map[1], 1, 0, gs, buf, 0, 1 << 30);
+    else issue_stores_range(a, 0, 0, gs, buf, 0, 1 << 30);
+  }
+  if (!load) return;
+  const LineIn& in = ld_fam == 2 ? a.in_g : a.in_f;
+  mbar_expect_tx(bar, (uint32_t)in.L * 16u);
+  if (store) bulk_wait_read_n(0);
+  bulk_load(buf, reinterpret_cast<const V*>(in.ptr[0]) + line_off(in, gl), (uint32_t)in.L * 16u, bar);
+}
+
 template <int MODE>
 __device__ __forceinline__ void handover(const PassArgs& a, int k_arr, int kk_out, bool store, int64_t bs,
                                          int64_t gs, bool load, int64_t bl, int64_t gl, V* buf, uint64_t* bar) {
@@ -683,12 +700,31 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t total = a.nbatch * a.ngroups;
+  const int64_t total1 = a.nbatch * a.ngroups;
+  const bool fam2 = QC == 9 && MODE == MODE_FWD && a.fam2;
+  const int64_t total = total1 + (fam2 ? a.nlines2 : 0);
   const int kk_out = MODE == MODE_FWD ? k_arr : 0;
 
   // ------------------------------------------------------------ producer warp
   if (tid >= nth) {
     if (!tma || tid != nth) return;
+    if (fam2) {  // two line families, plain rows (one batch entry each)
+      int64_t wl = blockIdx.x;
+      for (int s2 = 0; s2 < 2 && wl < total; ++s2, wl += gridDim.x)
+        handover_fam2(a, false, 1, 0, true, wl < total1 ? 1 : 2, wl < total1 ? wl : wl - total1,
+                      stage0 + s2 * SB, &full[s2]);
+      int it = 0;
+      for (int64_t w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+        const int st = it & 1;
+        mbar_wait(&done[st], (uint32_t)(it >> 1) & 1u);
+        const bool load = wl < total;
+        handover_fam2(a, true, w < total1 ? 1 : 2, w < total1 ? w : w - total1, load, wl < total1 ? 1 : 2,
+                      wl < total1 ? wl : wl - total1, stage0 + st * SB, &full[st]);
+        if (load) wl += gridDim.x;
+      }
+      bulk_wait0();
+      return;
+    }
     int64_t wl = blockIdx.x;  // next item to load
     for (int s2 = 0; s2 < 2 && wl < total; ++s2, wl += gridDim.x) {
       int64_t g, b;
@@ -738,8 +774,10 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     V* buf = stage0 + st * SB;
     V* gbuf = buf + q * M;
     int64_t g, b;
-    split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
-    const bool live = g < a.nlines;
+    const bool in2 = fam2 && w >= total1;  // an item of the second family
+    if (fam2) { b = 0; g = in2 ? w - total1 : w; }
+    else split_item(w, a.nbatch, a.ngroups, a.batch_fastest, b, g);
+    const bool live = g < (in2 ? a.nlines2 : a.nlines);
     V* Fr = buf + r * M;  // this warp's residue row (also its FFT exchange area)
     pc.mark(7);
     // CONV, q = 9, TMA: the fold of item it + 1 is done by the light warps during
@@ -768,7 +806,8 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
         if (a.in_f.p <= 4) fold9_rp<4>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
         else fold9_rp<8>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
       } else {
-        fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twc, tid, nth);
+        const LineIn& fin = in2 ? a.in_g : a.in_f;
+        fold_all<QC>(buf, fin.p, (int)fin.L, live, q, zt, twm, twc, tid, nth);
       }
     }
     pc.mark(1);

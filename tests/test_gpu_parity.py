@@ -701,3 +701,18 @@ def test_graph_dropped_when_workspace_grows(H):
         assert oracle.rel_l2(host(h), oracle.conv(f, g)) < 1e-11
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("sf,sg", [((40, 4000), (9, 300)),      # x: q = 9 -> f and g rows in one launch
+                                   ((3, 4096), (255, 255)),     # more g rows than f rows
+                                   ((257, 4096), (1, 255))])    # one g row
+def test_merged_forward_launch(ctx, H, sf, sg):
+    """2-D, one pair, x on the staged q = 9 kernel: the f rows and the g rows go
+    through one forward launch (PassArgs fam2); three launches per convolution."""
+    f, g = synth.random_pair(1800 + sf[0], sf, sg)
+    plan = H.Plan.make(2, [{"m": 512, "C": 1, "S": 2}] * 2)
+    n0 = ctx.launch_count()
+    h = host(ctx.conv(dev(f), dev(g), plan=plan))
+    assert ctx.launch_count() - n0 == 3
+    idx = synth.sample_indices(h.shape, n_random=400)
+    assert oracle.rel_l2(h[tuple(idx.T)], oracle.conv_sampled(f, g, idx)) < 1e-11
