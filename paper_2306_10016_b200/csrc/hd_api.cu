@@ -884,7 +884,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     // (one pair, one batch entry, staged q = 9 x axis: both families in one launch,
     // so the g rows fill the f rows' last wave instead of a launch of their own)
     bool merged = false;
-    if (P.s512[1] && x.q == 9 && x.lines == 1 && N == 1 && B == 1 && Bg == 1 && !P.rf.on) {
+    if (P.s512[1] && x.q == 9 && x.lines == 1 && N == 1 && B == 1 && Bg == 1) {
       Launch L = make_launch(ctx, P, hd::MODE_FWD, "fwd_x", 1, twm[1], twM1[1], twst[1]);
       L.a.in_f.ptr[0] = P.f[0]; L.a.out.ptr[0] = Xf[0];
       L.a.in_f.L = x.Lf; L.a.in_f.p = x.pf; in_rows(L.a.in_f, x.Lf);
@@ -898,6 +898,12 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
       L.a.out2.ptr[0] = Xg[0]; L.a.out2.s_b = Kxp * y.Lg; out_elem_tiled(L.a.out2, Sy, Sy, y.Lg * Sy);
       L.a.out2.L = Kx;
       L.a.nlines2 = y.Lg;
+      if (P.rf.on) {  // the f rows as real row pairs (hd_conv_real, fused pack)
+        L.a.rp = 1;
+        L.a.in_f.ptr[0] = P.rf.f;
+        L.a.rp_off = P.rf.A * x.Lf;
+        L.a.rp_rows = P.rf.Lf0 - P.rf.A;
+      }
       hd_status_t s = launch(ctx, P.dt, L, st);
       if (s == HD_OK) merged = true;
       else if (s != HD_ERR_UNSUPPORTED) return s;

@@ -259,7 +259,13 @@ __device__ __forceinline__ void handover_fam2(const PassArgs& a, bool store, int
     else issue_stores_range(a, 0, 0, gs, buf, 0, 1 << 30);
   }
   if (!load) return;
-  const LineIn& in = ld_fam == 2 ? a.in_g : a.in_f;
+  if (ld_fam == 1) {  // the first family as in any forward pass (plain rows or real pairs)
+    issue_loads_arm<MODE_FWD>(a, gl, bar);
+    if (store) bulk_wait_read_n(0);
+    issue_loads_range<MODE_FWD>(a, 0, 0, gl, buf, bar, 0, 1 << 30);
+    return;
+  }
+  const LineIn& in = a.in_g;
   mbar_expect_tx(bar, (uint32_t)in.L * 16u);
   if (store) bulk_wait_read_n(0);
   bulk_load(buf, reinterpret_cast<const V*>(in.ptr[0]) + line_off(in, gl), (uint32_t)in.L * 16u, bar);
@@ -802,7 +808,7 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
     } else {
-      if (QC == 9 && MODE == MODE_FWD && a.rp) {
+      if (QC == 9 && MODE == MODE_FWD && a.rp && !in2) {
         if (a.in_f.p <= 4) fold9_rp<4>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
         else fold9_rp<8>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
       } else {
