@@ -38,6 +38,8 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
 template <int MODE>
 static LaunchFn pick_s512(int q) {
   if (q == 9) return launch_s512_impl<MODE, 320, 9>;
+  if (q == 7) return launch_s512_impl<MODE, 256, 7>;  // BASELINE config 5's x axis
+  if (q == 5) return launch_s512_impl<MODE, 192, 5, 1>;  // the real path's packed y axis (lean)
   if (q <= kS512LeanQ) return launch_s512_impl<MODE, 32 * (kS512LeanQ + 1), 0, 1>;
   return launch_s512_impl<MODE, 32 * (s512::kQMax + 1), 0>;
 }
