@@ -613,7 +613,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   if (s128 || s512c) {
     // set above
   } else if (mconv) {
-    fn = hd::lookup_s512_mconv();
+    fn = hd::lookup_s512_mconv(L.a.q);
     threads = 32 * (L.a.q + 1);
     smem = hd::s512_smem_bytes(L.a.q, hd::MODE_MCONV);
   } else if (staged) {

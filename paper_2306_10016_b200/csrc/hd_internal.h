@@ -27,7 +27,7 @@ size_t s2048c_smem_bytes();
 size_t s512_smem_bytes(int q, int mode);
 int s512_threads(int q, int mode);
 // staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()
-LaunchFn lookup_s512_mconv();
+LaunchFn lookup_s512_mconv(int q);
 int s512_mconv_qmax();
 // staged engine for m = 128 complex float, 4 lines per item (hd_s128.cuh);
 // blockDim = 32 (q + 1), q <= kS128QMax

@@ -52,9 +52,10 @@ LaunchFn lookup_s512(int mode, int q) {
   }
 }
 
+template <int QC>
 static cudaError_t launch_s512_mconv(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   constexpr int NT = 32 * (s512::kMconvQMax + 1);
-  auto kern = s512::s512_mconv_kernel<NT>;
+  auto kern = s512::s512_mconv_kernel<NT, QC>;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -73,7 +74,8 @@ static cudaError_t launch_s512_mconv(const PassArgs& a, dim3 grid, int nt, size_
   return cudaGetLastError();
 }
 
-LaunchFn lookup_s512_mconv() { return launch_s512_mconv; }
+// q = 6 (BASELINE config 5's convolution axis) at compile time; other q at run time
+LaunchFn lookup_s512_mconv(int q) { return q == 6 ? launch_s512_mconv<6> : launch_s512_mconv<0>; }
 int s512_mconv_qmax() { return s512::kMconvQMax; }
 
 // compute warps + the producer warp

@@ -923,7 +923,7 @@ __device__ __forceinline__ void issue_loads_pair(const PassArgs& a, int64_t b, i
   }
 }
 
-template <int NTMAX>
+template <int NTMAX, int QC = 0>
 __global__ void __launch_bounds__(NTMAX, 1) s512_mconv_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -932,7 +932,7 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_mconv_kernel(const __grid_const
   V* twtab = zt + kQF * kQF;
   V* twcol = twtab + w512::kTwRows * 32;
   V* stage0 = twcol + M;
-  const int q = a.q, N = a.npairs;
+  const int q = QC > 0 ? QC : a.q, N = a.npairs;
   const int tid = threadIdx.x, lane = tid & 31, r = tid >> 5;
   const int nth = 32 * q;
   const int SB = 2 * q * M;
@@ -1001,8 +1001,8 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_mconv_kernel(const __grid_const
       V* Fr = buf + r * M;
       V* Gr = buf + (q + r) * M;
       mbar_wait(&full[st], (uint32_t)(sg >> 1) & 1u);
-      fold_all<0>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twcol, tid, nth);
-      fold_all<0>(buf + q * M, a.in_g.p, (int)a.in_g.L, live, q, zt, twm, twcol, tid, nth);
+      fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twcol, tid, nth);
+      fold_all<QC>(buf + q * M, a.in_g.p, (int)a.in_g.L, live, q, zt, twm, twcol, tid, nth);
       compute_sync(nth);
       V v[16];
 #pragma unroll
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_mconv_kernel(const __grid_const
 #pragma unroll
       for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = acc[i];
       compute_sync(nth);
-      unfold_all<0>(buf, q, a.out.T, zt, twcol, tid, nth);
+      unfold_all<QC>(buf, q, a.out.T, zt, twcol, tid, nth);
       fence_async_smem();
       mbar_arrive(&done[st]);
     }
