@@ -76,7 +76,8 @@ typedef enum {
                                       later calls with identical arguments (pointers, extents,
                                       plan, window, stream) replay it with one graph launch.
                                       Dropped when the context reallocates its workspace or is
-                                      destroyed.  Not with profiling enabled. */
+                                      destroyed; at most 64 are kept (the cache then starts
+                                      over).  Not with profiling enabled. */
 
 /* Per-axis parameters (L, M, C, m, D per dimension).
  *  m  : FFT size, a power of two in [2, 4096]

@@ -1285,6 +1285,10 @@ static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64
   e = cudaGraphInstantiate(&ex, gr, 0);
   cudaGraphDestroy(gr);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+  if (ctx->graphs.size() >= 64) {  // bounded cache: start over rather than grow without limit
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    ctx->graphs.clear();
+  }
   ctx->graphs[key] = ex;
   return HD_OK;
 }
