@@ -144,7 +144,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) s512c_kernel(
   const int T = a.out.T;
   const int T0 = (T + 1) / 2;                               // CTA 0 owns blocks t < T0
   const int tlo = c == 0 ? 0 : T0, thi = c == 0 ? T0 : T;
-  const int r_w = w < nres ? sp.residue_of_row(c, w) : 0;
   const V* tw = twtab + lane;
   const LineIn &fi = a.in_f, &gi = a.in_g;
   const LineOut& o = a.out;
