@@ -78,6 +78,13 @@ typedef enum {
                                       Dropped when the context reallocates its workspace or is
                                       destroyed; at most 64 are kept (the cache then starts
                                       over).  Not with profiling enabled. */
+#define HD_FLAG_STAGED_ORDER 0x10u /* hd_pass only: the forward / inverse passes may run on the
+                                      staged engines (m = 512 complex double with C = 1, D = q,
+                                      p <= 8; m = 128 complex float with C = 4), whose spectral
+                                      order differs from hd_spectral_permutation: a FWD output
+                                      is then valid only as the input of an INV (or CONV) pass
+                                      of the same axis, plan and flag.  HD_ERR_UNSUPPORTED when
+                                      the staged engine does not apply to the pass. */
 
 /* Per-axis parameters (L, M, C, m, D per dimension).
  *  m  : FFT size, a power of two in [2, 4096]

@@ -430,7 +430,8 @@ bool tma_desc_in(const LineIn& in, int64_t nlines, int64_t nbatch, int narr, hd:
                  CUtensorMap* maps, bool c64 = false) {
   t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = in.nbi > 0 ? in.nbi : 1;
   t.bcast = (in.s_b == 0 ? 1 : 0) | (in.s_bo == 0 ? 2 : 0);
-  if (in.jd > 0 || narr > hd::kTmaArrays) return false;
+  // element tiling wider than the line (jd >= L): every element is in tile 0
+  if ((in.jd > 0 && in.jd < in.L) || narr > hd::kTmaArrays) return false;
   if (in.tl >= 30) {
     if (in.s_j != 1) return false;
     if (c64 && !bulk_ok_f32(in.ptr, narr, {in.L, in.s_l, in.s_b, in.s_bo})) return false;
@@ -455,7 +456,7 @@ bool tma_desc_out(const LineOut& o, int64_t nlines, int64_t nbatch, int narr, hd
                   CUtensorMap* maps, bool c64 = false) {
   t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = o.nbi > 0 ? o.nbi : 1;
   t.bcast = (o.s_b == 0 ? 1 : 0) | (o.s_bo == 0 ? 2 : 0);
-  if (o.jd > 0 || narr > hd::kTmaArrays) return false;
+  if ((o.jd > 0 && o.jd < o.L + o.j0) || narr > hd::kTmaArrays) return false;
   const int64_t nbo = ceil_div64(nbatch, t.nbi);
   if (o.tl >= 30 && o.so_log2 >= 30) {
     if (o.s_js != 1) return false;
@@ -1872,8 +1873,11 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   L.flags = d->flags;
   L.mode = d->mode;
   L.name = d->mode == HD_PASS_FWD ? "pass_fwd" : (d->mode == HD_PASS_INV ? "pass_inv" : "pass_conv");
-  L.s512_axis = d->mode == HD_PASS_CONV;  // fwd/inv keep the documented spectral order
-  L.s128_axis = d->mode == HD_PASS_CONV;
+  // forward / inverse keep the documented spectral order unless the caller opts into
+  // the staged engines' own order (HD_FLAG_STAGED_ORDER, the same for both passes)
+  const bool staged_order = (d->flags & HD_FLAG_STAGED_ORDER) != 0;
+  L.s512_axis = d->mode == HD_PASS_CONV || staged_order;
+  L.s128_axis = d->mode == HD_PASS_CONV || staged_order;
   L.m = ap.m;
   L.lines = C;
   L.threads = ap.threads ? ap.threads : default_threads(C, D, ap.m);
@@ -1900,6 +1904,8 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   L.a.nlines = d->nlines; L.a.nbatch = d->nbatch; L.a.batch_fastest = d->batch_fastest ? 1 : 0;
   L.narrays = d->mode == HD_PASS_FWD ? narr : 1;
   L.ngroups = cdiv(d->nlines, C); L.nbatch = d->nbatch;
+  if (staged_order && d->mode != HD_PASS_CONV && !use_s512(dtype, L) && !use_s128(dtype, L))
+    return fail(ctx, HD_ERR_UNSUPPORTED, "HD_FLAG_STAGED_ORDER: no staged engine for this pass");
   return launch(ctx, dtype, L, (cudaStream_t)stream);
 }
 

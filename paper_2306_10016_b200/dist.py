@@ -3,7 +3,9 @@
 SURVEY §8(e): rank k holds a contiguous slab of f's rows (g is replicated);
   1. forward along x of the local rows (pass A)       -> X[dest][kx_local][y_local]
   2. all-to-all (exchange 1): rank k' receives the spectral columns of its slab
-  3. convolution along y of the local columns (pass B) -> Y[dest][kx_local][yo_local]
+  3. convolution along y of the local columns (pass B) -> Y[dest][yo_local][kx_local]
+     (row-major blocks: pass C then reads contiguous runs of every output row; the
+     compute-bound pass B absorbs the strided stores)
   4. all-to-all (exchange 2): rank k receives its output rows for every column
   5. inverse along x of the local output rows (pass C) -> h rows
 Every arithmetic step runs in libhdconv.so (`hd_pass`); this module only computes
@@ -147,6 +149,12 @@ class GpuBackend:
         self.ax = p           # [y, x] completed axis plans (m, q, M1, C, D, threads)
         self.scale = 1.0 / (p[0]["M1"] * p[1]["M1"])
         self.dev = torch.device("cuda", torch.cuda.current_device())
+        # the x passes (forward of f and g rows, inverse of the output rows) on the staged
+        # m = 512 engine in its own spectral order when every one of them qualifies
+        x = p[1]
+        self.x_flags = (H.HD_FLAG_STAGED_ORDER
+                        if dtype == H.HD_C128 and x["m"] == 512 and x["q"] <= 11 and x["p_f"] <= 8
+                        and x["p_g"] <= 8 else 0)
 
     def empty(self, n):
         return self.torch.empty(max(1, n), dtype=self.tdt, device=self.dev)
@@ -157,6 +165,8 @@ class GpuBackend:
         d.mode, d.npairs, d.nlines, d.nbatch, d.M = mode, 1, nlines, 1, M
         a = self.ax[axis]
         d.axis.m, d.axis.C, d.axis.D, d.axis.threads = a["m"], 1, 0, 0
+        if axis == 1:
+            d.flags = self.x_flags
         return d
 
     def fwd_rows(self, f_rows, nrows, out, P):
@@ -184,7 +194,10 @@ class GpuBackend:
         d.in_f = H.Lines.make([xrecv.data_ptr()], P.Lf[0], s_l=P.R, s_j=1, jd=P.R, s_jt=P.Ks * P.R)
         eb = xg.element_size()
         d.in_g = H.Lines.make([xg.data_ptr() + col0 * P.Lg[0] * eb], P.Lg[0], s_l=P.Lg[0])
-        d.out = H.Lines.make([out.data_ptr()], P.Oy, s_l=P.Ro, s_j=1, jd=P.Ro, s_jt=P.Ks * P.Ro)
+        # output row yo of local column c -> (yo / Ro)*(Ks*Ro) + (yo % Ro)*Ks + c
+        # (lines as tiles of width 1: TMA can store the 16-byte pieces when one block
+        #  holds every output row, i.e. Ro >= Oy)
+        d.out = H.Lines.make([out.data_ptr()], P.Oy, s_l=1, s_j=P.Ks, jd=P.Ro, s_jt=P.Ks * P.Ro, tl=0, s_t=1)
         d.scale = self.scale
         self.ctx.hd_pass(self.dt, d)
 
@@ -194,7 +207,8 @@ class GpuBackend:
             return h
         H = self.H
         d = self._desc(H.HD_PASS_INV, 1, nrows, self.ax[1]["M1"])
-        d.in_f = H.Lines.make([yrecv.data_ptr()], P.Kx, s_l=1, s_j=P.Ro, jd=P.Ks, s_jt=P.Ks * P.Ro)
+        # element kx of local output row y -> (kx / Ks)*(Ks*Ro) + y*Ks + kx % Ks
+        d.in_f = H.Lines.make([yrecv.data_ptr()], P.Kx, s_l=P.Ks, s_j=1, jd=P.Ks, s_jt=P.Ks * P.Ro)
         d.out = H.Lines.make([h.data_ptr()], P.Ox, s_l=P.Ox)
         self.ctx.hd_pass(self.dt, d)
         return h

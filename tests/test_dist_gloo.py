@@ -46,13 +46,13 @@ class NumpyBackend:
             G = np.fft.ifft(gcol, n=self.Ky) * self.Ky
             V = np.fft.fft(F * G) / (P.Kx * self.Ky)             # - exponent, scaled
             yo = np.arange(P.Oy)
-            out[(yo // P.Ro) * (P.Ks * P.Ro) + c * P.Ro + yo % P.Ro] = V[: P.Oy]
+            out[(yo // P.Ro) * (P.Ks * P.Ro) + (yo % P.Ro) * P.Ks + c] = V[: P.Oy]
 
     def inv_rows(self, yrecv, nrows, P):
         h = np.zeros((nrows, P.Ox), dtype=np.complex128)
         kx = np.arange(P.Kx)
         for y in range(nrows):
-            row = yrecv[(kx // P.Ks) * (P.Ks * P.Ro) + (kx % P.Ks) * P.Ro + y]
+            row = yrecv[(kx // P.Ks) * (P.Ks * P.Ro) + y * P.Ks + kx % P.Ks]
             h[y] = np.fft.fft(row)[: P.Ox]
         return h
 
