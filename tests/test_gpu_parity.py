@@ -716,3 +716,38 @@ def test_merged_forward_launch(ctx, H, sf, sg):
     assert ctx.launch_count() - n0 == 3
     idx = synth.sample_indices(h.shape, n_random=400)
     assert oracle.rel_l2(h[tuple(idx.T)], oracle.conv_sampled(f, g, idx)) < 1e-11
+
+
+@pytest.mark.parametrize("dtype,m,C,L,q", [(np.complex128, 512, 1, 3000, 7),
+                                           (np.complex64, 128, 4, 500, 5),
+                                           (np.complex128, 512, 1, 4096, 9)])
+def test_pass_staged_order_round_trip(ctx, H, dtype, m, C, L, q):
+    """hd_pass with HD_FLAG_STAGED_ORDER: forward then inverse on the staged engine in
+    its own spectral order returns q m x exactly as the documented-order passes do;
+    the flag is refused (HD_ERR_UNSUPPORTED) where no staged engine applies."""
+    nl = 8
+    x = synth.random_pair(1900 + m, (nl, L), (1,))[0].astype(dtype)
+    dt = H.HD_C128 if dtype == np.complex128 else H.HD_C64
+    M1 = q * m
+    xd = dev(x)
+    X = torch.empty(nl * M1, dtype=xd.dtype, device="cuda")
+    y = torch.empty(nl * L, dtype=xd.dtype, device="cuda")
+
+    def desc(mode, inp, Lin, s_in, out, Lout, s_out):
+        d = H.PassDesc()
+        d.mode, d.npairs, d.nlines, d.nbatch, d.M = mode, 1, nl, 1, M1
+        d.axis.m, d.axis.C, d.axis.D, d.axis.threads = m, C, 0, 0
+        d.in_f = H.Lines.make([inp.data_ptr()], Lin, s_l=s_in)
+        d.out = H.Lines.make([out.data_ptr()], Lout, s_l=s_out)
+        d.flags = H.HD_FLAG_STAGED_ORDER
+        return d
+    n0 = ctx.engine_launches(H.HD_ENGINE_S512) + ctx.engine_launches(H.HD_ENGINE_S128)
+    ctx.hd_pass(dt, desc(H.HD_PASS_FWD, xd, L, L, X, M1, M1))
+    ctx.hd_pass(dt, desc(H.HD_PASS_INV, X, M1, M1, y, L, L))
+    assert ctx.engine_launches(H.HD_ENGINE_S512) + ctx.engine_launches(H.HD_ENGINE_S128) - n0 == 2
+    got = host(y).reshape(nl, L) / M1
+    assert oracle.rel_l2(got, x) < (1e-13 if dtype == np.complex128 else 1e-5)
+    bad = desc(H.HD_PASS_FWD, xd, L, L, X, M1, M1)
+    bad.axis.C = 2 if C == 1 else 1   # no staged engine with this line count
+    with pytest.raises(H.HDError):
+        ctx.hd_pass(dt, bad)
