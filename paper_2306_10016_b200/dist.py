@@ -247,6 +247,25 @@ class SlabPlan3D:
         return min(k * self.Kys, self.Ky), min((k + 1) * self.Kys, self.Ky)
 
     @property
+    def T(self):
+        """kx tile of the exchange blocks: T consecutive kx of one (ky, z) are adjacent,
+        so a pass over kx lines in groups of T moves T-element pieces (the 3-D
+        pipeline's tiled layouts)."""
+        return 4 if self.Kx % 4 == 0 else 1
+
+    def ex1(self, blk, kyl, kx, zl):
+        """Element offset in the first exchange buffer: block `blk` (destination ky
+        range on the sender, source z slab on the receiver) [kyl][kx/T][zl][kx%T]."""
+        T = self.T
+        return blk * self.block1 + kyl * (self.Kx * self.Rz) + (kx // T) * (self.Rz * T) + zl * T + kx % T
+
+    def ex2(self, blk, zol, kx, kyl):
+        """Element offset in the second exchange buffer: block `blk` (destination z
+        range on the sender, source ky range on the receiver) [zol][kx/T][kyl][kx%T]."""
+        T = self.T
+        return blk * self.block2 + zol * (self.Kx * self.Kys) + (kx // T) * (self.Kys * T) + kyl * T + kx % T
+
+    @property
     def block1(self):
         return self.Kys * self.Kx * self.Rz
 
@@ -329,7 +348,10 @@ def emulate_ranks_3d(convs, f, g, empty):
 
 
 class GpuBackend3D:
-    """3-D slab passes on libhdconv.so (hd_pass descriptors, device tensors)."""
+    """3-D slab passes on libhdconv.so (hd_pass descriptors, device tensors), in the
+    3-D pipeline's tiled layouts (hd_api.cu run_pipeline, ndim 3): kx tiles of T = 4
+    lines, so complex64 axes with m = 128 run on the staged engine (hd_s128.cuh; the
+    forward/inverse passes with HD_FLAG_STAGED_ORDER, the same on both sides)."""
 
     def __init__(self, ctx, plan, dtype):
         import torch
@@ -344,69 +366,93 @@ class GpuBackend3D:
     def empty(self, n):
         return self.torch.empty(max(1, n), dtype=self.tdt, device=self.dev)
 
-    def _desc(self, mode, axis, nlines, nbatch):
+    def _staged(self, axis):
+        """hd_s128.cuh's conditions for every pass along `axis` (api use_s128)."""
+        a = self.ax[axis]
+        return self.dt == self.H.HD_C64 and a["m"] == 128 and a["q"] <= 8 and max(a["p_f"], a["p_g"]) <= 8
+
+    def _desc(self, mode, axis, nlines, nbatch, T):
         d = self.H.PassDesc()
         a = self.ax[axis]
         d.mode, d.npairs, d.nlines, d.nbatch, d.M = mode, 1, nlines, nbatch, a["M1"]
-        d.axis.m, d.axis.C, d.axis.D, d.axis.threads = a["m"], 1, 0, 0
+        staged = T == 4 and self._staged(axis)
+        d.axis.m, d.axis.C, d.axis.D, d.axis.threads = a["m"], 4 if staged else 1, 0, 0
+        if staged and mode != self.H.HD_PASS_CONV:
+            d.flags = self.H.HD_FLAG_STAGED_ORDER
         return d
 
-    def _xy(self, src, nz, Ly, Lx, out_ptr, s_ky, s_kx, s_z, jd=0, s_jt=0):
+    @staticmethod
+    def _lt(T, s_t):
+        """line l at (l / T) * s_t + l % T (plain stride s_t when T = 1)."""
+        return dict(tl=T.bit_length() - 1, s_t=s_t, s_l=1) if T > 1 else dict(s_l=s_t)
+
+    @staticmethod
+    def _et(T, s_jt, s_l):
+        """line stride s_l, element j at (j / T) * s_jt + j % T (plain when T = 1)."""
+        return dict(s_l=s_l, s_j=1, jd=T, s_jt=s_jt) if T > 1 else dict(s_l=s_l, s_j=s_jt)
+
+    def _xy(self, src, nz, Ly, Lx, out_ptr, s_ky, s_t, s_z, T, jd=0, s_jt=0):
         """x then y forward transforms of nz planes [z][y][x]; spectral element (z, ky, kx)
-        -> out + (ky tiling) + kx * s_kx + z * s_z."""
-        H, P = self.H, None
-        x1 = self.empty(nz * self.ax[2]["M1"] * Ly)                   # X1[z][kx][y]
+        -> out + (ky tiling) + (kx / T) * s_t + kx % T + z * s_z."""
+        H = self.H
         Kx = self.ax[2]["M1"]
-        d = self._desc(H.HD_PASS_FWD, 2, Ly, nz)
+        x1 = self.empty(nz * Kx * Ly)                                 # X1[z][kx/T][y][kx%T]
+        d = self._desc(H.HD_PASS_FWD, 2, Ly, nz, T)
         d.in_f = H.Lines.make([src.data_ptr()], Lx, s_l=Lx, s_b=Ly * Lx, nbi=nz)
-        d.out = H.Lines.make([x1.data_ptr()], Kx, s_l=1, s_j=Ly, s_b=Kx * Ly, nbi=nz)
+        d.out = H.Lines.make([x1.data_ptr()], Kx, **self._et(T, Ly * T, T), s_b=Kx * Ly, nbi=nz)
         self.ctx.hd_pass(self.dt, d)
-        d = self._desc(H.HD_PASS_FWD, 1, Kx, nz)
-        d.in_f = H.Lines.make([x1.data_ptr()], Ly, s_l=Ly, s_b=Kx * Ly, nbi=nz)
-        d.out = H.Lines.make([out_ptr], self.ax[1]["M1"], s_l=s_kx, s_j=s_ky, jd=jd, s_jt=s_jt, s_b=s_z, nbi=nz)
+        d = self._desc(H.HD_PASS_FWD, 1, Kx, nz, T)
+        d.in_f = H.Lines.make([x1.data_ptr()], Ly, **self._lt(T, Ly * T), s_j=T, s_b=Kx * Ly, nbi=nz)
+        d.out = H.Lines.make([out_ptr], self.ax[1]["M1"], **self._lt(T, s_t), s_j=s_ky, jd=jd, s_jt=s_jt,
+                             s_b=s_z, nbi=nz)
+        d.batch_fastest = 1
         self.ctx.hd_pass(self.dt, d)
 
     def fwd_planes(self, f_planes, nz, send, P):
         if nz <= 0:
             return
-        # element (zl, ky, kx) -> [ky / Kys][ky % Kys][kx][zl] of the send buffer
-        self._xy(f_planes, nz, P.Lf[1], P.Lf[2], send.data_ptr(), s_ky=P.Kx * P.Rz, s_kx=P.Rz, s_z=1,
-                 jd=P.Kys, s_jt=P.Kys * P.Kx * P.Rz)
+        # element (zl, ky, kx) -> P.ex1(ky / Kys, ky % Kys, kx, zl)
+        tiled = P.Kys < P.Ky
+        self._xy(f_planes, nz, P.Lf[1], P.Lf[2], send.data_ptr(), s_ky=P.Kx * P.Rz, s_t=P.Rz * P.T, s_z=P.T,
+                 T=P.T, jd=P.Kys if tiled else 0, s_jt=P.block1 if tiled else 0)
 
     def fwd_g(self, g, xyg, P):
-        # XYg[ky][kx][z]
-        self._xy(g, P.Lg[0], P.Lg[1], P.Lg[2], xyg.data_ptr(), s_ky=P.Kx * P.Lg[0], s_kx=P.Lg[0], s_z=1)
+        # XYg[ky][kx/T][z][kx%T]
+        self._xy(g, P.Lg[0], P.Lg[1], P.Lg[2], xyg.data_ptr(), s_ky=P.Kx * P.Lg[0], s_t=P.Lg[0] * P.T,
+                 s_z=P.T, T=P.T)
 
     def conv_lines(self, recv1, xyg, ky0, nky, send2, P):
         if nky <= 0:
             return
-        H = self.H
+        H, T = self.H, P.T
         eb = xyg.element_size()
-        d = self._desc(H.HD_PASS_CONV, 0, P.Kx, nky)
-        # element z = src * Rz + zl of line (kyl, kx): [src][kyl][kx][zl]
-        d.in_f = H.Lines.make([recv1.data_ptr()], P.Lf[0], s_l=P.Rz, s_j=1, jd=P.Rz, s_jt=P.block1,
-                              s_b=P.Kx * P.Rz, nbi=nky)
-        d.in_g = H.Lines.make([xyg.data_ptr() + ky0 * P.Kx * P.Lg[0] * eb], P.Lg[0], s_l=P.Lg[0],
-                              s_b=P.Kx * P.Lg[0], nbi=nky)
-        d.out = H.Lines.make([send2.data_ptr()], P.O[0], s_l=P.Roz, s_j=1, jd=P.Roz, s_jt=P.block2,
-                             s_b=P.Kx * P.Roz, nbi=nky)
+        d = self._desc(H.HD_PASS_CONV, 0, P.Kx, nky, T)
+        # element z = src * Rz + zl of line kx, batch kyl: P.ex1(src, kyl, kx, zl)
+        d.in_f = H.Lines.make([recv1.data_ptr()], P.Lf[0], **self._lt(T, P.Rz * T), s_j=T,
+                              jd=P.Rz if P.Rz < P.Lf[0] else 0, s_jt=P.block1, s_b=P.Kx * P.Rz, nbi=nky)
+        d.in_g = H.Lines.make([xyg.data_ptr() + ky0 * P.Kx * P.Lg[0] * eb], P.Lg[0], **self._lt(T, P.Lg[0] * T), s_j=T, s_b=P.Kx * P.Lg[0], nbi=nky)
+        # element zo = dst * Roz + zol: P.ex2(dst, zol, kx, kyl)
+        d.out = H.Lines.make([send2.data_ptr()], P.O[0], **self._lt(T, P.Kys * T), s_j=P.Kx * P.Kys,
+                             jd=P.Roz if P.Roz < P.O[0] else 0, s_jt=P.block2, s_b=T, nbi=nky)
         d.scale = self.scale
+        d.batch_fastest = 1
         self.ctx.hd_pass(self.dt, d)
 
     def inv_planes(self, recv2, nzo, P):
         h = self.torch.empty((max(nzo, 0), P.O[1], P.O[2]), dtype=self.tdt, device=self.dev)
         if nzo <= 0:
             return h
-        H = self.H
-        w = self.empty(nzo * P.O[1] * P.Kx)                           # W[zol][y][kx]
-        d = self._desc(H.HD_PASS_INV, 1, P.Kx, nzo)
-        # element ky = src * Kys + kyl of line (zol, kx): [src][kyl][kx][zol]
-        d.in_f = H.Lines.make([recv2.data_ptr()], P.Ky, s_l=P.Roz, s_j=P.Kx * P.Roz, jd=P.Kys, s_jt=P.block2,
-                              s_b=1, nbi=nzo)
-        d.out = H.Lines.make([w.data_ptr()], P.O[1], s_l=1, s_j=P.Kx, s_b=P.O[1] * P.Kx, nbi=nzo)
+        H, T = self.H, P.T
+        Oyp = -(-P.O[1] // T) * T
+        w = self.empty(nzo * Oyp * P.Kx)                               # W[zol][y/T][kx][y%T]
+        d = self._desc(H.HD_PASS_INV, 1, P.Kx, nzo, T)
+        # element ky = src * Kys + kyl of line kx, batch zol: P.ex2(src, zol, kx, kyl)
+        d.in_f = H.Lines.make([recv2.data_ptr()], P.Ky, **self._lt(T, P.Kys * T), s_j=T,
+                              jd=P.Kys if P.Kys < P.Ky else 0, s_jt=P.block2, s_b=P.Kx * P.Kys, nbi=nzo)
+        d.out = H.Lines.make([w.data_ptr()], P.O[1], **self._et(T, P.Kx * T, T), s_b=Oyp * P.Kx, nbi=nzo)
         self.ctx.hd_pass(self.dt, d)
-        d = self._desc(H.HD_PASS_INV, 2, P.O[1], nzo)
-        d.in_f = H.Lines.make([w.data_ptr()], P.Kx, s_l=P.Kx, s_b=P.O[1] * P.Kx, nbi=nzo)
+        d = self._desc(H.HD_PASS_INV, 2, P.O[1], nzo, T)
+        d.in_f = H.Lines.make([w.data_ptr()], P.Kx, **self._lt(T, P.Kx * T), s_j=T, s_b=Oyp * P.Kx, nbi=nzo)
         d.out = H.Lines.make([h.data_ptr()], P.O[2], s_l=P.O[2], s_b=P.O[1] * P.O[2], nbi=nzo)
         self.ctx.hd_pass(self.dt, d)
         return h

@@ -138,10 +138,10 @@ class NumpyBackend3D:
 
     def fwd_planes(self, f_planes, nz, send, P):
         S = self._xy(f_planes, P.Ky, P.Kx)
+        kx = np.arange(P.Kx)
         for zl in range(nz):
             for ky in range(P.Ky):
-                base = (ky // P.Kys) * P.block1 + (ky % P.Kys) * P.Kx * P.Rz + zl
-                send[base + np.arange(P.Kx) * P.Rz] = S[zl, ky]
+                send[P.ex1(ky // P.Kys, ky % P.Kys, kx, zl)] = S[zl, ky]
 
     def fwd_g(self, g, xyg, P):
         S = self._xy(g, P.Ky, P.Kx)                               # [z][ky][kx]
@@ -151,12 +151,12 @@ class NumpyBackend3D:
         zs, zo = np.arange(P.Lf[0]), np.arange(P.O[0])
         for kyl in range(nky):
             for kx in range(P.Kx):
-                fcol = recv1[(zs // P.Rz) * P.block1 + kyl * P.Kx * P.Rz + kx * P.Rz + zs % P.Rz]
+                fcol = recv1[P.ex1(zs // P.Rz, kyl, kx, zs % P.Rz)]
                 gcol = xyg[((ky0 + kyl) * P.Kx + kx) * P.Lg[0] + np.arange(P.Lg[0])]
                 F = np.fft.ifft(fcol, n=self.Kz) * self.Kz
                 G = np.fft.ifft(gcol, n=self.Kz) * self.Kz
                 V = np.fft.fft(F * G) / (self.Kz * P.Ky * P.Kx)
-                send2[(zo // P.Roz) * P.block2 + kyl * P.Kx * P.Roz + kx * P.Roz + zo % P.Roz] = V[: P.O[0]]
+                send2[P.ex2(zo // P.Roz, zo % P.Roz, kx, kyl)] = V[: P.O[0]]
 
     def inv_planes(self, recv2, nzo, P):
         h = np.zeros((nzo, P.O[1], P.O[2]), dtype=np.complex128)
@@ -164,7 +164,7 @@ class NumpyBackend3D:
         for zol in range(nzo):
             W = np.zeros((P.O[1], P.Kx), dtype=np.complex128)
             for kx in range(P.Kx):
-                row = recv2[(ky // P.Kys) * P.block2 + (ky % P.Kys) * P.Kx * P.Roz + kx * P.Roz + zol]
+                row = recv2[P.ex2(ky // P.Kys, zol, kx, ky % P.Kys)]
                 W[:, kx] = np.fft.fft(row)[: P.O[1]]
             h[zol] = np.fft.fft(W, axis=1)[:, : P.O[2]]
         return h
@@ -216,3 +216,21 @@ def test_slab3d_plan_partitions():
         assert sum(b - a for a, b in (P.out_planes(k) for k in range(world))) == 640
         assert sum(b - a for a, b in (P.kys(k) for k in range(world))) == 640
         assert P.bytes_sent_per_rank(8) == (world - 1) * (P.block1 + P.block2) * 8
+
+
+def test_slab3d_exchange_layout_is_a_bijection():
+    """ex1/ex2 place every (block, row, kx, plane) element once inside its block, with
+    T = 4 consecutive kx adjacent (the tiled layouts GpuBackend3D describes to hd_pass)."""
+    for world, K in ((1, (640, 640)), (3, (640, 640)), (2, (12, 9))):
+        P = SlabPlan3D(world, (20, 7, 5), (5, 3, 2), *K)
+        assert P.T == (4 if K[1] % 4 == 0 else 1)
+        kyl, kx, zl = np.meshgrid(np.arange(P.Kys), np.arange(P.Kx), np.arange(P.Rz), indexing="ij")
+        for blk in range(world):
+            o = P.ex1(blk, kyl, kx, zl).ravel()
+            assert np.array_equal(np.sort(o), blk * P.block1 + np.arange(P.block1))
+        zol, kx2, kyl2 = np.meshgrid(np.arange(P.Roz), np.arange(P.Kx), np.arange(P.Kys), indexing="ij")
+        for blk in range(world):
+            o = P.ex2(blk, zol, kx2, kyl2).ravel()
+            assert np.array_equal(np.sort(o), blk * P.block2 + np.arange(P.block2))
+        if P.T == 4:
+            assert P.ex1(0, 0, 1, 0) - P.ex1(0, 0, 0, 0) == 1 and P.ex2(0, 0, 3, 0) - P.ex2(0, 0, 0, 0) == 3

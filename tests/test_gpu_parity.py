@@ -528,10 +528,13 @@ def test_slab3d_emulated_ranks(ctx, H, world, dtype, m, C):
     Ky, Kx = plan.axis[1].M1, plan.axis[2].M1
     be = GpuBackend3D(ctx, plan, dt)
     convs = [SlabConv3D(be, None, world, k, Lf, Lg, Ky, Kx) for k in range(world)]
+    n0 = ctx.engine_launches(H.HD_ENGINE_S128)
     parts = emulate_ranks_3d(convs, dev(f), dev(g), be.empty)
     h = np.concatenate([host(p) for p in parts], axis=0)
     tol = 1e-11 if dtype == np.complex128 else 1e-5
     assert oracle.rel_l2(h, oracle.conv(f, g)) < tol
+    if m == 128:  # kx tiles of 4: all seven passes of every rank on the staged engine
+        assert ctx.engine_launches(H.HD_ENGINE_S128) - n0 == 7 * world
 
 
 # ---------------------------------------------------------------- staged engine (m = 128, complex64)
