@@ -57,4 +57,10 @@ cudaError_t launch_lambda_product(bool is_double, const void* Xf, void* Xg, cons
                                   const int32_t* iperm_f, int64_t nlines, int m, int Lam, int qg, double scale,
                                   cudaStream_t st);
 constexpr size_t kMaxSmem = 227 * 1024;
+// Launcher helpers (hd_kernels.cu), thread-safe and per device (the dynamic
+// shared-memory opt-in is a per-device function attribute): allow `smem` bytes of
+// dynamic shared memory for kernel `fn` on the current device (no-op at <= 48 KB
+// or when already allowed), and the current device's SM count.
+cudaError_t allow_dynamic_smem(const void* fn, size_t smem);
+int device_sm_count();
 }  // namespace hd

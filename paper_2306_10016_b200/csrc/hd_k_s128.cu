@@ -10,19 +10,9 @@ namespace hd {
 template <int MODE, int NT, int QC, int MINB = 2, int ILK = 0, int OUTK = 0>
 static cudaError_t launch_s128_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   auto kern = s128::s128_kernel<MODE, NT, QC, MINB, ILK, OUTK>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < 64 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   int occ = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
   if (e != cudaSuccess) return e;
@@ -70,19 +60,9 @@ LaunchFn lookup_s128(int mode, int q, int in_kind, int out_kind, int out_slog) {
 static cudaError_t launch_s128_bg_fwd(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   constexpr int NT = 32 * (s128::kBG * 5 + 1);
   auto kern = s128::s128_bg_fwd_kernel<5>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt != NT) return cudaErrorInvalidConfiguration;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   int occ = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
   if (e != cudaSuccess) return e;

@@ -9,19 +9,9 @@ namespace hd {
 template <int MODE, int NTMAX, int QC, int LEAN = 0>
 static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   auto kern = s512::s512_kernel<MODE, NTMAX, QC, LEAN>;
-  static size_t configured = 0;  // per instantiation
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < 32 || nt > NTMAX || nt % 32) return cudaErrorInvalidConfiguration;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   int occ = 1;
   if (LEAN) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
@@ -56,19 +46,9 @@ template <int QC>
 static cudaError_t launch_s512_mconv(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   constexpr int NT = 32 * (s512::kMconvQMax + 1);
   auto kern = s512::s512_mconv_kernel<NT, QC>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < 64 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   if ((int64_t)grid.x > sms) grid.x = (unsigned)sms;
   kern<<<grid, nt, smem, st>>>(a);
   return cudaGetLastError();
@@ -99,19 +79,9 @@ namespace hd {
 static cudaError_t launch_s512c(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   constexpr int NT = 32 * s512c::kRMax;
   auto kern = s512c::s512c_kernel<NT>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < 32 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   // one cluster of two CTAs per line, persistent: at most one CTA per SM
   int64_t ncl = (int64_t)a.nlines;
   if (ncl > sms / 2) ncl = sms / 2;
@@ -138,19 +108,9 @@ namespace hd {
 static cudaError_t launch_s2048c(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   constexpr int NT = s2048c::kGT * s2048c::kRMax;
   auto kern = s2048c::s2048c_kernel<NT>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < s2048c::kGT || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   int64_t ncl = (int64_t)a.nlines;
   if (ncl > sms / 2) ncl = sms / 2;
   grid.x = (unsigned)(2 * ncl);

@@ -1,10 +1,40 @@
 // hd_kernels.cu -- launcher lookup over the instantiated slices (hd_k_*.cu: every
 // FFT size m = 2..4096, both precisions, 256 or 512 threads, three pass modes)
 // and the explicit-padding copy kernels.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "hd_device.cuh"
 #include "hd_internal.h"
 
 namespace hd {
+
+cudaError_t allow_dynamic_smem(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> allowed;  // (kernel, device) -> bytes
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = allowed[{fn, dev}];
+  if (smem <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+
+int device_sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 1;
+  static std::mutex mu;
+  static std::map<int, int> sms;
+  std::lock_guard<std::mutex> lk(mu);
+  int& n = sms[dev];
+  if (!n && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 0;
+  return n > 0 ? n : 1;
+}
 
 LaunchFn lookup_f64_256(int m, int mode);
 LaunchFn lookup_f64_576(int m, int mode);

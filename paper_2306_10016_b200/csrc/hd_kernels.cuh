@@ -10,23 +10,13 @@ namespace hd {
 template <typename T, int M, int NT, int MODE>
 static cudaError_t launch_pass_impl(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
   auto kern = pass_kernel<T, M, NT, MODE>;
-  static size_t configured = 0;  // largest dynamic smem size already allowed
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < 32 || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
   // persistent grid: every SM gets as many CTAs as fit; grid.x work items are
   // strided over them (grid.x on entry = total work items)
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static int occ_nt = -1, occ_val = 1;
-  static size_t occ_smem = 0;
+  const int sms = device_sm_count();
+  thread_local int occ_nt = -1, occ_val = 1;  // per thread: no shared mutable state
+  thread_local size_t occ_smem = 0;
   if (occ_nt != nt || occ_smem != smem) {
     int nb = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem) != cudaSuccess || nb < 1) nb = 1;

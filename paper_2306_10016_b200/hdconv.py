@@ -197,7 +197,9 @@ def _stream_ptr(stream):
     if stream is None:
         import torch
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    return ctypes.c_void_p(int(stream))
+    if hasattr(stream, "cuda_stream"):  # torch.cuda.Stream
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))  # a raw cudaStream_t
 
 
 def _ptr(t):

@@ -754,3 +754,42 @@ def test_pass_staged_order_round_trip(ctx, H, dtype, m, C, L, q):
     bad.axis.C = 2 if C == 1 else 1   # no staged engine with this line count
     with pytest.raises(H.HDError):
         ctx.hd_pass(dt, bad)
+
+
+# ---------------------------------------------------------------- threads
+def test_contexts_on_concurrent_threads(H):
+    """Two host threads, each with its own context and stream, convolve different
+    problems at once (staged and generic engines, > 48 KB of shared memory): the
+    launchers' per-device caches are shared and locked (hd_kernels.cu)."""
+    import threading
+    cases = [(((1100, 700), (255, 60)), np.complex128), (((300, 260), (31, 17)), np.complex128),
+             (((150, 18, 24), (5, 7, 4)), np.complex64), (((5000,), (900,)), np.complex128)]
+    data = [synth.random_pair(900 + i, Lf, Lg, dtype=dt) for i, ((Lf, Lg), dt) in enumerate(cases)]
+    results, errors = {}, []
+
+    def worker(k):
+        try:
+            c = H.Context(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    for i in range(k, len(cases), 2):
+                        f, g = data[i]
+                        h = c.conv(dev(f), dev(g), stream=s)
+                        s.synchronize()
+                        results[(i, rep)] = h.cpu().numpy()
+            c.close()
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errors, errors
+    for (i, rep), h in results.items():
+        f, g = data[i]
+        tol = 1e-11 if cases[i][1] == np.complex128 else 1e-5
+        assert oracle.rel_l2(h, oracle.conv(f, g)) < tol, (i, rep)
+    assert len(results) == 3 * len(cases)
