@@ -357,6 +357,10 @@ def run_ours(args, rank, world, local_rank):
     # roofline of the dominant kernel (largest share of the step)
     peak, peak_src = peaks()
     ab = alg_bytes(ndim, N, Lf, Lg, Lout, eb, batch)
+    if slab is not None:
+        # slab mode: each rank's one "pass_conv" launch convolves 1/world of the
+        # spectral lines of the pipeline's convolution pass
+        ab = dict(ab, pass_conv=ab["conv_y" if ndim == 2 else "conv_z"] // world)
     dom = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
     roof = None
     if dom:
@@ -368,7 +372,9 @@ def run_ours(args, rank, world, local_rank):
                 "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_src,
                 "alg_bytes_per_launch": ab_dom, "avg_launch_ms": avg,
                 "share_of_step": dms / sum(v[0] for v in prof.values())}
-        fl = conv_flops(ndim, N, Lf, Lg, Lout, plan, batch) if dom.startswith("conv") else None
+        fl = None
+        if dom.startswith("conv") or dom == "pass_conv":
+            fl = conv_flops(ndim, N, Lf, Lg, Lout, plan, batch) / (world if dom == "pass_conv" else 1)
         if fl and eb == 16:
             # the convolution pass is FP64-issue bound: its flops
             # against the FP64 pipe, 64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz
@@ -389,7 +395,7 @@ def run_ours(args, rank, world, local_rank):
                              "alg_flops_per_launch": fl, "flops": fp64["flops"], "hbm": hbm})
             else:
                 roof["fp64"] = fp64
-    total_ab = sum(ab.values())
+    total_ab = sum(v for k, v in ab.items() if k != "pass_conv")
     whole = {"alg_bytes_per_step": total_ab,
              "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,
              "frac_of_hbm": total_ab / (ms * 1e-3 / args.steps) / 1e9 / peak,
