@@ -17,7 +17,6 @@ packing.  The partition/exchange logic is shared with a CPU test backend
 """
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 

@@ -4,7 +4,6 @@ refuses compute without a device (no CPU fallback)."""
 import os
 import re
 
-import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

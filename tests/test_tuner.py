@@ -5,7 +5,6 @@ GPU: hd_tune_ex's search logic with the cost-injection hook (deterministic costs
 no timing noise): random search with n1 >= |space| equals the grid search, a fixed
 seed is repeatable, ties break lexicographically, and the skinny proxy returns an
 admissible plan that convolves correctly."""
-import numpy as np
 import pytest
 
 import oracle
