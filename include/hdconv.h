@@ -37,7 +37,14 @@
  *    plan; an explicit plan is honoured exactly (fields p_f, p_g, q, M1 are
  *    recomputed and returned by hd_plan_complete).
  *  - ws = NULL lets the context allocate (and cache) the workspace; otherwise
- *    ws_bytes must be >= hd_workspace_bytes() for the same arguments.
+ *    ws_bytes must be >= hd_workspace_bytes() for the same arguments.  The
+ *    context's scratch (workspace, real-path and host-I/O buffers) is shared
+ *    by every call that passes no workspace, on whatever stream: each such
+ *    call is ordered after the previous one's last use of it (an event wait
+ *    on the caller's stream), so calls on different streams serialise on the
+ *    device; pass a caller-owned ws per stream for concurrency.  A context may
+ *    be used from several host threads (calls hold a per-context lock while
+ *    they enqueue).
  *  - No CPU fallback exists: without a CUDA device every compute call returns
  *    HD_ERR_CUDA.
  */

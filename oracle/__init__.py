@@ -54,6 +54,7 @@ def _load():
             lib.oracle_dft.argtypes = [I64, I64, P, ctypes.c_int, P]
             lib.oracle_poly_eval.argtypes = [ctypes.c_int, P, P, I64, P, P]
             lib.oracle_num_threads.restype = ctypes.c_int
+            lib.oracle_poly_eps.restype = ctypes.c_double
             _lib = lib
     return _lib
 
@@ -185,8 +186,14 @@ def lambda_conv(f, g, m: int, Lam: int, M: int | None = None) -> np.ndarray:
     return h[:Lout]
 
 
+def poly_eps() -> float:
+    """Unit roundoff of poly_eval's accumulation (long double in oracle.c)."""
+    return float(_load().oracle_poly_eps())
+
+
 def poly_eval(a, z) -> np.ndarray:
-    """P_a(z) = sum_o a[o] prod_i z_i^{o_i} at points z[p, :] (nested Horner)."""
+    """P_a(z) = sum_o a[o] prod_i z_i^{o_i} at points z[p, :] (nested Horner,
+    accumulated in long double, rounded to double once)."""
     a = _c128(a)
     ndim = a.ndim
     z = _c128(z).reshape(-1, ndim)

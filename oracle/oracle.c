@@ -32,6 +32,7 @@
  *
  * Parallelism: OpenMP over output samples; every sample is independent.
  */
+#include <float.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -172,7 +173,15 @@ int oracle_dft(int64_t M, int64_t L, const double* x, int sign, double* X) {
 }
 
 /* P_a(z) = sum_o a[o] prod_i z_i^{o_i} by nested Horner, at npts points
- * z[p*ndim + i] (complex).  Used for the polynomial identity P_h = P_f P_g. */
+ * z[p*ndim + i] (complex).  Used for the polynomial identity P_h = P_f * P_g.
+ * Accumulated in long double (x86-64: 64-bit mantissa) so that the Horner
+ * rounding, (sum_i deg_i) * oracle_poly_eps() * ||a||_1 for |z_i| = 1, stays far
+ * below the parity tolerances even for 10^7-sample outputs; the result is
+ * rounded to double once. */
+typedef struct { long double re, im; } lcplx;
+
+double oracle_poly_eps(void) { return (double)LDBL_EPSILON; }
+
 int oracle_poly_eval(int ndim, const int64_t* L, const double* a, int64_t npts,
                      const double* z, double* out) {
   if (ndim < 1 || ndim > ORACLE_MAXDIM) return -1;
@@ -183,25 +192,29 @@ int oracle_poly_eval(int ndim, const int64_t* L, const double* a, int64_t npts,
   cplx* oc = (cplx*)out;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t p = 0; p < npts; ++p) {
-    cplx zz[3] = {{1, 0}, {1, 0}, {1, 0}};
-    for (int i = 0; i < ndim; ++i) zz[3 - ndim + i] = zc[p * ndim + i];
-    cplx s0 = {0, 0};
+    lcplx zz[3] = {{1, 0}, {1, 0}, {1, 0}};
+    for (int i = 0; i < ndim; ++i) {
+      zz[3 - ndim + i].re = zc[p * ndim + i].re;
+      zz[3 - ndim + i].im = zc[p * ndim + i].im;
+    }
+    lcplx s0 = {0, 0};
     for (int64_t a0 = A[0] - 1; a0 >= 0; --a0) {
-      cplx s1 = {0, 0};
+      lcplx s1 = {0, 0};
       for (int64_t a1 = A[1] - 1; a1 >= 0; --a1) {
-        cplx s2 = {0, 0};
+        lcplx s2 = {0, 0};
         const cplx* row = ac + (a0 * A[1] + a1) * A[2];
         for (int64_t a2 = A[2] - 1; a2 >= 0; --a2) {
-          cplx t = {s2.re * zz[2].re - s2.im * zz[2].im, s2.re * zz[2].im + s2.im * zz[2].re};
+          lcplx t = {s2.re * zz[2].re - s2.im * zz[2].im, s2.re * zz[2].im + s2.im * zz[2].re};
           s2.re = t.re + row[a2].re; s2.im = t.im + row[a2].im;
         }
-        cplx t = {s1.re * zz[1].re - s1.im * zz[1].im, s1.re * zz[1].im + s1.im * zz[1].re};
+        lcplx t = {s1.re * zz[1].re - s1.im * zz[1].im, s1.re * zz[1].im + s1.im * zz[1].re};
         s1.re = t.re + s2.re; s1.im = t.im + s2.im;
       }
-      cplx t = {s0.re * zz[0].re - s0.im * zz[0].im, s0.re * zz[0].im + s0.im * zz[0].re};
+      lcplx t = {s0.re * zz[0].re - s0.im * zz[0].im, s0.re * zz[0].im + s0.im * zz[0].re};
       s0.re = t.re + s1.re; s0.im = t.im + s1.im;
     }
-    oc[p] = s0;
+    oc[p].re = (double)s0.re;
+    oc[p].im = (double)s0.im;
   }
   return 0;
 }

@@ -28,7 +28,7 @@ thread_local std::string g_tls_error;
 struct hd_ctx {
   int device = 0;
   std::string err;
-  std::mutex mu;
+  std::recursive_mutex mu;            // held for a whole entry point (entries nest: real -> run_entry)
   std::map<int64_t, void*> tw64, tw32;  // N -> device zeta_N^k tables
   std::map<int64_t, void*> st64, st32;  // m -> device stage twiddle tables
   std::map<int64_t, int32_t*> perm;     // 2n (+1: inverse) -> device spectral permutation
@@ -45,8 +45,11 @@ struct hd_ctx {
   };
   HostSlot hslot[2];
   int hnext = 0;
-  cudaEvent_t compute_done = nullptr;   // last enqueued convolution (shared workspace)
-  bool compute_pending = false;
+  // Context scratch (ws, io, rio, host slots) is shared by every call that passes
+  // no workspace, whatever stream it is on: each such call waits for the previous
+  // one's last scratch use (scratch_done) and records its own.
+  cudaEvent_t scratch_done = nullptr;
+  bool scratch_pending = false;
   std::map<std::string, hd_plan_t> plan_cache;
   std::vector<std::pair<hd_plan_t, double>> tune_log;
   // profiling
@@ -82,6 +85,41 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int ilog2(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
 size_t elem_bytes(hd_dtype_t dt) { return dt == HD_C128 ? 16 : 8; }
+
+// Order a call that uses context scratch after the previous such call (any stream).
+// Not during graph capture: a captured launch sequence is ordered by its replay.
+hd_status_t scratch_acquire(hd_ctx* ctx, cudaStream_t st) {
+  if (ctx->capturing) return HD_OK;
+  if (!ctx->scratch_done) {
+    cudaError_t e = cudaEventCreateWithFlags(&ctx->scratch_done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaEventCreate(scratch)");
+  }
+  if (ctx->scratch_pending) {
+    cudaError_t e = cudaStreamWaitEvent(st, ctx->scratch_done, 0);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamWaitEvent(scratch)");
+  }
+  return HD_OK;
+}
+hd_status_t scratch_release(hd_ctx* ctx, cudaStream_t st) {
+  if (ctx->capturing || !ctx->scratch_done) return HD_OK;
+  cudaError_t e = cudaEventRecord(ctx->scratch_done, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaEventRecord(scratch)");
+  ctx->scratch_pending = true;
+  return HD_OK;
+}
+// Grow one context scratch buffer.  Captured graphs may address any scratch buffer,
+// so they are dropped first; cudaFree waits for in-flight work on the device.
+hd_status_t grow_scratch(hd_ctx* ctx, void** buf, size_t* size, size_t need, const char* what) {
+  if (*size >= need) return HD_OK;
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  ctx->graphs.clear();
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr; *size = 0;
+  cudaError_t e = cudaMalloc(buf, need);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+  *size = need;
+  return HD_OK;
+}
 
 // ---------------------------------------------------------------------------
 // twiddle tables zeta_N^k = exp(2 pi i k / N), k < N, computed in long double
@@ -835,15 +873,8 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
   const size_t need = ws_regions(P, el);
   if (need > 0) {
     if (!ws) {
-      if (ctx->ws_size < need) {
-        for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);  // they address the old workspace
-        ctx->graphs.clear();
-        if (ctx->ws) cudaFree(ctx->ws);
-        ctx->ws = nullptr; ctx->ws_size = 0;
-        cudaError_t e = cudaMalloc(&ctx->ws, need);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(workspace)");
-        ctx->ws_size = need;
-      }
+      hd_status_t sg = grow_scratch(ctx, &ctx->ws, &ctx->ws_size, need, "cudaMalloc(workspace)");
+      if (sg != HD_OK) return sg;
       ws = ctx->ws;
     } else if (ws_bytes < need) {
       return fail(ctx, HD_ERR_WORKSPACE, "workspace too small");
@@ -1171,7 +1202,7 @@ hd_status_t hd_destroy(hd_ctx_t ctx) {
     if (sl.st) { cudaStreamSynchronize(sl.st); cudaStreamDestroy(sl.st); }
     if (sl.io) cudaFree(sl.io);
   }
-  if (ctx->compute_done) cudaEventDestroy(ctx->compute_done);
+  if (ctx->scratch_done) cudaEventDestroy(ctx->scratch_done);
   for (auto& p : ctx->prof)
     for (auto& ev : p.pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
   delete ctx;
@@ -1233,6 +1264,10 @@ size_t hd_workspace_bytes(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t 
   return ws_regions(P, el);
 }
 
+static hd_status_t run_graph_or_pipeline(hd_ctx_t ctx, Problem& P, hd_dtype_t dt, int ndim, int N, int64_t batch,
+                                         const int64_t* Lf, const int64_t* Lg, void* h, const int64_t* M,
+                                         const Problem::RealFuse* rf, void* ws, size_t ws_bytes, void* stream);
+
 static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64_t batch,
                              const void* const* f, const int64_t* Lf, const void* const* g,
                              const int64_t* Lg, void* h, const int64_t* M, const hd_plan_t* plan,
@@ -1242,9 +1277,22 @@ static hd_status_t run_entry(hd_ctx_t ctx, hd_dtype_t dt, int ndim, int N, int64
   hd_status_t s = setup(ctx, P, dt, ndim, N, batch, f, Lf, g, Lg, h, M, plan, true, win_lo, win_n);
   if (s != HD_OK) return s;
   if (rf) P.rf = *rf;
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (ws) return run_graph_or_pipeline(ctx, P, dt, ndim, N, batch, Lf, Lg, h, M, rf, ws, ws_bytes, stream);
+  s = scratch_acquire(ctx, st);
+  if (s != HD_OK) return s;
+  s = run_graph_or_pipeline(ctx, P, dt, ndim, N, batch, Lf, Lg, h, M, rf, ws, ws_bytes, stream);
+  hd_status_t r = scratch_release(ctx, st);
+  return s != HD_OK ? s : r;
+}
+
+static hd_status_t run_graph_or_pipeline(hd_ctx_t ctx, Problem& P, hd_dtype_t dt, int ndim, int N, int64_t batch,
+                                         const int64_t* Lf, const int64_t* Lg, void* h, const int64_t* M,
+                                         const Problem::RealFuse* rf, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  hd_status_t s;
   if (!(P.plan.flags & HD_FLAG_GRAPH) || rf || ctx->profiling) return run_pipeline(ctx, P, ws, ws_bytes, st);
   // HD_FLAG_GRAPH: replay the captured launches of an identical earlier call
   std::string key = problem_key(dt, ndim, N, batch, Lf, Lg, M, P.plan.flags);
@@ -1321,6 +1369,11 @@ static bool real_fusable(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, int64_t batch
   return P.s512[1] && x.q == 9 && x.lines == 1 && x.D == 9 && x.pf <= 8 && x.o0 == 0 && x.O == Lout1;
 }
 
+static hd_status_t real_locked(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch, const void* f,
+                               const int64_t* Lf, const void* g, const int64_t* Lg, void* h, const hd_plan_t* plan,
+                               void* stream, int64_t A, const int64_t* Lz, int64_t rest_f, int64_t rest_g,
+                               int64_t rest_o, size_t bz, size_t bgc, int64_t Ow0, int64_t Lout0);
+
 hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch, const void* f,
                          const int64_t* Lf, const void* g, const int64_t* Lg, void* h, const hd_plan_t* plan,
                          void* stream) {
@@ -1344,17 +1397,24 @@ hd_status_t hd_conv_real(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t b
   const size_t bgc = align256((size_t)(batch * Lg[0] * rest_g) * cb);
   const size_t bw = align256((size_t)(batch * Ow0 * rest_o) * cb);
   cudaStream_t st = (cudaStream_t)stream;
-  {
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
-    if (ctx->rio_size < bz + bgc + bw) {
-      if (ctx->rio) cudaFree(ctx->rio);
-      ctx->rio = nullptr; ctx->rio_size = 0;
-      cudaError_t e = cudaMalloc(&ctx->rio, bz + bgc + bw);
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(real path)");
-      ctx->rio_size = bz + bgc + bw;
-    }
-  }
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);  // held while rio is in use
+  cudaSetDevice(ctx->device);
+  hd_status_t sg = grow_scratch(ctx, &ctx->rio, &ctx->rio_size, bz + bgc + bw, "cudaMalloc(real path)");
+  if (sg != HD_OK) return sg;
+  sg = scratch_acquire(ctx, st);
+  if (sg != HD_OK) return sg;
+  hd_status_t sr = real_locked(ctx, dtype, ndim, batch, f, Lf, g, Lg, h, plan, stream, A, Lz, rest_f, rest_g, rest_o,
+                               bz, bgc, Ow0, Lout0);
+  sg = scratch_release(ctx, st);
+  return sr != HD_OK ? sr : sg;
+}
+
+static hd_status_t real_locked(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int64_t batch, const void* f,
+                               const int64_t* Lf, const void* g, const int64_t* Lg, void* h, const hd_plan_t* plan,
+                               void* stream, int64_t A, const int64_t* Lz, int64_t rest_f, int64_t rest_g,
+                               int64_t rest_o, size_t bz, size_t bgc, int64_t Ow0, int64_t Lout0) {
+  const bool dbl = dtype == HD_C128;
+  cudaStream_t st = (cudaStream_t)stream;
   char* z = (char*)ctx->rio;
   char* gc = z + bz;
   char* w = gc + bgc;
@@ -1420,6 +1480,10 @@ hd_status_t hd_multiconv(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   return run_entry(ctx, dtype, ndim, N, 1, f, Lf, g, Lg, h, M, plan, ws, ws_bytes, stream);
 }
 
+static hd_status_t explicit_locked(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, const void* const* f,
+                                   const int64_t* Lf, const void* const* g, const int64_t* Lg, void* h, Problem& E,
+                                   const int64_t* Me, const int64_t* Lo, size_t inb, size_t wsb, cudaStream_t st);
+
 hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
                              const void* const* f, const int64_t* Lf, const void* const* g,
                              const int64_t* Lg, void* h, const hd_plan_t* plan, void* stream) {
@@ -1427,7 +1491,7 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
   Problem H;
   hd_status_t s = setup(ctx, H, dtype, ndim, N, 1, f, Lf, g, Lg, h, nullptr, plan);
   if (s != HD_OK) return s;
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t eb = elem_bytes(dtype);
@@ -1461,13 +1525,19 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
   const size_t wsb = ws_regions(E, el);
   const size_t inb = align256((size_t)nin * eb);
   const size_t need = (2 * N + 1) * inb + wsb;
-  if (ctx->io_size < need) {
-    if (ctx->io) cudaFree(ctx->io);
-    ctx->io = nullptr; ctx->io_size = 0;
-    cudaError_t e = cudaMalloc(&ctx->io, need);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(explicit scratch)");
-    ctx->io_size = need;
-  }
+  s = grow_scratch(ctx, &ctx->io, &ctx->io_size, need, "cudaMalloc(explicit scratch)");
+  if (s != HD_OK) return s;
+  s = scratch_acquire(ctx, st);
+  if (s != HD_OK) return s;
+  s = explicit_locked(ctx, dtype, ndim, N, f, Lf, g, Lg, h, E, Me, Lo, inb, wsb, st);
+  hd_status_t r = scratch_release(ctx, st);
+  return s != HD_OK ? s : r;
+}
+
+static hd_status_t explicit_locked(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, const void* const* f,
+                                   const int64_t* Lf, const void* const* g, const int64_t* Lg, void* h, Problem& E,
+                                   const int64_t* Me, const int64_t* Lo, size_t inb, size_t wsb, cudaStream_t st) {
+  hd_status_t s;
   char* base = (char*)ctx->io;
   int64_t L3[3], P3[3];
   auto to3 = [&](const int64_t* v, int64_t* o) {
@@ -1503,7 +1573,7 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   Problem P;
   hd_status_t s = setup(ctx, P, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan);
   if (s != HD_OK) return s;
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t eb = elem_bytes(dtype);
@@ -1511,13 +1581,10 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   for (int i = 0; i < ndim; ++i) { nf *= Lf[i]; ng *= Lg[i]; nh *= P.ax[i].O; }
   const size_t bf = align256((size_t)nf * eb), bg = align256((size_t)ng * eb), bh = align256((size_t)nh * eb);
   const size_t need = N * (bf + bg) + bh;
-  if (ctx->io_size < need) {
-    if (ctx->io) cudaFree(ctx->io);
-    ctx->io = nullptr; ctx->io_size = 0;
-    cudaError_t e = cudaMalloc(&ctx->io, need);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(host io)");
-    ctx->io_size = need;
-  }
+  s = grow_scratch(ctx, &ctx->io, &ctx->io_size, need, "cudaMalloc(host io)");
+  if (s != HD_OK) return s;
+  s = scratch_acquire(ctx, st);
+  if (s != HD_OK) return s;
   char* base = (char*)ctx->io;
   for (int k = 0; k < N; ++k) {
     char* df = base + k * bf;
@@ -1535,6 +1602,8 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
   if (s != HD_OK) return s;
   cudaError_t e = cudaMemcpyAsync(hh, P.h, (size_t)nh * eb, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(h)");
+  s = scratch_release(ctx, st);
+  if (s != HD_OK) return s;
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamSynchronize");
   return HD_OK;
@@ -1546,7 +1615,7 @@ hd_status_t hd_conv_host_async(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int
   Problem P;
   hd_status_t s = setup(ctx, P, dtype, ndim, N, batch, f, Lf, g, Lg, h, M, plan);
   if (s != HD_OK) return s;
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   hd_ctx::HostSlot& sl = ctx->hslot[ctx->hnext];
   ctx->hnext ^= 1;
@@ -1554,10 +1623,6 @@ hd_status_t hd_conv_host_async(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int
   if (!sl.st) {
     e = cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamCreate");
-  }
-  if (!ctx->compute_done) {
-    e = cudaEventCreateWithFlags(&ctx->compute_done, cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaEventCreate");
   }
   const size_t eb = elem_bytes(dtype);
   int64_t nf = batch, ng = P.shared_g ? 1 : batch, nh = batch;
@@ -1585,12 +1650,13 @@ hd_status_t hd_conv_host_async(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int
     P.g[k] = dg;
   }
   P.h = base + N * (bf + bg);
-  // the convolutions share the context workspace: run after the previous one
-  if (ctx->compute_pending) cudaStreamWaitEvent(sl.st, ctx->compute_done, 0);
+  // the convolutions share the context workspace: run after the previous user of it
+  s = scratch_acquire(ctx, sl.st);
+  if (s != HD_OK) return s;
   s = run_pipeline(ctx, P, nullptr, 0, sl.st);
   if (s != HD_OK) return s;
-  cudaEventRecord(ctx->compute_done, sl.st);
-  ctx->compute_pending = true;
+  s = scratch_release(ctx, sl.st);
+  if (s != HD_OK) return s;
   e = cudaMemcpyAsync(h, P.h, (size_t)nh * eb, cudaMemcpyDeviceToHost, sl.st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync(h)");
   return HD_OK;
@@ -1698,7 +1764,7 @@ hd_status_t hd_forward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines, 
   if (!x || !X || nlines < 1 || L < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
   if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < L)
     return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= L");
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   return forward_residues_locked(ctx, dtype, nlines, x, L, m, q, X, (cudaStream_t)stream);
 }
@@ -1709,13 +1775,17 @@ hd_status_t hd_backward_residues(hd_ctx_t ctx, hd_dtype_t dtype, int64_t nlines,
   if (!x || !X || nlines < 1 || Lout < 1) return fail(ctx, HD_ERR_INVALID, "bad arguments");
   if (!is_pow2(m) || m < 2 || m > 4096 || q < 1 || (int64_t)q * m < Lout)
     return fail(ctx, HD_ERR_INVALID, "need m a power of two in [2,4096] and q*m >= Lout");
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   return backward_residues_locked(ctx, dtype, nlines, X, m, q, x, Lout, (cudaStream_t)stream);
 }
 
 // Row f1: short f with size-m residues (q_f = Lambda q_g), long g
 // with size-(Lambda m) residues (q_g), matched product, size-(Lambda m) inverse.
+static hd_status_t lambda_locked(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
+                                 const void* g, int64_t Lg, void* h, int32_t m, int32_t Lambda, int32_t Lm,
+                                 int32_t qg, int32_t qf, int64_t M1, int64_t Lout, cudaStream_t st);
+
 hd_status_t hd_conv1d_lambda(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
                              const void* g, int64_t Lg, void* h, int64_t M, int32_t m, int32_t Lambda,
                              void* stream) {
@@ -1733,17 +1803,24 @@ hd_status_t hd_conv1d_lambda(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, cons
   if (qg64 * Lambda > (1 << 20)) return fail(ctx, HD_ERR_UNSUPPORTED, "too many residues");
   const int32_t qg = (int32_t)qg64, qf = Lambda * qg;
   const int64_t M1 = (int64_t)qg * Lm;
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   const size_t eb = elem_bytes(dtype);
   const size_t need = 2 * align256((size_t)batch * M1 * eb);
-  if (ctx->ws_size < need) {
-    if (ctx->ws) cudaFree(ctx->ws);
-    ctx->ws = nullptr; ctx->ws_size = 0;
-    cudaError_t e = cudaMalloc(&ctx->ws, need);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(workspace)");
-    ctx->ws_size = need;
-  }
+  hd_status_t sg = grow_scratch(ctx, &ctx->ws, &ctx->ws_size, need, "cudaMalloc(workspace)");
+  if (sg != HD_OK) return sg;
+  cudaStream_t st = (cudaStream_t)stream;
+  sg = scratch_acquire(ctx, st);
+  if (sg != HD_OK) return sg;
+  sg = lambda_locked(ctx, dtype, batch, f, Lf, g, Lg, h, m, Lambda, Lm, qg, qf, M1, Lout, st);
+  hd_status_t r = scratch_release(ctx, st);
+  return sg != HD_OK ? sg : r;
+}
+
+static hd_status_t lambda_locked(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
+                                 const void* g, int64_t Lg, void* h, int32_t m, int32_t Lambda, int32_t Lm,
+                                 int32_t qg, int32_t qf, int64_t M1, int64_t Lout, cudaStream_t st) {
+  const size_t eb = elem_bytes(dtype);
   char* Xf = (char*)ctx->ws;
   char* Xg = Xf + align256((size_t)batch * M1 * eb);
   const int32_t *perm_g = nullptr, *iperm_f = nullptr;
@@ -1751,7 +1828,6 @@ hd_status_t hd_conv1d_lambda(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, cons
   if (s != HD_OK) return s;
   s = get_perm(ctx, m, true, &iperm_f);
   if (s != HD_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
   s = forward_residues_locked(ctx, dtype, batch, f, Lf, m, qf, Xf, st);
   if (s != HD_OK) return s;
   s = forward_residues_locked(ctx, dtype, batch, g, Lg, Lm, qg, Xg, st);
@@ -1856,7 +1932,7 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   const int D = ap.D ? ap.D : q;
   if (D < 1 || D > q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
   if (ap.threads && !valid_threads(ap.threads)) return fail(ctx, HD_ERR_INVALID, "bad threads");
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   const bool dbl = dtype == HD_C128;
   const int64_t M1 = (int64_t)q * ap.m;
@@ -1990,9 +2066,13 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
   if (s != HD_OK) return s;
   const int reps = opts->reps > 0 ? opts->reps : 5;
   const bool fake = opts->fake_cost != 0;
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (!fake) {
+    s = scratch_acquire(ctx, st);
+    if (s != HD_OK) return s;
+  }
   const size_t eb = elem_bytes(dtype);
   // synthetic scratch operands of the problem's shape (timing is value independent)
   int64_t nf = batch, ng = batch, nh = batch;
@@ -2149,6 +2229,7 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
     if (best_t >= 1e300) time_plan(best, &best_t);
   }
   ctx->profiling = prof_was;
+  if (!fake) scratch_release(ctx, st);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   if (scratch) cudaFree(scratch);

@@ -352,24 +352,72 @@ class Context:
         import torch
         return torch.empty(shape, dtype=like.dtype, device=like.device)
 
+    def _arg(self, t, name, dtype, shape=None):
+        """Validate a device tensor before its pointer crosses the ABI: the kernels
+        trust dtype, extents, contiguity and device."""
+        if not hasattr(t, "data_ptr") or not hasattr(t, "device"):
+            raise TypeError(f"{name} must be a torch tensor")
+        if t.device.type != "cuda" or (t.device.index or 0) != int(self.device):
+            raise ValueError(f"{name} is on {t.device}, the context is on cuda:{self.device}")
+        if t.dtype != dtype:
+            raise TypeError(f"{name} has dtype {t.dtype}, expected {dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if shape is not None and list(t.shape) != [int(v) for v in shape]:
+            raise ValueError(f"{name} has shape {list(t.shape)}, expected {[int(v) for v in shape]}")
+        return t
+
+    def _pairs(self, fs, gs, batch=False, shared_g=False):
+        """Validate the operand lists of a (multi-)convolution: every f_k shares f_0's
+        dtype and shape, every g_k g_0's; the batch axis of g is 1 or absent only with
+        shared_g."""
+        if len(fs) != len(gs) or not fs:
+            raise ValueError("need the same number (>= 1) of f and g arrays")
+        f0, g0 = fs[0], gs[0]
+        _dtype_code(f0)
+        nd = f0.dim() - (1 if batch else 0)
+        if not 1 <= nd <= 3:
+            raise ValueError("ndim must be 1, 2 or 3")
+        for k, f in enumerate(fs):
+            self._arg(f, f"f[{k}]", f0.dtype, f0.shape)
+        if batch and not shared_g:
+            gshape = [f0.shape[0]] + list(g0.shape[-nd:])
+        elif batch and g0.dim() == nd + 1:
+            gshape = [1] + list(g0.shape[-nd:])
+        else:
+            gshape = list(g0.shape[-nd:])
+        if g0.dim() not in (nd, nd + 1) or (g0.dim() == nd + 1 and not batch):
+            raise ValueError(f"g has {g0.dim()} dims, expected {nd}" + (" (+ batch)" if batch else ""))
+        for k, g in enumerate(gs):
+            self._arg(g, f"g[{k}]", f0.dtype, gshape)
+        return nd
+
+    def _h(self, h, like, shape):
+        if h is None:
+            return self._out(like, shape)
+        return self._arg(h, "h", like.dtype, shape)
+
     def conv(self, f, g, M=None, plan=None, h=None, batch=False, shared_g=False, stream=None):
         """Full linear convolution of torch tensors f, g (1-3 dims, leading batch
         axis when batch=True)."""
-        nd = f.dim() - (1 if batch else 0)
+        nd = self._pairs([f], [g], batch, shared_g)
         B = f.shape[0] if batch else 1
         Lf = list(f.shape[-nd:])
         Lg = list(g.shape[-nd:])
         if plan is None and shared_g:
             plan = self.default_plan(_dtype_code(f), Lf, Lg, M)
-        if plan is not None and shared_g:
-            plan.flags |= HD_FLAG_SHARED_G
+        if plan is not None:
+            plan = Plan.from_buffer_copy(plan)  # never mutate the caller's plan
+            if shared_g:
+                plan.flags |= HD_FLAG_SHARED_G
+            else:
+                plan.flags &= ~HD_FLAG_SHARED_G
         out_shape = ([B] if batch else []) + [a + b - 1 for a, b in zip(Lf, Lg)]
         if plan is not None and (plan.flags & HD_FLAG_ALLOW_ALIAS):
             pc = hd_plan_complete(_dtype_code(f), Lf, Lg, Plan.from_buffer_copy(plan), M)
             out_shape = ([B] if batch else []) + [min(a + b - 1, pc.axis[i].M1)
                                                   for i, (a, b) in enumerate(zip(Lf, Lg))]
-        if h is None:
-            h = self._out(f, out_shape)
+        h = self._h(h, f, out_shape)
         dt = _dtype_code(f)
         Mv = _i64arr(M) if M is not None else _i64arr([0] * nd)
         pp = ctypes.byref(plan) if plan is not None else None
@@ -399,10 +447,9 @@ class Context:
     def hd_multiconv(self, fs, gs, M=None, plan=None, h=None, stream=None):
         """h = sum_k fs[k] * gs[k]."""
         N = len(fs)
-        nd = fs[0].dim()
+        nd = self._pairs(fs, gs)
         Lf, Lg = list(fs[0].shape), list(gs[0].shape)
-        if h is None:
-            h = self._out(fs[0], [a + b - 1 for a, b in zip(Lf, Lg)])
+        h = self._h(h, fs[0], [a + b - 1 for a, b in zip(Lf, Lg)])
         fp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in fs])
         gp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in gs])
         Mv = _i64arr(M) if M is not None else None
@@ -417,11 +464,10 @@ class Context:
         """Window [lo, lo + n) (per axis) of sum_k fs[k] * gs[k]; fs/gs lists of tensors
         (leading batch axis when batch=True).  See window_for_mode for the paper's modes."""
         N = len(fs)
-        nd = fs[0].dim() - (1 if batch else 0)
+        nd = self._pairs(fs, gs, batch)
         B = fs[0].shape[0] if batch else 1
         Lf, Lg = list(fs[0].shape[-nd:]), list(gs[0].shape[-nd:])
-        if h is None:
-            h = self._out(fs[0], ([B] if batch else []) + [int(v) for v in n])
+        h = self._h(h, fs[0], ([B] if batch else []) + [int(v) for v in n])
         fp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in fs])
         gp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in gs])
         Mv = _i64arr(M) if M is not None else None
@@ -445,11 +491,15 @@ class Context:
             dt = HD_C64
         else:
             raise TypeError(f"unsupported dtype {f.dtype} (float32 / float64 only)")
-        if g.dtype != f.dtype or not f.is_contiguous() or not g.is_contiguous():
-            raise TypeError("f and g must be contiguous tensors of the same real dtype")
+        self._arg(f, "f", f.dtype)
+        self._arg(g, "g", f.dtype, ([B] if batch else []) + Lg)
+        if g.dim() != f.dim():
+            raise ValueError("g must have f's number of dims (per-entry g when batch=True)")
+        oshape = ([B] if batch else []) + [a + b - 1 for a, b in zip(Lf, Lg)]
         if h is None:
-            h = torch.empty(([B] if batch else []) + [a + b - 1 for a, b in zip(Lf, Lg)], dtype=f.dtype,
-                            device=f.device)
+            h = torch.empty(oshape, dtype=f.dtype, device=f.device)
+        else:
+            self._arg(h, "h", f.dtype, oshape)
         pp = ctypes.byref(plan) if plan is not None else None
         self._chk(_lib.hd_conv_real(self.h, dt, nd, B, _ptr(f), _i64arr(Lf), _ptr(g), _i64arr(Lg), _ptr(h), pp,
                                     _stream_ptr(stream)))
@@ -459,10 +509,9 @@ class Context:
 
     def hd_conv_explicit(self, fs, gs, plan=None, h=None, stream=None):
         N = len(fs)
-        nd = fs[0].dim()
+        nd = self._pairs(fs, gs)
         Lf, Lg = list(fs[0].shape), list(gs[0].shape)
-        if h is None:
-            h = self._out(fs[0], [a + b - 1 for a, b in zip(Lf, Lg)])
+        h = self._h(h, fs[0], [a + b - 1 for a, b in zip(Lf, Lg)])
         fp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in fs])
         gp = (ctypes.c_void_p * N)(*[t.data_ptr() for t in gs])
         pp = ctypes.byref(plan) if plan is not None else None
@@ -470,18 +519,46 @@ class Context:
                                         _i64arr(Lg), _ptr(h), pp, _stream_ptr(stream)))
         return h
 
+    @staticmethod
+    def _host_args(fs, gs, h, ndim, batch, plan=None):
+        """Validate host operands of hd_conv_host(_async): the library copies exactly
+        batch * prod(L) elements of each input and batch * prod(L_out) into h."""
+        def info(a, name):
+            if isinstance(a, np.ndarray):
+                if not a.flags.c_contiguous:
+                    raise ValueError(f"{name} must be C-contiguous")
+                return str(a.dtype), list(a.shape), a.nbytes, a.ctypes.data
+            if not hasattr(a, "data_ptr") or a.device.type != "cpu" or not a.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous CPU tensor or numpy array")
+            return str(a.dtype).replace("torch.", ""), list(a.shape), a.numel() * a.element_size(), a.data_ptr()
+        nd = int(ndim)
+        if not 1 <= nd <= 3 or len(fs) != len(gs) or not fs:
+            raise ValueError("bad ndim or operand lists")
+        dt0, sf, _, _ = info(fs[0], "f[0]")
+        if dt0 not in ("complex128", "complex64"):
+            raise TypeError(f"unsupported dtype {dt0}")
+        esz = 16 if dt0 == "complex128" else 8
+        Lf, Lg = sf[-nd:], list(info(gs[0], "g[0]")[1])[-nd:]
+        shared = plan is not None and bool(plan.flags & HD_FLAG_SHARED_G)
+        nf, ng = int(np.prod(Lf)) * batch, int(np.prod(Lg)) * (1 if shared else batch)
+        for k, (f, g) in enumerate(zip(fs, gs)):
+            for a, name, n, L in ((f, f"f[{k}]", nf, Lf), (g, f"g[{k}]", ng, Lg)):
+                dt, shp, nb, _ = info(a, name)
+                if dt != dt0 or shp[-nd:] != L or nb != n * esz:
+                    raise ValueError(f"{name}: dtype {dt} shape {shp} does not match f[0] ({dt0}, batch {batch})")
+        dth, _, nbh, ptr = info(h, "h")
+        nh = batch * int(np.prod([a + b - 1 for a, b in zip(Lf, Lg)]))
+        if dth != dt0 or nbh != nh * esz:
+            raise ValueError(f"h must hold {nh} {dt0} elements ({nh * esz} bytes), got {dth} with {nbh} bytes")
+        return nd, Lf, Lg, (HD_C128 if dt0 == "complex128" else HD_C64), ptr
+
     def hd_conv_host(self, fs, gs, h, ndim, batch=1, M=None, plan=None, stream=None):
         """End-to-end with HOST buffers: fs, gs lists of (pinned) CPU tensors or numpy
         arrays ([batch] + extents), h a CPU tensor / numpy array receiving the result."""
         N = len(fs)
         def hp(a):
             return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
-        nd = int(ndim)
-        Lf = list(fs[0].shape)[-nd:]
-        Lg = list(gs[0].shape)[-nd:]
-        is128 = (fs[0].dtype == np.complex128) if isinstance(fs[0], np.ndarray) else \
-            (str(fs[0].dtype) == "torch.complex128")
-        dt = HD_C128 if is128 else HD_C64
+        nd, Lf, Lg, dt, _ = self._host_args(fs, gs, h, ndim, batch, plan)
         fp = (ctypes.c_void_p * N)(*[hp(t) for t in fs])
         gp = (ctypes.c_void_p * N)(*[hp(t) for t in gs])
         Mv = _i64arr(M) if M is not None else None
@@ -496,12 +573,7 @@ class Context:
         N = len(fs)
         def hp(a):
             return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
-        nd = int(ndim)
-        Lf = list(fs[0].shape)[-nd:]
-        Lg = list(gs[0].shape)[-nd:]
-        is128 = (fs[0].dtype == np.complex128) if isinstance(fs[0], np.ndarray) else \
-            (str(fs[0].dtype) == "torch.complex128")
-        dt = HD_C128 if is128 else HD_C64
+        nd, Lf, Lg, dt, _ = self._host_args(fs, gs, h, ndim, batch, plan)
         fp = (ctypes.c_void_p * N)(*[hp(t) for t in fs])
         gp = (ctypes.c_void_p * N)(*[hp(t) for t in gs])
         Mv = _i64arr(M) if M is not None else None
@@ -538,10 +610,14 @@ class Context:
             squeeze = True
         else:
             squeeze = False
+        _dtype_code(f)
+        if f.dim() != 2 or g.dim() != 2:
+            raise ValueError("f, g must be [L] or [batch, L]")
         nb, Lf = f.shape
         Lg = g.shape[1]
-        if h is None:
-            h = self._out(f, [nb, Lf + Lg - 1])
+        self._arg(f, "f", f.dtype)
+        self._arg(g, "g", f.dtype, [nb, Lg])
+        h = self._h(h, f, [nb, Lf + Lg - 1])
         self._chk(_lib.hd_conv1d_lambda(self.h, _dtype_code(f), nb, _ptr(f), Lf, _ptr(g), Lg, _ptr(h),
                                         0 if M is None else int(M), int(m), int(Lambda), _stream_ptr(stream)))
         return h[0] if squeeze else h

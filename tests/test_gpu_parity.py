@@ -793,3 +793,89 @@ def test_contexts_on_concurrent_threads(H):
         tol = 1e-11 if cases[i][1] == np.complex128 else 1e-5
         assert oracle.rel_l2(h, oracle.conv(f, g)) < tol, (i, rep)
     assert len(results) == 3 * len(cases)
+
+
+# ---------------------------------------------------------------- context scratch
+def test_graph_survives_lambda_workspace_growth(H):
+    """A larger hd_conv1d_lambda regrows the context workspace: captured graphs that
+    addressed the old one are dropped (re-captured), never replayed on freed memory."""
+    c = H.Context(0)
+    try:
+        f, g = synth.random_pair(1730, (40, 50), (9, 7))
+        plan = H.Plan.make(2, [{"m": 32, "C": 2, "S": 2}] * 2, flags=H.HD_FLAG_GRAPH)
+        fd, gd = dev(f), dev(g)
+        h = c.conv(fd, gd, plan=plan)
+        c.conv(fd, gd, plan=plan, h=h)
+        assert c.graph_replays() == 1
+        a, b = synth.random_pair(1731, (64, 3000), (64, 8192))
+        hl = host(c.conv1d_lambda(dev(a), dev(b), m=512, Lambda=2))   # grows ctx->ws
+        assert oracle.rel_l2(hl[5], oracle.conv(a[5], b[5])) < 1e-11
+        c.conv(fd, gd, plan=plan, h=h)               # re-captured, not replayed
+        assert c.graph_replays() == 1
+        c.conv(fd, gd, plan=plan, h=h)
+        assert c.graph_replays() == 2
+        assert oracle.rel_l2(host(h), oracle.conv(f, g)) < 1e-11
+    finally:
+        c.close()
+
+
+def test_shared_scratch_ordered_across_streams(H):
+    """Calls without a caller workspace share the context scratch: calls enqueued
+    back to back on two different streams (no host sync between) must not overwrite
+    each other's intermediates."""
+    c = H.Context(0)
+    try:
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        cases = [synth.random_pair(1740 + i, (700, 900), (120, 77)) for i in range(4)]
+        ins = [(dev(f), dev(g)) for f, g in cases]
+        torch.cuda.synchronize()
+        outs = []
+        for i, (fd, gd) in enumerate(ins):
+            s = s1 if i % 2 == 0 else s2
+            with torch.cuda.stream(s):
+                outs.append(c.conv(fd, gd, stream=s))
+        rf, rg = synth.random_pair(1745, (300, 200), (31, 17))
+        with torch.cuda.stream(s2):
+            rr = c.conv_real(dev(rf.real.copy()), dev(rg.real.copy()), stream=s2)
+        torch.cuda.synchronize()
+        for (f, g), h in zip(cases, outs):
+            idx = synth.sample_indices(h.shape, n_random=300)
+            got = h.cpu().numpy()[tuple(idx.T)]
+            assert oracle.rel_l2(got, oracle.conv_sampled(f, g, idx)) < 1e-11
+        assert oracle.rel_l2(rr.cpu().numpy(), oracle.conv(rf.real, rg.real)) < 1e-11
+    finally:
+        c.close()
+
+
+def test_binding_validates_operands(ctx, H):
+    """The binding refuses operands the kernels would misread."""
+    f, g = synth.random_pair(1750, (50,), (20,))
+    fd, gd = dev(f), dev(g)
+    with pytest.raises(TypeError):
+        ctx.conv(fd, gd.to(torch.complex64))
+    with pytest.raises(ValueError):
+        ctx.conv(fd[::2], gd)
+    with pytest.raises(ValueError):
+        ctx.conv(fd.unsqueeze(0).expand(4, 50).contiguous(), gd.unsqueeze(0).expand(3, 20).contiguous(), batch=True)
+    with pytest.raises(ValueError):
+        ctx.conv(fd, gd, h=torch.empty(10, dtype=fd.dtype, device="cuda"))
+    with pytest.raises(ValueError):
+        ctx.multiconv([fd, fd], [gd, gd[:10].contiguous()])
+    with pytest.raises(ValueError):
+        ctx.hd_conv_host([f], [g], np.zeros(10, dtype=np.complex128), ndim=1)
+    with pytest.raises(ValueError):
+        ctx.conv(fd.cpu(), gd.cpu())
+
+
+def test_shared_g_does_not_mutate_plan(ctx, H):
+    """conv(..., shared_g=True, plan=p) must not set HD_FLAG_SHARED_G on p: a later
+    per-entry-g call with the same plan uses every g_b."""
+    B = 3
+    f, _ = synth.random_pair(1760, (B, 200), (1,))
+    g = synth.random_pair(1761, (B, 60), (1,))[0]
+    plan = H.Plan.make(1, [{"m": 64}])
+    ctx.conv(dev(f), dev(g[0]), batch=True, shared_g=True, plan=plan)
+    assert not (plan.flags & H.HD_FLAG_SHARED_G)
+    h = host(ctx.conv(dev(f), dev(g), batch=True, plan=plan))
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
