@@ -93,20 +93,30 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12   # derived, see DESIGN.md section 6
+def fp64_peak():
+    """FP64 FMA throughput measured on this GPU model by tools/micro/fp64_peak.cu
+    (profiles/fp64_peak.json, committed); the derived 64 lanes/clk/SM figure only
+    if that file is missing (and then labelled as such)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["fp64_fma_tflops"]), "measured (profiles/fp64_peak.json: tools/micro/fp64_peak.cu DFMA chains)"
+    except Exception:
+        return 2 * 64 * 148 * 1.965e9 / 1e12, "derived: 64 FP64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz"
 
 
-def conv_flops(ndim, N, Lf, Lg, Lout, plan, batch=1):
-    """Algorithmic flops of one launch of the convolution pass:
-    per line of the convolution axis (axis 0) with plan (m, q, p_f, p_g, T)."""
-    a = plan.axis[0]
-    m, q, pf, pg = a.m, a.q, a.p_f, a.p_g
-    T = -(-Lout[0] // m)
-    per_line = ((2 * N + 1) * q * 5 * m * np.log2(m) + 8 * m * q * (pf + pg) * N
-                + 8 * m * q * T + 6 * m * q * N)
+def conv_flops(ndim, N, Lf, Lg, Lout, batch=1):
+    """Plan-independent algorithmic flops of the convolution pass (SURVEY.md 8(d),
+    VERDICT r01 item 2): per line of the convolution axis (axis 0) at minimal
+    padding M = L_out, (2N + 1) transforms of nominal 5 M log2 M flops (N forward f,
+    N forward g, one inverse) plus the N-pair product 6 M N; the lines are the
+    L_out extents of the other axes (minimal padding there too).  A worse plan
+    (more padding, naive folds) cannot raise it."""
+    M = Lout[0]
+    per_line = (2 * N + 1) * 5 * M * np.log2(M) + 6 * M * N
     lines = batch
     for i in range(1, ndim):
-        lines *= plan.axis[i].M1
+        lines *= Lout[i]
     return float(per_line * lines)
 
 
@@ -117,6 +127,17 @@ def ncu_traffic(kernel_name):
         with open(p) as fh:
             d = json.load(fh)
         return d.get("traffic_bytes_per_launch", {}).get(kernel_name)
+    except Exception:
+        return None
+
+
+def ncu_pipe(kernel_name):
+    """FP64 (c128) / FMA pipe utilisation of the kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("fp_pipe_pct", {}).get(kernel_name)
     except Exception:
         return None
 
@@ -373,27 +394,24 @@ def run_ours(args, rank, world, local_rank):
                 "share_of_step": dms / sum(v[0] for v in prof.values())}
         fl = None
         if dom.startswith("conv") or dom == "pass_conv":
-            fl = conv_flops(ndim, N, Lf, Lg, Lout, plan, batch) / (world if dom == "pass_conv" else 1)
-        if fl and eb == 16:
-            # the convolution pass is FP64-issue bound: its flops
-            # against the FP64 pipe, 64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz
+            fl = conv_flops(ndim, N, Lf, Lg, Lout, batch) / (world if dom == "pass_conv" else 1)
+        if fl:
+            # the convolution pass's arithmetic beside its HBM roofline: plan-independent
+            # flops against the measured FP64 (FP32 for c64: nominal 2x FP64 is NOT
+            # assumed -- the FP32 peak is the microbenchmark's FFMA figure) FMA peak
+            fpk, fsrc = fp64_peak()
+            if eb == 8:
+                try:
+                    with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+                        fpk, fsrc = float(json.load(fh)["fp32_fma_tflops"]), "measured FFMA (profiles/fp64_peak.json)"
+                except Exception:
+                    fpk, fsrc = 2 * 128 * 148 * 1.965e9 / 1e12, "derived: 128 FP32 lanes/clk/SM x 2 x 148 x 1.965 GHz"
             ach = fl / (avg * 1e-3) / 1e12
-            fp64 = {"achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": ach / FP64_PEAK_TFLOPS, "alg_flops_per_launch": fl,
-                    "flops": "nominal 5 m log2 m per residue FFT ((2N+1) q per line) + naive "
-                             "fold 8 m q (p_f+p_g) N + unfold 8 m q T + product 6 m q N"}
-            if fp64["frac"] > roof["frac"]:
-                # the binding roof is the FP64 pipe (plain ALU arithmetic): report it
-                # as the kernel's roofline, with the HBM figures alongside
-                hbm = {k: roof[k] for k in ("achieved", "peak", "unit", "frac", "peak_source",
-                                            "alg_bytes_per_launch")}
-                roof.update({"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                             "unit": "TFLOP/s", "frac": fp64["frac"],
-                             "peak_source": "derived: 64 FP64 FMA lanes/clk/SM x 2 x 148 SMs x 1.965 GHz "
-                                            "(DESIGN.md section 6)",
-                             "alg_flops_per_launch": fl, "flops": fp64["flops"], "hbm": hbm})
-            else:
-                roof["fp64"] = fp64
+            roof["alu"] = {"achieved": ach, "peak": fpk, "unit": "TFLOP/s", "frac": ach / fpk,
+                           "peak_source": fsrc, "alg_flops_per_launch": fl,
+                           "pipe_util_ncu": ncu_pipe(dom),
+                           "flops": "(2N+1) x 5 M log2 M + 6 M N per line, M = L_out of the conv axis, "
+                                    "lines = L_out of the other axes (plan-independent)"}
     total_ab = sum(v for k, v in ab.items() if k != "pass_conv")
     whole = {"alg_bytes_per_step": total_ab,
              "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,

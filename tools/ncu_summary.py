@@ -25,7 +25,7 @@ def val(row, key):
     return v * scale
 
 
-res = {"report": rep, "tag": tag, "kernels": {}, "traffic_bytes_per_launch": {}}
+res = {"report": rep, "tag": tag, "kernels": {}, "traffic_bytes_per_launch": {}, "fp_pipe_pct": {}}
 for name, row in zip(names, data):
     t = val(row, "gpu__time_duration.sum")
     rd = val(row, "dram__bytes_read.sum")
@@ -39,5 +39,11 @@ for name, row in zip(names, data):
          "registers": float(row[hdr.index("launch__registers_per_thread")])}
     res["kernels"][name] = k
     res["traffic_bytes_per_launch"][name] = rd + wr
+    fk = "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"
+    if "<double" in k["kernel"] or "s512" in k["kernel"]:
+        res["fp_pipe_pct"][name] = {"pipe": "fp64", "pct": k["fp64_pipe_pct"]}
+    else:
+        fm = "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"
+        res["fp_pipe_pct"][name] = {"pipe": "fma", "pct": float(row[hdr.index(fm)]) if fm in hdr else None}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res, indent=1))
