@@ -879,3 +879,4 @@ def test_shared_g_does_not_mutate_plan(ctx, H):
     h = host(ctx.conv(dev(f), dev(g), batch=True, plan=plan))
     for b in range(B):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
+
