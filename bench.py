@@ -10,9 +10,12 @@ complete hybrid-dealiased convolution (all three passes) through the C ABI.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config 3] [--no-tune] [--no-cpu]
 
-N > 1 runs under torchrun (one process per GPU, NCCL); each rank convolves its
-own image (weak scaling, no data-path collective: the 2D problems are
-independent), timing is the max over ranks.  `--impl reference` times the CPU
+N > 1: one process per GPU (bench.py spawns them with torch.distributed.run when
+it is not already under torchrun).  The headline is ONE problem slab-decomposed
+over the ranks (strong scaling; the NCCL all-to-alls run inside libhdconv,
+hd_conv2d_dist / hd_conv3d_dist, overlapped chunk by chunk with the passes);
+`weak_scaling` reports every rank convolving its own whole problem.  Timing is
+the max over ranks of CUDA-event time.  `--impl reference` times the CPU
 oracle (oracle/, plain direct convolution) on the host cores on a bounded
 sample of the same workload (rank 0 only).
 """
@@ -298,29 +301,30 @@ def run_ours(args, rank, world, local_rank):
     if plan is None:
         plan = ctx.default_plan(dtc, Lf, Lg, npairs=N)
     plan = H.hd_plan_complete(dtc, Lf, Lg, plan, npairs=N)
+    if dist:  # one plan for every rank (the slab exchange layouts depend on it): rank 0's
+        obj = [bytes(plan)]
+        dist.broadcast_object_list(obj, src=0)
+        plan = H.Plan.from_buffer_copy(obj[0])
 
     slab = None
-    if args.mode == "slab":
+    mode = args.mode if args.mode != "auto" else ("slab" if world > 1 and ndim >= 2 and N == 1 and batch == 1
+                                                  else "independent")
+    if mode == "slab":
         if ndim < 2 or N != 1 or batch != 1:
             raise SystemExit("--mode slab: 2D/3D single-pair configs only")
-        from paper_2306_10016_b200.dist import (GpuBackend, GpuBackend3D, SlabConv2D, SlabConv3D,
-                                                torch_exchange)
-
-        def local_exchange(send, recv, block):
-            recv[:block].copy_(send[:block])
-        exch = torch_exchange() if dist else local_exchange
-        if ndim == 2:
-            slab = SlabConv2D(GpuBackend(ctx, plan, dtc), exch, world, rank, Lf, Lg, plan.axis[1].M1)
-            r0, r1 = slab.plan.rows(rank)
-        else:
-            slab = SlabConv3D(GpuBackend3D(ctx, plan, dtc), exch, world, rank, Lf, Lg, plan.axis[1].M1,
-                              plan.axis[2].M1)
-            r0, r1 = slab.plan.planes(rank)
-        f_local = fd[0][r0:r1].contiguous()
+        # one problem over all ranks (strong scaling): libhdconv's NCCL slab path
+        # (hd_conv2d_dist / hd_conv3d_dist); Python only broadcasts the NCCL id
+        ctx.dist_init()
+        slab = ctx.slab(dtc, Lf, Lg, 0, plan)
+        f_local = fd[0][slab.in_lo:slab.in_hi].contiguous()
+        h_local = torch.empty([slab.out_hi - slab.out_lo] + Lout[1:], dtype=fd[0].dtype, device=dev)
 
     def step():
         if slab is not None:
-            slab(f_local, gd[0])
+            if ndim == 2:
+                ctx.conv2d_dist(f_local, gd[0], Lf, plan=plan, h=h_local)
+            else:
+                ctx.conv3d_dist(f_local, gd[0], Lf, plan=plan, h=h_local)
         elif N > 1:
             ctx.multiconv(fd, gd, plan=plan, h=hd_)
         else:
@@ -374,6 +378,28 @@ def run_ours(args, rank, world, local_rank):
     # weak: every rank convolves its own problem; strong (slab): one problem over all ranks
     value = (1 if slab is not None else world) * samples_per_step * args.steps / (ms * 1e-3)
 
+    # N > 1 in slab mode: also the weak-scaling figure (every rank its own whole problem
+    # on the single-GPU pipeline, no collective), max over ranks
+    weak = None
+    if slab is not None and world > 1:
+        def step_weak():
+            ctx.conv(fd[0], gd[0], plan=plan, h=hd_)
+        for _ in range(args.warmup):
+            step_weak()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_weak()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        wms = float(tt.item())
+        weak = {"value": world * samples_per_step * args.steps / (wms * 1e-3), "unit": UNIT,
+                "ms_per_step": wms / args.steps, "scaling": "weak",
+                "what": "every rank convolves its own whole problem (single-GPU pipeline), no collective"}
+
     # roofline of the dominant kernel (largest share of the step)
     peak, peak_src = peaks()
     ab = alg_bytes(ndim, N, Lf, Lg, Lout, eb, batch)
@@ -421,6 +447,30 @@ def run_ours(args, rank, world, local_rank):
 
     # end to end through the host-buffer C-ABI entry point (copies inside)
     e2e = None
+    if not args.no_e2e and slab is not None:
+        # end to end at N ranks: this rank's f slab and g from pinned host memory, the
+        # distributed call, its h slab back to pinned host memory, every step
+        fh_l = fh[0][slab.in_lo:slab.in_hi].contiguous().pin_memory()
+        hh_l = torch.empty(list(h_local.shape), dtype=h_local.dtype).pin_memory()
+        k2 = max(4, min(args.steps, 20))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(k2):
+            f_local.copy_(fh_l, non_blocking=True)
+            gd[0].copy_(gh[0], non_blocking=True)
+            step()
+            hh_l.copy_(h_local, non_blocking=True)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t
+        if dist:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": samples_per_step * k2 / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(fh_l.numel() * eb + sum(a.nbytes for a in g)),
+               "d2h_bytes_per_step": int(hh_l.numel() * eb), "steps": k2, "per": "rank (max over ranks)"}
     if not args.no_e2e and slab is None:
         # two result buffers: step k writes hh[k % 2] (asynchronous, double-buffered
         # entry point: the copy-in of step k+1 overlaps the copy-out of step k)
@@ -509,11 +559,47 @@ def run_ours(args, rank, world, local_rank):
             "roofline": roof, "whole_step": whole, "cpu_baseline": cpu, "e2e": e2e,
             "explicit_variant": explicit, "real_input_variant": real, "gpu_launches": int(launches), "clocks": clk,
         }
+        if slab is not None:
+            line["slab"] = {k: getattr(slab, k) for k in ("nchunks", "R", "Ro", "Ks", "block1", "block2",
+                                                          "bytes_sent")}
+            line["weak_scaling"] = weak
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     ctx.close()
+    return 0
+
+
+def spawn(args):
+    """--gpus N > 1 without a torchrun environment: launch N ranks of this script with
+    torch.distributed.run on this node (127.0.0.1) and pass its exit code through
+    (rank 0 prints the JSON line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")   # communicator lines on stderr (NVLS / rings)
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank launch plumbing without a GPU (gloo, one all_reduce)."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    else:
+        n = 1
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": n, "gpus_flag": args.gpus}), flush=True)
     return 0
 
 
@@ -529,13 +615,22 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-explicit", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--mode", default="independent", choices=["independent", "slab"],
-                    help="N>1: independent problems per rank (weak) or one slab-decomposed problem (strong)")
+    ap.add_argument("--mode", default="auto", choices=["auto", "independent", "slab"],
+                    help="auto: N = 1 single-GPU pipeline; N > 1 one slab-decomposed problem (strong "
+                         "scaling, NCCL exchanges in libhdconv) with weak scaling as an extra key; "
+                         "independent: each rank its own problem (weak); slab: slab path at any N")
+    ap.add_argument("--dry-run", action="store_true", help="launch plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.dry_run:
+        return run_dry(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local_rank)

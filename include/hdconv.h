@@ -69,7 +69,7 @@ typedef enum {
   HD_ERR_INVALID = 1,      /* bad sizes, pointers, plan */
   HD_ERR_UNSUPPORTED = 2,  /* valid request this build does not implement */
   HD_ERR_CUDA = 3,         /* CUDA runtime error (or no device) */
-  HD_ERR_NCCL = 4,         /* reserved for the distributed entry points */
+  HD_ERR_NCCL = 4,         /* NCCL missing or failed (distributed entry points) */
   HD_ERR_WORKSPACE = 5     /* caller workspace too small */
 } hd_status_t;
 
@@ -283,10 +283,96 @@ typedef struct {
   double scale;               /* CONV: product scale (1 / prod M1 over all axes) */
   int32_t batch_fastest;      /* 1: consecutive CTAs take consecutive batch entries */
   uint32_t flags;             /* HD_FLAG_GENERIC_FFT */
+  int32_t r_begin, r_end;     /* CONV only: residues [r_begin, r_end) (0, 0 = all q); the
+                                 output is then the partial sum over those residues of
+                                 the backward transform -- residue
+                                 sharding.  A partial range runs the generic engine. */
 } hd_pass_desc_t;
 /* Validate and launch one pass on `stream`.  Device pointers.  Returns
  * HD_ERR_INVALID on bad sizes/layouts, HD_ERR_UNSUPPORTED if no kernel exists. */
 hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* desc, void* stream);
+
+/* ---- multi-GPU: one process per GPU, NCCL over NVLink --------
+ * Bring-up: rank 0 calls hd_dist_unique_id and broadcasts the 128-byte id to the other
+ * ranks (the harness's own channel, e.g. torch.distributed); every rank then calls
+ * hd_dist_init on its context (device already selected).  nranks = 1 needs no id and
+ * no NCCL (the exchanges become local).  NCCL is bound at run time (libnccl.so.2: the
+ * copy already loaded in the process, else the system one); HD_ERR_NCCL if missing.
+ * The communicator and a communication stream belong to the context (released by
+ * hd_dist_init again or hd_destroy).  Errors of the calls below that are not a pass
+ * launch's are described by hd_dist_last_error() (thread-local). */
+hd_status_t hd_dist_unique_id(void* id /* 128 bytes out */);
+hd_status_t hd_dist_init(hd_ctx_t ctx, const void* id, int32_t nranks, int32_t rank);
+const char* hd_dist_last_error(void);
+/* The library's contiguous partition of `extent` items: rank gets [lo, hi), blocks of
+ * ceil(extent / nranks) (the last ones may be short or empty). */
+hd_status_t hd_dist_partition(int64_t extent, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
+
+/* 1-D: batch of independent pairs f[b] * g[b] (BASELINE config 2).
+ *  HD_SHARD_BATCH   f, g, h hold ONLY this rank's batch slice [lo, hi) of
+ *                   hd_dist_partition(batch): no collective.
+ *  HD_SHARD_RESIDUE f, g hold the WHOLE batch on every rank; the q residues of every
+ *                   line are split over the ranks (hd_dist_partition(q)) -- residues are
+ *                   independent (Forward Eq. PAPER.md:528) -- each rank
+ *                   computes its residues' backward contributions for all
+ *                   lines and an NCCL reduce-scatter (sum) leaves h = the rank's batch
+ *                   slice [lo, hi) of hd_dist_partition(batch), (hi - lo) x (Lf+Lg-1). */
+#define HD_SHARD_BATCH   0u
+#define HD_SHARD_RESIDUE 1u
+hd_status_t hd_conv1d_dist(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const void* f, int64_t Lf,
+                           const void* g, int64_t Lg, void* h, const hd_plan_t* plan, uint32_t shard,
+                           void* stream);
+
+/* 2-D / 3-D slab decomposition along axis 0 (separable passes).
+ * hd_dist_slab_plan (host only) gives a rank's share and the exchange layout:
+ *  in_lo/in_hi   rows (2-D) / planes (3-D) of f this rank holds (row-major, contiguous)
+ *  out_lo/out_hi rows / planes of h it receives
+ *  spec_lo/hi    spectral lines of axis 1 (2-D: kx columns; 3-D: ky rows) it convolves
+ *  R, Ro, Ks     per-rank input, output and spectral extents (2-D: R and Ks padded to
+ *                multiples of nchunks); chunk_rows = R / nchunks, chunk_cols = Ks / nchunks
+ *                (3-D: chunk_cols = the kx tile of the exchange blocks)
+ *  block1/2      elements of one (sender, receiver) block in the two all-to-alls
+ *  bytes_sent    bytes leaving this rank per call (both exchanges, self excluded)
+ *  scale         1 / prod M1 (the product's normalisation)
+ *  plan          the completed plan of the global problem
+ * 2-D overlap: pass A (forward along x) runs by row chunks and each chunk's all-to-all
+ * starts on the communication stream as soon as its chunk is written; pass B
+ * (convolution along y) runs by column chunks, each chunk's all-to-all likewise; pass C
+ * (inverse along x) waits for the second exchange.  nchunks = 0: 4 (1 at nranks = 1). */
+typedef struct {
+  int32_t ndim, nranks, rank, nchunks;
+  int64_t in_lo, in_hi, out_lo, out_hi, spec_lo, spec_hi;
+  int64_t R, Ro, Ks, chunk_rows, chunk_cols;
+  int64_t block1, block2, bytes_sent;
+  double scale;
+  hd_plan_t plan;
+} hd_slab_plan_t;
+hd_status_t hd_dist_slab_plan(hd_dtype_t dtype, int32_t ndim, int32_t nranks, int32_t rank, int32_t nchunks,
+                              const int64_t* Lf, const int64_t* Lg, const hd_plan_t* plan, hd_slab_plan_t* out);
+/* One rank's compute stages without the exchanges (the building blocks of
+ * hd_conv2d_dist / hd_conv3d_dist; also lets a caller run its own exchange, e.g. to
+ * check the layouts with emulated ranks).  Device buffers; `S` from hd_dist_slab_plan:
+ *   stage 0: in = g (whole)               -> out = transformed g (hd_slab_g_bytes)
+ *   stage 1: in = f slab                  -> out = send1 (nranks x block1 elements)
+ *   stage 2: in = recv1, gt = stage 0 out -> out = send2 (nranks x block2 elements)
+ *   stage 3: in = recv2                   -> out = h slab
+ * recv = the all-to-all of send: block b of rank k's recv is block k of rank b's send.
+ * 3-D stages 0, 1, 3 need `scratch` of hd_slab_scratch_bytes (2-D: unused). */
+hd_status_t hd_slab_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_plan_t* S, const int64_t* Lf,
+                          const int64_t* Lg, int32_t stage, const void* in, const void* gt, void* out,
+                          void* scratch, void* stream);
+size_t hd_slab_scratch_bytes(hd_dtype_t dtype, const hd_slab_plan_t* S, const int64_t* Lf, const int64_t* Lg);
+size_t hd_slab_g_bytes(hd_dtype_t dtype, const hd_slab_plan_t* S, const int64_t* Lg);
+/* f_rows: rows [in_lo, in_hi) of f ([rows][Lf[1]], device); g: the whole g on every
+ * rank; h_rows: rows [out_lo, out_hi) of h ([rows][Lf[1]+Lg[1]-1]).  Lf, Lg: GLOBAL
+ * extents.  Every rank must call with the same extents, plan and nchunks. */
+hd_status_t hd_conv2d_dist(hd_ctx_t ctx, hd_dtype_t dtype, const void* f_rows, const int64_t Lf[2],
+                           const void* g, const int64_t Lg[2], void* h_rows, const hd_plan_t* plan,
+                           int32_t nchunks, void* stream);
+/* The same with planes of 3-D arrays (f_planes [planes][Lf1][Lf2], h_planes likewise). */
+hd_status_t hd_conv3d_dist(hd_ctx_t ctx, hd_dtype_t dtype, const void* f_planes, const int64_t Lf[3],
+                           const void* g, const int64_t Lg[3], void* h_planes, const hd_plan_t* plan,
+                           void* stream);
 
 /* ---- tuning (the paper's "experience") -------------------- */
 #define HD_TUNE_PER_AXIS   0x0u   /* search each axis independently */

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhdconv.so")
 BUILD = os.path.join(HERE, "csrc", "build")
-SOURCES = ["hd_kernels.cu", "hd_api.cu", "hd_k_s512.cu", "hd_k_s128.cu"] + [f"hd_k_{d}_{n}.cu" for d in ("f64", "f32") for n in (256, 576, 1024)]
+SOURCES = ["hd_kernels.cu", "hd_api.cu", "hd_dist.cu", "hd_k_s512.cu", "hd_k_s128.cu"] + [f"hd_k_{d}_{n}.cu" for d in ("f64", "f32") for n in (256, 576, 1024)]
 HEADERS = ["hd_device.cuh", "hd_internal.h", "hd_kernels.cuh", "hd_w512.cuh", "hd_s512.cuh", "hd_s128.cuh", "hd_s512c.cuh", "hd_s2048c.cuh", "hd_tma.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(_compile, SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -1188,6 +1188,7 @@ hd_status_t hd_create(hd_ctx_t* out, int device) {
 hd_status_t hd_destroy(hd_ctx_t ctx) {
   if (!ctx) return HD_OK;
   cudaSetDevice(ctx->device);
+  hd::dist_release(ctx);
   for (auto& kv : ctx->tw64) cudaFree(kv.second);
   for (auto& kv : ctx->tw32) cudaFree(kv.second);
   for (auto& kv : ctx->st64) cudaFree(kv.second);
@@ -1932,6 +1933,11 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   const int D = ap.D ? ap.D : q;
   if (D < 1 || D > q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
   if (ap.threads && !valid_threads(ap.threads)) return fail(ctx, HD_ERR_INVALID, "bad threads");
+  const bool rrange = d->r_begin != 0 || (d->r_end != 0 && d->r_end != q);
+  if (d->r_begin < 0 || d->r_end < 0 || d->r_end > q || (d->r_end != 0 && d->r_begin >= d->r_end) ||
+      (d->r_end == 0 && d->r_begin != 0))
+    return fail(ctx, HD_ERR_INVALID, "residue range must satisfy 0 <= r_begin < r_end <= q");
+  if (rrange && d->mode != HD_PASS_CONV) return fail(ctx, HD_ERR_INVALID, "a residue range needs HD_PASS_CONV");
   std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   const bool dbl = dtype == HD_C128;
@@ -1945,7 +1951,7 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   if (s != HD_OK) return s;
   Launch L;
   std::memset(&L, 0, sizeof(L));
-  L.flags = d->flags;
+  L.flags = d->flags | (rrange ? HD_FLAG_GENERIC_FFT : 0u);  // residue subsets: generic engine
   L.mode = d->mode;
   L.name = d->mode == HD_PASS_FWD ? "pass_fwd" : (d->mode == HD_PASS_INV ? "pass_inv" : "pass_conv");
   // forward / inverse keep the documented spectral order unless the caller opts into
@@ -1977,6 +1983,8 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   L.a.npairs = d->mode == HD_PASS_CONV ? d->npairs : 1;
   L.a.scale = d->mode == HD_PASS_CONV ? d->scale : 1.0;
   L.a.nlines = d->nlines; L.a.nbatch = d->nbatch; L.a.batch_fastest = d->batch_fastest ? 1 : 0;
+  L.a.r_lo = rrange ? d->r_begin : 0;
+  L.a.r_hi = rrange ? d->r_end : 0;
   L.narrays = d->mode == HD_PASS_FWD ? narr : 1;
   L.ngroups = cdiv(d->nlines, C); L.nbatch = d->nbatch;
   if (staged_order && d->mode != HD_PASS_CONV && !use_s512(dtype, L) && !use_s128(dtype, L))

@@ -327,6 +327,10 @@ struct PassArgs {
   int64_t rp_off, rp_rows;
   int64_t rs_A, rs_side_rows, rs_rows;
   void* rs_side;
+  // residue range [r_lo, r_hi) of a generic-engine CONV pass (r_hi = 0: all q): the
+  // output is the partial sum over those residues of the backward transform
+  // (PAPER.md:531), e.g. one rank's share under residue sharding (hd_conv1d_dist)
+  int32_t r_lo, r_hi;
 };
 
 enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2, MODE_MCONV = 3 /* staged engine only */ };
@@ -792,8 +796,9 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
       prefetch_lines<V>(a.in_f, MODE == MODE_FWD ? k_arr : 0, bn, gn, C, a.nlines);
     }
   }
-  for (int r0 = 0; r0 < q; r0 += D) {
-    const int nd = (q - r0) < D ? (q - r0) : D;
+  const int rlo = a.r_lo, rhi = a.r_hi > 0 ? a.r_hi : q;
+  for (int r0 = rlo; r0 < rhi; r0 += D) {
+    const int nd = (rhi - r0) < D ? (rhi - r0) : D;
     if constexpr (MODE == MODE_FWD) {
       fold<V, M, NT>(bufF, a.in_f, k_arr, b, g, a.nlines, C, clog, r0, nd, q, zq, zt, twm, twM1);
       __syncthreads();
@@ -804,7 +809,7 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
       inv_first_load<V, M, NT>(bufF, a.in_f, b, g, a.nlines, C, clog, r0, nd, twst);
       __syncthreads();
       fft_inv_from<V, M, NT, NST - 2>(bufF, C * nd, twst);
-      unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
+      unfold<V, M, NT>(bufF, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > rlo, zq, zt, twm, twM1);
       __syncthreads();
     } else {
       const T scale = (T)a.scale;
@@ -824,7 +829,7 @@ __global__ void __launch_bounds__(NT) pass_kernel(const __grid_constant__ PassAr
         __syncthreads();
       }
       fft_inv_from<V, M, NT, NST - 2>(P, C * nd, twst);
-      unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > 0, zq, zt, twm, twM1);
+      unfold<V, M, NT>(P, a.out, 0, b, g, a.nlines, C, clog, r0, nd, q, r0 > rlo, zq, zt, twm, twM1);
       __syncthreads();
     }
   }

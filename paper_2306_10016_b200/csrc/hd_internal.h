@@ -63,4 +63,6 @@ constexpr size_t kMaxSmem = 227 * 1024;
 // or when already allowed), and the current device's SM count.
 cudaError_t allow_dynamic_smem(const void* fn, size_t smem);
 int device_sm_count();
+// hd_dist.cu: release a context's communicator and exchange buffers (hd_destroy)
+void dist_release(struct hd_ctx* ctx);
 }  // namespace hd

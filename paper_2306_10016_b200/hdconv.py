@@ -43,7 +43,11 @@ EXPORTED = [
     "hd_conv_host_async", "hd_host_sync",
     "hd_forward_residues", "hd_backward_residues", "hd_tune", "hd_tune_ex", "hd_tune_log",
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_graph_replays", "hd_pass", "hd_conv1d_lambda",
+    "hd_dist_unique_id", "hd_dist_init", "hd_dist_last_error", "hd_dist_partition", "hd_dist_slab_plan",
+    "hd_conv1d_dist", "hd_conv2d_dist", "hd_conv3d_dist", "hd_slab_stage", "hd_slab_scratch_bytes",
+    "hd_slab_g_bytes",
 ]
+HD_SHARD_BATCH, HD_SHARD_RESIDUE = 0, 1
 HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
 
 
@@ -109,7 +113,25 @@ class PassDesc(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("npairs", ctypes.c_int32), ("nlines", ctypes.c_int64),
                 ("nbatch", ctypes.c_int64), ("M", ctypes.c_int64), ("axis", AxisPlan),
                 ("in_f", Lines), ("in_g", Lines), ("out", Lines), ("scale", ctypes.c_double),
-                ("batch_fastest", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("batch_fastest", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("r_begin", ctypes.c_int32), ("r_end", ctypes.c_int32)]
+
+
+class SlabPlan(ctypes.Structure):
+    """hd_slab_plan_t: one rank's share of a 2-D / 3-D slab decomposition (include/hdconv.h)."""
+    _fields_ = [("ndim", ctypes.c_int32), ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("nchunks", ctypes.c_int32),
+                ("in_lo", ctypes.c_int64), ("in_hi", ctypes.c_int64), ("out_lo", ctypes.c_int64),
+                ("out_hi", ctypes.c_int64), ("spec_lo", ctypes.c_int64), ("spec_hi", ctypes.c_int64),
+                ("R", ctypes.c_int64), ("Ro", ctypes.c_int64), ("Ks", ctypes.c_int64),
+                ("chunk_rows", ctypes.c_int64), ("chunk_cols", ctypes.c_int64),
+                ("block1", ctypes.c_int64), ("block2", ctypes.c_int64), ("bytes_sent", ctypes.c_int64),
+                ("scale", ctypes.c_double), ("plan", Plan)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "plan"}
+        d["plan"] = self.plan.as_dict()
+        return d
 
 
 class HDError(RuntimeError):
@@ -158,6 +180,18 @@ def _load():
         "hd_graph_replays": ([P], I64),
         "hd_conv1d_lambda": ([P, ctypes.c_int, I64, P, I64, P, I64, P, I64, I32, I32, P], ctypes.c_int),
         "hd_pass": ([P, ctypes.c_int, ctypes.POINTER(PassDesc), P], ctypes.c_int),
+        "hd_dist_unique_id": ([P], ctypes.c_int),
+        "hd_dist_init": ([P, P, I32, I32], ctypes.c_int),
+        "hd_dist_last_error": ([], ctypes.c_char_p),
+        "hd_dist_partition": ([I64, I32, I32, P, P], ctypes.c_int),
+        "hd_dist_slab_plan": ([ctypes.c_int, I32, I32, I32, I32, P, P, PP, ctypes.POINTER(SlabPlan)],
+                              ctypes.c_int),
+        "hd_conv1d_dist": ([P, ctypes.c_int, I64, P, I64, P, I64, P, PP, U32, P], ctypes.c_int),
+        "hd_conv2d_dist": ([P, ctypes.c_int, P, P, P, P, P, PP, I32, P], ctypes.c_int),
+        "hd_conv3d_dist": ([P, ctypes.c_int, P, P, P, P, P, PP, P], ctypes.c_int),
+        "hd_slab_stage": ([P, ctypes.c_int, ctypes.POINTER(SlabPlan), P, P, I32, P, P, P, P, P], ctypes.c_int),
+        "hd_slab_scratch_bytes": ([ctypes.c_int, ctypes.POINTER(SlabPlan), P, P], SZ),
+        "hd_slab_g_bytes": ([ctypes.c_int, ctypes.POINTER(SlabPlan), P], SZ),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -182,6 +216,39 @@ def _check(status, ctx=None):
     if status != HD_OK:
         msg = _lib.hd_last_error(ctx)
         raise HDError(status, msg.decode() if msg else "")
+
+
+def _check_dist(status, ctx=None):
+    """Status of a distributed entry point: its own message, else the pass's."""
+    if status != HD_OK:
+        msg = _lib.hd_dist_last_error() or b""
+        if not msg and ctx is not None:
+            msg = _lib.hd_last_error(ctx) or b""
+        raise HDError(status, msg.decode())
+
+
+def dist_partition(extent, nranks, rank):
+    """[lo, hi) of `extent` items owned by `rank` (hd_dist_partition)."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check_dist(_lib.hd_dist_partition(int(extent), int(nranks), int(rank), ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def slab_buffer_elems(dtype, sp, Lf, Lg):
+    """Element counts of a rank's slab buffers: transformed g, send/recv 1 and 2, 3-D scratch."""
+    esz = 16 if dtype == HD_C128 else 8
+    g = _lib.hd_slab_g_bytes(dtype, ctypes.byref(sp), _i64arr(Lg)) // esz
+    sc = _lib.hd_slab_scratch_bytes(dtype, ctypes.byref(sp), _i64arr(Lf), _i64arr(Lg)) // esz
+    return dict(g=int(g), x1=int(sp.nranks * sp.block1), x2=int(sp.nranks * sp.block2), scratch=int(sc))
+
+
+def slab_plan(dtype, Lf, Lg, nranks, rank, nchunks=0, plan=None):
+    """hd_dist_slab_plan (host only): this rank's rows/planes, spectral lines, exchange blocks."""
+    sp = SlabPlan()
+    pp = ctypes.byref(plan) if plan is not None else None
+    _check_dist(_lib.hd_dist_slab_plan(dtype, len(Lf), int(nranks), int(rank), int(nchunks), _i64arr(Lf),
+                                       _i64arr(Lg), pp, ctypes.byref(sp)))
+    return sp
 
 
 def _dtype_code(t):
@@ -332,6 +399,7 @@ class Context:
         _check(_lib.hd_create(ctypes.byref(h), int(device)))
         self.h = h
         self.device = device
+        self.world, self.rank = 1, 0
 
     def close(self):
         if self.h:
@@ -691,6 +759,77 @@ class Context:
     def engine_launches(self, engine):
         """Pass launches on one engine (HD_ENGINE_*) since the context was created."""
         return int(_lib.hd_engine_launches(self.h, engine))
+
+    # ---- multi-GPU (include/hdconv.h "multi-GPU"): NCCL inside libhdconv ---------
+    def dist_init(self, group=None):
+        """Create this context's NCCL communicator over the torch.distributed group: rank
+        0 draws the unique id (hd_dist_unique_id) and the group broadcasts it (the only
+        Python-side step); a group of one needs no NCCL."""
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if world > 1:
+            if rank == 0:
+                _check_dist(_lib.hd_dist_unique_id(uid))
+            obj = [bytes(uid.raw)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        _check_dist(_lib.hd_dist_init(self.h, uid, world, rank))
+        self.world, self.rank = world, rank
+        return world, rank
+
+    def conv1d_dist(self, f, g, batch, shard=HD_SHARD_BATCH, plan=None, h=None, stream=None):
+        """1-D batch of pairs over the ranks (hd_conv1d_dist): HD_SHARD_BATCH with f, g this
+        rank's slice; HD_SHARD_RESIDUE with f, g the whole batch.  Returns this rank's rows."""
+        Lf, Lg = f.shape[-1], g.shape[-1]
+        lo, hi = dist_partition(batch, self.world, self.rank)
+        nb = hi - lo if shard == HD_SHARD_BATCH else batch
+        self._arg(f, "f", f.dtype, [nb, Lf])
+        self._arg(g, "g", f.dtype, [nb, Lg])
+        h = self._h(h, f, [hi - lo, Lf + Lg - 1])
+        pp = ctypes.byref(plan) if plan is not None else None
+        _check_dist(_lib.hd_conv1d_dist(self.h, _dtype_code(f), int(batch), _ptr(f), Lf, _ptr(g), Lg, _ptr(h), pp,
+                                        int(shard), _stream_ptr(stream)), self.h)
+        return h
+
+    def slab(self, dtype, Lf, Lg, nchunks=0, plan=None):
+        return slab_plan(dtype, Lf, Lg, self.world, self.rank, nchunks, plan)
+
+    def conv2d_dist(self, f_rows, g, Lf, plan=None, nchunks=0, h=None, stream=None):
+        """This rank's output rows of f * g with f row-slab decomposed (hd_conv2d_dist);
+        f_rows = rows [in_lo, in_hi) of f (Lf: global extents), g replicated."""
+        dt = _dtype_code(g)
+        Lg = list(g.shape)
+        sp = self.slab(dt, Lf, Lg, nchunks, plan)
+        self._arg(f_rows, "f_rows", g.dtype, [sp.in_hi - sp.in_lo, Lf[1]])
+        self._arg(g, "g", g.dtype)
+        h = self._h(h, g, [sp.out_hi - sp.out_lo, Lf[1] + Lg[1] - 1])
+        pp = ctypes.byref(plan) if plan is not None else None
+        _check_dist(_lib.hd_conv2d_dist(self.h, dt, _ptr(f_rows), _i64arr(Lf), _ptr(g), _i64arr(Lg), _ptr(h), pp,
+                                        int(nchunks), _stream_ptr(stream)), self.h)
+        return h
+
+    def conv3d_dist(self, f_planes, g, Lf, plan=None, h=None, stream=None):
+        """This rank's output planes of f * g with f z-slab decomposed (hd_conv3d_dist)."""
+        dt = _dtype_code(g)
+        Lg = list(g.shape)
+        sp = self.slab(dt, Lf, Lg, 1, plan)
+        self._arg(f_planes, "f_planes", g.dtype, [sp.in_hi - sp.in_lo, Lf[1], Lf[2]])
+        self._arg(g, "g", g.dtype)
+        h = self._h(h, g, [sp.out_hi - sp.out_lo] + [a + b - 1 for a, b in zip(Lf[1:], Lg[1:])])
+        pp = ctypes.byref(plan) if plan is not None else None
+        _check_dist(_lib.hd_conv3d_dist(self.h, dt, _ptr(f_planes), _i64arr(Lf), _ptr(g), _i64arr(Lg), _ptr(h), pp,
+                                        _stream_ptr(stream)), self.h)
+        return h
+
+    def slab_stage(self, dtype, sp, Lf, Lg, stage, inp, out, gt=None, scratch=None, stream=None):
+        """One compute stage of a slab decomposition (hd_slab_stage), no exchange."""
+        p = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _check_dist(_lib.hd_slab_stage(self.h, dtype, ctypes.byref(sp), _i64arr(Lf), _i64arr(Lg), int(stage),
+                                       p(inp), p(gt), p(out), p(scratch), _stream_ptr(stream)), self.h)
+        return out
 
     def hd_pass(self, dtype, desc, stream=None):
         """One pass with explicit layouts (include/hdconv.h hd_pass)."""

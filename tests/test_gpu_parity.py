@@ -496,47 +496,6 @@ def test_s512_residues_match_dft(ctx, H, L, q):
             assert oracle.rel_l2(got, full[l][r::q]) < 1e-12
 
 
-# ---------------------------------------------------------------- slab decomposition (hd_pass)
-@pytest.mark.parametrize("world", [1, 2, 3, 4])
-@pytest.mark.parametrize("shape,m", [(((300, 260), (31, 17)), 64), (((1100, 700), (255, 60)), 512)])
-def test_slab_decomposition_emulated_ranks(ctx, H, world, shape, m):
-    """The multi-GPU slab path's kernels (hd_pass with the exchange layouts), with the
-    NCCL all-to-all replaced by device block copies between emulated ranks."""
-    from paper_2306_10016_b200.dist import GpuBackend, SlabConv2D, emulate_ranks
-    (Lf, Lg) = shape
-    f, g = synth.random_pair(400 + world, Lf, Lg)
-    plan = H.hd_plan_complete(H.HD_C128, list(Lf), list(Lg), H.Plan.make(2, [{"m": m}, {"m": m}]))
-    Kx = plan.axis[1].M1
-    be = GpuBackend(ctx, plan, H.HD_C128)
-    convs = [SlabConv2D(be, None, world, k, Lf, Lg, Kx) for k in range(world)]
-    parts = emulate_ranks(convs, dev(f), dev(g), be.empty)
-    h = np.concatenate([host(p) for p in parts], axis=0)
-    assert oracle.rel_l2(h, oracle.conv(f, g)) < 1e-11
-
-
-@pytest.mark.parametrize("world", [1, 2, 3])
-@pytest.mark.parametrize("dtype,m,C", [(np.complex128, 16, 1), (np.complex64, 16, 1), (np.complex128, 32, 1),
-                                       (np.complex64, 128, 4)])  # last: the c64 staged conv pass in hd_pass
-def test_slab3d_emulated_ranks(ctx, H, world, dtype, m, C):
-    """3-D z-slab path (dist.SlabConv3D on hd_pass) with the all-to-alls replaced by
-    block copies between emulated ranks."""
-    from paper_2306_10016_b200.dist import GpuBackend3D, SlabConv3D, emulate_ranks_3d
-    Lf, Lg = (21, 18, 24) if m < 128 else (150, 18, 24), (5, 7, 4)
-    f, g = synth.random_pair(820 + world, Lf, Lg, dtype=dtype)
-    dt = H.HD_C128 if dtype == np.complex128 else H.HD_C64
-    plan = H.hd_plan_complete(dt, list(Lf), list(Lg), H.Plan.make(3, [{"m": m, "C": C}] * 3))
-    Ky, Kx = plan.axis[1].M1, plan.axis[2].M1
-    be = GpuBackend3D(ctx, plan, dt)
-    convs = [SlabConv3D(be, None, world, k, Lf, Lg, Ky, Kx) for k in range(world)]
-    n0 = ctx.engine_launches(H.HD_ENGINE_S128)
-    parts = emulate_ranks_3d(convs, dev(f), dev(g), be.empty)
-    h = np.concatenate([host(p) for p in parts], axis=0)
-    tol = 1e-11 if dtype == np.complex128 else 1e-5
-    assert oracle.rel_l2(h, oracle.conv(f, g)) < tol
-    if m == 128:  # kx tiles of 4: all seven passes of every rank on the staged engine
-        assert ctx.engine_launches(H.HD_ENGINE_S128) - n0 == 7 * world
-
-
 # ---------------------------------------------------------------- staged engine (m = 128, complex64)
 # hd_s128.cuh runs every pass of a complex64 axis with m = 128, C = 4 lines per item
 # and D = q <= 8 (automatic engine choice); HD_ENGINE_S128 counts its launches.
