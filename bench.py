@@ -428,8 +428,8 @@ def run_ours(args, rank, world, local_rank):
             fpk, fsrc = fp64_peak()
             if eb == 8:
                 try:
-                    with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
-                        fpk, fsrc = float(json.load(fh)["fp32_fma_tflops"]), "measured FFMA (profiles/fp64_peak.json)"
+                    with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fp:
+                        fpk, fsrc = float(json.load(fp)["fp32_fma_tflops"]), "measured FFMA (profiles/fp64_peak.json)"
                 except Exception:
                     fpk, fsrc = 2 * 128 * 148 * 1.965e9 / 1e12, "derived: 128 FP32 lanes/clk/SM x 2 x 148 x 1.965 GHz"
             ach = fl / (avg * 1e-3) / 1e12

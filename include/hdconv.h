@@ -292,6 +292,27 @@ typedef struct {
  * HD_ERR_INVALID on bad sizes/layouts, HD_ERR_UNSUPPORTED if no kernel exists. */
 hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* desc, void* stream);
 
+/* ---- image filtering ------------------------
+ * The paper's demo convolves every channel of an image with one of eight small named
+ * kernels (Identity, Ridge_detection_1, Ridge_detection_2, Sharpen,
+ * Box_blur, Gaussian_blur, Gaussian_blur_5, Unsharpen_masking -- ids 0..7 in that order)
+ * and keeps the real part of each channel's result.
+ * hd_filter_kernel (host only): kernel `id` -> its n x n weights (row-major, scale
+ * applied; w may be NULL), n and its name.  hd_filter_image: img is a REAL H x W image
+ * with C channels (double for HD_C128, float for HD_C64; channel_last = 1: [H][W][C] as
+ * decoded images are, 0: [C][H][W]); every channel is convolved with the kernel through
+ * the real-input path (hd_conv_real, the channels as one batch), and the window
+ * [win_lo, win_lo + win_n) of the full (H + n - 1) x (W + n - 1) result (NULL = all) is
+ * written to out in the same channel layout (real values; the listing's further crop
+ * and uint8 cast belong to its PNG round trip, which is not built).  Device pointers;
+ * scratch is stream-ordered (cudaMallocAsync).  Errors: hd_filter_last_error(). */
+#define HD_FILTER_COUNT 8
+hd_status_t hd_filter_kernel(int32_t id, double* w, int32_t* n, const char** name);
+hd_status_t hd_filter_image(hd_ctx_t ctx, hd_dtype_t dtype, const void* img, int64_t H, int64_t W, int32_t C,
+                            int32_t channel_last, int32_t id, const int64_t* win_lo, const int64_t* win_n,
+                            void* out, void* stream);
+const char* hd_filter_last_error(void);
+
 /* ---- multi-GPU: one process per GPU, NCCL over NVLink --------
  * Bring-up: rank 0 calls hd_dist_unique_id and broadcasts the 128-byte id to the other
  * ranks (the harness's own channel, e.g. torch.distributed); every rank then calls

@@ -464,6 +464,8 @@ static hd_status_t slab2d_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_pl
       elem_tiled(d.in_f, Rc, Ks * Rc, 1);
       d.in_g = lines(const_cast<void*>(off(xg, (S.spec_lo + k0) * Lg[0], eb)), Lg[0], Lg[0]);
       d.out = lines(off(out, cc * Ro * Kc, eb), Oy, 1);
+      d.out.tl = 0;  // lines as tiles of width 1 (same addresses): TMA stores of the
+      d.out.s_t = 1; // 16-byte pieces when one block holds every output row (hd_api.cu)
       elem_tiled(d.out, Ro, S.block2, Kc);
       d.scale = S.scale;
       s = hd_pass(ctx, dtype, &d, stream);

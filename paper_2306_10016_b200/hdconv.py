@@ -45,8 +45,11 @@ EXPORTED = [
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_graph_replays", "hd_pass", "hd_conv1d_lambda",
     "hd_dist_unique_id", "hd_dist_init", "hd_dist_last_error", "hd_dist_partition", "hd_dist_slab_plan",
     "hd_conv1d_dist", "hd_conv2d_dist", "hd_conv3d_dist", "hd_slab_stage", "hd_slab_scratch_bytes",
-    "hd_slab_g_bytes",
+    "hd_slab_g_bytes", "hd_filter_kernel", "hd_filter_image", "hd_filter_last_error",
 ]
+HD_FILTER_COUNT = 8
+FILTER_NAMES = ["Identity", "Ridge_detection_1", "Ridge_detection_2", "Sharpen", "Box_blur", "Gaussian_blur",
+                "Gaussian_blur_5", "Unsharpen_masking"]
 HD_SHARD_BATCH, HD_SHARD_RESIDUE = 0, 1
 HD_PASS_FWD, HD_PASS_INV, HD_PASS_CONV = 0, 1, 2
 
@@ -192,6 +195,9 @@ def _load():
         "hd_slab_stage": ([P, ctypes.c_int, ctypes.POINTER(SlabPlan), P, P, I32, P, P, P, P, P], ctypes.c_int),
         "hd_slab_scratch_bytes": ([ctypes.c_int, ctypes.POINTER(SlabPlan), P, P], SZ),
         "hd_slab_g_bytes": ([ctypes.c_int, ctypes.POINTER(SlabPlan), P], SZ),
+        "hd_filter_kernel": ([I32, P, ctypes.POINTER(I32), ctypes.POINTER(ctypes.c_char_p)], ctypes.c_int),
+        "hd_filter_image": ([P, ctypes.c_int, P, I64, I64, I32, I32, I32, P, P, P, P], ctypes.c_int),
+        "hd_filter_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -232,6 +238,17 @@ def dist_partition(extent, nranks, rank):
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
     _check_dist(_lib.hd_dist_partition(int(extent), int(nranks), int(rank), ctypes.byref(lo), ctypes.byref(hi)))
     return lo.value, hi.value
+
+
+def filter_kernel(kernel):
+    """(name, n x n weights) of the paper's filter dictionary entry (id or name)."""
+    kid = FILTER_NAMES.index(kernel) if isinstance(kernel, str) else int(kernel)
+    w = np.zeros(25, dtype=np.float64)
+    n, name = ctypes.c_int32(), ctypes.c_char_p()
+    st = _lib.hd_filter_kernel(kid, w.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n), ctypes.byref(name))
+    if st != HD_OK:
+        raise HDError(st, (_lib.hd_filter_last_error() or b"").decode())
+    return name.value.decode(), w[: n.value * n.value].reshape(n.value, n.value)
 
 
 def slab_buffer_elems(dtype, sp, Lf, Lg):
@@ -823,6 +840,33 @@ class Context:
         _check_dist(_lib.hd_conv3d_dist(self.h, dt, _ptr(f_planes), _i64arr(Lf), _ptr(g), _i64arr(Lg), _ptr(h), pp,
                                         _stream_ptr(stream)), self.h)
         return h
+
+    def filter_image(self, img, kernel, window=None, channel_last=True, out=None, stream=None):
+        """The paper's image filter (hd_filter_image): every channel of the real image
+        `img` ([H][W][C] or [C][H][W]) convolved with dictionary kernel `kernel` (id or
+        name), real part, window (lo, n) of the full result (None: all)."""
+        import torch
+        kid = FILTER_NAMES.index(kernel) if isinstance(kernel, str) else int(kernel)
+        if img.dtype == torch.float64:
+            dt = HD_C128
+        elif img.dtype == torch.float32:
+            dt = HD_C64
+        else:
+            raise TypeError("img must be float64 or float32")
+        if img.dim() != 3:
+            raise ValueError("img must be [H][W][C] or [C][H][W]")
+        H, W, C = (img.shape[0], img.shape[1], img.shape[2]) if channel_last else (img.shape[1], img.shape[2],
+                                                                                   img.shape[0])
+        self._arg(img, "img", img.dtype)
+        n = filter_kernel(kid)[1].shape[0]
+        lo, nn = (window if window is not None else ([0, 0], [H + n - 1, W + n - 1]))
+        shape = [nn[0], nn[1], C] if channel_last else [C, nn[0], nn[1]]
+        out = self._h(out, img, shape)
+        st = _lib.hd_filter_image(self.h, dt, _ptr(img), H, W, C, 1 if channel_last else 0, kid, _i64arr(lo),
+                                  _i64arr(nn), _ptr(out), _stream_ptr(stream))
+        if st != HD_OK:
+            raise HDError(st, (_lib.hd_filter_last_error() or b"").decode())
+        return out
 
     def slab_stage(self, dtype, sp, Lf, Lg, stage, inp, out, gt=None, scratch=None, stream=None):
         """One compute stage of a slab decomposition (hd_slab_stage), no exchange."""

@@ -109,3 +109,19 @@ def test_window_modes_match_the_paper_formulas(H):
     assert H.window_for_mode("same_big", [3], [100]) == ([0], [100])
     with pytest.raises(ValueError):
         H.window_for_mode("nope", [3], [5])
+
+
+def test_filter_dictionary_matches_paper(H, golden):
+    """hd_filter_kernel returns the eight kernels of the paper's image-filter listing
+    (PAPER.md:1511-1520), in its dictionary order, with the listed scale factors."""
+    import numpy as np
+    d = golden("filter_kernels.json")
+    assert H.FILTER_NAMES == d["order"]
+    for i, name in enumerate(d["order"]):
+        k = d["kernels"][name]
+        ref = np.asarray(k["rows"], dtype=np.float64) * k["scale"][0] / k["scale"][1]
+        got_name, w = H.filter_kernel(i)
+        assert got_name == name
+        assert w.shape == ref.shape and np.array_equal(w, ref)
+    with pytest.raises(H.HDError):
+        H.filter_kernel(8)

@@ -839,3 +839,24 @@ def test_shared_g_does_not_mutate_plan(ctx, H):
     for b in range(B):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
 
+
+
+# ---------------------------------------------------------------- image filter (row f3)
+@pytest.mark.parametrize("kid", range(8))
+@pytest.mark.parametrize("channel_last,dtype", [(True, np.float64), (False, np.float64), (True, np.float32)])
+def test_filter_image_dictionary(ctx, H, kid, channel_last, dtype):
+    """The paper's image-filter demo on a synthetic 3-channel
+    100 x 120 image of integer pixel values: every channel convolved with dictionary
+    kernel `kid`, real part kept, a window of the full result, against the oracle."""
+    s = synth.Stream(4000 + kid)
+    img = np.floor(s.real_uniform((100, 120, 3), 0.0, 256.0))
+    name, w = H.filter_kernel(kid)
+    n = w.shape[0]
+    lo, nn = [1, 2], [100 + n - 3, 120 + n - 4]
+    x = img if channel_last else np.ascontiguousarray(np.transpose(img, (2, 0, 1)))
+    out = host(ctx.filter_image(dev(x.astype(dtype)), kid, window=(lo, nn), channel_last=channel_last))
+    tol = 1e-11 if dtype == np.float64 else 1e-5
+    for c in range(3):
+        ref = np.real(oracle.conv(img[:, :, c], w))[lo[0]:lo[0] + nn[0], lo[1]:lo[1] + nn[1]]
+        got = out[:, :, c] if channel_last else out[c]
+        assert oracle.rel_l2(got, ref) < tol, (name, c)
