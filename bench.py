@@ -496,17 +496,27 @@ def run_ours(args, rank, world, local_rank):
     explicit = None
     if not args.no_explicit and ndim >= 2 and slab is None:
         try:
-            ctx.hd_conv_explicit(fd, gd, plan=plan, h=hd_)
+            # the explicit variant with ITS OWN tuned plan (hd_tune_explicit; untimed), so the
+            # comparison is hybrid vs explicit padding on equal terms
+            t = time.perf_counter()
+            xplan = ctx.tune_explicit(dtc, Lf, Lg, N=N, reps=3)
+            xtune_s = time.perf_counter() - t
+            ctx.hd_conv_explicit(fd, gd, h=hd_)
             torch.cuda.synchronize()
             k3 = max(2, min(args.steps, 20))
             e0.record(stream)
             for _ in range(k3):
-                ctx.hd_conv_explicit(fd, gd, plan=plan, h=hd_)
+                ctx.hd_conv_explicit(fd, gd, h=hd_)
             e1.record(stream)
             torch.cuda.synchronize()
             xms = e0.elapsed_time(e1) / k3
+            m_exp = [1 << int(np.ceil(np.log2(o))) for o in Lout]
+            predicted = float(np.prod(m_exp) / np.prod([a["M1"] for a in plan.as_dict()["axis"]]))
             explicit = {"value": samples_per_step / (xms * 1e-3), "ms_per_step": xms,
-                        "hybrid_speedup": xms / (ms / args.steps)}
+                        "hybrid_speedup": xms / (ms / args.steps),
+                        "predicted_work_ratio": predicted,
+                        "padded_extents": m_exp, "tune_seconds": xtune_s,
+                        "plan": [{k: a[k] for k in ("m", "C", "S", "D", "q")} for a in xplan.as_dict()["axis"]]}
         except Exception as ex:  # report, never hide
             explicit = {"error": str(ex)}
 

@@ -85,6 +85,9 @@ typedef enum {
                                       Dropped when the context reallocates its workspace or is
                                       destroyed; at most 64 are kept (the cache then starts
                                       over).  Not with profiling enabled. */
+#define HD_FLAG_EXPLICIT_PLAN 0x20u /* hd_conv_explicit only: the plan is the PADDED problem's own
+                                      (m <= M_exp, C, S, D), e.g. from hd_tune_explicit, rather
+                                      than a hybrid plan to derive one from */
 #define HD_FLAG_STAGED_ORDER 0x10u /* hd_pass only: the forward / inverse passes may run on the
                                       staged engines (m = 512 complex double with C = 1, D = q,
                                       p <= 8; m = 128 complex float with C = 4), whose spectral
@@ -292,6 +295,15 @@ typedef struct {
  * HD_ERR_INVALID on bad sizes/layouts, HD_ERR_UNSUPPORTED if no kernel exists. */
 hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* desc, void* stream);
 
+/* Tune the explicit-padding baseline's own plan (hd_conv_explicit's padded problem,
+ * M_exp = next power of two >= L_out per axis): per-axis search over m in {64, ...,
+ * min(4096, M_exp)}, C in {1, 2, 4} (C > 1 only for m <= 256), S in {1, 2, 4, 8}
+ * (ndim > 1), each timed as whole hd_conv_explicit calls (1 warm-up, median of reps,
+ * 0 = 3) on zero operands.  The result (flags = HD_FLAG_EXPLICIT_PLAN) is cached: later
+ * hd_conv_explicit calls with plan = NULL use it.  hd_tune_log lists the candidates. */
+hd_status_t hd_tune_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, const int64_t* Lf,
+                             const int64_t* Lg, int32_t reps, void* stream, hd_plan_t* out);
+
 /* ---- image filtering ------------------------
  * The paper's demo convolves every channel of an image with one of eight small named
  * kernels (Identity, Ridge_detection_1, Ridge_detection_2, Sharpen,
@@ -401,7 +413,26 @@ hd_status_t hd_conv3d_dist(hd_ctx_t ctx, hd_dtype_t dtype, const void* f_planes,
 /* Time candidate plans on the device (CUDA events, 2 warm-ups, median of `reps`
  * >= 1 runs; 0 = 5) and return the fastest; ties break lexicographically on
  * (m, C, S, D).  Inputs are synthetic scratch of the problem's shape.  The
- * result is cached in the context for plan = NULL calls on the same problem. */
+ * result is cached in the context for plan = NULL calls on the same problem.
+ * Search space per axis i (hd_tune_space lists it):
+ *   m a power of two in [16, 4096] with q = ceil(M_i / m) <= 1024;
+ *   C in {1, 2, 4, 8};  D in {q, ceil(q/2), ceil(q/4), ..., 1};
+ *   S in {1, 2, 4, 8, 16} (1 when ndim = 1);
+ *   threads in {0 (automatic engine), d, 256} with d the sweep-matched default of
+ *   (C, D, m), plus {768, 1024} when C*D*m/8 >= 512 and the pass uses more than half
+ *   of the 227 KB of shared memory;
+ *   excluding candidates whose generic pass exceeds 227 KB of shared memory:
+ *   16 bytes (c128) / 8 (c64) x (r(q) + r(256) + nbuf r(C D m)), r(n) = n rounded up
+ *   to a multiple of 64 (c128) / 128 (c64) slots, nbuf = 2 (3 with N > 1) on axis 0,
+ *   else 1.
+ * Pruning: a candidate whose first warm-up takes more than 3x the best median so far
+ * is logged with that time and not repeated.  HD_TUNE_EXHAUSTIVE times the whole
+ * cross product of the per-axis spaces and fails (HD_ERR_UNSUPPORTED) above 2^22
+ * plans instead of truncating. */
+/* Host only: the number of candidates of axis `axis` in the space above (-1 on bad
+ * arguments); the first min(cap, count) are written to out (m, C, S, D, threads). */
+int32_t hd_tune_space(hd_dtype_t dtype, int32_t ndim, int32_t N, const int64_t* Lf, const int64_t* Lg,
+                      const int64_t* M, int32_t axis, hd_axis_plan_t* out, int32_t cap);
 hd_status_t hd_tune(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
                     int64_t batch, const int64_t* Lf, const int64_t* Lg, const int64_t* M,
                     uint32_t flags, int32_t reps, void* stream, hd_plan_t* out);

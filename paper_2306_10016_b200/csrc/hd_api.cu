@@ -1488,9 +1488,11 @@ static hd_status_t explicit_locked(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim,
 hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
                              const void* const* f, const int64_t* Lf, const void* const* g,
                              const int64_t* Lg, void* h, const hd_plan_t* plan, void* stream) {
-  // Validate against the hybrid problem first (also gives the user's m, C, S).
+  // Validate against the hybrid problem first (also gives the user's m, C, S).  A plan
+  // flagged HD_FLAG_EXPLICIT_PLAN is the padded problem's own (hd_tune_explicit).
+  const bool own = plan && (plan->flags & HD_FLAG_EXPLICIT_PLAN);
   Problem H;
-  hd_status_t s = setup(ctx, H, dtype, ndim, N, 1, f, Lf, g, Lg, h, nullptr, plan);
+  hd_status_t s = setup(ctx, H, dtype, ndim, N, 1, f, Lf, g, Lg, h, nullptr, own ? nullptr : plan);
   if (s != HD_OK) return s;
   std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
@@ -1504,8 +1506,16 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
     while (Me[i] < Lo[i]) Me[i] *= 2;
     nin *= Me[i];
   }
-  // explicit plan: same m (capped by M_exp), same C/S, D reduced until it fits
+  // explicit plan: the caller's own (HD_FLAG_EXPLICIT_PLAN), else the tuned one cached
+  // by hd_tune_explicit, else the hybrid plan's m (capped by M_exp), C, S; D reduced
+  // until the pass fits shared memory
   hd_plan_t pe = H.plan;
+  if (own) {
+    pe = *plan;
+  } else if (!plan) {
+    auto it = ctx->plan_cache.find(problem_key(dtype, ndim, N, 1, Lf, Lg, nullptr, HD_FLAG_EXPLICIT_PLAN));
+    if (it != ctx->plan_cache.end()) pe = it->second;
+  }
   pe.flags = HD_FLAG_ALLOW_ALIAS;
   for (int i = 0; i < ndim; ++i) {
     hd_axis_plan_t& a = pe.axis[i];
@@ -1513,7 +1523,7 @@ hd_status_t hd_conv_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32
     const int q = (int)(Me[i] / a.m);
     const int lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(N) : 1;
-    a.D = q;
+    if (!own || a.D <= 0 || a.D > q) a.D = q;
     while (a.D > 1 && pass_smem(eb, q, lines, a.D, a.m, nbuf) > hd::kMaxSmem) --a.D;
   }
   // scratch: N padded f, N padded g, padded output, pipeline workspace
@@ -2013,27 +2023,36 @@ bool cand_less(const AxisCand& a, const AxisCand& b) {
   return a.threads < b.threads;
 }
 
+// The documented per-axis search space (include/hdconv.h hd_tune):
+// m a power of two in [16, 4096] with q = ceil(M/m) <= 1024; C in {1, 2, 4, 8};
+// D in {q, ceil(q/2), ceil(q/4), ..., 1}; S in {1, 2, 4, 8, 16} (1 in 1-D); threads in
+// {automatic, the sweep-matched default, 256} plus {768, 1024} for passes whose shared
+// memory leaves one CTA per SM and whose butterfly sweep has >= 512 items; a candidate
+// whose generic pass exceeds the shared memory is not in the space.
 std::vector<AxisCand> axis_candidates(const hd_plan_t& base, int i, int ndim, int npairs,
                                       const int64_t* Lf, const int64_t* Lg, const int64_t* M,
                                       size_t eb) {
+  (void)base;
   std::vector<AxisCand> out;
   const int64_t Lout = Lf[i] + Lg[i] - 1;
   const int64_t Mi = (M && M[i] > 0) ? M[i] : Lout;
-  const int m0 = base.axis[i].m;
   const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
-  std::vector<int> Ss = (ndim == 1) ? std::vector<int>{1} : std::vector<int>{1, 2, 4, 8};
-  for (int m = std::max(2, m0 / 2); m <= std::min(4096, m0 * 2); m *= 2) {
-    const int q = (int)cdiv(Mi, m);
+  const std::vector<int> Ss = (ndim == 1) ? std::vector<int>{1} : std::vector<int>{1, 2, 4, 8, 16};
+  for (int m = 16; m <= 4096; m *= 2) {
+    const int64_t q64 = cdiv(Mi, m);
+    if (q64 > 1024) continue;
+    const int q = (int)q64;
+    std::vector<int> Ds;
+    for (int D = q;; D = (D + 1) / 2) {
+      Ds.push_back(D);
+      if (D == 1) break;
+    }
     for (int C : {1, 2, 4, 8}) {
-      if (C > 2 && m > 256) continue;  // wide line groups only pay for short lines
-      std::vector<int> Ds = {q};
-      if (q > 1) Ds.push_back((q + 1) / 2);
       for (int D : Ds) {
         if (pass_smem(eb, q, C, D, m, nbuf) > hd::kMaxSmem) continue;
         const int dt = default_threads(C, D, m);
         std::vector<int> ths = {0, dt};  // 0: automatic engine (warp engine where it applies)
         if (dt != 256) ths.push_back(256);
-        // wide CTAs for passes whose shared memory allows one CTA per SM (latency hiding)
         const int64_t bflies = (int64_t)C * D * (m / 8);
         if (bflies >= 512 && pass_smem(eb, q, C, D, m, nbuf) > hd::kMaxSmem / 2)
           for (int t : {768, 1024}) if (t != dt) ths.push_back(t);
@@ -2129,6 +2148,7 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
     return 1.0 + (double)(h >> 11) * (1.0 / 9007199254740992.0);
   };
 
+  double abort_ref = 1e300;  // best time so far (early-abort reference)
   auto time_plan_on = [&](hd_plan_t pl, const int64_t* lf, const int64_t* lg, const int64_t* mm,
                           double* secs) -> bool {
     Problem P;
@@ -2143,8 +2163,22 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
       ctx->tune_log.push_back({pl, *secs});
       return true;
     }
-    for (int w = 0; w < 2; ++w)
+    // first warm-up timed: a candidate > 3x the best time so far is recorded with that
+    // time and not repeated (documented pruning: it cannot win)
+    {
+      cudaEventRecord(e0, st);
       if (run_pipeline(ctx, P, nullptr, 0, st) != HD_OK) return false;
+      cudaEventRecord(e1, st);
+      if (cudaEventSynchronize(e1) != cudaSuccess) return false;
+      float ms0 = 0;
+      cudaEventElapsedTime(&ms0, e0, e1);
+      if (abort_ref < 1e299 && ms0 * 1e-3 > 3.0 * abort_ref) {
+        *secs = ms0 * 1e-3;
+        ctx->tune_log.push_back({pl, *secs});
+        return true;
+      }
+    }
+    if (run_pipeline(ctx, P, nullptr, 0, st) != HD_OK) return false;
     std::vector<double> ts;
     for (int r = 0; r < reps; ++r) {
       cudaEventRecord(e0, st);
@@ -2181,7 +2215,15 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
       lists.push_back(axis_candidates(base, i, ndim, N, Lf, Lg, M, eb));
       combos *= std::max<size_t>(1, lists.back().size());
     }
-    combos = std::min<size_t>(combos, 4096);
+    if (combos > ((size_t)1 << 22)) {
+      ctx->profiling = prof_was;
+      if (!fake) scratch_release(ctx, st);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+      if (scratch) cudaFree(scratch);
+      return fail(ctx, HD_ERR_UNSUPPORTED, "search space of " + std::to_string(combos) +
+                                               " plans exceeds 2^22: use the per-axis or random search");
+    }
     std::vector<size_t> order(combos);
     for (size_t c = 0; c < combos; ++c) order[c] = c;
     size_t count = combos;
@@ -2212,16 +2254,19 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
       if (!time_plan(pl, &t)) continue;
       const bool tie = std::fabs(t - best_t) <= 1e-12 * best_t;
       if ((t < best_t && !tie) || (tie && plan_less(pl, best))) { best_t = t; best = pl; }
+      abort_ref = std::min(abort_ref, best_t);
     }
   } else {
     if (!time_plan(best, &best_t)) best_t = 1e300;
     for (int i = 0; i < ndim; ++i) {
+      abort_ref = (proxy && i > 0) ? 1e300 : best_t;
       const bool on_proxy = proxy && i > 0;
       std::vector<AxisCand> cands = axis_candidates(best, i, ndim, N, on_proxy ? Lfp : Lf, on_proxy ? Lgp : Lg,
                                                     on_proxy ? Mp : M, eb);
       AxisCand bc{best.axis[i].m, best.axis[i].C, best.axis[i].S, best.axis[i].D, best.axis[i].threads};
       double ref_t = best_t;
       if (on_proxy && !time_plan_on(best, Lfp, Lgp, Mp, &ref_t)) ref_t = 1e300;
+      if (on_proxy) abort_ref = ref_t;
       for (const AxisCand& c : cands) {
         hd_plan_t pl = best;
         apply_cand(pl, i, ndim, c);
@@ -2230,6 +2275,7 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
         const bool tie = std::fabs(t - ref_t) <= 1e-12 * ref_t;
         if (t < ref_t && !tie) { ref_t = t; best = pl; bc = c; }
         else if (tie && cand_less(c, bc)) { best = pl; bc = c; }
+        abort_ref = std::min(abort_ref, ref_t);
       }
       if (on_proxy) best_t = 1e300;  // the full problem's time of the final plan is taken below
       else best_t = ref_t;
@@ -2246,6 +2292,104 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
   if (s != HD_OK) return s;
   best.tuned_seconds = best_t;
   ctx->plan_cache[problem_key(dtype, ndim, N, batch, Lf, Lg, M, 0)] = best;
+  *out = best;
+  return HD_OK;
+}
+
+// Size (and optionally the list) of the per-axis search space of hd_tune for axis i.
+int32_t hd_tune_space(hd_dtype_t dtype, int32_t ndim, int32_t N, const int64_t* Lf, const int64_t* Lg,
+                      const int64_t* M, int32_t axis, hd_axis_plan_t* out, int32_t cap) {
+  if (!Lf || !Lg || ndim < 1 || ndim > HD_MAX_DIM || axis < 0 || axis >= ndim || N < 1) return -1;
+  if (dtype != HD_C64 && dtype != HD_C128) return -1;
+  hd_plan_t base;
+  std::memset(&base, 0, sizeof(base));
+  const std::vector<AxisCand> c = axis_candidates(base, axis, ndim, N, Lf, Lg, M, elem_bytes(dtype));
+  for (int32_t k = 0; out && k < cap && k < (int32_t)c.size(); ++k) {
+    std::memset(&out[k], 0, sizeof(out[k]));
+    out[k].m = c[k].m; out[k].C = c[k].C; out[k].S = c[k].S; out[k].D = c[k].D; out[k].threads = c[k].threads;
+  }
+  return (int32_t)c.size();
+}
+
+// The explicit-padding baseline's own plan (PAPER.md:602-605 with the tuner's search,
+// PAPER.md:758-766): per axis of the padded problem (M_exp = next power of two >= L_out,
+// p = q), m in {64, ..., min(4096, M_exp)}, C in {1, 2, 4} (C > 1 for m <= 256), S in
+// {1, 2, 4, 8} (ndim > 1), timed as whole hd_conv_explicit calls on zero operands.
+hd_status_t hd_tune_explicit(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, const int64_t* Lf,
+                             const int64_t* Lg, int32_t reps, void* stream, hd_plan_t* out) {
+  if (!ctx || !Lf || !Lg || !out) return fail(ctx, HD_ERR_INVALID, "null argument");
+  if (ndim < 1 || ndim > HD_MAX_DIM || N < 1 || N > HD_MAX_PAIRS) return fail(ctx, HD_ERR_INVALID, "bad ndim or N");
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t eb = elem_bytes(dtype);
+  int64_t nf = 1, ng = 1, nh = 1, Me[HD_MAX_DIM];
+  for (int i = 0; i < ndim; ++i) {
+    nf *= Lf[i]; ng *= Lg[i]; nh *= Lf[i] + Lg[i] - 1;
+    Me[i] = 1;
+    while (Me[i] < Lf[i] + Lg[i] - 1) Me[i] *= 2;
+  }
+  const size_t bf = align256((size_t)nf * eb), bg = align256((size_t)ng * eb), bh = align256((size_t)nh * eb);
+  char* buf = nullptr;
+  if (cudaMalloc(&buf, N * (bf + bg) + bh) != cudaSuccess) return fail(ctx, HD_ERR_CUDA, "cudaMalloc(tune scratch)");
+  cudaMemsetAsync(buf, 0, N * (bf + bg) + bh, st);
+  const void* fp[HD_MAX_PAIRS];
+  const void* gp[HD_MAX_PAIRS];
+  for (int k = 0; k < N; ++k) { fp[k] = buf + k * bf; gp[k] = buf + N * bf + k * bg; }
+  void* hp = buf + N * (bf + bg);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int nrep = reps > 0 ? reps : 3;
+  auto time_plan = [&](hd_plan_t pl, double* secs) -> bool {
+    pl.flags = HD_FLAG_EXPLICIT_PLAN;
+    if (hd_conv_explicit(ctx, dtype, ndim, N, fp, Lf, gp, Lg, hp, &pl, st) != HD_OK) return false;
+    std::vector<double> ts;
+    for (int r = 0; r < nrep; ++r) {
+      cudaEventRecord(e0, st);
+      if (hd_conv_explicit(ctx, dtype, ndim, N, fp, Lf, gp, Lg, hp, &pl, st) != HD_OK) return false;
+      cudaEventRecord(e1, st);
+      if (cudaEventSynchronize(e1) != cudaSuccess) return false;
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms * 1e-3);
+    }
+    std::sort(ts.begin(), ts.end());
+    *secs = ts[ts.size() / 2];
+    ctx->tune_log.push_back({pl, *secs});
+    return true;
+  };
+  ctx->tune_log.clear();
+  hd_plan_t best;
+  std::memset(&best, 0, sizeof(best));
+  best.ndim = ndim;
+  for (int i = 0; i < ndim; ++i) {
+    best.axis[i].m = (int)std::min<int64_t>(512, Me[i]);
+    best.axis[i].C = 1;
+    best.axis[i].S = ndim > 1 ? 2 : 1;
+  }
+  double best_t = 1e300;
+  if (!time_plan(best, &best_t)) best_t = 1e300;
+  for (int i = 0; i < ndim; ++i) {
+    for (int m = 64; m <= std::min<int64_t>(4096, Me[i]); m *= 2)
+      for (int C : {1, 2, 4}) {
+        if (C > 1 && m > 256) continue;
+        for (int S : {1, 2, 4, 8}) {
+          if (ndim == 1 && S > 1) continue;
+          hd_plan_t pl = best;
+          pl.axis[i].m = m; pl.axis[i].C = C; pl.axis[i].S = S; pl.axis[i].D = 0;
+          double t;
+          if (time_plan(pl, &t) && t < best_t) { best_t = t; best = pl; }
+        }
+      }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  if (best_t >= 1e300) return fail(ctx, HD_ERR_UNSUPPORTED, "no explicit plan could be timed");
+  best.flags = HD_FLAG_EXPLICIT_PLAN;
+  best.tuned_seconds = best_t;
+  ctx->plan_cache[problem_key(dtype, ndim, N, 1, Lf, Lg, nullptr, HD_FLAG_EXPLICIT_PLAN)] = best;
   *out = best;
   return HD_OK;
 }

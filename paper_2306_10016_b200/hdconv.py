@@ -26,6 +26,7 @@ HD_FLAG_SHARED_G = 0x2
 HD_FLAG_GENERIC_FFT = 0x4
 HD_FLAG_GRAPH = 0x8
 HD_FLAG_STAGED_ORDER = 0x10
+HD_FLAG_EXPLICIT_PLAN = 0x20
 HD_ENGINE_GENERIC, HD_ENGINE_S512, HD_ENGINE_S512_MCONV, HD_ENGINE_S128, HD_ENGINE_S512C = 0, 1, 2, 3, 4
 HD_TUNE_PER_AXIS = 0x0
 HD_TUNE_EXHAUSTIVE = 0x1
@@ -45,7 +46,7 @@ EXPORTED = [
     "hd_profile_enable", "hd_profile_read", "hd_profile_reset", "hd_launch_count", "hd_engine_launches", "hd_graph_replays", "hd_pass", "hd_conv1d_lambda",
     "hd_dist_unique_id", "hd_dist_init", "hd_dist_last_error", "hd_dist_partition", "hd_dist_slab_plan",
     "hd_conv1d_dist", "hd_conv2d_dist", "hd_conv3d_dist", "hd_slab_stage", "hd_slab_scratch_bytes",
-    "hd_slab_g_bytes", "hd_filter_kernel", "hd_filter_image", "hd_filter_last_error",
+    "hd_slab_g_bytes", "hd_tune_explicit", "hd_tune_space", "hd_filter_kernel", "hd_filter_image", "hd_filter_last_error",
 ]
 HD_FILTER_COUNT = 8
 FILTER_NAMES = ["Identity", "Ridge_detection_1", "Ridge_detection_2", "Sharpen", "Box_blur", "Gaussian_blur",
@@ -196,6 +197,8 @@ def _load():
         "hd_slab_scratch_bytes": ([ctypes.c_int, ctypes.POINTER(SlabPlan), P, P], SZ),
         "hd_slab_g_bytes": ([ctypes.c_int, ctypes.POINTER(SlabPlan), P], SZ),
         "hd_filter_kernel": ([I32, P, ctypes.POINTER(I32), ctypes.POINTER(ctypes.c_char_p)], ctypes.c_int),
+        "hd_tune_explicit": ([P, ctypes.c_int, I32, I32, P, P, I32, P, PP], ctypes.c_int),
+        "hd_tune_space": ([ctypes.c_int, I32, I32, P, P, P, I32, ctypes.POINTER(AxisPlan), I32], I32),
         "hd_filter_image": ([P, ctypes.c_int, P, I64, I64, I32, I32, I32, P, P, P, P], ctypes.c_int),
         "hd_filter_last_error": ([], ctypes.c_char_p),
     }
@@ -238,6 +241,17 @@ def dist_partition(extent, nranks, rank):
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
     _check_dist(_lib.hd_dist_partition(int(extent), int(nranks), int(rank), ctypes.byref(lo), ctypes.byref(hi)))
     return lo.value, hi.value
+
+
+def tune_space(dtype, Lf, Lg, axis, M=None, N=1):
+    """hd_tune_space: the per-axis candidates of hd_tune as (m, C, S, D, threads) tuples."""
+    Mv = _i64arr(M) if M is not None else None
+    n = _lib.hd_tune_space(dtype, len(Lf), N, _i64arr(Lf), _i64arr(Lg), Mv, axis, None, 0)
+    if n < 0:
+        raise HDError(HD_ERR_INVALID, "bad tune_space arguments")
+    arr = (AxisPlan * max(n, 1))()
+    _lib.hd_tune_space(dtype, len(Lf), N, _i64arr(Lf), _i64arr(Lg), Mv, axis, arr, n)
+    return [(a.m, a.C, a.S, a.D, a.threads) for a in arr[:n]]
 
 
 def filter_kernel(kernel):
@@ -721,6 +735,14 @@ class Context:
         return p
 
     tune = hd_tune
+
+    def tune_explicit(self, dtype, Lf, Lg, N=1, reps=3, stream=None):
+        """hd_tune_explicit: the explicit-padding baseline's own tuned plan (cached for
+        hd_conv_explicit(plan=None))."""
+        p = Plan()
+        self._chk(_lib.hd_tune_explicit(self.h, dtype, len(Lf), N, _i64arr(Lf), _i64arr(Lg), reps,
+                                        _stream_ptr(stream), ctypes.byref(p)))
+        return p
 
     def hd_tune_ex(self, dtype, Lf, Lg, M=None, N=1, batch=1, mode="per_axis", n1=16, seed=0,
                    proxy_rows=0, reps=5, fake_cost=0, stream=None):

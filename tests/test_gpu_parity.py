@@ -860,3 +860,18 @@ def test_filter_image_dictionary(ctx, H, kid, channel_last, dtype):
         ref = np.real(oracle.conv(img[:, :, c], w))[lo[0]:lo[0] + nn[0], lo[1]:lo[1] + nn[1]]
         got = out[:, :, c] if channel_last else out[c]
         assert oracle.rel_l2(got, ref) < tol, (name, c)
+
+
+def test_explicit_variant_tuned_plan(ctx, H):
+    """hd_tune_explicit tunes the padded problem's own plan; hd_conv_explicit(plan=None)
+    then uses it, and an HD_FLAG_EXPLICIT_PLAN plan is honoured as the padded plan."""
+    f, g = synth.random_pair(4100, (300, 260), (31, 17))
+    p = ctx.tune_explicit(H.HD_C128, [300, 260], [31, 17], reps=1)
+    assert p.flags & H.HD_FLAG_EXPLICIT_PLAN and p.tuned_seconds > 0
+    assert len(ctx.hd_tune_log()) > 10
+    h = host(ctx.hd_conv_explicit([dev(f)], [dev(g)]))
+    ref = oracle.conv(f, g)
+    assert oracle.rel_l2(h, ref) < 1e-11
+    own = H.Plan.make(2, [{"m": 64, "C": 2, "S": 4}, {"m": 128, "C": 1, "S": 2}], flags=H.HD_FLAG_EXPLICIT_PLAN)
+    h2 = host(ctx.hd_conv_explicit([dev(f)], [dev(g)], plan=own))
+    assert oracle.rel_l2(h2, ref) < 1e-11
