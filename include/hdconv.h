@@ -426,7 +426,10 @@ hd_status_t hd_conv3d_dist(hd_ctx_t ctx, hd_dtype_t dtype, const void* f_planes,
  *   to a multiple of 64 (c128) / 128 (c64) slots, nbuf = 2 (3 with N > 1) on axis 0,
  *   else 1.
  * Pruning: a candidate whose first warm-up takes more than 3x the best median so far
- * is logged with that time and not repeated.  HD_TUNE_EXHAUSTIVE times the whole
+ * is logged with that time and not repeated; in the per-axis search the candidates
+ * come in groups of equal (m, C) (the order above), and when a group's first member
+ * is more than 3x slower than the best so far the rest of the group is logged with
+ * time +inf (not timed).  Every candidate of the space appears in hd_tune_log.  HD_TUNE_EXHAUSTIVE times the whole
  * cross product of the per-axis spaces and fails (HD_ERR_UNSUPPORTED) above 2^22
  * plans instead of truncating. */
 /* Host only: the number of candidates of axis `axis` in the space above (-1 on bad

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <mutex>
 #include <string>
@@ -2267,11 +2268,28 @@ hd_status_t hd_tune_ex(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N, 
       double ref_t = best_t;
       if (on_proxy && !time_plan_on(best, Lfp, Lgp, Mp, &ref_t)) ref_t = 1e300;
       if (on_proxy) abort_ref = ref_t;
+      // candidates come in groups of equal (m, C); the group's first member is timed
+      // first and, if it is more than 3x slower than the best so far, the rest of the
+      // group is logged as pruned (time +inf) without being timed
+      int gm = -1, gC = -1;
+      bool gpruned = false;
       for (const AxisCand& c : cands) {
         hd_plan_t pl = best;
         apply_cand(pl, i, ndim, c);
+        const bool first = c.m != gm || c.C != gC;
+        if (!first && gpruned && !fake) {
+          ctx->tune_log.push_back({pl, std::numeric_limits<double>::infinity()});
+          continue;
+        }
         double t;
-        if (!(on_proxy ? time_plan_on(pl, Lfp, Lgp, Mp, &t) : time_plan(pl, &t))) continue;
+        if (!(on_proxy ? time_plan_on(pl, Lfp, Lgp, Mp, &t) : time_plan(pl, &t))) {
+          if (first) { gm = c.m; gC = c.C; gpruned = true; }
+          continue;
+        }
+        if (first) {
+          gm = c.m; gC = c.C;
+          gpruned = ref_t < 1e299 && t > 3.0 * ref_t;
+        }
         const bool tie = std::fabs(t - ref_t) <= 1e-12 * ref_t;
         if (t < ref_t && !tie) { ref_t = t; best = pl; bc = c; }
         else if (tie && cand_less(c, bc)) { best = pl; bc = c; }

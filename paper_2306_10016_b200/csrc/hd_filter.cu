@@ -100,7 +100,7 @@ hd_status_t run(hd_ctx_t ctx, hd_dtype_t dtype, const void* img, int64_t H, int6
   T* full = reinterpret_cast<T*>(reinterpret_cast<char*>(g) + bg);
   KernelArg k;
   for (int i = 0; i < nn; ++i) k.w[i] = fk.num * fk.v[i] / fk.den;
-  fill_kernel<T><<<1, 64, 0, st>>>(g, k, nn, C);
+  fill_kernel<T><<<(unsigned)((nn * C + 63) / 64), 64, 0, st>>>(g, k, nn, C);
   if (channel_last) deinterleave_kernel<T><<<blocks_for(H * W * C), 256, 0, st>>>(static_cast<const T*>(img), planes, H * W, C);
   const int64_t Lf[2] = {H, W}, Lg[2] = {fk.n, fk.n};
   hd_status_t s = hd_conv_real(ctx, dtype, 2, C, planes, Lf, g, Lg, full, nullptr, st);
