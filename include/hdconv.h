@@ -503,7 +503,9 @@ int64_t     hd_launch_count(hd_ctx_t ctx);
 #define HD_ENGINE_S512_MCONV 2  /* its multi-pair convolution pass */
 #define HD_ENGINE_S128 3        /* staged engine, m = 128 complex float (C = 4) */
 #define HD_ENGINE_S512C 4       /* 1-D pass of long lines on two-CTA clusters, complex double,
-                                   m = 512 (12 <= q <= 22) or m = 2048 (4 <= q <= 6) */
+                                   m = 512 (12 <= q <= 22) */
+#define HD_ENGINE_S2048R 5      /* 1-D pass of long lines, complex double, m = 2048, one CTA per
+                                   line, residues in pairs (D = q <= 8, p <= 8) */
 int64_t     hd_engine_launches(hd_ctx_t ctx, int32_t engine);
 /* Calls served by replaying a captured CUDA graph (HD_FLAG_GRAPH) since creation;
  * -1 for a null context.  Replays do not add to hd_launch_count. */

@@ -63,7 +63,7 @@ struct hd_ctx {
   };
   std::vector<ProfEntry> prof;
   int64_t launches = 0;
-  int64_t engine_launches[5] = {0, 0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
+  int64_t engine_launches[6] = {0, 0, 0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
   // HD_FLAG_GRAPH: captured pass sequences keyed by their full argument list
   std::map<std::string, cudaGraphExec_t> graphs;
   cudaStream_t capture_stream = nullptr;
@@ -297,9 +297,10 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
       return fail(ctx, HD_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 1024]");
     x.lines = lines_for(a, i, ndim);
     const int nbuf = (i == 0) ? conv_nbuf(npairs) : 1;
-    // the 1-D two-CTA cluster pass (hd_s512c.cuh) holds at most 11 residue rows per CTA
+    // the 1-D two-CTA cluster pass (hd_s512c.cuh) holds at most 11 residue rows per CTA;
+    // the 1-D m = 2048 engine (hd_s2048r.cuh) keeps two residues in shared memory at a time
     const bool cluster_q = (x.m == 512 && x.q >= hd::kS512cQMin && x.q <= hd::kS512cQMax) ||
-                           (x.m == 2048 && x.q >= hd::kS2048cQMin && x.q <= hd::kS2048cQMax);
+                           (x.m == 2048 && x.q <= hd::s2048r_qmax() && x.pf <= 8 && x.pg <= 8);
     const bool cluster_1d = dt == HD_C128 && ndim == 1 && npairs == 1 && cluster_q && x.D == x.q &&
                             x.lines == 1 && x.auto_engine && !(plan->flags & HD_FLAG_GENERIC_FFT);
     if (!cluster_1d && pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
@@ -372,6 +373,12 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
       const bool p_ok = cdiv(Lf[i], 512) <= 8 && cdiv(Lg[i], 512) <= 8;
       const bool q_ok = (conv && npairs > 1) ? q5 <= 6 : q5 <= hd::kS512QMax;
       if (p_ok && q_ok) { bm = 512; bD = (int)q5; }
+    }
+    // 1-D complex double at m = 2048: every residue in one pass (the one-CTA-per-line
+    // engine, hd_s2048r.cuh, q <= 8, p <= 8)
+    if (dt == HD_C128 && ndim == 1 && bm == 2048) {
+      const int64_t q2 = cdiv(Mi, 2048);
+      if (q2 <= hd::s2048r_qmax() && cdiv(Lf[i], 2048) <= 8 && cdiv(Lg[i], 2048) <= 8) bD = (int)q2;
     }
     // one line per CTA where the staged m = 512 engine applies (hd_s512.cuh); four
     // lines per item and tiles of four for the staged complex-float m = 128 engine
@@ -604,16 +611,28 @@ bool use_s128_bg(const Launch& L) {
 // The 1-D convolution pass of long lines on two-CTA clusters (hd_s512c.cuh): m = 512,
 // complex double, all residues (D = q), 12 <= q <= 22, one pair, plain rows.
 bool use_s512c(hd_dtype_t dt, const Launch& L) {
-  if (dt != HD_C128 || (L.m != 512 && L.m != 2048) || L.lines != 1 || L.mode != hd::MODE_CONV ||
-      (L.flags & HD_FLAG_GENERIC_FFT))
+  if (dt != HD_C128 || L.m != 512 || L.lines != 1 || L.mode != hd::MODE_CONV || (L.flags & HD_FLAG_GENERIC_FFT))
     return false;
   if (!L.auto_engine || !L.s512c_axis || L.a.D != L.a.q) return false;
-  if (L.m == 512 && (L.a.q < hd::kS512cQMin || L.a.q > hd::kS512cQMax)) return false;
-  if (L.m == 2048 && (L.a.q < hd::kS2048cQMin || L.a.q > hd::kS2048cQMax)) return false;
+  if (L.a.q < hd::kS512cQMin || L.a.q > hd::kS512cQMax) return false;
   const PassArgs& a = L.a;
   return a.npairs == 1 && a.nbatch == 1 && a.in_f.p <= 32 && a.in_g.p <= 32 && a.out.T <= 32 && a.in_f.tl >= 30 && a.in_f.s_j == 1 && a.in_g.tl >= 30 &&
          a.in_g.s_j == 1 && a.out.tl >= 30 && a.out.so_log2 >= 30 && a.out.s_js == 1 && a.in_f.jd <= 0 &&
          a.in_g.jd <= 0 && a.out.jd <= 0;
+}
+
+// The 1-D m = 2048 engine (hd_s2048r.cuh): one pair of plain rows per line, every
+// residue (D = q <= 8), p <= 8, no output window offset.  HD_NO_S2048R=1: A/B switch.
+bool use_s2048r(hd_dtype_t dt, const Launch& L) {
+  static const bool off = getenv("HD_NO_S2048R") != nullptr;
+  if (off || dt != HD_C128 || L.m != 2048 || L.mode != hd::MODE_CONV || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
+  if (!L.auto_engine || !L.s512c_axis || L.a.D != L.a.q || L.a.q > hd::s2048r_qmax()) return false;
+  const PassArgs& a = L.a;
+  const LineIn &f = a.in_f, &g = a.in_g;
+  const LineOut& o = a.out;
+  return a.npairs == 1 && a.nbatch == 1 && f.p <= 8 && g.p <= 8 && f.tl >= 30 && f.s_j == 1 && f.jd <= 0 &&
+         g.tl >= 30 && g.s_j == 1 && g.jd <= 0 && o.tl >= 30 && o.so_log2 >= 30 && o.s_js == 1 && o.jd <= 0 &&
+         o.j0 == 0 && o.L <= (int64_t)o.T * 2048 && f.L < (1 << 30) && g.L < (1 << 30);
 }
 
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
@@ -621,15 +640,16 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   hd::LaunchFn fn = nullptr;
   size_t smem = 0;
   int threads = L.threads;
-  bool staged = use_s512(dt, L);
+  const bool s2048r = use_s2048r(dt, L);
+  bool staged = !s2048r && use_s512(dt, L);
   bool mconv = false;
   const bool s128 = use_s128(dt, L);
-  const bool s512c = !staged && use_s512c(dt, L);
+  const bool s512c = !staged && !s2048r && use_s512c(dt, L);
   if (L.a.fam2 && (!staged || s128 || s512c)) return HD_ERR_UNSUPPORTED;
-  if (s512c && L.m == 2048) {
-    fn = hd::lookup_s2048c();
-    threads = hd::s2048c_threads(L.a.q);
-    smem = hd::s2048c_smem_bytes();
+  if (s2048r) {
+    fn = hd::lookup_s2048r();
+    threads = hd::s2048r_threads();
+    smem = hd::s2048r_smem_bytes();
   } else if (s512c) {
     fn = hd::lookup_s512c();
     threads = hd::s512c_threads(L.a.q);
@@ -649,7 +669,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     prepare_tma(L);
     mconv = L.a.tm_in.kind == hd::TMA_LINE_TILED || L.a.tm_in.kind == hd::TMA_BULK;
   }
-  if (s128 || s512c) {
+  if (s128 || s512c || s2048r) {
     // set above
   } else if (mconv) {
     fn = hd::lookup_s512_mconv(L.a.q);
@@ -700,7 +720,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   static const bool dbg_launch = getenv("HD_DEBUG_LAUNCH") != nullptr;
   if (dbg_launch)
     fprintf(stderr, "[launch] %-8s engine=%s m=%d C=%d q=%d D=%d items=%lld threads=%d smem=%zu tma in=%d g=%d out=%d\n",
-            L.name, s512c ? "s512c" : s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m,
+            L.name, s2048r ? "s2048r" : s512c ? "s512c" : s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m,
             L.lines, L.a.q, L.a.D,
             (long long)total, threads, smem, L.a.tm_in.kind, L.a.tm_in_g.kind, L.a.tm_out.kind);
   cudaError_t e = fn(L.a, grid, threads, smem, st);
@@ -719,8 +739,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     fprintf(stderr, "\n");
   }
   if (!ctx->capturing) ctx->launches += 1;
-  if (!ctx->capturing) ctx->engine_launches[s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128 : mconv ? HD_ENGINE_S512_MCONV
-                       : staged ? HD_ENGINE_S512 : HD_ENGINE_GENERIC] += 1;
+  if (!ctx->capturing) ctx->engine_launches[s2048r ? HD_ENGINE_S2048R : s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128
+                       : mconv ? HD_ENGINE_S512_MCONV : staged ? HD_ENGINE_S512 : HD_ENGINE_GENERIC] += 1;
   if (ctx->profiling) {
     cudaEventRecord(e1, st);
     hd_ctx::ProfEntry* pe = nullptr;
@@ -1891,7 +1911,7 @@ int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 int64_t hd_graph_replays(hd_ctx_t ctx) { return ctx ? ctx->graph_replays : -1; }
 
 int64_t hd_engine_launches(hd_ctx_t ctx, int32_t engine) {
-  if (!ctx || engine < 0 || engine > HD_ENGINE_S512C) return -1;
+  if (!ctx || engine < 0 || engine > HD_ENGINE_S2048R) return -1;
   return ctx->engine_launches[engine];
 }
 

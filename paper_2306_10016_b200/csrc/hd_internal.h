@@ -17,13 +17,13 @@ constexpr int kS512LeanQ = 5;  // q <= 5: two CTAs per SM (zeta_{M1}^s from glob
 // per line, 12 <= q <= 22
 constexpr int kS512cQMin = 12, kS512cQMax = 22;
 LaunchFn lookup_s512c();
+// 1-D convolution pass of long lines at m = 2048, one CTA per line (hd_s2048r.cuh), q <= 8
+LaunchFn lookup_s2048r();
+int s2048r_threads();
+int s2048r_qmax();
+size_t s2048r_smem_bytes();
 int s512c_threads(int q);
 size_t s512c_smem_bytes();
-// the same at m = 2048 with four warps per residue (hd_s2048c.cuh), 4 <= q <= 6
-constexpr int kS2048cQMin = 4, kS2048cQMax = 6;
-LaunchFn lookup_s2048c();
-int s2048c_threads(int q);
-size_t s2048c_smem_bytes();
 size_t s512_smem_bytes(int q, int mode);
 int s512_threads(int q, int mode);
 // staged multi-pair convolution pass (MODE_MCONV): q <= s512_mconv_qmax()

@@ -100,30 +100,3 @@ int s512c_threads(int q) {
 size_t s512c_smem_bytes() { return s512c::smem_bytes(); }
 }  // namespace hd
 
-// ---------------------------------------------------------------------------
-// 1-D long lines at m = 2048: two-CTA clusters, four warps per residue (hd_s2048c.cuh)
-// ---------------------------------------------------------------------------
-#include "hd_s2048c.cuh"
-namespace hd {
-static cudaError_t launch_s2048c(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
-  constexpr int NT = s2048c::kGT * s2048c::kRMax;
-  auto kern = s2048c::s2048c_kernel<NT>;
-  if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
-  if (nt < s2048c::kGT || nt > NT || nt % 32) return cudaErrorInvalidConfiguration;
-  const int sms = device_sm_count();
-  int64_t ncl = (int64_t)a.nlines;
-  if (ncl > sms / 2) ncl = sms / 2;
-  grid.x = (unsigned)(2 * ncl);
-  grid.y = 1;
-  grid.z = 1;
-  kern<<<grid, nt, smem, st>>>(a);
-  return cudaGetLastError();
-}
-LaunchFn lookup_s2048c() { return launch_s2048c; }
-int s2048c_threads(int q) {
-  const int P = (q - 1) / 2, K0 = (q & 1) ? (P + 1) / 2 : P / 2;
-  const int n0 = 1 + 2 * K0, n1 = 2 * (P - K0) + ((q & 1) ? 0 : 1);
-  return s2048c::kGT * (n0 > n1 ? n0 : n1);
-}
-size_t s2048c_smem_bytes() { return s2048c::smem_bytes(); }
-}  // namespace hd

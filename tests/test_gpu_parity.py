@@ -588,9 +588,12 @@ def test_lambda_conv_config2_shape_and_padding(ctx, H):
 def test_s512c_cluster_conv1d(ctx, H, B, Lf, Lg, m):
     f, g = synth.random_pair(1500 + Lf + m, (B, Lf), (B, Lg))
     plan = H.Plan.make(1, [{"m": m, "C": 1}])
-    n0 = ctx.engine_launches(H.HD_ENGINE_S512C)
+    # m = 2048 runs on the one-CTA-per-line engine (hd_s2048r.cuh), which superseded
+    # the two-CTA cluster variant at that size
+    eng = H.HD_ENGINE_S512C if m == 512 else H.HD_ENGINE_S2048R
+    n0 = ctx.engine_launches(eng)
     h = host(ctx.conv(dev(f), dev(g), plan=plan, batch=True))
-    assert ctx.engine_launches(H.HD_ENGINE_S512C) - n0 == 1
+    assert ctx.engine_launches(eng) - n0 == 1
     for b in range(B):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
 
@@ -875,3 +878,31 @@ def test_explicit_variant_tuned_plan(ctx, H):
     own = H.Plan.make(2, [{"m": 64, "C": 2, "S": 4}, {"m": 128, "C": 1, "S": 2}], flags=H.HD_FLAG_EXPLICIT_PLAN)
     h2 = host(ctx.hd_conv_explicit([dev(f)], [dev(g)], plan=own))
     assert oracle.rel_l2(h2, ref) < 1e-11
+
+
+# ---------------------------------------------------------------- 1-D m = 2048 engine (hd_s2048r.cuh)
+@pytest.mark.parametrize("B,Lf,Lg", [(5, 8192, 3000),    # config 2's lines: q = 6, p_f = 4, p_g = 2
+                                     (3, 6000, 3000),    # q = 5 (last pair has one residue)
+                                     (2, 8192, 8192),    # q = 8, p = 4 both
+                                     (4, 1000, 9000),    # f shorter than g (roles as given)
+                                     (3, 2048, 1),       # q = 1
+                                     (7, 4097, 2049)])   # ragged blocks
+def test_s2048r_engine(ctx, H, B, Lf, Lg):
+    f, g = synth.random_pair(4200 + Lf + Lg, (B, Lf), (B, Lg))
+    plan = H.Plan.make(1, [{"m": 2048}])
+    n0 = ctx.engine_launches(H.HD_ENGINE_S2048R)
+    h = host(ctx.conv(dev(f), dev(g), plan=plan, batch=True))
+    assert ctx.engine_launches(H.HD_ENGINE_S2048R) - n0 == 1
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11, b
+
+
+def test_s2048r_shared_g_and_default_plan(ctx, H):
+    B = 6
+    f, _ = synth.random_pair(4300, (B, 8192), (1,))
+    g = synth.random_pair(4301, (3000,), (1,))[0]
+    n0 = ctx.engine_launches(H.HD_ENGINE_S2048R)
+    h = host(ctx.conv(dev(f), dev(g), batch=True, shared_g=True))   # default plan: m = 2048, D = q
+    assert ctx.engine_launches(H.HD_ENGINE_S2048R) - n0 == 1
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g)) < 1e-11
