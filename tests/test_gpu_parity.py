@@ -906,3 +906,4 @@ def test_s2048r_shared_g_and_default_plan(ctx, H):
     assert ctx.engine_launches(H.HD_ENGINE_S2048R) - n0 == 1
     for b in range(B):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g)) < 1e-11
+
