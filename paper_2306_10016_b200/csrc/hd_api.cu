@@ -630,6 +630,7 @@ bool use_s2048r(hd_dtype_t dt, const Launch& L) {
   const PassArgs& a = L.a;
   const LineIn &f = a.in_f, &g = a.in_g;
   const LineOut& o = a.out;
+  if (a.q > 2 && a.scr == nullptr) return false;  // no residue slots (ws_regions)
   return a.npairs == 1 && a.nbatch == 1 && f.p <= 8 && g.p <= 8 && f.tl >= 30 && f.s_j == 1 && f.jd <= 0 &&
          g.tl >= 30 && g.s_j == 1 && g.jd <= 0 && o.tl >= 30 && o.so_log2 >= 30 && o.s_js == 1 && o.jd <= 0 &&
          o.j0 == 0 && o.L <= (int64_t)o.T * 2048 && f.L < (1 << 30) && g.L < (1 << 30);
@@ -805,7 +806,14 @@ size_t ws_regions(const Problem& P, std::vector<int64_t>& elems) {
   elems.clear();
   const int64_t B = P.batch, Bg = P.shared_g ? 1 : P.batch;
   const AxisInfo* a = P.ax;
-  if (P.ndim == 2) {
+  if (P.ndim == 1) {
+    // residue slots of the 1-D m = 2048 engine (PassArgs::scr): one CTA per SM or line
+    const AxisInfo& x = a[0];
+    if (P.dt == HD_C128 && x.m == 2048 && x.q > 2 && x.q <= hd::s2048r_qmax() && P.N == 1) {
+      const int64_t ctas = std::min<int64_t>(B, hd::device_sm_count());
+      elems.push_back(ctas * 2 * (cdiv(x.q, 2) - 1) * 2048);
+    }
+  } else if (P.ndim == 2) {
     const int64_t Kxp = pad16(a[1].M1), Sx = a[1].S;
     const int64_t Oyp = cdiv(a[0].O, Sx) * Sx;
     for (int k = 0; k < P.N; ++k) elems.push_back(B * Kxp * a[0].Lf);
@@ -921,6 +929,7 @@ hd_status_t run_pipeline(hd_ctx* ctx, Problem& P, void* ws, size_t ws_bytes, cud
     L.a.scale = scale;
     L.a.nlines = B; L.a.nbatch = 1;
     L.ngroups = cdiv(B, x.lines); L.nbatch = 1;
+    if (!reg.empty()) L.a.scr = reg[0];
     return launch(ctx, P.dt, L, st);
   }
 

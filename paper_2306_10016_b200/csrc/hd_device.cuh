@@ -331,6 +331,10 @@ struct PassArgs {
   // output is the partial sum over those residues of the backward transform
   // (PAPER.md:531), e.g. one rank's share under residue sharding (hd_conv1d_dist)
   int32_t r_lo, r_hi;
+  // the 1-D m = 2048 engine (hd_s2048r.cuh): per-CTA slots for the inverse-transformed
+  // residues of all but the last pair of a line (gridDim.x x 2 (ceil(q/2) - 1) x 2048
+  // elements), so that the line's unfold runs once over every residue
+  void* scr;
 };
 
 enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2, MODE_MCONV = 3 /* staged engine only */ };

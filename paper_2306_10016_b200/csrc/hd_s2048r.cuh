@@ -15,10 +15,11 @@
 //             sub-problem k1 = w in registers (hd_w256.cuh)
 //   F parked in shared memory, G transformed the same way, product x 1/M1
 //   (PAPER.md:190-192), inverse FFT-2048 (exact adjoint) ending with
-//   zeta_{M1}^{-r s}: w_r[s] = zeta_{M1}^{-r s} V_r[s] stored to the group's row
-//   unfold    (all 512 threads) h[2048 t + s] (+)= sum_{r in pair} zeta_q^{-t r} w_r[s]
-//             (Backward Eq. PAPER.md:531); the first pair writes h, later pairs
-//             read-add-write it (the line stays in L2)
+//   zeta_{M1}^{-r s}: w_r[s] = zeta_{M1}^{-r s} V_r[s], stored to the CTA's residue
+//   slots in global memory (PassArgs::scr; they stay in L2) for every pair but the
+//   last, whose w_r go to the groups' shared rows
+//   unfold    (all 512 threads, once per line) h[2048 t + s] = sum_{r<q} zeta_q^{-t r}
+//             w_r[s] (Backward Eq. PAPER.md:531): h is written once
 // The next line's f and g are prefetched into L2 (bulk prefetch) while this one runs.
 // Shared memory: [E_A | E_B | P_A | P_B] (4 x 2048 slots) + stage twiddles zeta_2048^{t k1}
 // (7 x 256) + FFT-256 twiddle columns (14 x 32) + zeta_q, zeta_{8q} (<= 72).
@@ -152,8 +153,10 @@ __global__ void __launch_bounds__(NT, 1) s2048r_kernel(const __grid_constant__ P
       bulk_prefetch_l2(reinterpret_cast<const V*>(fi.ptr[0]) + line_off(fi, l + gridDim.x), (uint32_t)Lf * 16u);
       bulk_prefetch_l2(reinterpret_cast<const V*>(gi.ptr[0]) + line_off(gi, l + gridDim.x), (uint32_t)Lg * 16u);
     }
+    V* slots = reinterpret_cast<V*>(a.scr) + (int64_t)blockIdx.x * (2 * (npr - 1)) * M;
     for (int pr = 0; pr < npr; ++pr) {
       const int r = 2 * pr + grp;
+      const bool last = pr == npr - 1;
       if (r < q) {
         const V c0 = ldg(twM1 + ((int64_t)r * tt) % M1);  // zeta_{M1}^{r tt}
         V y[8];
@@ -167,33 +170,35 @@ __global__ void __launch_bounds__(NT, 1) s2048r_kernel(const __grid_constant__ P
 #pragma unroll
         for (int k = 0; k < 8; ++k) y[k] = cscale(cmul(Pw[k * 32 + lane], y[k]), scale);
         inv2048(y, c0, tw8, E, grp, tt, wg, lane, tw, r, q, z8q);
+        V* w = last ? P : slots + (int64_t)r * M;  // w_r[s], s = tt + 256 i
 #pragma unroll
-        for (int i = 0; i < 8; ++i) P[tt + GT * i] = y[i];  // w_r[s], s = tt + 256 i
+        for (int i = 0; i < 8; ++i) w[tt + GT * i] = y[i];
       }
-      __syncthreads();
-      // unfold of the pair: h[2048 t + s] (+)= sum_r zeta_q^{-t r} w_r[s]
-      const int r0 = 2 * pr, r1 = 2 * pr + 1;
-      const bool two = r1 < q;
-#pragma unroll 1
-      for (int c = 0; c < M / NT; ++c) {
-        const int s = tid + NT * c;
-        const V w0 = Pbase[s];
-        const V w1 = two ? Pbase[M + s] : cmk<V>(0, 0);
-        V acc[kQMax];
-        // the previous pairs' partial sums: every load issued before any use
-#pragma unroll
-        for (int t = 0; t < kQMax; ++t)
-          acc[t] = (pr > 0 && t < T && M * t + s < Lout) ? h[M * t + s] : cmk<V>(0, 0);
-#pragma unroll
-        for (int t = 0; t < kQMax; ++t) {
-          if (t >= T || M * t + s >= Lout) break;
-          V val = cfmac(acc[t], w0, zq[(t * r0) % q]);
-          if (two) val = cfmac(val, w1, zq[(t * r1) % q]);
-          h[M * t + s] = val;
-        }
-      }
-      __syncthreads();
     }
+    __syncthreads();
+    // unfold of the line: h[2048 t + s] = sum_{r<q} zeta_q^{-t r} w_r[s]
+    const int rl = 2 * (npr - 1);  // residues in shared memory: rl, rl + 1
+#pragma unroll 1
+    for (int c = 0; c < M / NT; ++c) {
+      const int s = tid + NT * c;
+      V w[kQMax];
+#pragma unroll
+      for (int r = 0; r < kQMax; ++r) {
+        if (r >= q) w[r] = cmk<V>(0, 0);
+        else if (r < rl) w[r] = __ldcs(slots + (int64_t)r * M + s);  // last use
+        else w[r] = Pbase[(r - rl) * M + s];
+      }
+#pragma unroll
+      for (int t = 0; t < kQMax; ++t) {
+        if (t >= T || M * t + s >= Lout) break;
+        V val = w[0];
+#pragma unroll
+        for (int r = 1; r < kQMax; ++r)
+          if (r < q) val = cfmac(val, w[r], zq[(t * r) % q]);
+        __stcs(h + M * t + s, val);  // streaming: keep L2 for the next lines' inputs and the slots
+      }
+    }
+    __syncthreads();
   }
 }
 
