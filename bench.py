@@ -213,12 +213,14 @@ def cpu_oracle_rate(f, g, Lout, target_s=12.0, seed=4242):
     """Oracle (as it stands) on host cores: output samples/s on a bounded random
     sample of output indices of the same workload."""
     import oracle
-    n = 256
+    # calibration: large enough that thread start-up does not dominate (a 256-sample
+    # probe underestimated the rate 3x and the measured sample ran 4 s, not target_s)
+    n = 8192
     idx = synth.sample_indices(Lout, n_random=n, seed=seed, edge=0)
     t = time.perf_counter()
     oracle.multiconv_sampled(f, g, idx)
     dt = time.perf_counter() - t
-    n2 = int(min(2_000_000, max(n, len(idx) * target_s / max(dt, 1e-6))))
+    n2 = int(min(8_000_000, max(n, len(idx) * target_s / max(dt, 1e-6))))
     idx = synth.sample_indices(Lout, n_random=n2, seed=seed + 1, edge=0)
     t = time.perf_counter()
     oracle.multiconv_sampled(f, g, idx)
