@@ -441,7 +441,12 @@ def run_ours(args, rank, world, local_rank):
                            "flops": "(2N+1) x 5 M log2 M + 6 M N per line, M = L_out of the conv axis, "
                                     "lines = L_out of the other axes (plan-independent)"}
     total_ab = sum(v for k, v in ab.items() if k != "pass_conv")
+    # compulsory bytes (stricter): the inputs read once, the output written once
+    comp = eb * batch * (N * (int(np.prod(Lf)) + int(np.prod(Lg))) + int(np.prod(Lout)))
+    step_s = ms * 1e-3 / args.steps
     whole = {"alg_bytes_per_step": total_ab,
+             "compulsory_bytes_per_step": comp,
+             "compulsory_frac_of_hbm": comp / step_s / 1e9 / peak,
              "achieved_gbs": total_ab / (ms * 1e-3 / args.steps) / 1e9,
              "frac_of_hbm": total_ab / (ms * 1e-3 / args.steps) / 1e9 / peak,
              "per_kernel_ms": {k: v[0] / v[1] for k, v in prof.items()},
