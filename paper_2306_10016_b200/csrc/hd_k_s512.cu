@@ -1,6 +1,7 @@
 // hd_k_s512.cu -- launchers of the staged m = 512 warp engine (hd_s512.cuh):
 // one persistent CTA per SM (two-stage cp.async ring, ~170 KB of shared memory),
 // blockDim = 32 q.
+#include <cstdlib>
 #include "hd_internal.h"
 #include "hd_s512.cuh"
 
@@ -23,11 +24,23 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
   return cudaGetLastError();
 }
 
+// q = 9: eight compute warps at 232 registers (s512_kernel's W8 layout, blockDim 384)
+// for the modes in the bit mask HD_S512_W8 (bit MODE_FWD, MODE_INV, MODE_CONV; default
+// kW8Default), the nine-warp layout at 168 registers (blockDim 320) for the others.
+constexpr int kW8Default = 1 << MODE_CONV;
+static bool s512_w8(int mode) {
+  static const int mask = [] {
+    const char* e = getenv("HD_S512_W8");
+    return e ? atoi(e) : kW8Default;
+  }();
+  return (mask >> mode) & 1;
+}
+
 // q = 9 (the BASELINE 2-D configs' axes) has a compile-time-q instantiation; other
 // q get a runtime-q kernel.  blockDim = 32 (q + 1): q compute warps + the producer.
 template <int MODE>
 static LaunchFn pick_s512(int q) {
-  if (q == 9) return launch_s512_impl<MODE, 320, 9>;
+  if (q == 9) return s512_w8(MODE) ? launch_s512_impl<MODE, 384, 9> : launch_s512_impl<MODE, 320, 9>;
   if (q == 7) return launch_s512_impl<MODE, 256, 7>;  // BASELINE config 5's x axis
   if (q == 5) return launch_s512_impl<MODE, 192, 5, 1>;  // the real path's packed y axis (lean)
   if (q <= kS512LeanQ) return launch_s512_impl<MODE, 32 * (kS512LeanQ + 1), 0, 1>;
@@ -59,14 +72,18 @@ LaunchFn lookup_s512_mconv(int q) { return q == 6 ? launch_s512_mconv<6> : launc
 int s512_mconv_qmax() { return s512::kMconvQMax; }
 
 // compute warps + the producer warp
-int s512_threads(int q, int mode) { (void)mode; return 32 * (q + 1); }
+int s512_threads(int q, int mode) {
+  if (q == 9 && mode != MODE_MCONV && s512_w8(mode)) return 384;
+  return 32 * (q + 1);
+}
 
 size_t s512_smem_bytes(int q, int mode) {
   if (mode == MODE_MCONV)
     return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 + 2 * (2 * q * 512));
   const bool lean = q <= kS512LeanQ && q != 9;
+  const bool x8 = q == 9 && mode == MODE_CONV && s512_w8(mode);  // W8: G_8's exchange area
   return 128 + sizeof(double2) * (size_t)(q * kQF + w512::kTwRows * 32 + (lean ? 0 : 512) +
-                                          2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)));
+                                          2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)) + (x8 ? 512 : 0));
 }
 
 }  // namespace hd

@@ -636,6 +636,26 @@ __device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, co
 // zeta_{M1}^{r s} g[s], s = lane + 32 i, then the size-512 FFT (E: exchange area).
 // LOWHALF (L_g <= 256): the upper half of w is zero.  Twiddles by four
 // interleaved recurrences of step zeta_{M1}^{128 r}.
+// g_transform's input step alone (all 16 values; zero beyond L_g)
+__device__ __forceinline__ void g_twist(V* v, const V* gbuf, int Lg, int r, int lane, const V* twM1, double scale) {
+  const V st1 = ldg(twM1 + r * 32);
+  const V st4 = ldg(twM1 + r * 128);
+  V wc[4];
+  wc[0] = cscale(ldg(twM1 + r * lane), scale);
+  wc[1] = cmul(wc[0], st1);
+  wc[2] = cmul(wc[1], st1);
+  wc[3] = cmul(wc[2], st1);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int s = lane + 32 * i;
+    v[i] = (s < Lg) ? cmul(gbuf[s], wc[i & 3]) : cmk<V>(0, 0);
+    if ((i & 3) == 3) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) wc[k] = cmul(wc[k], st4);
+    }
+  }
+}
+
 template <bool LOWHALF>
 __device__ __forceinline__ void g_transform(V* v, const V* gbuf, int Lg, int r, int lane, const V* twM1,
                                             double scale, V* E, const V* tw) {
@@ -664,18 +684,29 @@ __device__ __forceinline__ void g_transform(V* v, const V* gbuf, int Lg, int r, 
 // column, so that two CTAs fit one SM (q + 1 <= 6 warps each at <= 168 registers):
 // the small-q passes (the real-input path's packed convolution axis, q = 5) then
 // run 12 warps per SM instead of 6.
+//
+// W8 (q = 9, blockDim 384 = three warpgroups): eight compute warps (warpgroups 0, 1)
+// grown to 232 registers with setmaxnreg, the producer in warpgroup 2 shrunk to 40
+// (its other three warps exit).  Two compute warps per SM sub-partition and no
+// register spills; residue 8 is shared out: FWD / INV: warp 7 transforms it after
+// its own residue; CONV: warp 1 transforms F_8 (parked lane-major in row 8), warp 2
+// transforms G_8 (exchange area X after the stages) and forms the product in row 8,
+// warp 3 inverse-transforms it after its own residue (named barriers 3 and 4 between
+// them), so every sub-partition carries 6-7 of the 27 transforms of a column instead
+// of 6-9.
 template <int MODE, int NTMAX, int QC, int LEAN = 0>
 __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* done = full + 2;
+  constexpr bool kW8 = QC == 9 && NTMAX == 384;
   const int q = QC > 0 ? QC : a.q;
   V* zt = reinterpret_cast<V*>(smem_raw + 128);  // zt[r * kQF + t], r < q
   V* twtab = zt + q * kQF;
   V* twcol = twtab + w512::kTwRows * 32;   // zeta_{M1}^s, s < 512 (not LEAN)
   V* stage0 = LEAN ? twcol : twcol + M;
   const int tid = threadIdx.x;
-  const int nth = 32 * q;                  // compute threads; warp q is the producer
+  const int nth = kW8 ? 256 : 32 * q;      // compute threads; the next warp is the producer
   const int lane = tid & 31;
   const int r = tid >> 5;                  // this warp's residue (compute warps)
   const int k_arr = blockIdx.z;
@@ -685,7 +716,9 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
   // stores: lines TMA could only write in 16-byte pieces, see hd_api.cu)
   const bool tma = a.tm_in.kind != TMA_NONE;
   const bool tma_st = tma && a.tm_out.kind != TMA_NONE;
-  constexpr bool kPipeFold = (MODE == MODE_CONV && QC == 9);
+  // (measured for W8 too -- light warps 0, 4-7 folding during the others' fourth
+  // transform: conv_y 308 -> 323 us -- so W8 folds every item up front)
+  constexpr bool kPipeFold = (MODE == MODE_CONV && QC == 9 && !kW8);
   const V* twm = reinterpret_cast<const V*>(a.tw_m);
   const V* twM1 = reinterpret_cast<const V*>(a.tw_M1);
   if (QC == 0) {
@@ -710,6 +743,10 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
   const bool fam2 = QC == 9 && MODE == MODE_FWD && a.fam2;
   const int64_t total = total1 + (fam2 ? a.nlines2 : 0);
   const int kk_out = MODE == MODE_FWD ? k_arr : 0;
+  if constexpr (kW8) {  // every warp of a warpgroup executes its group's setmaxnreg
+    if (tid >= nth) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+  }
 
   // ------------------------------------------------------------ producer warp
   if (tid >= nth) {
@@ -800,13 +837,17 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     if (folded) {
       // done during the previous item
     } else if constexpr (MODE == MODE_INV) {
-      V v[16];
+#pragma unroll 1
+      for (int rr = r; rr < (kW8 && r == 7 ? 9 : r + 1); ++rr) {  // W8: warp 7 also takes row 8
+        V* Fx = buf + rr * M;
+        V v[16];
 #pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fr[k2 * 32 + lane];
-      w512::fft_inv(v, Fr, lane, tw);
-      __syncwarp();
+        for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fx[k2 * 32 + lane];
+        w512::fft_inv(v, Fx, lane, tw);
+        __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
+        for (int i = 0; i < 16; ++i) Fx[lane + 32 * i] = v[i];
+      }
     } else {
       if (QC == 9 && MODE == MODE_FWD && a.rp && !in2) {
         if (a.in_f.p <= 4) fold9_rp<4>(buf, (int)a.in_f.L, live, g < a.rp_rows, rp_im_slot(a), twc, tid, nth);
@@ -830,13 +871,73 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     }
     pc.mark(3);
     if constexpr (MODE == MODE_FWD) {
-      V v[16];
+#pragma unroll 1
+      for (int rr = r; rr < (kW8 && r == 7 ? 9 : r + 1); ++rr) {  // W8: warp 7 also takes row 8
+        V* Fx = buf + rr * M;
+        V v[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = Fr[lane + 32 * i];
-      w512::fft_fwd(v, Fr, lane, tw);
-      __syncwarp();
+        for (int i = 0; i < 16; ++i) v[i] = Fx[lane + 32 * i];
+        w512::fft_fwd(v, Fx, lane, tw);
+        __syncwarp();
 #pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) Fr[k2 * 32 + lane] = v[k2];  // lane-major spectrum
+        for (int k2 = 0; k2 < 16; ++k2) Fx[k2 * 32 + lane] = v[k2];  // lane-major spectrum
+      }
+    } else if constexpr (MODE == MODE_CONV && kW8) {
+      // Few FFT bodies (instruction cache): F_r in registers (one forward body); then
+      // a second forward body runs the warp's other jobs in a loop -- residue 8's share
+      // (warp 1: F_8 -> row 8; warp 2: G_8 x F_8 -> row 8), then G_r (exchange in row
+      // r, free once F_r is in registers); one inverse body for V_r and (warp 3)
+      // residue 8.
+      V* R8 = buf + 8 * M;
+      V* X = stage0 + 2 * SB;
+      const int Lg = live ? (int)a.in_g.L : 0;
+      V F[16], v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) F[i] = Fr[lane + 32 * i];
+      w512::fft_fwd(F, Fr, lane, tw);
+#pragma unroll 1
+      for (int j = (r == 1 || r == 2) ? -1 : 0; j < 1; ++j) {
+        const bool fromrow = j < 0 && r == 1;  // F_8 (folded in row 8), else a G transform
+        V* Ex = j < 0 ? (r == 1 ? R8 : X) : Fr;
+        __syncwarp();
+        if (fromrow) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = R8[lane + 32 * i];
+        } else {
+          g_twist(v, gbuf, Lg, j < 0 ? 8 : r, lane, twM1, a.scale);
+        }
+        __syncwarp();
+        w512::fft_fwd_rt(v, Ex, lane, tw, !fromrow && Lg <= M / 2);
+        if (j < 0) {
+          __syncwarp();
+          if (r == 1) {  // F_8 parked lane-major in row 8
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = v[k2];
+            asm volatile("bar.arrive 3, 64;" ::: "memory");
+          } else {  // G_8 x F_8 -> row 8
+            asm volatile("bar.sync 3, 64;" ::: "memory");
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = cmul(R8[k2 * 32 + lane], v[k2]);
+            asm volatile("bar.arrive 4, 64;" ::: "memory");
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = cmul(F[k], v[k]);
+#pragma unroll 1
+      for (int j = 0; j < (r == 3 ? 2 : 1); ++j) {
+        V* Ex = j == 0 ? Fr : R8;
+        if (j == 1) {
+          asm volatile("bar.sync 4, 64;" ::: "memory");
+#pragma unroll
+          for (int k2 = 0; k2 < 16; ++k2) v[k2] = R8[k2 * 32 + lane];
+        }
+        __syncwarp();
+        w512::fft_inv(v, Ex, lane, tw);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Ex[lane + 32 * i] = v[i];
+      }
     } else if constexpr (MODE == MODE_CONV) {
       V F[16];
 #pragma unroll
