@@ -713,8 +713,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   static unsigned long long* d_phase = nullptr;
   L.a.phase_prof = nullptr;
   if (phase_prof && use_s512(dt, L)) {
-    if (!d_phase) cudaMalloc(&d_phase, 40 * sizeof(unsigned long long));
-    cudaMemsetAsync(d_phase, 0, 40 * sizeof(unsigned long long), st);
+    if (!d_phase) cudaMalloc(&d_phase, 8 * 17 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_phase, 0, 8 * 17 * sizeof(unsigned long long), st);
     L.a.phase_prof = d_phase;
   }
   // debug: HD_DEBUG_LAUNCH=1 prints each pass's engine, TMA kinds and shape
@@ -727,17 +727,19 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   cudaError_t e = fn(L.a, grid, threads, smem, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, L.name);
   if (L.a.phase_prof) {
-    unsigned long long h[40];
+    unsigned long long h[8 * 17];
     cudaMemcpyAsync(h, d_phase, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    const int cw = threads / 32 - 1;  // compute warps (hd_s512.cuh: one producer warp)
+    const int cw = threads == 384 ? 8 : threads / 32 - 1;  // compute warps (hd_s512.cuh: W8 or q + producer)
     const double n = (double)total * cw;
     fprintf(stderr, "[phase] %-8s", L.name);
     for (int i = 0; i < 8; ++i) fprintf(stderr, " %7.0f", h[i] / n);
-    fprintf(stderr, "\n[phase] %-8s per-warp transform/barrier:", L.name);
-    for (int w = 0; w < 16 && w < cw; ++w)
-      fprintf(stderr, " %d:%.0f/%.0f", w, h[8 + 2 * w] / (double)total, h[9 + 2 * w] / (double)total);
     fprintf(stderr, "\n");
+    for (int w = 0; w < 16 && w < cw; ++w) {
+      fprintf(stderr, "[phase] %-8s warp %2d", L.name, w);
+      for (int i = 0; i < 8; ++i) fprintf(stderr, " %7.0f", h[8 * (1 + w) + i] / (double)total);
+      fprintf(stderr, "\n");
+    }
   }
   if (!ctx->capturing) ctx->launches += 1;
   if (!ctx->capturing) ctx->engine_launches[s2048r ? HD_ENGINE_S2048R : s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128

@@ -74,9 +74,9 @@ struct PhaseClock {
     if (on && (threadIdx.x & 31) == 0) {
 #pragma unroll
       for (int i = 0; i < kPhases; ++i) atomicAdd(out + i, acc[i]);
-      // per warp: transform phase (4) and its barrier (5)
-      atomicAdd(out + kPhases + 2 * (threadIdx.x >> 5), acc[4]);
-      atomicAdd(out + kPhases + 2 * (threadIdx.x >> 5) + 1, acc[5]);
+      // per warp: every phase
+#pragma unroll
+      for (int i = 0; i < kPhases; ++i) atomicAdd(out + kPhases * (1 + (threadIdx.x >> 5)) + i, acc[i]);
     }
   }
 };
@@ -892,38 +892,38 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
       V* X = stage0 + 2 * SB;
       const int Lg = live ? (int)a.in_g.L : 0;
       V F[16], v[16];
+      // F_r and G_r together (one exchange area: row r)
 #pragma unroll
       for (int i = 0; i < 16; ++i) F[i] = Fr[lane + 32 * i];
-      w512::fft_fwd(F, Fr, lane, tw);
-#pragma unroll 1
-      for (int j = (r == 1 || r == 2) ? -1 : 0; j < 1; ++j) {
-        const bool fromrow = j < 0 && r == 1;  // F_8 (folded in row 8), else a G transform
-        V* Ex = j < 0 ? (r == 1 ? R8 : X) : Fr;
+      g_twist(v, gbuf, Lg, r, lane, twM1, a.scale);
+      w512::fft_fwd2(F, v, Fr, lane, tw, Lg <= M / 2);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) F[k] = cmul(F[k], v[k]);  // F_r G_r
+      if (r == 1 || r == 2) {  // residue 8's share: warp 1 F_8 -> row 8; warp 2 G_8 x F_8 -> row 8
+        V* Ex = r == 1 ? R8 : X;
         __syncwarp();
-        if (fromrow) {
+        if (r == 1) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = R8[lane + 32 * i];
         } else {
-          g_twist(v, gbuf, Lg, j < 0 ? 8 : r, lane, twM1, a.scale);
+          g_twist(v, gbuf, Lg, 8, lane, twM1, a.scale);
         }
         __syncwarp();
-        w512::fft_fwd_rt(v, Ex, lane, tw, !fromrow && Lg <= M / 2);
-        if (j < 0) {
-          __syncwarp();
-          if (r == 1) {  // F_8 parked lane-major in row 8
+        w512::fft_fwd_rt(v, Ex, lane, tw, r == 2 && Lg <= M / 2);
+        __syncwarp();
+        if (r == 1) {
 #pragma unroll
-            for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = v[k2];
-            asm volatile("bar.arrive 3, 64;" ::: "memory");
-          } else {  // G_8 x F_8 -> row 8
-            asm volatile("bar.sync 3, 64;" ::: "memory");
+          for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = v[k2];
+          asm volatile("bar.arrive 3, 64;" ::: "memory");
+        } else {
+          asm volatile("bar.sync 3, 64;" ::: "memory");
 #pragma unroll
-            for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = cmul(R8[k2 * 32 + lane], v[k2]);
-            asm volatile("bar.arrive 4, 64;" ::: "memory");
-          }
+          for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = cmul(R8[k2 * 32 + lane], v[k2]);
+          asm volatile("bar.arrive 4, 64;" ::: "memory");
         }
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = cmul(F[k], v[k]);
+      for (int k = 0; k < 16; ++k) v[k] = F[k];
 #pragma unroll 1
       for (int j = 0; j < (r == 3 ? 2 : 1); ++j) {
         V* Ex = j == 0 ? Fr : R8;

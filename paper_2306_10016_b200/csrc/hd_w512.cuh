@@ -156,6 +156,50 @@ __device__ __forceinline__ void fft_fwd_rt(V* a, V* E, int lane, const V* tw, bo
   }
 }
 
+// Two forward FFT-512s interleaved stage by stage (independent data, so the radix-16
+// stages of one overlap the other's shared-memory exchange); one 512-slot exchange
+// area, used by a then b.  lowb: b's upper half is zero (fft_fwd<true>).
+__device__ __forceinline__ void fft_fwd2(V* a, V* b, V* E, int lane, const V* tw, bool lowb) {
+  dft16<+1>(a);
+  if (lowb) dft16<+1, true>(b);
+  else dft16<+1>(b);
+#pragma unroll
+  for (int j = 1; j < 16; ++j) {
+    const V w = tw[(j - 1) * 32];
+    a[j] = cmul(a[j], w);
+    b[j] = cmul(b[j], w);
+  }
+  const int jj = lane >> 1, t2 = lane & 1;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) E[ex(j, lane)] = a[j];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = E[ex(jj, t2 + 2 * i)];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) E[ex(j, lane)] = b[j];
+  dft16<+1>(a);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) b[i] = E[ex(jj, t2 + 2 * i)];
+  dft16<+1>(b);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const V sa = t2 ? a[k] : a[k + 8], sb = t2 ? b[k] : b[k + 8];
+    const V ra = shfl_x1(sa), rb = shfl_x1(sb);
+    if (t2) { a[k] = ra; b[k] = rb; } else { a[k + 8] = ra; b[k + 8] = rb; }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const V w = tw[(15 + k) * 32];
+    const V wa = cmul(a[k + 8], w), wb = cmul(b[k + 8], w);
+    const V A = a[k], B = b[k];
+    a[k] = cadd(A, wa); a[k + 8] = csub(A, wa);
+    b[k] = cadd(B, wb); b[k + 8] = csub(B, wb);
+  }
+}
+
 // Inverse FFT-512 (adjoint of fft_fwd).  In: a[k] = Y[freq_of(lane, k)].
 // Out: a[i] = sum_f zeta_512^{-(lane + 32 i) f} Y[f].
 __device__ __forceinline__ void fft_inv(V* a, V* E, int lane, const V* tw) {
