@@ -81,9 +81,11 @@ size_t s512_smem_bytes(int q, int mode) {
   if (mode == MODE_MCONV)
     return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 + 2 * (2 * q * 512));
   const bool lean = q <= kS512LeanQ && q != 9;
-  const bool x8 = q == 9 && mode == MODE_CONV && s512_w8(mode);  // W8: G_8's exchange area
+  // W8 convolution: G_8's halves (X) and the FFT-256 twiddle columns
+  const bool x8 = q == 9 && mode == MODE_CONV && s512_w8(mode);
   return 128 + sizeof(double2) * (size_t)(q * kQF + w512::kTwRows * 32 + (lean ? 0 : 512) +
-                                          2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)) + (x8 ? 512 : 0));
+                                          2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)) +
+                                          (x8 ? 512 + w256::kTwRows * 32 : 0));
 }
 
 }  // namespace hd

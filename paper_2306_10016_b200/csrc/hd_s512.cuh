@@ -30,6 +30,7 @@
 #include "hd_internal.h"
 #include "hd_tma.cuh"
 #include "hd_w512.cuh"
+#include "hd_w256.cuh"
 #include "hd_zq_table.h"
 
 namespace hd {
@@ -460,7 +461,10 @@ __device__ __forceinline__ void unfold9_rs(V* buf, int T, const V* twcol, int ti
   }
 }
 
-template <int NC>
+// SPLIT8: row 8 holds residue 8's inverse as two halves a (slots [0, 256)) and
+// zeta_512^{-n} b (slots [256, 512)) of the last radix-2 step; V_8[n] = a +- zeta^{-n} b
+// is formed here (columns s and s + 256 of one thread: NC = 2, s = {t, t + 256}).
+template <int NC, bool SPLIT8 = false>
 __device__ __forceinline__ void unfold_col9(V* buf, const int* s, int T, const V* w1) {
   V x[NC][9];
 #pragma unroll
@@ -470,8 +474,13 @@ __device__ __forceinline__ void unfold_col9(V* buf, const int* s, int T, const V
     V wo = w1[c], we = w2;
 #pragma unroll
     for (int r = 1; r < 9; ++r) {
-      if (r & 1) { x[c][r] = cmulc(buf[r * M + s[c]], wo); wo = cmul(wo, w2); }
-      else { x[c][r] = cmulc(buf[r * M + s[c]], we); we = cmul(we, w2); }
+      V y = buf[r * M + s[c]];
+      if (SPLIT8 && r == 8) {
+        const V lo = buf[8 * M + (s[c] & 255)], hi = buf[8 * M + 256 + (s[c] & 255)];
+        y = s[c] < 256 ? cadd(lo, hi) : csub(lo, hi);
+      }
+      if (r & 1) { x[c][r] = cmulc(y, wo); wo = cmul(wo, w2); }
+      else { x[c][r] = cmulc(y, we); we = cmul(we, w2); }
     }
   }
 #pragma unroll
@@ -598,13 +607,13 @@ __device__ __forceinline__ void unfold_col(V* buf, int s, int qrt, int T, const 
   }
 }
 
-template <int QC>
+template <int QC, bool SPLIT8 = false>
 __device__ __forceinline__ void unfold_all(V* buf, int q, int T, const V* zt, const V* twcol, int tid, int nth) {
   if constexpr (QC == 9) {
     if (tid < M / 2) {
       const int sc[2] = {tid, tid + M / 2};
       const V w1[2] = {twcol[sc[0]], twcol[sc[1]]};
-      unfold_col9<2>(buf, sc, T, w1);
+      unfold_col9<2, SPLIT8>(buf, sc, T, w1);
     }
   } else {
     for (int s = tid; s < M; s += nth) {
@@ -704,7 +713,9 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
   V* zt = reinterpret_cast<V*>(smem_raw + 128);  // zt[r * kQF + t], r < q
   V* twtab = zt + q * kQF;
   V* twcol = twtab + w512::kTwRows * 32;   // zeta_{M1}^s, s < 512 (not LEAN)
-  V* stage0 = LEAN ? twcol : twcol + M;
+  constexpr bool kHalf8 = kW8 && MODE == MODE_CONV;  // residue 8 as FFT-256 halves
+  V* tw256 = LEAN ? twcol : twcol + M;     // FFT-256 twiddle columns (kHalf8)
+  V* stage0 = tw256 + (kHalf8 ? w256::kTwRows * 32 : 0);
   const int tid = threadIdx.x;
   const int nth = kW8 ? 256 : 32 * q;      // compute threads; the next warp is the producer
   const int lane = tid & 31;
@@ -730,6 +741,8 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
   for (int i = tid; i < w512::kTwRows * 32; i += blockDim.x) twtab[i] = w512::tw_entry(twm, i >> 5, i & 31);
   if (!LEAN)
     for (int i = tid; i < M; i += blockDim.x) twcol[i] = ldg(twM1 + i);
+  if (kHalf8)
+    for (int i = tid; i < w256::kTwRows * 32; i += blockDim.x) tw256[i] = w256::tw_entry(twm, M, i >> 5, i & 31);
   const V* twc = LEAN ? twM1 : twcol;
   if (tid == nth) {
     mbar_init(&full[0], 1);
@@ -883,60 +896,75 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
         for (int k2 = 0; k2 < 16; ++k2) Fx[k2 * 32 + lane] = v[k2];  // lane-major spectrum
       }
     } else if constexpr (MODE == MODE_CONV && kW8) {
-      // Few FFT bodies (instruction cache): F_r in registers (one forward body); then
-      // a second forward body runs the warp's other jobs in a loop -- residue 8's share
-      // (warp 1: F_8 -> row 8; warp 2: G_8 x F_8 -> row 8), then G_r (exchange in row
-      // r, free once F_r is in registers); one inverse body for V_r and (warp 3)
-      // residue 8.
+      // Residue 8 runs as six FFT-256 half jobs (one radix-2 step of the size-512
+      // transform): forward X[2k] = FFT256(w[n] + w[n+256]), X[2k+1] =
+      // FFT256((w[n] - w[n+256]) zeta_512^n); inverse halves a = IFFT256(Y[2k]),
+      // b = IFFT256(Y[2k+1]) zeta_512^{-n}, combined y = a +- b in the unfold.
+      //   warps 4, 5: F_8 halves 0, 1 (row 8 -> row 8, slots [256 h, 256 h + 256))
+      //   warps 6, 7: G_8 halves 0, 1 (twisted g -> X)
+      //   warps 0, 1: product and inverse of half 0, 1 (row 8), after their own residue
+      // so every warp carries three transforms and at most one half (sub-partitions
+      // (w + c) mod 4: 7, 7, 6.5, 6.5 transforms).  Named barriers: 5 (warps 4, 5: both
+      // halves read row 8 before either overwrites it), 3 / 4 (half 0 / 1 ready:
+      // arrive by the F and G warps, sync by warp 0 / 1).
       V* R8 = buf + 8 * M;
       V* X = stage0 + 2 * SB;
       const int Lg = live ? (int)a.in_g.L : 0;
+      const V* tq = tw256 + lane;
       V F[16], v[16];
-      // F_r and G_r together (one exchange area: row r)
+      if (r >= 4) {
+        const int h = r & 1;
+        const bool isF = r < 6;
+        V* E = (isF ? R8 : X) + 256 * h;
+        V a8[8];
+        if (isF) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) { v[i] = R8[lane + 32 * i]; v[i + 8] = R8[lane + 32 * i + 256]; }
+        } else {
+          g_twist(v, gbuf, Lg, 8, lane, twM1, a.scale);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          a8[i] = h ? cmul(csub(v[i], v[i + 8]), ldg(twm + lane + 32 * i)) : cadd(v[i], v[i + 8]);
+        if (isF) asm volatile("bar.sync 5, 64;" ::: "memory");
+        __syncwarp();
+        w256::fft256_fwd(a8, E, lane, tq);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) E[k * 32 + lane] = a8[k];
+        if (h) asm volatile("bar.arrive 4, 96;" ::: "memory");
+        else asm volatile("bar.arrive 3, 96;" ::: "memory");
+      }
+      // F_r and G_r together (one exchange area: row r), product
 #pragma unroll
       for (int i = 0; i < 16; ++i) F[i] = Fr[lane + 32 * i];
       g_twist(v, gbuf, Lg, r, lane, twM1, a.scale);
       w512::fft_fwd2(F, v, Fr, lane, tw, Lg <= M / 2);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) F[k] = cmul(F[k], v[k]);  // F_r G_r
-      if (r == 1 || r == 2) {  // residue 8's share: warp 1 F_8 -> row 8; warp 2 G_8 x F_8 -> row 8
-        V* Ex = r == 1 ? R8 : X;
-        __syncwarp();
-        if (r == 1) {
+      for (int k = 0; k < 16; ++k) v[k] = cmul(F[k], v[k]);
+      __syncwarp();
+      w512::fft_inv(v, Fr, lane, tw);
+      __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = R8[lane + 32 * i];
-        } else {
-          g_twist(v, gbuf, Lg, 8, lane, twM1, a.scale);
+      for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
+      if (r < 2) {  // half r of residue 8: product, inverse FFT-256
+        const int h = r;
+        if (h) asm volatile("bar.sync 4, 96;" ::: "memory");
+        else asm volatile("bar.sync 3, 96;" ::: "memory");
+        V* E = R8 + 256 * h;
+        const V* Xh = X + 256 * h;
+        V a8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a8[k] = cmul(E[k * 32 + lane], Xh[k * 32 + lane]);
+        __syncwarp();
+        w256::fft256_inv(a8, E, lane, tq);
+        if (h) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a8[i] = cmulc(a8[i], ldg(twm + lane + 32 * i));
         }
         __syncwarp();
-        w512::fft_fwd_rt(v, Ex, lane, tw, r == 2 && Lg <= M / 2);
-        __syncwarp();
-        if (r == 1) {
 #pragma unroll
-          for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = v[k2];
-          asm volatile("bar.arrive 3, 64;" ::: "memory");
-        } else {
-          asm volatile("bar.sync 3, 64;" ::: "memory");
-#pragma unroll
-          for (int k2 = 0; k2 < 16; ++k2) R8[k2 * 32 + lane] = cmul(R8[k2 * 32 + lane], v[k2]);
-          asm volatile("bar.arrive 4, 64;" ::: "memory");
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = F[k];
-#pragma unroll 1
-      for (int j = 0; j < (r == 3 ? 2 : 1); ++j) {
-        V* Ex = j == 0 ? Fr : R8;
-        if (j == 1) {
-          asm volatile("bar.sync 4, 64;" ::: "memory");
-#pragma unroll
-          for (int k2 = 0; k2 < 16; ++k2) v[k2] = R8[k2 * 32 + lane];
-        }
-        __syncwarp();
-        w512::fft_inv(v, Ex, lane, tw);
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) Ex[lane + 32 * i] = v[i];
+        for (int i = 0; i < 8; ++i) E[lane + 32 * i] = a8[i];
       }
     } else if constexpr (MODE == MODE_CONV) {
       V F[16];
@@ -972,7 +1000,7 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
       compute_sync(nth);
       pc.mark(5);
       if (QC == 9 && MODE == MODE_INV && a.rs) unfold9_rs(buf, a.out.T, twc, tid, nth);
-      else unfold_all<QC>(buf, q, a.out.T, zt, twc, tid, nth);
+      else unfold_all<QC, kHalf8>(buf, q, a.out.T, zt, twc, tid, nth);
     }
     pc.mark(6);
     // results are in stage slots j < out.L

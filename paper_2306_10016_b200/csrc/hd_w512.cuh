@@ -126,36 +126,6 @@ __device__ __forceinline__ void fft_fwd(V* a, V* E, int lane, const V* tw) {
   }
 }
 
-// fft_fwd with the LOWHALF choice at run time: only the first radix-16 stage is
-// duplicated, so call sites that need both share one body (instruction cache)
-__device__ __forceinline__ void fft_fwd_rt(V* a, V* E, int lane, const V* tw, bool low) {
-  if (low) dft16<+1, true>(a);
-  else dft16<+1>(a);
-#pragma unroll
-  for (int j = 1; j < 16; ++j) a[j] = cmul(a[j], tw[(j - 1) * 32]);
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 16; ++j) E[ex(j, lane)] = a[j];
-  __syncwarp();
-  const int jj = lane >> 1, t2 = lane & 1;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = E[ex(jj, t2 + 2 * i)];
-  dft16<+1>(a);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const V snd = t2 ? a[k] : a[k + 8];
-    const V rcv = shfl_x1(snd);
-    if (t2) a[k] = rcv; else a[k + 8] = rcv;
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const V wb = cmul(a[k + 8], tw[(15 + k) * 32]);
-    const V A = a[k];
-    a[k] = cadd(A, wb);
-    a[k + 8] = csub(A, wb);
-  }
-}
-
 // Two forward FFT-512s interleaved stage by stage (independent data, so the radix-16
 // stages of one overlap the other's shared-memory exchange); one 512-slot exchange
 // area, used by a then b.  lowb: b's upper half is zero (fft_fwd<true>).
