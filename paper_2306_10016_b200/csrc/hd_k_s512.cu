@@ -24,16 +24,17 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
   return cudaGetLastError();
 }
 
-// q = 9: eight compute warps at 232 registers (s512_kernel's W8 layout, blockDim 384)
-// for the modes in the bit mask HD_S512_W8 (bit MODE_FWD, MODE_INV, MODE_CONV; default
-// kW8Default), the nine-warp layout at 168 registers (blockDim 320) for the others.
-constexpr int kW8Default = 1 << MODE_CONV;
+// q = 9: eight compute warps at 232 registers (s512_kernel's W8 layout, blockDim 384),
+// else nine at 168 (blockDim 320).  HD_S512_W8 (A/B switch) = bit mask: 1 the x passes
+// (forward and inverse together: W8 stores residue 8's spectrum as two FFT-256 halves,
+// an order both passes of an axis must share), 2 the convolution pass.
+constexpr int kW8Default = 2;
 static bool s512_w8(int mode) {
   static const int mask = [] {
     const char* e = getenv("HD_S512_W8");
     return e ? atoi(e) : kW8Default;
   }();
-  return (mask >> mode) & 1;
+  return (mask >> (mode == MODE_CONV ? 1 : 0)) & 1;
 }
 
 // q = 9 (the BASELINE 2-D configs' axes) has a compile-time-q instantiation; other
@@ -81,11 +82,11 @@ size_t s512_smem_bytes(int q, int mode) {
   if (mode == MODE_MCONV)
     return 128 + sizeof(double2) * (size_t)(kQF * kQF + w512::kTwRows * 32 + 512 + 2 * (2 * q * 512));
   const bool lean = q <= kS512LeanQ && q != 9;
-  // W8 convolution: G_8's halves (X) and the FFT-256 twiddle columns
-  const bool x8 = q == 9 && mode == MODE_CONV && s512_w8(mode);
+  // W8: the FFT-256 twiddle columns; the convolution pass also G_8's halves (X)
+  const bool w8 = q == 9 && s512_w8(mode);
   return 128 + sizeof(double2) * (size_t)(q * kQF + w512::kTwRows * 32 + (lean ? 0 : 512) +
                                           2 * (q * 512 + (mode == MODE_CONV ? 512 : 0)) +
-                                          (x8 ? 512 + w256::kTwRows * 32 : 0));
+                                          (w8 ? w256::kTwRows * 32 + (mode == MODE_CONV ? 512 : 0) : 0));
 }
 
 }  // namespace hd

@@ -425,6 +425,7 @@ __device__ __forceinline__ void fold9_rp(V* buf, int L, bool live, bool im_ok, i
 // unfold_col9 with the real-split output (a.rs): Re of h[t m + s] -> double t m + s of
 // the stage, Im -> double T9SLOTS + t m + s, after a barrier (the doubles overlap
 // other columns' residues)
+template <bool SPLIT8 = false>  // row 8 as two halves (see unfold_col9)
 __device__ __forceinline__ void unfold9_rs(V* buf, int T, const V* twcol, int tid, int nth) {
   constexpr int NC = 2;
   const bool act = tid < M / 2;
@@ -439,8 +440,13 @@ __device__ __forceinline__ void unfold9_rs(V* buf, int T, const V* twcol, int ti
       V wo = w1, we = w2;
 #pragma unroll
       for (int r = 1; r < 9; ++r) {
-        if (r & 1) { x[c][r] = cmulc(buf[r * M + s[c]], wo); wo = cmul(wo, w2); }
-        else { x[c][r] = cmulc(buf[r * M + s[c]], we); we = cmul(we, w2); }
+        V y = buf[r * M + s[c]];
+        if (SPLIT8 && r == 8) {
+          const V lo = buf[8 * M + tid], hi = buf[8 * M + 256 + tid];
+          y = c == 0 ? cadd(lo, hi) : csub(lo, hi);
+        }
+        if (r & 1) { x[c][r] = cmulc(y, wo); wo = cmul(wo, w2); }
+        else { x[c][r] = cmulc(y, we); we = cmul(we, w2); }
       }
     }
   }
@@ -713,7 +719,7 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
   V* zt = reinterpret_cast<V*>(smem_raw + 128);  // zt[r * kQF + t], r < q
   V* twtab = zt + q * kQF;
   V* twcol = twtab + w512::kTwRows * 32;   // zeta_{M1}^s, s < 512 (not LEAN)
-  constexpr bool kHalf8 = kW8 && MODE == MODE_CONV;  // residue 8 as FFT-256 halves
+  constexpr bool kHalf8 = kW8;  // residue 8 as FFT-256 halves
   V* tw256 = LEAN ? twcol : twcol + M;     // FFT-256 twiddle columns (kHalf8)
   V* stage0 = tw256 + (kHalf8 ? w256::kTwRows * 32 : 0);
   const int tid = threadIdx.x;
@@ -850,16 +856,30 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     if (folded) {
       // done during the previous item
     } else if constexpr (MODE == MODE_INV) {
-#pragma unroll 1
-      for (int rr = r; rr < (kW8 && r == 7 ? 9 : r + 1); ++rr) {  // W8: warp 7 also takes row 8
-        V* Fx = buf + rr * M;
+      {
         V v[16];
 #pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fx[k2 * 32 + lane];
-        w512::fft_inv(v, Fx, lane, tw);
+        for (int k2 = 0; k2 < 16; ++k2) v[k2] = Fr[k2 * 32 + lane];
+        w512::fft_inv(v, Fr, lane, tw);
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) Fx[lane + 32 * i] = v[i];
+        for (int i = 0; i < 16; ++i) Fr[lane + 32 * i] = v[i];
+      }
+      if (kW8 && (r == 2 || r == 3)) {  // residue 8's inverse halves (combined in the unfold)
+        const int h = r - 2;
+        V* E = buf + 8 * M + 256 * h;
+        V a8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a8[k] = E[k * 32 + lane];
+        __syncwarp();
+        w256::fft256_inv(a8, E, lane, tw256 + lane);
+        if (h) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a8[i] = cmulc(a8[i], ldg(twm + lane + 32 * i));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) E[lane + 32 * i] = a8[i];
       }
     } else {
       if (QC == 9 && MODE == MODE_FWD && a.rp && !in2) {
@@ -884,17 +904,29 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     }
     pc.mark(3);
     if constexpr (MODE == MODE_FWD) {
-#pragma unroll 1
-      for (int rr = r; rr < (kW8 && r == 7 ? 9 : r + 1); ++rr) {  // W8: warp 7 also takes row 8
-        V* Fx = buf + rr * M;
-        V v[16];
+      if (kW8 && (r == 2 || r == 3)) {  // residue 8's forward halves: X[2k] / X[2k+1]
+        const int h = r - 2;
+        V* R8 = buf + 8 * M;
+        V* E = R8 + 256 * h;
+        V a8[8];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = Fx[lane + 32 * i];
-        w512::fft_fwd(v, Fx, lane, tw);
+        for (int i = 0; i < 8; ++i) {
+          const V x0 = R8[lane + 32 * i], x1 = R8[lane + 32 * i + 256];
+          a8[i] = h ? cmul(csub(x0, x1), ldg(twm + lane + 32 * i)) : cadd(x0, x1);
+        }
+        asm volatile("bar.sync 5, 64;" ::: "memory");  // both halves read row 8
+        w256::fft256_fwd(a8, E, lane, tw256 + lane);
         __syncwarp();
 #pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) Fx[k2 * 32 + lane] = v[k2];  // lane-major spectrum
+        for (int k = 0; k < 8; ++k) E[k * 32 + lane] = a8[k];
       }
+      V v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = Fr[lane + 32 * i];
+      w512::fft_fwd(v, Fr, lane, tw);
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) Fr[k2 * 32 + lane] = v[k2];  // lane-major spectrum
     } else if constexpr (MODE == MODE_CONV && kW8) {
       // Residue 8 runs as six FFT-256 half jobs (one radix-2 step of the size-512
       // transform): forward X[2k] = FFT256(w[n] + w[n+256]), X[2k+1] =
@@ -999,7 +1031,7 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
     if constexpr (MODE != MODE_FWD) {
       compute_sync(nth);
       pc.mark(5);
-      if (QC == 9 && MODE == MODE_INV && a.rs) unfold9_rs(buf, a.out.T, twc, tid, nth);
+      if (QC == 9 && MODE == MODE_INV && a.rs) unfold9_rs<kHalf8>(buf, a.out.T, twc, tid, nth);
       else unfold_all<QC, kHalf8>(buf, q, a.out.T, zt, twc, tid, nth);
     }
     pc.mark(6);
