@@ -631,7 +631,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-explicit", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--mode", default="auto", choices=["auto", "independent", "slab"],
                     help="auto: N = 1 single-GPU pipeline; N > 1 one slab-decomposed problem (strong "
                          "scaling, NCCL exchanges in libhdconv) with weak scaling as an extra key; "
