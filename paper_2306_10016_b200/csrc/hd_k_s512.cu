@@ -12,6 +12,8 @@ static cudaError_t launch_s512_impl(const PassArgs& a, dim3 grid, int nt, size_t
   auto kern = s512::s512_kernel<MODE, NTMAX, QC, LEAN>;
   if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt < 32 || nt > NTMAX || nt % 32) return cudaErrorInvalidConfiguration;
+  // W8: setmaxnreg acts on whole warpgroups -- exactly three of them
+  if (QC == 9 && NTMAX == 384 && nt != 384) return cudaErrorInvalidConfiguration;
   const int sms = device_sm_count();
   int occ = 1;
   if (LEAN) {
