@@ -361,8 +361,9 @@ hd_status_t hd_conv1d_dist(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const 
  *  in_lo/in_hi   rows (2-D) / planes (3-D) of f this rank holds (row-major, contiguous)
  *  out_lo/out_hi rows / planes of h it receives
  *  spec_lo/hi    spectral lines of axis 1 (2-D: kx columns; 3-D: ky rows) it convolves
- *  R, Ro, Ks     per-rank input, output and spectral extents (2-D: R and Ks padded to
- *                multiples of nchunks); chunk_rows = R / nchunks, chunk_cols = Ks / nchunks
+ *  R, Ro, Ks     per-rank input, output and spectral extents (2-D: R padded to a
+ *                multiple of nchunks, Ks to nchunks x a multiple of 16); chunk_rows =
+ *                R / nchunks, chunk_cols = Ks / nchunks
  *                (3-D: chunk_cols = the kx tile of the exchange blocks)
  *  block1/2      elements of one (sender, receiver) block in the two all-to-alls
  *  bytes_sent    bytes leaving this rank per call (both exchanges, self excluded)
@@ -389,7 +390,11 @@ hd_status_t hd_dist_slab_plan(hd_dtype_t dtype, int32_t ndim, int32_t nranks, in
  *   stage 1: in = f slab                  -> out = send1 (nranks x block1 elements)
  *   stage 2: in = recv1, gt = stage 0 out -> out = send2 (nranks x block2 elements)
  *   stage 3: in = recv2                   -> out = h slab
- * recv = the all-to-all of send: block b of rank k's recv is block k of rank b's send.
+ * recv2 = the all-to-all of send2: block b of rank k's recv2 is block k of rank b's
+ * send2.  2-D first exchange, by pieces of P1 = Ks * chunk_rows elements: send1 is
+ * chunk-major (piece for rank d of row chunk c at (c * nranks + d) * P1), recv1
+ * source-major (piece from rank s of chunk c at s * block1 + c * P1); with one chunk
+ * this is the plain all-to-all.  (3-D: both exchanges are plain all-to-alls.)
  * 3-D stages 0, 1, 3 need `scratch` of hd_slab_scratch_bytes (2-D: unused). */
 hd_status_t hd_slab_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_plan_t* S, const int64_t* Lf,
                           const int64_t* Lg, int32_t stage, const void* in, const void* gt, void* out,

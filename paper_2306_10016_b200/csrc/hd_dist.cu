@@ -177,6 +177,27 @@ const void* off(const void* p, int64_t elems, size_t eb) { return static_cast<co
 
 // one chunk of an all-to-all of equal blocks: rank d's piece at send + d * block + c_off
 // goes to d's recv + rank * block + c_off (self included)
+// piece p of the send buffer at send_off + p * send_stride, piece p of the receive
+// buffer (from rank p) at recv_off + p * recv_stride, `count` elements each
+hd_status_t exchange_pieces(Dist* D, void* send, int64_t send_off, int64_t send_stride, void* recv,
+                            int64_t recv_off, int64_t recv_stride, int64_t count, size_t eb) {
+  if (count <= 0) return HD_OK;
+  Nccl& N = nccl();
+  const ncclDataType_t ty = eb == 16 ? ncclFloat64 : ncclFloat32;  // complex = 2 reals
+  const size_t cnt = (size_t)count * 2;
+  ncclResult_t r = N.GroupStart();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+  for (int p = 0; p < D->n; ++p) {
+    r = N.Send(off(send, send_off + p * send_stride, eb), cnt, ty, p, D->comm, D->cs);
+    if (r != ncclSuccess) { N.GroupEnd(); return nccl_fail(r, "ncclSend"); }
+    r = N.Recv(off(recv, recv_off + p * recv_stride, eb), cnt, ty, p, D->comm, D->cs);
+    if (r != ncclSuccess) { N.GroupEnd(); return nccl_fail(r, "ncclRecv"); }
+  }
+  r = N.GroupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+  return HD_OK;
+}
+
 hd_status_t exchange_chunk(Dist* D, void* send, void* recv, int64_t block, int64_t c_off, int64_t count,
                            size_t eb) {
   if (count <= 0) return HD_OK;
@@ -315,7 +336,7 @@ hd_status_t hd_dist_slab_plan(hd_dtype_t dtype, int32_t ndim, int32_t nranks, in
     const int64_t Kx = p.axis[1].M1;
     o.chunk_rows = cdiv(cdiv(Lf[0], nranks), C);
     o.R = C * o.chunk_rows;
-    o.chunk_cols = cdiv(cdiv(Kx, nranks), C);
+    o.chunk_cols = cdiv(cdiv(cdiv(Kx, nranks), C), 16) * 16;  // 16-wide kx tiles (send1)
     o.Ks = C * o.chunk_cols;
     o.Ro = cdiv(O0, nranks);
     o.block1 = o.Ks * o.R;
@@ -416,10 +437,16 @@ hd_status_t hd_conv1d_dist(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const 
 }
 
 // ---------------------------------------------------------------- 2-D slabs
-// Layouts (elements; R, Ks padded to chunk multiples, Rc = R / C, Kc = Ks / C):
+// Layouts (elements; R, Ks padded to chunk multiples, Rc = R / C, Kc = Ks / C, Kc a
+// multiple of 16; P1 = Ks Rc, one (rank, chunk) piece of the first exchange):
 //   xg    [kx][y]                                   g forward along x (replicated)
-//   send1 [dest][row chunk][kx_local][y % Rc]       pass A output, chunk c = rows [c Rc, (c+1) Rc)
-//   recv1 [src ][row chunk][kx_local][y % Rc]       = element (kx_local, y) at (y / Rc) Ks Rc + kx_local Rc + y % Rc
+//   send1 [row chunk][kx / 16][y % Rc][kx % 16]     pass A output, chunk c = rows [c Rc, (c+1) Rc):
+//                                                   the 16-wide kx tiles of the pipeline's X, so the
+//                                                   pass stores 256-byte pieces by TMA; the piece for
+//                                                   dest d of chunk c is contiguous, at (c nranks + d) P1
+//   recv1 [src ][row chunk][kx_local / 16][y % Rc][kx_local % 16]
+//                                                   piece (src, c) at (src C + c) P1: element (kx_local, y)
+//                                                   at (y / Rc) P1 + (kx_local / 16) 16 Rc + (y % Rc) 16 + kx_local % 16
 //   send2 [dest][col chunk][yo % Ro][kx % Kc]       pass B output, chunk cc = local columns [cc Kc, (cc+1) Kc)
 //   recv2 [src ][col chunk][yo_local][kx % Kc]      = element (yo_local, kx) at (kx / Kc) Ro Kc + yo_local Kc + kx % Kc
 // One chunk of one stage (c < 0: every chunk of the stage).
@@ -453,15 +480,16 @@ static hd_status_t slab2d_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_pl
       hd_pass_desc_t d = pass(HD_PASS_FWD, y1 - y0, 1, Kx, ax, 1);
       d.flags = xflags;
       d.in_f = lines(const_cast<void*>(off(in, y0 * Lf[1], eb)), Lf[1], Lf[1]);
-      d.out = lines(off(out, cc * Ks * Rc, eb), Kx, 1);
-      elem_tiled(d.out, Ks, S.block1, Rc);
+      d.out = lines(off(out, cc * S.nranks * Ks * Rc, eb), Kx, 16);
+      elem_tiled(d.out, 16, 16 * Rc, 1);
       s = hd_pass(ctx, dtype, &d, stream);
     } else if (stage == 2) {  // pass B: columns of chunk cc, recv1 + xg -> send2
       const int64_t k0 = cc * Kc, k1 = std::min<int64_t>((cc + 1) * Kc, ncols);
       if (k1 <= k0) continue;
       hd_pass_desc_t d = pass(HD_PASS_CONV, k1 - k0, 1, ay.M1, ay, 1);
-      d.in_f = lines(const_cast<void*>(off(in, k0 * Rc, eb)), Lf[0], Rc);
-      elem_tiled(d.in_f, Rc, Ks * Rc, 1);
+      d.in_f = lines(const_cast<void*>(off(in, k0 * Rc, eb)), Lf[0], 1);
+      line_tiled(d.in_f, 16, 16 * Rc);
+      elem_tiled(d.in_f, Rc, Ks * Rc, 16);
       d.in_g = lines(const_cast<void*>(off(xg, (S.spec_lo + k0) * Lg[0], eb)), Lg[0], Lg[0]);
       d.out = lines(off(out, cc * Ro * Kc, eb), Oy, 1);
       d.out.tl = 0;  // lines as tiles of width 1 (same addresses): TMA stores of the
@@ -680,6 +708,14 @@ static hd_status_t slab_dist(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, const voi
     cudaStreamWaitEvent(D->cs, D->ev[evi], 0);
     return exchange_chunk(D, send, recv, block, c_off, count, eb);
   };
+  // the first 2-D exchange: send1 is chunk-major (piece for dest d of chunk c at
+  // (c n + d) P1), recv1 source-major (piece from src s of chunk c at (s C + c) P1)
+  auto exchange1 = [&](int evi, int c, int64_t P1) {
+    if (one) return HD_OK;
+    cudaEventRecord(D->ev[evi], st);
+    cudaStreamWaitEvent(D->cs, D->ev[evi], 0);
+    return exchange_pieces(D, send1, c * D->n * P1, P1, recv1, c * P1, S.block1, P1, eb);
+  };
   auto join = [&]() {
     if (one) return;
     cudaEventRecord(D->evx, D->cs);
@@ -690,7 +726,8 @@ static hd_status_t slab_dist(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, const voi
   const int64_t piece2 = ndim == 2 ? S.Ro * S.chunk_cols : S.block2;
   for (int c = 0; c < C; ++c) {
     if ((s = stage(1, c, f, nullptr, send1)) != HD_OK) return ctx_fail(ctx, s);
-    if ((s = exchange(c, send1, recv1, S.block1, c * piece1, piece1)) != HD_OK) return s;
+    if ((s = ndim == 2 ? exchange1(c, c, piece1) : exchange(c, send1, recv1, S.block1, c * piece1, piece1)) != HD_OK)
+      return s;
   }
   join();
   for (int c = 0; c < C; ++c) {

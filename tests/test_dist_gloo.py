@@ -46,13 +46,15 @@ class Model2D:
         return xg
 
     def stage1(self, f_rows):
+        """send1 [row chunk][kx / 16][y % Rc][kx % 16] (chunk-major, 16-wide kx tiles)."""
         sp = self.sp
+        Rc = sp.chunk_rows
         out = np.zeros(sp.nranks * sp.block1, dtype=np.complex128)
         kx = np.arange(self.Kx)
         for yl in range(sp.in_hi - sp.in_lo):
-            c, yi = divmod(yl, sp.chunk_rows)
+            c, yi = divmod(yl, Rc)
             X = np.fft.ifft(f_rows[yl], n=self.Kx) * self.Kx       # + exponent, unnormalised
-            out[(kx // sp.Ks) * sp.block1 + c * sp.Ks * sp.chunk_rows + (kx % sp.Ks) * sp.chunk_rows + yi] = X
+            out[c * sp.nranks * sp.Ks * Rc + (kx // 16) * (16 * Rc) + yi * 16 + kx % 16] = X
         return out
 
     def stage2(self, recv1, xg):
@@ -62,7 +64,8 @@ class Model2D:
         for c in range(sp.spec_hi - sp.spec_lo):
             cc, ci = divmod(c, sp.chunk_cols)
             kx = sp.spec_lo + c
-            fcol = recv1[(ys // sp.chunk_rows) * (sp.Ks * sp.chunk_rows) + c * sp.chunk_rows + ys % sp.chunk_rows]
+            Rc = sp.chunk_rows
+            fcol = recv1[(ys // Rc) * (sp.Ks * Rc) + (c // 16) * (16 * Rc) + (ys % Rc) * 16 + c % 16]
             gcol = xg[kx * self.Lg[0] + np.arange(self.Lg[0])]
             F = np.fft.ifft(fcol, n=self.Ky) * self.Ky
             G = np.fft.ifft(gcol, n=self.Ky) * self.Ky
@@ -151,6 +154,20 @@ def _exchange(send, block):
     return recv
 
 
+def _exchange1_2d(send, sp):
+    """The 2-D first exchange (include/hdconv.h): per row chunk c, the pieces of P1
+    elements for every rank (chunk-major in send1) go to source-major slots of recv1."""
+    P1, C, n = sp.Ks * sp.chunk_rows, sp.nchunks, sp.nranks
+    recv = np.zeros_like(send)
+    for c in range(C):
+        tmp = np.zeros(n * P1, dtype=send.dtype)
+        s = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(send[c * n * P1:(c + 1) * n * P1])))
+        dist.all_to_all_single(torch.view_as_real(torch.from_numpy(tmp)), s)
+        for src in range(n):
+            recv[src * sp.block1 + c * P1:src * sp.block1 + (c + 1) * P1] = tmp[src * P1:(src + 1) * P1]
+    return recv
+
+
 def _worker(rank, world, port, ndim, Lf, Lg, m, nchunks, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -161,7 +178,8 @@ def _worker(rank, world, port, ndim, Lf, Lg, m, nchunks, q):
         sp = H.slab_plan(H.HD_C128, Lf, Lg, world, rank, nchunks, _plan(H, ndim, m))
         M = (Model2D if ndim == 2 else Model3D)(sp, Lf, Lg)
         gt = M.stage0(g)
-        r1 = _exchange(M.stage1(np.ascontiguousarray(f[sp.in_lo:sp.in_hi])), sp.block1)
+        s1 = M.stage1(np.ascontiguousarray(f[sp.in_lo:sp.in_hi]))
+        r1 = _exchange1_2d(s1, sp) if ndim == 2 else _exchange(s1, sp.block1)
         r2 = _exchange(M.stage2(r1, gt), sp.block2)
         h = M.stage3(r2)
         parts = [None] * world

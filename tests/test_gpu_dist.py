@@ -130,7 +130,18 @@ def _emulate(ctx, H, dt, Lf, Lg, f, g, world, nchunks, plan):
             for dst in range(world):
                 recvs[dst][src * block:(src + 1) * block] = sends[src][dst * block:(dst + 1) * block]
         return recvs
-    r1 = a2a(s1, sps[0].block1)
+
+    def a2a_pieces(sends, sp):
+        """2-D first exchange (include/hdconv.h): send1 chunk-major, recv1 source-major."""
+        P1, C = sp.Ks * sp.chunk_rows, sp.nchunks
+        recvs = [torch.zeros_like(s) for s in sends]
+        for src in range(world):
+            for dst in range(world):
+                for c in range(C):
+                    recvs[dst][src * sp.block1 + c * P1:src * sp.block1 + (c + 1) * P1] = \
+                        sends[src][(c * world + dst) * P1:(c * world + dst + 1) * P1]
+        return recvs
+    r1 = a2a_pieces(s1, sps[0]) if len(Lf) == 2 else a2a(s1, sps[0].block1)
     s2 = []
     for k, sp in enumerate(sps):
         out = new(el[k]["x2"])
