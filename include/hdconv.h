@@ -390,11 +390,11 @@ hd_status_t hd_dist_slab_plan(hd_dtype_t dtype, int32_t ndim, int32_t nranks, in
  *   stage 1: in = f slab                  -> out = send1 (nranks x block1 elements)
  *   stage 2: in = recv1, gt = stage 0 out -> out = send2 (nranks x block2 elements)
  *   stage 3: in = recv2                   -> out = h slab
- * recv2 = the all-to-all of send2: block b of rank k's recv2 is block k of rank b's
- * send2.  2-D first exchange, by pieces of P1 = Ks * chunk_rows elements: send1 is
- * chunk-major (piece for rank d of row chunk c at (c * nranks + d) * P1), recv1
- * source-major (piece from rank s of chunk c at s * block1 + c * P1); with one chunk
- * this is the plain all-to-all.  (3-D: both exchanges are plain all-to-alls.)
+ * 2-D exchanges, by pieces of P1 = Ks * chunk_rows (first) and P2 = Ro * chunk_cols
+ * (second) elements: send is chunk-major (piece for rank d of chunk c at
+ * (c * nranks + d) * P), recv source-major (piece from rank s of chunk c at
+ * s * block + c * P); with one chunk this is the plain all-to-all.  3-D: both
+ * exchanges are plain all-to-alls (block b of rank k's recv = block k of rank b's send).
  * 3-D stages 0, 1, 3 need `scratch` of hd_slab_scratch_bytes (2-D: unused). */
 hd_status_t hd_slab_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_plan_t* S, const int64_t* Lf,
                           const int64_t* Lg, int32_t stage, const void* in, const void* gt, void* out,

@@ -447,8 +447,13 @@ hd_status_t hd_conv1d_dist(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const 
 //   recv1 [src ][row chunk][kx_local / 16][y % Rc][kx_local % 16]
 //                                                   piece (src, c) at (src C + c) P1: element (kx_local, y)
 //                                                   at (y / Rc) P1 + (kx_local / 16) 16 Rc + (y % Rc) 16 + kx_local % 16
-//   send2 [dest][col chunk][yo % Ro][kx % Kc]       pass B output, chunk cc = local columns [cc Kc, (cc+1) Kc)
-//   recv2 [src ][col chunk][yo_local][kx % Kc]      = element (yo_local, kx) at (kx / Kc) Ro Kc + yo_local Kc + kx % Kc
+//   send2 [col chunk][yo][kx % Kc]                  pass B output, chunk cc = local columns [cc Kc, (cc+1) Kc):
+//                                                   chunk-major (P2 = Ro Kc; the piece for dest d of chunk cc
+//                                                   is rows [d Ro, (d+1) Ro), at (cc nranks + d) P2), so a
+//                                                   column is one line of element stride Kc (TMA stores)
+//   recv2 [src ][col chunk][yo_local][kx % Kc]      piece (src, cc) at (src C + cc) P2: element (yo_local, kx)
+//                                                   at (kx / Kc) Ro Kc + yo_local Kc + kx % Kc (plain rows
+//                                                   at one rank: pass C loads each by one bulk copy)
 // One chunk of one stage (c < 0: every chunk of the stage).
 static hd_status_t slab2d_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_plan_t& S, const int64_t* Lf,
                                 const int64_t* Lg, int stage, int c, const void* in, const void* xg, void* out,
@@ -491,10 +496,10 @@ static hd_status_t slab2d_stage(hd_ctx_t ctx, hd_dtype_t dtype, const hd_slab_pl
       line_tiled(d.in_f, 16, 16 * Rc);
       elem_tiled(d.in_f, Rc, Ks * Rc, 16);
       d.in_g = lines(const_cast<void*>(off(xg, (S.spec_lo + k0) * Lg[0], eb)), Lg[0], Lg[0]);
-      d.out = lines(off(out, cc * Ro * Kc, eb), Oy, 1);
+      d.out = lines(off(out, cc * S.nranks * Ro * Kc, eb), Oy, 1);
       d.out.tl = 0;  // lines as tiles of width 1 (same addresses): TMA stores of the
-      d.out.s_t = 1; // 16-byte pieces when one block holds every output row (hd_api.cu)
-      elem_tiled(d.out, Ro, S.block2, Kc);
+      d.out.s_t = 1; // 16-byte pieces, element stride Kc (hd_api.cu)
+      d.out.s_j = Kc;
       d.scale = S.scale;
       s = hd_pass(ctx, dtype, &d, stream);
     } else if (stage == 3) {  // pass C: recv2 -> output rows (all chunks at once)
@@ -710,11 +715,13 @@ static hd_status_t slab_dist(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, const voi
   };
   // the first 2-D exchange: send1 is chunk-major (piece for dest d of chunk c at
   // (c n + d) P1), recv1 source-major (piece from src s of chunk c at (s C + c) P1)
-  auto exchange1 = [&](int evi, int c, int64_t P1) {
+  // 2-D exchanges: send chunk-major (piece for dest d of chunk c at (c n + d) P), recv
+  // source-major (piece from src s of chunk c at s block + c P)
+  auto exchange_cm = [&](int evi, void* send, void* recv, int64_t block, int c, int64_t P) {
     if (one) return HD_OK;
     cudaEventRecord(D->ev[evi], st);
     cudaStreamWaitEvent(D->cs, D->ev[evi], 0);
-    return exchange_pieces(D, send1, c * D->n * P1, P1, recv1, c * P1, S.block1, P1, eb);
+    return exchange_pieces(D, send, c * D->n * P, P, recv, c * P, block, P, eb);
   };
   auto join = [&]() {
     if (one) return;
@@ -726,13 +733,16 @@ static hd_status_t slab_dist(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, const voi
   const int64_t piece2 = ndim == 2 ? S.Ro * S.chunk_cols : S.block2;
   for (int c = 0; c < C; ++c) {
     if ((s = stage(1, c, f, nullptr, send1)) != HD_OK) return ctx_fail(ctx, s);
-    if ((s = ndim == 2 ? exchange1(c, c, piece1) : exchange(c, send1, recv1, S.block1, c * piece1, piece1)) != HD_OK)
+    if ((s = ndim == 2 ? exchange_cm(c, send1, recv1, S.block1, c, piece1)
+                       : exchange(c, send1, recv1, S.block1, c * piece1, piece1)) != HD_OK)
       return s;
   }
   join();
   for (int c = 0; c < C; ++c) {
     if ((s = stage(2, c, recv1, gt, send2)) != HD_OK) return ctx_fail(ctx, s);
-    if ((s = exchange(C + c, send2, recv2, S.block2, c * piece2, piece2)) != HD_OK) return s;
+    if ((s = ndim == 2 ? exchange_cm(C + c, send2, recv2, S.block2, c, piece2)
+                       : exchange(C + c, send2, recv2, S.block2, c * piece2, piece2)) != HD_OK)
+      return s;
   }
   join();
   if ((s = stage(3, -1, recv2, nullptr, h)) != HD_OK) return ctx_fail(ctx, s);

@@ -70,8 +70,8 @@ class Model2D:
             F = np.fft.ifft(fcol, n=self.Ky) * self.Ky
             G = np.fft.ifft(gcol, n=self.Ky) * self.Ky
             V = np.fft.fft(F * G) * sp.scale                        # - exponent, 1 / (M1_y M1_x)
-            out[(yo // sp.Ro) * sp.block2 + cc * sp.Ro * sp.chunk_cols + (yo % sp.Ro) * sp.chunk_cols + ci] = \
-                V[: self.Oy]
+            Kc = sp.chunk_cols       # send2 [chunk][yo][kx % Kc] (chunk-major)
+            out[cc * sp.nranks * sp.Ro * Kc + yo * Kc + ci] = V[: self.Oy]
         return out
 
     def stage3(self, recv2):
@@ -154,17 +154,17 @@ def _exchange(send, block):
     return recv
 
 
-def _exchange1_2d(send, sp):
-    """The 2-D first exchange (include/hdconv.h): per row chunk c, the pieces of P1
-    elements for every rank (chunk-major in send1) go to source-major slots of recv1."""
-    P1, C, n = sp.Ks * sp.chunk_rows, sp.nchunks, sp.nranks
+def _exchange_2d(send, block, P, sp):
+    """A 2-D exchange (include/hdconv.h): per chunk c, the pieces of P elements for
+    every rank (chunk-major in send) go to source-major slots (block, c) of recv."""
+    C, n = sp.nchunks, sp.nranks
     recv = np.zeros_like(send)
     for c in range(C):
-        tmp = np.zeros(n * P1, dtype=send.dtype)
-        s = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(send[c * n * P1:(c + 1) * n * P1])))
+        tmp = np.zeros(n * P, dtype=send.dtype)
+        s = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(send[c * n * P:(c + 1) * n * P])))
         dist.all_to_all_single(torch.view_as_real(torch.from_numpy(tmp)), s)
         for src in range(n):
-            recv[src * sp.block1 + c * P1:src * sp.block1 + (c + 1) * P1] = tmp[src * P1:(src + 1) * P1]
+            recv[src * block + c * P:src * block + (c + 1) * P] = tmp[src * P:(src + 1) * P]
     return recv
 
 
@@ -179,8 +179,12 @@ def _worker(rank, world, port, ndim, Lf, Lg, m, nchunks, q):
         M = (Model2D if ndim == 2 else Model3D)(sp, Lf, Lg)
         gt = M.stage0(g)
         s1 = M.stage1(np.ascontiguousarray(f[sp.in_lo:sp.in_hi]))
-        r1 = _exchange1_2d(s1, sp) if ndim == 2 else _exchange(s1, sp.block1)
-        r2 = _exchange(M.stage2(r1, gt), sp.block2)
+        if ndim == 2:
+            r1 = _exchange_2d(s1, sp.block1, sp.Ks * sp.chunk_rows, sp)
+            r2 = _exchange_2d(M.stage2(r1, gt), sp.block2, sp.Ro * sp.chunk_cols, sp)
+        else:
+            r1 = _exchange(s1, sp.block1)
+            r2 = _exchange(M.stage2(r1, gt), sp.block2)
         h = M.stage3(r2)
         parts = [None] * world
         dist.all_gather_object(parts, (sp.out_lo, h))

@@ -131,23 +131,24 @@ def _emulate(ctx, H, dt, Lf, Lg, f, g, world, nchunks, plan):
                 recvs[dst][src * block:(src + 1) * block] = sends[src][dst * block:(dst + 1) * block]
         return recvs
 
-    def a2a_pieces(sends, sp):
-        """2-D first exchange (include/hdconv.h): send1 chunk-major, recv1 source-major."""
-        P1, C = sp.Ks * sp.chunk_rows, sp.nchunks
+    def a2a_pieces(sends, block, P, C):
+        """2-D exchanges (include/hdconv.h): send chunk-major, recv source-major."""
         recvs = [torch.zeros_like(s) for s in sends]
         for src in range(world):
             for dst in range(world):
                 for c in range(C):
-                    recvs[dst][src * sp.block1 + c * P1:src * sp.block1 + (c + 1) * P1] = \
-                        sends[src][(c * world + dst) * P1:(c * world + dst + 1) * P1]
+                    recvs[dst][src * block + c * P:src * block + (c + 1) * P] = \
+                        sends[src][(c * world + dst) * P:(c * world + dst + 1) * P]
         return recvs
-    r1 = a2a_pieces(s1, sps[0]) if len(Lf) == 2 else a2a(s1, sps[0].block1)
+    sp0 = sps[0]
+    two = len(Lf) == 2
+    r1 = a2a_pieces(s1, sp0.block1, sp0.Ks * sp0.chunk_rows, sp0.nchunks) if two else a2a(s1, sp0.block1)
     s2 = []
     for k, sp in enumerate(sps):
         out = new(el[k]["x2"])
         ctx.slab_stage(dt, sp, Lf, Lg, 2, r1[k], out, gt=gts[k])
         s2.append(out)
-    r2 = a2a(s2, sps[0].block2)
+    r2 = a2a_pieces(s2, sp0.block2, sp0.Ro * sp0.chunk_cols, sp0.nchunks) if two else a2a(s2, sp0.block2)
     parts = []
     for k, sp in enumerate(sps):
         O = [sp.out_hi - sp.out_lo] + [a + b - 1 for a, b in zip(Lf[1:], Lg[1:])]
