@@ -703,12 +703,12 @@ __device__ __forceinline__ void g_transform(V* v, const V* gbuf, int Lg, int r, 
 // W8 (q = 9, blockDim 384 = three warpgroups): eight compute warps (warpgroups 0, 1)
 // grown to 232 registers with setmaxnreg, the producer in warpgroup 2 shrunk to 40
 // (its other three warps exit).  Two compute warps per SM sub-partition and no
-// register spills; residue 8 is shared out: FWD / INV: warp 7 transforms it after
-// its own residue; CONV: warp 1 transforms F_8 (parked lane-major in row 8), warp 2
-// transforms G_8 (exchange area X after the stages) and forms the product in row 8,
-// warp 3 inverse-transforms it after its own residue (named barriers 3 and 4 between
-// them), so every sub-partition carries 6-7 of the 27 transforms of a column instead
-// of 6-9.
+// register spills; residue 8 runs as FFT-256 halves (hd_w256.cuh, one radix-2 step
+// of the FFT-512): CONV: warps 4, 5 transform F_8's halves, warps 6, 7 G_8's (into
+// the area X after the stages), warps 0, 1 multiply and inverse-transform half 0 / 1
+// after their own residue (named barriers 5, 3, 4), the unfold combines the halves;
+// FWD / INV (HD_S512_W8 bit 1): warps 2, 3 take the halves.  Every sub-partition then
+// carries 6.5-7 of the 27 transforms of a column instead of 6-9.
 template <int MODE, int NTMAX, int QC, int LEAN = 0>
 __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
