@@ -66,6 +66,11 @@ def test_plan_validation(H):
                            H.Plan.make(3, [{"m": 8, "S": 3}, {"m": 8, "S": 1}, {"m": 8}]))
     with pytest.raises(H.HDError):  # threads must be a multiple of 32
         H.hd_plan_complete(H.HD_C128, [10], [10], H.Plan.make(1, [{"m": 4, "threads": 100}]))
+    for Lf, Lg in [([0], [5]), ([5], [0]), ([4, 0], [3, 3]), ([-1], [2])]:  # empty / negative extents
+        with pytest.raises(H.HDError):
+            H.hd_plan_complete(H.HD_C128, Lf, Lg, H.Plan.make(len(Lf), [{"m": 4}] * len(Lf)))
+        with pytest.raises(H.HDError):
+            H.hd_plan_default(H.HD_C128, Lf, Lg)
 
 
 def test_default_plans_are_admissible(H):
