@@ -266,6 +266,19 @@ def run_reference(args, rank, world):
     return 0
 
 
+def pick_mode(world, ndim, npairs, batch):
+    """--mode auto: one GPU -> the single-GPU pipeline ("independent"); N > 1 -> one
+    problem over all ranks: 2-D / 3-D single pairs by slabs, 1-D batches by pairs
+    (strong scaling); anything else -> every rank its own problem (weak)."""
+    if world <= 1:
+        return "independent"
+    if ndim >= 2 and npairs == 1 and batch == 1:
+        return "slab"
+    if ndim == 1 and npairs == 1 and batch > 1:
+        return "batch"
+    return "independent"
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2306_10016_b200 import hdconv as H
@@ -309,8 +322,8 @@ def run_ours(args, rank, world, local_rank):
         plan = H.Plan.from_buffer_copy(obj[0])
 
     slab = None
-    mode = args.mode if args.mode != "auto" else ("slab" if world > 1 and ndim >= 2 and N == 1 and batch == 1
-                                                  else "independent")
+    shard = None  # 1-D batch sharding: (lo, hi) pairs of this rank
+    mode = args.mode if args.mode != "auto" else pick_mode(world, ndim, N, batch)
     if mode == "slab":
         if ndim < 2 or N != 1 or batch != 1:
             raise SystemExit("--mode slab: 2D/3D single-pair configs only")
@@ -320,9 +333,21 @@ def run_ours(args, rank, world, local_rank):
         slab = ctx.slab(dtc, Lf, Lg, 0, plan)
         f_local = fd[0][slab.in_lo:slab.in_hi].contiguous()
         h_local = torch.empty([slab.out_hi - slab.out_lo] + Lout[1:], dtype=fd[0].dtype, device=dev)
+    elif mode == "batch":
+        if ndim != 1 or N != 1 or batch < 2:
+            raise SystemExit("--mode batch: 1-D batched single-pair configs only")
+        # one batch over all ranks (strong scaling): hd_conv1d_dist with HD_SHARD_BATCH,
+        # B / N pairs per rank, no data-path collective (the pairs are independent)
+        ctx.dist_init()
+        shard = H.dist_partition(batch, world, rank)
+        f_local = fd[0][shard[0]:shard[1]].contiguous()
+        g_local = gd[0][shard[0]:shard[1]].contiguous()
+        h_local = torch.empty([shard[1] - shard[0], Lout[0]], dtype=fd[0].dtype, device=dev)
 
     def step():
-        if slab is not None:
+        if shard is not None:
+            ctx.conv1d_dist(f_local, g_local, batch, shard=H.HD_SHARD_BATCH, plan=plan, h=h_local)
+        elif slab is not None:
             if ndim == 2:
                 ctx.conv2d_dist(f_local, gd[0], Lf, plan=plan, h=h_local)
             else:
@@ -378,14 +403,15 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     samples_per_step = batch * int(np.prod(Lout))
     # weak: every rank convolves its own problem; strong (slab): one problem over all ranks
-    value = (1 if slab is not None else world) * samples_per_step * args.steps / (ms * 1e-3)
+    strong = slab is not None or shard is not None
+    value = (1 if strong else world) * samples_per_step * args.steps / (ms * 1e-3)
 
     # N > 1 in slab mode: also the weak-scaling figure (every rank its own whole problem
     # on the single-GPU pipeline, no collective), max over ranks
     weak = None
-    if slab is not None and world > 1:
+    if strong and world > 1:
         def step_weak():
-            ctx.conv(fd[0], gd[0], plan=plan, h=hd_)
+            ctx.conv(fd[0], gd[0], plan=plan, h=hd_, batch=(ndim == 1 and batch > 1))
         for _ in range(args.warmup):
             step_weak()
         dist.barrier()
@@ -409,6 +435,8 @@ def run_ours(args, rank, world, local_rank):
         # slab mode: each rank's one "pass_conv" launch convolves 1/world of the
         # spectral lines of the pipeline's convolution pass
         ab = dict(ab, pass_conv=ab["conv_y" if ndim == 2 else "conv_z"] // world)
+    if shard is not None:  # batch mode: this rank's launch convolves its pairs only
+        ab = {k: v * (shard[1] - shard[0]) // batch for k, v in ab.items()}
     dom = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
     roof = None
     if dom:
@@ -423,6 +451,8 @@ def run_ours(args, rank, world, local_rank):
         fl = None
         if dom.startswith("conv") or dom == "pass_conv":
             fl = conv_flops(ndim, N, Lf, Lg, Lout, batch) / (world if dom == "pass_conv" else 1)
+            if shard is not None:
+                fl = fl * (shard[1] - shard[0]) / batch
         if fl:
             # the convolution pass's arithmetic beside its HBM roofline: plan-independent
             # flops against the measured FP64 (FP32 for c64: nominal 2x FP64 is NOT
@@ -442,7 +472,8 @@ def run_ours(args, rank, world, local_rank):
                                     "lines = L_out of the other axes (plan-independent)"}
     total_ab = sum(v for k, v in ab.items() if k != "pass_conv")
     # compulsory bytes (stricter): the inputs read once, the output written once
-    comp = eb * batch * (N * (int(np.prod(Lf)) + int(np.prod(Lg))) + int(np.prod(Lout)))
+    nb_local = (shard[1] - shard[0]) if shard is not None else batch
+    comp = eb * nb_local * (N * (int(np.prod(Lf)) + int(np.prod(Lg))) + int(np.prod(Lout)))
     step_s = ms * 1e-3 / args.steps
     whole = {"alg_bytes_per_step": total_ab,
              "compulsory_bytes_per_step": comp,
@@ -478,7 +509,32 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": samples_per_step * k2 / te, "unit": UNIT,
                "h2d_bytes_per_step": int(fh_l.numel() * eb + sum(a.nbytes for a in g)),
                "d2h_bytes_per_step": int(hh_l.numel() * eb), "steps": k2, "per": "rank (max over ranks)"}
-    if not args.no_e2e and slab is None:
+    if not args.no_e2e and shard is not None:
+        # end to end at N ranks: this rank's pairs from pinned host memory, the sharded
+        # call, its rows back to pinned host memory, every step
+        fh_l = fh[0][shard[0]:shard[1]].contiguous().pin_memory()
+        gh_l = gh[0][shard[0]:shard[1]].contiguous().pin_memory()
+        hh_l = torch.empty(list(h_local.shape), dtype=h_local.dtype).pin_memory()
+        k2 = max(4, min(args.steps, 20))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(k2):
+            f_local.copy_(fh_l, non_blocking=True)
+            g_local.copy_(gh_l, non_blocking=True)
+            step()
+            hh_l.copy_(h_local, non_blocking=True)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t
+        if dist:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": samples_per_step * k2 / te, "unit": UNIT,
+               "h2d_bytes_per_step": int((fh_l.numel() + gh_l.numel()) * eb),
+               "d2h_bytes_per_step": int(hh_l.numel() * eb), "steps": k2, "per": "rank (max over ranks)"}
+    if not args.no_e2e and slab is None and shard is None:
         # two result buffers: step k writes hh[k % 2] (asynchronous, double-buffered
         # entry point: the copy-in of step k+1 overlaps the copy-out of step k)
         hh = [torch.empty(out_shape, dtype=fd[0].dtype).pin_memory() for _ in range(2)]
@@ -589,7 +645,7 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if slab is not None else "weak", "vs_baseline": None,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f64" if eb == 16 else "f32",
             "data": "synthetic",
             "config": {"workload": name, "Lf": Lf, "Lg": Lg, "Lout": Lout, "pairs": N, "batch": batch,
@@ -597,6 +653,8 @@ def run_ours(args, rank, world, local_rank):
                        "tune_seconds": tune_s,
                        "parallelism": (f"slab x{world} ({'rows' if ndim == 2 else 'z-planes'}; NCCL all-to-all "
                                        "transposes)" if slab is not None
+                                       else f"batch x{world} (B/N pairs per rank, no collective)"
+                                       if shard is not None
                                        else f"weak x{world} (independent problems)"),
                        "l2": "inputs larger than L2 (image 268 MB > 126 MB L2); no flush needed"},
             "roofline": roof, "whole_step": whole, "cpu_baseline": cpu, "e2e": e2e,
@@ -605,6 +663,7 @@ def run_ours(args, rank, world, local_rank):
         if slab is not None:
             line["slab"] = {k: getattr(slab, k) for k in ("nchunks", "R", "Ro", "Ks", "block1", "block2",
                                                           "bytes_sent")}
+        if strong:
             line["weak_scaling"] = weak
         print(json.dumps(line), flush=True)
     if dist:
@@ -658,10 +717,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-explicit", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--mode", default="auto", choices=["auto", "independent", "slab"],
-                    help="auto: N = 1 single-GPU pipeline; N > 1 one slab-decomposed problem (strong "
-                         "scaling, NCCL exchanges in libhdconv) with weak scaling as an extra key; "
-                         "independent: each rank its own problem (weak); slab: slab path at any N")
+    ap.add_argument("--mode", default="auto", choices=["auto", "independent", "slab", "batch"],
+                    help="auto: N = 1 single-GPU pipeline; N > 1 one problem over the ranks (strong "
+                         "scaling: 2-D/3-D slabs with NCCL exchanges in libhdconv, 1-D batches by "
+                         "pairs) with weak scaling as an extra key; independent: each rank its own "
+                         "problem (weak); slab / batch: those paths at any N")
     ap.add_argument("--dry-run", action="store_true", help="launch plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

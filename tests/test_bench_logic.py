@@ -81,3 +81,14 @@ def test_bench_refuses_mismatched_world():
     out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--dry-run"],
                          capture_output=True, text=True, timeout=120, env=env)
     assert out.returncode != 0 and "WORLD_SIZE" in (out.stderr + out.stdout)
+
+
+def test_auto_mode_is_strong_for_one_problem(bench):
+    """--mode auto at N > 1: the BASELINE configs run one problem over all ranks (2-D /
+    3-D by slabs, the 1-D batch by pairs); one GPU keeps the single-GPU pipeline."""
+    assert bench.pick_mode(1, 2, 1, 1) == "independent"
+    assert bench.pick_mode(8, 2, 1, 1) == "slab"      # config 3
+    assert bench.pick_mode(8, 3, 1, 1) == "slab"      # config 4
+    assert bench.pick_mode(8, 1, 1, 4096) == "batch"  # config 2
+    assert bench.pick_mode(8, 2, 6, 1) == "independent"  # config 5 (multi-pair): weak
+    assert bench.pick_mode(2, 1, 1, 1) == "independent"
