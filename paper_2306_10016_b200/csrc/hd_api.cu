@@ -681,6 +681,8 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     threads = hd::s512_threads(L.a.q, L.mode);
     smem = hd::s512_smem_bytes(L.a.q, L.mode);
     prepare_tma(L);
+    static const int dbg_skip = getenv("HD_DEBUG_SKIP") ? atoi(getenv("HD_DEBUG_SKIP")) : 0;
+    L.a.dbg = dbg_skip;
     if (L.a.fam2 && !(L.mode == hd::MODE_FWD && L.a.q == 9 && L.narrays == 1 && L.a.nbatch == 1 &&
                       L.a.tm_in.kind == hd::TMA_BULK && L.a.tm_in_g.kind == hd::TMA_BULK &&
                       L.a.tm_out.kind != hd::TMA_NONE && L.a.tm_out2.kind != hd::TMA_NONE && L.a.out.j0 == 0 &&

@@ -335,6 +335,9 @@ struct PassArgs {
   // residues of all but the last pair of a line (gridDim.x x 2 (ceil(q/2) - 1) x 2048
   // elements), so that the line's unfold runs once over every residue
   void* scr;
+  // debug (HD_DEBUG_SKIP, timing experiments only -- results are garbage): bit 0 the
+  // staged engine's producer skips the stores, bit 1 the loads
+  int32_t dbg;
 };
 
 enum { MODE_FWD = 0, MODE_INV = 1, MODE_CONV = 2, MODE_MCONV = 3 /* staged engine only */ };
