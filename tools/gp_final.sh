@@ -3,5 +3,5 @@ set -u
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 bash tools/profile_bench.sh 3 r02g > gpurun_out/profile_bench.log 2>&1
+timeout 600 bash tools/profile_bench.sh 3 r02h > gpurun_out/profile_bench.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
