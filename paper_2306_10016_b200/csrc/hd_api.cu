@@ -469,14 +469,35 @@ bool bulk_ok_f32(const void* const* ptr, int narr, std::initializer_list<int64_t
   return true;
 }
 
-// input lines -> TMA_BULK (plain rows) or TMA_LINE_TILED (lines tiled by S, element stride s_j).
+// input lines -> TMA_BULK (plain rows) or TMA_LINE_TILED (lines tiled by S, element stride s_j);
+// with elem2 (the staged m = 512 engine), lines whose element axis is tiled by jd < L
+// (the slab exchanges' pieces) -> TMA_ELEM2 when jd divides L and has a divisor
+// <= 256 that is a multiple of 8 (the box).
 // c64 (the m = 128 engine, 4 lines per item): boxes of 128 elements x 4 lines (S >= 4).
 bool tma_desc_in(const LineIn& in, int64_t nlines, int64_t nbatch, int narr, hd::TmaLine& t,
-                 CUtensorMap* maps, bool c64 = false) {
+                 CUtensorMap* maps, bool c64 = false, bool elem2 = false) {
   t.kind = hd::TMA_NONE; t.slog = 0; t.nbi = in.nbi > 0 ? in.nbi : 1;
   t.bcast = (in.s_b == 0 ? 1 : 0) | (in.s_bo == 0 ? 2 : 0);
-  // element tiling wider than the line (jd >= L): every element is in tile 0
-  if ((in.jd > 0 && in.jd < in.L) || narr > hd::kTmaArrays) return false;
+  t.box = 0; t.jd = 0;
+  if (narr > hd::kTmaArrays) return false;
+  if (in.jd > 0 && in.jd < in.L) {
+    if (!elem2 || c64 || in.L % in.jd != 0 || t.nbi != nbatch) return false;
+    if (in.tl < 30 && in.s_l != 1) return false;
+    int box = 0;
+    for (int d = 256; d >= 8; d -= 8)
+      if (in.jd % d == 0) { box = d; break; }
+    if (!box) return false;
+    const int64_t S = in.tl < 30 ? (int64_t(1) << in.tl) : 1;
+    const int64_t nlt = in.tl < 30 ? ceil_div64(nlines, S) : nlines;
+    const uint64_t dims[5] = {(uint64_t)(2 * S), (uint64_t)in.jd, (uint64_t)(in.L / in.jd), (uint64_t)nlt,
+                              (uint64_t)nbatch};
+    const int64_t str[4] = {in.s_j, in.s_jt, in.tl < 30 ? in.s_t : in.s_l, in.s_b};
+    const uint32_t box5[5] = {2u, (uint32_t)box, 1, 1, 1};
+    for (int k = 0; k < narr; ++k)
+      if (!encode_lines(&maps[k], in.ptr[k], dims, str, box5)) return false;
+    t.kind = hd::TMA_ELEM2; t.slog = in.tl < 30 ? in.tl : 0; t.box = box; t.jd = in.jd;
+    return true;
+  }
   if (in.tl >= 30) {
     if (in.s_j != 1) return false;
     if (c64 && !bulk_ok_f32(in.ptr, narr, {in.L, in.s_l, in.s_b, in.s_bo})) return false;
@@ -536,11 +557,12 @@ bool tma_desc_out(const LineOut& o, int64_t nlines, int64_t nbatch, int narr, hd
 
 // Fill the staged engine's TMA descriptions of a launch (falls back to per-thread
 // copies for anything a tensor map cannot express).
-void prepare_tma(Launch& L, bool c64 = false) {
+void prepare_tma(Launch& L, bool c64 = false, bool elem2 = false) {
   PassArgs& a = L.a;
   const int narr_in = L.mode == hd::MODE_FWD ? (int)L.narrays : (L.mode == hd::MODE_CONV ? a.npairs : 1);
   const int narr_out = L.mode == hd::MODE_FWD ? (int)L.narrays : 1;
-  if (!tma_desc_in(a.in_f, a.nlines, a.nbatch, narr_in, a.tm_in, a.tm_in_map, c64)) a.tm_in.kind = hd::TMA_NONE;
+  if (!tma_desc_in(a.in_f, a.nlines, a.nbatch, narr_in, a.tm_in, a.tm_in_map, c64, elem2 && !a.rp))
+    a.tm_in.kind = hd::TMA_NONE;
   if (L.mode == hd::MODE_CONV) {
     // both inputs of the convolution pass move by TMA or both by per-thread copies
     if (!tma_desc_in(a.in_g, a.nlines, a.nbatch, a.npairs, a.tm_in_g, a.tm_in_g_map, c64) ||
@@ -680,7 +702,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     fn = hd::lookup_s512(L.mode, L.a.q);
     threads = hd::s512_threads(L.a.q, L.mode);
     smem = hd::s512_smem_bytes(L.a.q, L.mode);
-    prepare_tma(L);
+    prepare_tma(L, false, true);
     static const int dbg_skip = getenv("HD_DEBUG_SKIP") ? atoi(getenv("HD_DEBUG_SKIP")) : 0;
     L.a.dbg = dbg_skip;
     if (L.a.fam2 && !(L.mode == hd::MODE_FWD && L.a.q == 9 && L.narrays == 1 && L.a.nbatch == 1 &&

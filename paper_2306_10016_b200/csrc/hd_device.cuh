@@ -280,13 +280,15 @@ __device__ __forceinline__ int64_t line_off(const LineOut& o, int64_t l) {
   return (l >> o.tl) * o.s_t + (l & ((int64_t(1) << o.tl) - 1)) * o.s_l;
 }
 // TMA description of a family of lines (hd_s512.cuh; host side: hd_api.cu tma_desc_*)
-enum { TMA_NONE = 0, TMA_BULK = 1, TMA_LINE_TILED = 2, TMA_ELEM_TILED = 3 };
+enum { TMA_NONE = 0, TMA_BULK = 1, TMA_LINE_TILED = 2, TMA_ELEM_TILED = 3, TMA_ELEM2 = 4 };
 struct TmaLine {
   int32_t kind;            // TMA_NONE: per-thread copies; TMA_BULK: one 1-D bulk copy per line
-  int32_t slog;            // log2 of the tile width S (LINE_TILED: lines, ELEM_TILED: elements)
+  int32_t slog;            // log2 of the tile width S (LINE_TILED / ELEM2: lines, ELEM_TILED: elements)
   int32_t bcast;           // bit 0 / bit 1: batch dimension 3 / 4 has stride 0 (coordinate 0)
-  int32_t pad_;
+  int32_t box;             // ELEM2: elements per box (a divisor of jd, <= 256, multiple of 8)
   int64_t nbi;             // two-level batch split (coordinates b % nbi, b / nbi)
+  int64_t jd;              // ELEM2 (input lines, element axis tiled by jd: the slab exchanges):
+                           // dims {2S (line in tile), j % jd, j / jd, line tile, batch}
 };
 constexpr int kTmaArrays = 6;  // arrays (multiconv pairs) with their own tensor maps
 

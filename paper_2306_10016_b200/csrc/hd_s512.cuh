@@ -101,7 +101,9 @@ __device__ __forceinline__ void issue_loads_arm(const PassArgs& a, int64_t g, ui
   }
   if (g < a.nlines) {
     const int L = (int)a.in_f.L;
-    bytes += a.tm_in.kind == TMA_BULK ? (uint32_t)L * 16u : (uint32_t)((L + kBox - 1) / kBox) * kBox * 16u;
+    bytes += a.tm_in.kind == TMA_BULK    ? (uint32_t)L * 16u
+             : a.tm_in.kind == TMA_ELEM2 ? (uint32_t)L * 16u  // boxes tile [0, L) exactly
+                                         : (uint32_t)((L + kBox - 1) / kBox) * kBox * 16u;
     if (MODE == MODE_CONV)
       bytes += a.tm_in_g.kind == TMA_BULK ? (uint32_t)a.in_g.L * 16u
                                            : (uint32_t)((a.in_g.L + kBox - 1) / kBox) * kBox * 16u;
@@ -131,8 +133,9 @@ __device__ __forceinline__ void issue_loads_range(const PassArgs& a, int k_arr, 
       bulk_load(buf + j0, x + j0, (uint32_t)(j1 - j0) * 16u, bar);
     } else {
       const CUtensorMap* map = &a.tm_in_map[kk];
+      const int step = a.tm_in.kind == TMA_ELEM2 ? a.tm_in.box : kBox;  // ELEM2: one range only
       int c[5];
-      for (int jb = j0; jb < j1; jb += kBox) {
+      for (int jb = j0; jb < j1; jb += step) {
         tma_coords(a.tm_in, b, g, jb, c);
         tma_load(buf + jb, map, c, bar);
       }
@@ -295,6 +298,14 @@ __device__ __forceinline__ void handover(const PassArgs& a, int k_arr, int kk_ou
         issue_stores_range(a, kk_out, bs, gs, buf, 0, 1 << 30);
       }
     }
+    if (!load) return;
+    issue_loads_arm<MODE>(a, gl, bar);
+    if (store) bulk_wait_read_n(0);
+    issue_loads_range<MODE>(a, k_arr, bl, gl, buf, bar, 0, 1 << 30);
+    return;
+  }
+  if (a.tm_in.kind == TMA_ELEM2) {  // boxes of jd-tiled lines: every store read out, then one load range
+    if (store) issue_stores_range(a, kk_out, bs, gs, buf, 0, 1 << 30);
     if (!load) return;
     issue_loads_arm<MODE>(a, gl, bar);
     if (store) bulk_wait_read_n(0);

@@ -72,6 +72,13 @@ __device__ __forceinline__ void tma_coords(const TmaLine& t, int64_t b, int64_t 
     c[0] = 2 * (int)(l & ((1 << t.slog) - 1));
     c[1] = j0;
     c[2] = (int)(l >> t.slog);
+  } else if (t.kind == TMA_ELEM2) {  // dims {2S (line in tile), j % jd, j / jd, line tile, batch}
+    const int jd = (int)t.jd;
+    c[0] = 2 * (int)(l & ((1 << t.slog) - 1));
+    c[1] = j0 % jd;
+    c[2] = j0 / jd;
+    c[3] = (int)(l >> t.slog);
+    c[4] = (t.bcast & 1) ? 0 : (int)b;
   } else {                          // TMA_ELEM_TILED: dims {2S (j in tile), line, j tile, ...}
     c[0] = 0;
     c[1] = (int)l;
