@@ -728,15 +728,18 @@ static hd_status_t slab_dist(hd_ctx_t ctx, hd_dtype_t dtype, int ndim, const voi
     cudaEventRecord(D->evx, D->cs);
     cudaStreamWaitEvent(st, D->evx, 0);
   };
-  if ((s = stage(0, -1, g, nullptr, gt)) != HD_OK) return ctx_fail(ctx, s);
   const int64_t piece1 = ndim == 2 ? S.Ks * S.chunk_rows : S.block1;
   const int64_t piece2 = ndim == 2 ? S.Ro * S.chunk_cols : S.block2;
+  // 3-D: stage 1 reads the transformed g (the y forward of g's planes happens there)
+  if (ndim == 3 && (s = stage(0, -1, g, nullptr, gt)) != HD_OK) return ctx_fail(ctx, s);
   for (int c = 0; c < C; ++c) {
     if ((s = stage(1, c, f, nullptr, send1)) != HD_OK) return ctx_fail(ctx, s);
     if ((s = ndim == 2 ? exchange_cm(c, send1, recv1, S.block1, c, piece1)
                        : exchange(c, send1, recv1, S.block1, c * piece1, piece1)) != HD_OK)
       return s;
   }
+  // 2-D: g's forward pass (needed from pass B on) runs while the last exchanges fly
+  if (ndim == 2 && (s = stage(0, -1, g, nullptr, gt)) != HD_OK) return ctx_fail(ctx, s);
   join();
   for (int c = 0; c < C; ++c) {
     if ((s = stage(2, c, recv1, gt, send2)) != HD_OK) return ctx_fail(ctx, s);
