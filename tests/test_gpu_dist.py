@@ -162,7 +162,11 @@ def _emulate(ctx, H, dt, Lf, Lg, f, g, world, nchunks, plan):
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("Lf,Lg,m,nchunks", [((300, 260), (31, 17), (64, 64), 0),
                                              ((1100, 700), (255, 60), (512, 512), 3),
-                                             ((257, 4000), (20, 255), (128, 512), 2)])
+                                             ((257, 4000), (20, 255), (128, 512), 2),
+                                             # pieces that tile the lines (1024 rows, 1024
+                                             # spectral columns): the staged passes load
+                                             # recv1 / recv2 by TMA_ELEM2 at worlds 2 and 4
+                                             ((1024, 700), (255, 60), (512, 512), 2)])
 def test_slab2d_emulated_ranks(ctx, H, world, Lf, Lg, m, nchunks):
     f, g = synth.random_pair(3400 + world, Lf, Lg)
     plan = H.Plan.make(2, [{"m": m[0]}, {"m": m[1]}])
