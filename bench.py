@@ -535,16 +535,16 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int((fh_l.numel() + gh_l.numel()) * eb),
                "d2h_bytes_per_step": int(hh_l.numel() * eb), "steps": k2, "per": "rank (max over ranks)"}
     if not args.no_e2e and slab is None and shard is None:
-        # two result buffers: step k writes hh[k % 2] (asynchronous, double-buffered
-        # entry point: the copy-in of step k+1 overlaps the copy-out of step k)
-        hh = [torch.empty(out_shape, dtype=fd[0].dtype).pin_memory() for _ in range(2)]
+        # three result buffers: step k writes hh[k % 3] (asynchronous, triple-buffered
+        # entry point: copy-in k+2 | convolution k+1 | copy-out k)
+        hh = [torch.empty(out_shape, dtype=fd[0].dtype).pin_memory() for _ in range(3)]
         k2 = max(4, min(args.steps, 20))
         ctx.hd_conv_host(fh, gh, hh[0], ndim=ndim, batch=batch, plan=plan)
         if dist:
             dist.barrier()
         t = time.perf_counter()
         for k in range(k2):
-            ctx.hd_conv_host_async(fh, gh, hh[k % 2], ndim=ndim, batch=batch, plan=plan)
+            ctx.hd_conv_host_async(fh, gh, hh[k % 3], ndim=ndim, batch=batch, plan=plan)
         ctx.host_sync()
         te = time.perf_counter() - t
         if dist:

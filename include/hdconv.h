@@ -223,11 +223,11 @@ hd_status_t hd_conv_host(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N
                          const int64_t* M, const hd_plan_t* plan, void* stream);
 
 /* Asynchronous form of hd_conv_host: enqueues copy-in, convolution and copy-out
- * on one of two context-owned streams with their own device buffers, alternating
- * per call, and returns.  The copy-in of call k+1 overlaps the convolution and
- * copy-out of call k (the convolutions themselves run one after another: they
- * share the context workspace).  f, g, h must stay valid (and h unread) until
- * hd_host_sync returns; pinned host memory is needed for the copies to overlap.
+ * on one of three context-owned streams with their own device buffers, in turn per
+ * call, and returns.  The copy-in of call k+2, the convolution of call k+1 and the
+ * copy-out of call k can run at once (the convolutions themselves run one after
+ * another: they share the context workspace).  f, g, h must stay valid (and h unread)
+ * until hd_host_sync returns; pinned host memory is needed for the copies to overlap.
  * Errors in enqueueing are returned; kernel faults surface at hd_host_sync. */
 hd_status_t hd_conv_host_async(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int32_t N,
                                int64_t batch, const void* const* f, const int64_t* Lf,

@@ -39,12 +39,13 @@ struct hd_ctx {
   size_t io_size = 0;
   void* rio = nullptr;                  // hd_conv_real: packed input, complex g, complex result
   size_t rio_size = 0;
-  struct HostSlot {                     // hd_conv_host_async: double-buffered host I/O
+  struct HostSlot {                     // hd_conv_host_async: triple-buffered host I/O
     void* io = nullptr;
     size_t size = 0;
     cudaStream_t st = nullptr;
   };
-  HostSlot hslot[2];
+  static constexpr int kHostSlots = 3;  // copy-in k+2 | compute k+1 | copy-out k
+  HostSlot hslot[kHostSlots];
   int hnext = 0;
   // Context scratch (ws, io, rio, host slots) is shared by every call that passes
   // no workspace, whatever stream it is on: each such call waits for the previous
@@ -1685,7 +1686,7 @@ hd_status_t hd_conv_host_async(hd_ctx_t ctx, hd_dtype_t dtype, int32_t ndim, int
   std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
   hd_ctx::HostSlot& sl = ctx->hslot[ctx->hnext];
-  ctx->hnext ^= 1;
+  ctx->hnext = (ctx->hnext + 1) % hd_ctx::kHostSlots;
   cudaError_t e;
   if (!sl.st) {
     e = cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking);

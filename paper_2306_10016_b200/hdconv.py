@@ -667,7 +667,7 @@ class Context:
         return h
 
     def hd_conv_host_async(self, fs, gs, h, ndim, batch=1, M=None, plan=None):
-        """Asynchronous hd_conv_host (double-buffered context streams): returns after
+        """Asynchronous hd_conv_host (triple-buffered context streams): returns after
         enqueueing; the buffers must stay alive and h unread until host_sync()."""
         N = len(fs)
         def hp(a):

@@ -258,8 +258,8 @@ def test_host_entry_point(ctx):
 
 
 def test_host_async_pipeline(ctx):
-    """hd_conv_host_async: five calls in flight over the two context slots (copy-in
-    of call k+1 overlapping call k), different inputs, sizes and output buffers;
+    """hd_conv_host_async: five calls in flight over the three context slots (copy-in
+    of call k+2 | convolution k+1 | copy-out k), different inputs, sizes and output buffers;
     every result checked after one hd_host_sync."""
     shapes = [((64, 50), (10, 12)), ((40, 33), (7, 9)), ((64, 50), (10, 12)), ((90, 20), (3, 31)),
               ((64, 50), (10, 12))]
