@@ -511,6 +511,8 @@ int64_t     hd_launch_count(hd_ctx_t ctx);
                                    m = 512 (12 <= q <= 22) */
 #define HD_ENGINE_S2048R 5      /* 1-D pass of long lines, complex double, m = 2048, one CTA per
                                    line, residues in pairs (D = q <= 8, p <= 8) */
+#define HD_ENGINE_S4096R 6      /* 1-D pass of long lines, complex double, m = 4096, one CTA per
+                                   line, eight warps, one residue at a time (D = q <= 4, p <= 4) */
 int64_t     hd_engine_launches(hd_ctx_t ctx, int32_t engine);
 /* Calls served by replaying a captured CUDA graph (HD_FLAG_GRAPH) since creation;
  * -1 for a null context.  Replays do not add to hd_launch_count. */

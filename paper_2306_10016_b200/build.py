@@ -15,8 +15,8 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhdconv.so")
 BUILD = os.path.join(HERE, "csrc", "build")
-SOURCES = ["hd_kernels.cu", "hd_api.cu", "hd_dist.cu", "hd_filter.cu", "hd_k_s512.cu", "hd_k_s2048r.cu", "hd_k_s128.cu"] + [f"hd_k_{d}_{n}.cu" for d in ("f64", "f32") for n in (256, 576, 1024)]
-HEADERS = ["hd_device.cuh", "hd_internal.h", "hd_kernels.cuh", "hd_w512.cuh", "hd_s512.cuh", "hd_s2048r.cuh", "hd_w256.cuh", "hd_s128.cuh", "hd_s512c.cuh", "hd_tma.cuh"]
+SOURCES = ["hd_kernels.cu", "hd_api.cu", "hd_dist.cu", "hd_filter.cu", "hd_k_s512.cu", "hd_k_s2048r.cu", "hd_k_s4096r.cu", "hd_k_s128.cu"] + [f"hd_k_{d}_{n}.cu" for d in ("f64", "f32") for n in (256, 576, 1024)]
+HEADERS = ["hd_device.cuh", "hd_internal.h", "hd_kernels.cuh", "hd_w512.cuh", "hd_s512.cuh", "hd_s2048r.cuh", "hd_s4096r.cuh", "hd_w256.cuh", "hd_s128.cuh", "hd_s512c.cuh", "hd_tma.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-I" + INCLUDE, "-I" + CSRC]

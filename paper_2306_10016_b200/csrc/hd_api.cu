@@ -64,7 +64,7 @@ struct hd_ctx {
   };
   std::vector<ProfEntry> prof;
   int64_t launches = 0;
-  int64_t engine_launches[6] = {0, 0, 0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
+  int64_t engine_launches[7] = {0, 0, 0, 0, 0, 0, 0};  // pass launches per engine (HD_ENGINE_*)
   // HD_FLAG_GRAPH: captured pass sequences keyed by their full argument list
   std::map<std::string, cudaGraphExec_t> graphs;
   cudaStream_t capture_stream = nullptr;
@@ -301,7 +301,9 @@ hd_status_t complete_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, cons
     // the 1-D two-CTA cluster pass (hd_s512c.cuh) holds at most 11 residue rows per CTA;
     // the 1-D m = 2048 engine (hd_s2048r.cuh) keeps two residues in shared memory at a time
     const bool cluster_q = (x.m == 512 && x.q >= hd::kS512cQMin && x.q <= hd::kS512cQMax) ||
-                           (x.m == 2048 && x.q <= hd::s2048r_qmax() && x.pf <= 8 && x.pg <= 8);
+                           (x.m == 2048 && x.q <= hd::s2048r_qmax() && x.pf <= 8 && x.pg <= 8) ||
+                           (x.m == 4096 && x.q <= hd::s4096r_qmax() && x.pf <= hd::s4096r_pmax() &&
+                            x.pg <= hd::s4096r_pmax());
     const bool cluster_1d = dt == HD_C128 && ndim == 1 && npairs == 1 && cluster_q && x.D == x.q &&
                             x.lines == 1 && x.auto_engine && !(plan->flags & HD_FLAG_GENERIC_FFT);
     if (!cluster_1d && pass_smem(eb, x.q, x.lines, x.D, x.m, nbuf) > hd::kMaxSmem)
@@ -374,6 +376,13 @@ hd_status_t default_plan(hd_ctx* ctx, hd_dtype_t dt, int ndim, int npairs, const
       const bool p_ok = cdiv(Lf[i], 512) <= 8 && cdiv(Lg[i], 512) <= 8;
       const bool q_ok = (conv && npairs > 1) ? q5 <= 6 : q5 <= hd::kS512QMax;
       if (p_ok && q_ok) { bm = 512; bD = (int)q5; }
+    }
+    // 1-D complex double, long lines: m = 4096 where the one-CTA-per-line engine
+    // hd_s4096r.cuh runs (2 <= q <= 4, p <= 4; config 2: 1.43 ms at m = 2048 -> see DESIGN)
+    if (dt == HD_C128 && ndim == 1 && npairs == 1 && bm >= 1024 && !getenv("HD_NO_S4096R")) {
+      const int64_t q4 = cdiv(Mi, 4096);
+      if (q4 >= 2 && q4 <= hd::s4096r_qmax() && cdiv(Lf[i], 4096) <= hd::s4096r_pmax() &&
+          cdiv(Lg[i], 4096) <= hd::s4096r_pmax()) { bm = 4096; bD = (int)q4; }
     }
     // 1-D complex double at m = 2048: every residue in one pass (the one-CTA-per-line
     // engine, hd_s2048r.cuh, q <= 8, p <= 8)
@@ -659,18 +668,38 @@ bool use_s2048r(hd_dtype_t dt, const Launch& L) {
          o.j0 == 0 && o.L <= (int64_t)o.T * 2048 && f.L < (1 << 30) && g.L < (1 << 30);
 }
 
+// The 1-D m = 4096 engine (hd_s4096r.cuh): one pair of plain rows per line, every
+// residue (D = q <= 4), p <= 4, no output window offset.  HD_NO_S4096R=1: A/B switch.
+bool use_s4096r(hd_dtype_t dt, const Launch& L) {
+  static const bool off = getenv("HD_NO_S4096R") != nullptr;
+  if (off || dt != HD_C128 || L.m != 4096 || L.mode != hd::MODE_CONV || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
+  if (!L.auto_engine || !L.s512c_axis || L.a.D != L.a.q || L.a.q > hd::s4096r_qmax()) return false;
+  const PassArgs& a = L.a;
+  const LineIn &f = a.in_f, &g = a.in_g;
+  const LineOut& o = a.out;
+  if (a.q > 1 && a.scr == nullptr) return false;  // no residue slots (ws_regions)
+  return a.npairs == 1 && a.nbatch == 1 && f.p <= hd::s4096r_pmax() && g.p <= hd::s4096r_pmax() && f.tl >= 30 &&
+         f.s_j == 1 && f.jd <= 0 && g.tl >= 30 && g.s_j == 1 && g.jd <= 0 && o.tl >= 30 && o.so_log2 >= 30 &&
+         o.s_js == 1 && o.jd <= 0 && o.j0 == 0 && o.L <= (int64_t)o.T * 4096 && f.L < (1 << 30) && g.L < (1 << 30);
+}
+
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   const bool dbl = dt == HD_C128;
   hd::LaunchFn fn = nullptr;
   size_t smem = 0;
   int threads = L.threads;
-  const bool s2048r = use_s2048r(dt, L);
-  bool staged = !s2048r && use_s512(dt, L);
+  const bool s4096r = use_s4096r(dt, L);
+  const bool s2048r = !s4096r && use_s2048r(dt, L);
+  bool staged = !s2048r && !s4096r && use_s512(dt, L);
   bool mconv = false;
   const bool s128 = use_s128(dt, L);
-  const bool s512c = !staged && !s2048r && use_s512c(dt, L);
+  const bool s512c = !staged && !s2048r && !s4096r && use_s512c(dt, L);
   if (L.a.fam2 && (!staged || s128 || s512c)) return HD_ERR_UNSUPPORTED;
-  if (s2048r) {
+  if (s4096r) {
+    fn = hd::lookup_s4096r();
+    threads = hd::s4096r_threads();
+    smem = hd::s4096r_smem_bytes();
+  } else if (s2048r) {
     fn = hd::lookup_s2048r();
     threads = hd::s2048r_threads();
     smem = hd::s2048r_smem_bytes();
@@ -693,7 +722,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     prepare_tma(L);
     mconv = L.a.tm_in.kind == hd::TMA_LINE_TILED || L.a.tm_in.kind == hd::TMA_BULK;
   }
-  if (s128 || s512c || s2048r) {
+  if (s128 || s512c || s2048r || s4096r) {
     // set above
   } else if (mconv) {
     fn = hd::lookup_s512_mconv(L.a.q);
@@ -746,7 +775,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   static const bool dbg_launch = getenv("HD_DEBUG_LAUNCH") != nullptr;
   if (dbg_launch)
     fprintf(stderr, "[launch] %-8s engine=%s m=%d C=%d q=%d D=%d items=%lld threads=%d smem=%zu tma in=%d g=%d out=%d\n",
-            L.name, s2048r ? "s2048r" : s512c ? "s512c" : s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m,
+            L.name, s4096r ? "s4096r" : s2048r ? "s2048r" : s512c ? "s512c" : s128 ? "s128" : mconv ? "s512_mconv" : staged ? "s512" : "generic", L.m,
             L.lines, L.a.q, L.a.D,
             (long long)total, threads, smem, L.a.tm_in.kind, L.a.tm_in_g.kind, L.a.tm_out.kind);
   cudaError_t e = fn(L.a, grid, threads, smem, st);
@@ -767,7 +796,7 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
     }
   }
   if (!ctx->capturing) ctx->launches += 1;
-  if (!ctx->capturing) ctx->engine_launches[s2048r ? HD_ENGINE_S2048R : s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128
+  if (!ctx->capturing) ctx->engine_launches[s4096r ? HD_ENGINE_S4096R : s2048r ? HD_ENGINE_S2048R : s512c ? HD_ENGINE_S512C : s128 ? HD_ENGINE_S128
                        : mconv ? HD_ENGINE_S512_MCONV : staged ? HD_ENGINE_S512 : HD_ENGINE_GENERIC] += 1;
   if (ctx->profiling) {
     cudaEventRecord(e1, st);
@@ -839,6 +868,11 @@ size_t ws_regions(const Problem& P, std::vector<int64_t>& elems) {
     if (P.dt == HD_C128 && x.m == 2048 && x.q > 2 && x.q <= hd::s2048r_qmax() && P.N == 1) {
       const int64_t ctas = std::min<int64_t>(B, hd::device_sm_count());
       elems.push_back(ctas * 2 * (cdiv(x.q, 2) - 1) * 2048);
+    }
+    // residue slots of the 1-D m = 4096 engine: q - 1 per CTA (hd_s4096r.cuh)
+    if (P.dt == HD_C128 && x.m == 4096 && x.q > 1 && x.q <= hd::s4096r_qmax() && P.N == 1) {
+      const int64_t ctas = std::min<int64_t>(B, hd::device_sm_count());
+      elems.push_back(ctas * (hd::s4096r_qmax() - 1) * 4096);
     }
   } else if (P.ndim == 2) {
     const int64_t Kxp = pad16(a[1].M1), Sx = a[1].S;
@@ -1947,7 +1981,7 @@ int64_t hd_launch_count(hd_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 int64_t hd_graph_replays(hd_ctx_t ctx) { return ctx ? ctx->graph_replays : -1; }
 
 int64_t hd_engine_launches(hd_ctx_t ctx, int32_t engine) {
-  if (!ctx || engine < 0 || engine > HD_ENGINE_S2048R) return -1;
+  if (!ctx || engine < 0 || engine > HD_ENGINE_S4096R) return -1;
   return ctx->engine_launches[engine];
 }
 

@@ -22,6 +22,12 @@ LaunchFn lookup_s2048r();
 int s2048r_threads();
 int s2048r_qmax();
 size_t s2048r_smem_bytes();
+// 1-D convolution pass of long lines at m = 4096, one CTA per line (hd_s4096r.cuh), q <= 4, p <= 4
+LaunchFn lookup_s4096r();
+int s4096r_threads();
+int s4096r_qmax();
+int s4096r_pmax();
+size_t s4096r_smem_bytes();
 int s512c_threads(int q);
 size_t s512c_smem_bytes();
 size_t s512_smem_bytes(int q, int mode);

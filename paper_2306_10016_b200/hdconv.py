@@ -27,7 +27,8 @@ HD_FLAG_GENERIC_FFT = 0x4
 HD_FLAG_GRAPH = 0x8
 HD_FLAG_STAGED_ORDER = 0x10
 HD_FLAG_EXPLICIT_PLAN = 0x20
-HD_ENGINE_GENERIC, HD_ENGINE_S512, HD_ENGINE_S512_MCONV, HD_ENGINE_S128, HD_ENGINE_S512C, HD_ENGINE_S2048R = range(6)
+HD_ENGINE_GENERIC, HD_ENGINE_S512, HD_ENGINE_S512_MCONV, HD_ENGINE_S128, HD_ENGINE_S512C, HD_ENGINE_S2048R, \
+    HD_ENGINE_S4096R = range(7)
 HD_TUNE_PER_AXIS = 0x0
 HD_TUNE_EXHAUSTIVE = 0x1
 HD_MAX_DIM = 3

@@ -897,13 +897,45 @@ def test_s2048r_engine(ctx, H, B, Lf, Lg):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11, b
 
 
-def test_s2048r_shared_g_and_default_plan(ctx, H):
+def test_s2048r_shared_g(ctx, H):
     B = 6
     f, _ = synth.random_pair(4300, (B, 8192), (1,))
     g = synth.random_pair(4301, (3000,), (1,))[0]
     n0 = ctx.engine_launches(H.HD_ENGINE_S2048R)
-    h = host(ctx.conv(dev(f), dev(g), batch=True, shared_g=True))   # default plan: m = 2048, D = q
+    h = host(ctx.conv(dev(f), dev(g), plan=H.Plan.make(1, [{"m": 2048}]), batch=True, shared_g=True))
     assert ctx.engine_launches(H.HD_ENGINE_S2048R) - n0 == 1
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g)) < 1e-11
+
+
+# ---------------------------------------------------------------- 1-D m = 4096 engine (hd_s4096r.cuh)
+@pytest.mark.parametrize("B,Lf,Lg", [(5, 8192, 3000),    # config 2's lines: q = 3, p_f = 2, p_g = 1
+                                     (3, 5000, 200),     # q = 2
+                                     (2, 9000, 5000),    # q = 4, p_f = 3, p_g = 2
+                                     (2, 16384, 1),      # q = 4, p_f = 4, L_out = 4 m exactly
+                                     (4, 1000, 9000),    # f shorter than g (roles as given)
+                                     (3, 4096, 1),       # q = 1 (no residue slots)
+                                     (7, 4097, 4097),    # ragged blocks, q = 3
+                                     (150, 700, 4000)])  # more lines than SMs on small GPUs' grids
+def test_s4096r_engine(ctx, H, B, Lf, Lg):
+    f, g = synth.random_pair(4400 + Lf + Lg, (B, Lf), (B, Lg))
+    plan = H.Plan.make(1, [{"m": 4096}])
+    n0 = ctx.engine_launches(H.HD_ENGINE_S4096R)
+    h = host(ctx.conv(dev(f), dev(g), plan=plan, batch=True))
+    assert ctx.engine_launches(H.HD_ENGINE_S4096R) - n0 == 1
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11, b
+
+
+def test_s4096r_shared_g_and_default_plan(ctx, H):
+    B = 6
+    f, _ = synth.random_pair(4500, (B, 8192), (1,))
+    g = synth.random_pair(4501, (3000,), (1,))[0]
+    pc = H.hd_plan_complete(H.HD_C128, [8192], [3000], ctx.default_plan(H.HD_C128, [8192], [3000]))
+    assert (pc.axis[0].m, pc.axis[0].q, pc.axis[0].D) == (4096, 3, 3), pc.as_dict()
+    n0 = ctx.engine_launches(H.HD_ENGINE_S4096R)
+    h = host(ctx.conv(dev(f), dev(g), batch=True, shared_g=True))   # default plan: m = 4096, D = q
+    assert ctx.engine_launches(H.HD_ENGINE_S4096R) - n0 == 1
     for b in range(B):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g)) < 1e-11
 
