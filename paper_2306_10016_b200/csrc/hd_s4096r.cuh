@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
     if (rn == q) { rn = 0; ln = l + gridDim.x; }
     const bool more = ln < a.nlines;
     V cn0 = cmk<V>(1, 0), cn1 = cmk<V>(1, 0);
-    V ug[2][8];
+    const V* cf = coefs + rn * (kPMax * 8);
     if (more) {
       if (rn == 0 && tid == 0 && ln + gridDim.x < a.nlines) {
         bulk_prefetch_l2(F0 + line_off(fi, ln + gridDim.x), (uint32_t)Lf * 16u);
@@ -206,13 +206,13 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
       }
       cn0 = ldg(twM1 + rn * tid);          // zeta_{M1}^{rn n1}, rn n1 < M1
       cn1 = ldg(twM1 + rn * (tid + 256));
-      const V* cf = coefs + rn * (kPMax * 8);
       stage_fwd(u, F0 + line_off(fi, ln), Lf, fi.p, tid, cf);
-      stage_fwd(ug, G0 + line_off(gi, ln), Lg, gi.p, tid, cf);
     }
     cta_sync();
-    // Eg is free (every warp read its slice): park the next item's g there
+    // Eg is free (every warp read its slice): the next item's g goes there
     if (more) {
+      V ug[2][8];
+      stage_fwd(ug, G0 + line_off(gi, ln), Lg, gi.p, tid, cf);
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
