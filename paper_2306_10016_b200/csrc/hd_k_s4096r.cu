@@ -23,7 +23,7 @@ int s4096r_threads() { return s4096r::NT; }
 int s4096r_qmax() { return s4096r::kQMax; }
 int s4096r_pmax() { return s4096r::kPMax; }
 size_t s4096r_smem_bytes() {
-  return sizeof(double2) * (size_t)(3 * 4096 + w512::kTwRows * 32 + 8 * s4096r::kQMax * s4096r::kPMax);
+  return sizeof(double2) * (size_t)(3 * 4096 + w512::kTwRows * 32 + 8 * s4096r::kQMax * s4096r::kPMax) + 16;
 }
 
 }  // namespace hd

@@ -97,28 +97,58 @@ __device__ __forceinline__ void stage_fwd(V (*u)[8], const V* x, int L, int p, i
   else stage_fwd_p<kPMax>(u, x, L, p, tid, coef);
 }
 
-// Thread-private twiddles of residue r: TW[k2 * 512 + n1] = zeta_{M1}^{n1 (r + q k2)}
-// = c w^{k2}, c = zeta_{M1}^{r n1}, w = zeta_4096^{n1} (13 products, no table of M1)
-__device__ __forceinline__ void fill_tw(V* TW, V c0, V c1, V w0, V w1, int tid) {
+// the eight twiddles zeta_{M1}^{n1 (r + q k2)} = c om^{k2}, c = zeta_{M1}^{r n1},
+// om = zeta_4096^{n1}, in registers (13 products)
+__device__ __forceinline__ void tw_regs(V* t, V c_, V om) {
+  const V w2 = cmul(om, om), w3 = cmul(w2, om), w4 = cmul(w2, w2);
+  t[0] = c_;
+  t[1] = cmul(c_, om); t[2] = cmul(c_, w2); t[3] = cmul(c_, w3); t[4] = cmul(c_, w4);
+  t[5] = cmul(c_, cmul(w4, om)); t[6] = cmul(c_, cmul(w4, w2)); t[7] = cmul(c_, cmul(w4, w3));
+}
+// z^e for 0 <= e < kQMax
+__device__ __forceinline__ V zpow(V z, int e) {
+  V p = cmk<V>(1, 0);
+#pragma unroll
+  for (int i = 0; i < kQMax - 1; ++i)
+    if (i < e) p = cmul(p, z);
+  return p;
+}
+
+// stage A of one item (fold, DFT-8, twiddles) for f into Ef and g into Eg, at the
+// thread's own slots [k2 * 512 + n1]
+__device__ __forceinline__ void stage_item(V* Ef, V* Eg, const V* f, int Lf, int pf, const V* g, int Lg, int pg,
+                                           int r, int tid, const V* cf, const V* z, const V* om) {
+  V uf[2][8], ug[2][8];
+  stage_fwd(uf, f, Lf, pf, tid, cf);
+  stage_fwd(ug, g, Lg, pg, tid, cf);
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
-    const V c_ = c ? c1 : c0, w = c ? w1 : w0;
-    const V w2 = cmul(w, w), w3 = cmul(w2, w), w4 = cmul(w2, w2);
-    const V wk[8] = {cmk<V>(1, 0), w, w2, w3, w4, cmul(w4, w), cmul(w4, w2), cmul(w4, w3)};
-    const int n1 = tid + 256 * c;
-    TW[n1] = c_;
+    V t[8];
+    tw_regs(t, zpow(z[c], r), om[c]);
 #pragma unroll
-    for (int k2 = 1; k2 < 8; ++k2) TW[k2 * 512 + n1] = cmul(c_, wk[k2]);
+    for (int k2 = 0; k2 < 8; ++k2) {
+      const int i = k2 * 512 + tid + 256 * c;
+      Ef[i] = cmul(uf[c][k2], t[k2]);
+      Eg[i] = cmul(ug[c][k2], t[k2]);
+    }
   }
 }
 
+// Items (line l, residue r) in order.  Exchange areas: f alternates between EA and EC
+// (the item's forward exchange, then each warp's w512 area and inverse output), g
+// always EB.  Two CTA barriers per item: bar2 (stage A visible) and bar3 (inverse
+// outputs visible); the next item's stage A runs before bar3 -- its f into the other
+// f area (last read before this item's bar2), its g into EB once every warp has
+// read its EB slice (an mbarrier with one arrival per warp, so the writers wait for
+// the early reads, not for the other warps' transforms).
 __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  V* Ef = reinterpret_cast<V*>(smem_raw);
-  V* Eg = Ef + M;
-  V* TW = Eg + M;                       // [k2][n1] = zeta_{M1}^{n1 (r + q k2)}
-  V* twt = TW + M;                      // FFT-512 twiddle columns
+  V* EA = reinterpret_cast<V*>(smem_raw);
+  V* EC = EA + M;
+  V* EB = EC + M;
+  V* twt = EB + M;                      // FFT-512 twiddle columns
   V* coefs = twt + w512::kTwRows * 32;  // [r][t * 8 + n2] = zeta_{8q}^{r (8 t + n2)}
+  uint64_t* bar_b = reinterpret_cast<uint64_t*>(coefs + kQMax * kPMax * 8);
   const int q = a.q;
   const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
   const V* twm = reinterpret_cast<const V*>(a.tw_m);     // zeta_4096^k
@@ -133,10 +163,9 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
     const int r = i / (kPMax * 8), tn = i % (kPMax * 8);
     coefs[i] = ldg(twM1 + (int64_t)((r * tn) % (8 * q)) * 512);  // zeta_{8q}^e = zeta_{M1}^{512 e}
   }
+  if (tid == 0) mbar_init(bar_b, NT / 32);
   __syncthreads();
   const V* tw = twt + lane;
-  V* Efw = Ef + wp * 512;  // warp k2 = wp: its slice (stage exchange, then w512 area)
-  V* Egw = Eg + wp * 512;
   const LineIn& fi = a.in_f;
   const LineIn& gi = a.in_g;
   const LineOut& o = a.out;
@@ -146,59 +175,44 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
   const uint64_t pol = policy_evict_last(), pol_ef = policy_evict_first();
   const V* F0 = reinterpret_cast<const V*>(fi.ptr[0]);
   const V* G0 = reinterpret_cast<const V*>(gi.ptr[0]);
-  const V w0 = ldg(twm + tid), w1 = ldg(twm + tid + 256);  // zeta_4096^{n1}
-  // items (line l, residue r) in order; the next item's loads, fold and DFT-8 run
-  // before the current item's last barrier (they hide that barrier and its loads)
+  const V z[2] = {ldg(twM1 + tid), ldg(twM1 + tid + 256)};  // zeta_{M1}^{n1}
+  const V om[2] = {ldg(twm + tid), ldg(twm + tid + 256)};   // zeta_4096^{n1}
   int64_t l = blockIdx.x;
   if (l >= a.nlines) return;
-  V u[2][8];
   if (tid == 0 && l + gridDim.x < a.nlines) {
     bulk_prefetch_l2(F0 + line_off(fi, l + gridDim.x), (uint32_t)Lf * 16u);
     bulk_prefetch_l2(G0 + line_off(gi, l + gridDim.x), (uint32_t)Lg * 16u);
   }
-  fill_tw(TW, cmk<V>(1, 0), cmk<V>(1, 0), w0, w1, tid);
-  stage_fwd(u, F0 + line_off(fi, l), Lf, fi.p, tid, coefs);
-  {
-    V ug[2][8];
-    stage_fwd(ug, G0 + line_off(gi, l), Lg, gi.p, tid, coefs);
-#pragma unroll
-  for (int c = 0; c < 2; ++c)
-#pragma unroll
-    for (int k2 = 0; k2 < 8; ++k2) {
-      const int i = k2 * 512 + tid + 256 * c;
-      u[c][k2] = cmul(u[c][k2], TW[i]);
-      Eg[i] = cmul(ug[c][k2], TW[i]);  // thread-private positions until the first barrier
-    }
-  }
+  stage_item(EA, EB, F0 + line_off(fi, l), Lf, fi.p, G0 + line_off(gi, l), Lg, gi.p, 0, tid, coefs, z, om);
   int r = 0;
+  uint32_t it = 0;
+  bool cur_a = true;
 #pragma unroll 1
   while (true) {
-    cta_sync();  // Ef free: every warp is past the previous item's exchange reads
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) Ef[k2 * 512 + tid + 256 * c] = u[c][k2];
-    cta_sync();
+    V* Ecur = cur_a ? EA : EC;
+    V* Enxt = cur_a ? EC : EA;
+    V* Ew = Ecur + wp * 512;  // warp k2 = wp: its slice
+    cta_sync();  // bar2: this item's stage A is visible
     {
       V a_[16], b_[16];
+      const V* Bw = EB + wp * 512;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) { a_[i] = Efw[lane + 32 * i]; b_[i] = Egw[lane + 32 * i]; }
+      for (int i = 0; i < 16; ++i) { a_[i] = Ew[lane + 32 * i]; b_[i] = Bw[lane + 32 * i]; }
       __syncwarp();
-      w512::fft_fwd2(a_, b_, Efw, lane, tw, false);
+      if (lane == 0) mbar_arrive(bar_b);  // this warp is done with its EB slice
+      w512::fft_fwd2(a_, b_, Ew, lane, tw, false);
 #pragma unroll
       for (int k = 0; k < 16; ++k) a_[k] = cscale(cmul(a_[k], b_[k]), scale);
-      w512::fft_inv(a_, Efw, lane, tw);
+      w512::fft_inv(a_, Ew, lane, tw);
       __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) Efw[lane + 32 * i] = a_[i];
+      for (int i = 0; i < 16; ++i) Ew[lane + 32 * i] = a_[i];
     }
-    // the next item: its loads, fold and DFT-8 (twiddles after this item's inverse)
+    // the next item's stage A
     int64_t ln = l;
     int rn = r + 1;
     if (rn == q) { rn = 0; ln = l + gridDim.x; }
     const bool more = ln < a.nlines;
-    V cn0 = cmk<V>(1, 0), cn1 = cmk<V>(1, 0);
-    const V* cf = coefs + rn * (kPMax * 8);
     if (more) {
       // the next line into L2 while this line's last residue runs (a whole line ahead
       // measured 0.1 ms slower on config 2: the early copies evict lines still in use)
@@ -206,28 +220,23 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
         bulk_prefetch_l2(F0 + line_off(fi, ln + gridDim.x), (uint32_t)Lf * 16u);
         bulk_prefetch_l2(G0 + line_off(gi, ln + gridDim.x), (uint32_t)Lg * 16u);
       }
-      cn0 = ldg(twM1 + rn * tid);          // zeta_{M1}^{rn n1}, rn n1 < M1
-      cn1 = ldg(twM1 + rn * (tid + 256));
-      stage_fwd(u, F0 + line_off(fi, ln), Lf, fi.p, tid, cf);
+      mbar_wait(bar_b, it & 1u);  // every warp has read its EB slice
+      stage_item(Enxt, EB, F0 + line_off(fi, ln), Lf, fi.p, G0 + line_off(gi, ln), Lg, gi.p, rn, tid,
+                 coefs + rn * (kPMax * 8), z, om);
     }
-    cta_sync();
-    // Eg is free (every warp read its slice): the next item's g goes there
-    if (more) {
-      V ug[2][8];
-      stage_fwd(ug, G0 + line_off(gi, ln), Lg, gi.p, tid, cf);
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) Eg[k2 * 512 + tid + 256 * c] = ug[c][k2];
-    }
-    // this item: DFT-8^-1 over k2 for the thread's two n1
+    cta_sync();  // bar3: this item's inverse outputs are visible
+    // this item: conjugate twiddles and DFT-8^-1 over k2 for the thread's two n1
     V* h = reinterpret_cast<V*>(o.ptr[0]) + line_off(o, l);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int n1 = tid + 256 * c;
       V v[8];
+      {
+        V t[8];
+        tw_regs(t, zpow(z[c], r), om[c]);
 #pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) v[k2] = cmulc(Ef[k2 * 512 + n1], TW[k2 * 512 + n1]);
+        for (int k2 = 0; k2 < 8; ++k2) v[k2] = cmulc(Ecur[k2 * 512 + n1], t[k2]);
+      }
       dft8<V, -1>(v);
       if (r < q - 1) {
 #pragma unroll
@@ -255,19 +264,10 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
       }
     }
     if (!more) break;
-    // the next item's twiddles (this item's inverse has read TW), applied to its DFT-8
-    fill_tw(TW, cn0, cn1, w0, w1, tid);
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) {
-        const int i = k2 * 512 + tid + 256 * c;
-        const V t_ = TW[i];
-        u[c][k2] = cmul(u[c][k2], t_);
-        Eg[i] = cmul(Eg[i], t_);
-      }
+    cur_a = !cur_a;
     l = ln;
     r = rn;
+    ++it;
   }
 }
 
