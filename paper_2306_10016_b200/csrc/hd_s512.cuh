@@ -1073,8 +1073,8 @@ __global__ void __launch_bounds__(NTMAX, LEAN ? 2 : 1) s512_kernel(const __grid_
 // (p_g <= 8).  One work item = one line; the producer streams its N pairs through
 // the two-stage ring (stage = 2q rows: f_k folded into rows 0..q-1, g_k into rows
 // q..2q-1).  Warp r keeps the running sum of F_k G_k of residue r in registers:
-//   fold f_k, g_k (thread per column) -> F-FFT in row r (spectrum parked there,
-//   lane-major) -> G-FFT in row q + r -> acc += F G;  after the last pair:
+//   fold f_k, g_k (thread per column) -> F-FFT and G-FFT of rows r and q + r
+//   interleaved in registers (w512::fft_fwd2) -> acc += F G;  after the last pair:
 //   inverse FFT of (1/prod M1) acc -> row r -> unfold -> the producer stores.
 // q <= 6 (two stages of 2q rows), blockDim = 32 (q + 1): at most two warps per
 // SM sub-partition, so acc and a transform fit in registers.
@@ -1180,23 +1180,19 @@ __global__ void __launch_bounds__(NTMAX, 1) s512_mconv_kernel(const __grid_const
       fold_all<QC>(buf, a.in_f.p, (int)a.in_f.L, live, q, zt, twm, twcol, tid, nth);
       fold_all<QC>(buf + q * M, a.in_g.p, (int)a.in_g.L, live, q, zt, twm, twcol, tid, nth);
       compute_sync(nth);
-      V v[16];
+      // F_k and G_k of residue r transformed together, stage by stage (w512::fft_fwd2:
+      // independent chains; the single transforms back to back left the warp latency-bound)
+      V v[16], u[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = Fr[lane + 32 * i];
-      w512::fft_fwd(v, Fr, lane, tw);
+      for (int i = 0; i < 16; ++i) { v[i] = Fr[lane + 32 * i]; u[i] = Gr[lane + 32 * i]; }
       __syncwarp();
-#pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) Fr[k2 * 32 + lane] = v[k2];  // F-hat parked, lane-major
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = Gr[lane + 32 * i];
-      w512::fft_fwd(v, Gr, lane, tw);
-      __syncwarp();
+      w512::fft_fwd2(v, u, Fr, lane, tw, false);
       if (k == 0) {
 #pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cmul(Fr[k2 * 32 + lane], v[k2]);
+        for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cmul(v[k2], u[k2]);
       } else {
 #pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cfma(acc[k2], Fr[k2 * 32 + lane], v[k2]);
+        for (int k2 = 0; k2 < 16; ++k2) acc[k2] = cfma(acc[k2], v[k2], u[k2]);
       }
       if (k < N - 1) {
         mbar_arrive(&done[st]);  // stage free for the producer
