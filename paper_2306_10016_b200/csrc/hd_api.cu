@@ -2031,9 +2031,16 @@ hd_status_t hd_pass(hd_ctx_t ctx, hd_dtype_t dtype, const hd_pass_desc_t* d, voi
   const int C = ap.C ? ap.C : 1;
   if (!valid_lines(C)) return fail(ctx, HD_ERR_INVALID, "C must be 1, 2, 4, 8 or 16");
   const int q = (int)cdiv(d->M, ap.m);
-  const int D = ap.D ? ap.D : q;
+  int D = ap.D ? ap.D : q;
   if (D < 1 || D > q) return fail(ctx, HD_ERR_INVALID, "D must be in [1, q]");
   if (ap.threads && !valid_threads(ap.threads)) return fail(ctx, HD_ERR_INVALID, "bad threads");
+  // a D whose residue group does not fit the generic engine's shared memory is lowered
+  // (the engine walks the groups of D residues in turn and the results do not depend on
+  // D; e.g. the residue-sharded 1-D pass of hd_conv1d_dist at m = 4096, D = q = 3)
+  {
+    const int nb = d->mode == HD_PASS_CONV ? conv_nbuf(d->npairs) : 1;
+    while (D > 1 && pass_smem(elem_bytes(dtype), q, C, D, ap.m, nb) > hd::kMaxSmem) --D;
+  }
   const bool rrange = d->r_begin != 0 || (d->r_end != 0 && d->r_end != q);
   if (d->r_begin < 0 || d->r_end < 0 || d->r_end > q || (d->r_end != 0 && d->r_begin >= d->r_end) ||
       (d->r_end == 0 && d->r_begin != 0))

@@ -74,6 +74,18 @@ def test_conv1d_dist_world1(ctx, H, shard):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
 
 
+@pytest.mark.parametrize("shard", [0, 1])
+def test_conv1d_dist_world1_default_plan_long_lines(ctx, H, shard):
+    """config 2's line shape with the default plan (m = 4096, D = q = 3): batch sharding
+    runs the one-CTA-per-line engine, residue sharding the generic pass with D lowered to
+    what its shared memory holds."""
+    B, Lf, Lg = 3, 8192, 3000
+    f, g = synth.random_pair(3250 + shard, (B, Lf), (B, Lg))
+    h = host(ctx.conv1d_dist(dev(f), dev(g), B, shard=shard))
+    for b in range(B):
+        assert oracle.rel_l2(h[b], oracle.conv(f[b], g[b])) < 1e-11
+
+
 @pytest.mark.parametrize("q_parts", [[0, 1, 4, 7], [0, 3, 7], [0, 7]])
 def test_residue_ranges_sum_to_the_convolution(ctx, H, q_parts):
     """hd_pass CONV over residues [r_begin, r_end): the partial backward sums over a
