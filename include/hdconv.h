@@ -281,7 +281,10 @@ typedef struct {
   int32_t npairs;             /* arrays (FWD/INV) or pairs (CONV), 1..16 */
   int64_t nlines, nbatch;
   int64_t M;                  /* padded length along this axis; q = ceil(M/m) */
-  hd_axis_plan_t axis;        /* m, C, D (0 = q), threads (0 = automatic) */
+  hd_axis_plan_t axis;        /* m, C, D (0 = q), threads (0 = automatic); a D whose group of
+                                 C D m elements exceeds the generic engine's shared memory
+                                 is lowered until it fits (same results: the groups are
+                                 walked in turn) */
   hd_lines_t in_f, in_g, out;
   double scale;               /* CONV: product scale (1 / prod M1 over all axes) */
   int32_t batch_fastest;      /* 1: consecutive CTAs take consecutive batch entries */
