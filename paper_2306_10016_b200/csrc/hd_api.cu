@@ -669,7 +669,7 @@ bool use_s2048r(hd_dtype_t dt, const Launch& L) {
 }
 
 // The 1-D m = 4096 engine (hd_s4096r.cuh): one pair of plain rows per line, every
-// residue (D = q <= 4), p <= 4, no output window offset.  HD_NO_S4096R=1: A/B switch.
+// residue (D = q <= 4), p <= 4, output windows.  HD_NO_S4096R=1: A/B switch.
 bool use_s4096r(hd_dtype_t dt, const Launch& L) {
   static const bool off = getenv("HD_NO_S4096R") != nullptr;
   if (off || dt != HD_C128 || L.m != 4096 || L.mode != hd::MODE_CONV || (L.flags & HD_FLAG_GENERIC_FFT)) return false;
@@ -680,7 +680,7 @@ bool use_s4096r(hd_dtype_t dt, const Launch& L) {
   if (a.q > 1 && a.scr == nullptr) return false;  // no residue slots (ws_regions)
   return a.npairs == 1 && a.nbatch == 1 && f.p <= hd::s4096r_pmax() && g.p <= hd::s4096r_pmax() && f.tl >= 30 &&
          f.s_j == 1 && f.jd <= 0 && g.tl >= 30 && g.s_j == 1 && g.jd <= 0 && o.tl >= 30 && o.so_log2 >= 30 &&
-         o.s_js == 1 && o.jd <= 0 && o.j0 == 0 && o.L <= (int64_t)o.T * 4096 && f.L < (1 << 30) && g.L < (1 << 30);
+         o.s_js == 1 && o.jd <= 0 && o.j0 + o.L <= (int64_t)o.T * 4096 && f.L < (1 << 30) && g.L < (1 << 30);
 }
 
 hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
@@ -743,6 +743,10 @@ hd_status_t launch(hd_ctx* ctx, hd_dtype_t dt, Launch& L, cudaStream_t st) {
   } else {
     if (L.a.fam2) return HD_ERR_UNSUPPORTED;
     fn = hd::lookup_launcher(dbl, L.m, L.mode, L.threads);
+    // a 1-D plan validated for a one-CTA-per-line engine (D = q, hd_s2048r / hd_s4096r)
+    // that falls back here (e.g. an output window on s2048r) walks its residues in
+    // groups that fit (the results do not depend on D)
+    while (L.a.D > 1 && pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf) > hd::kMaxSmem) --L.a.D;
     smem = pass_smem(elem_bytes(dt), L.a.q, L.lines, L.a.D, L.m, L.nbuf);
   }
   if (!fn) return fail(ctx, HD_ERR_UNSUPPORTED, "no kernel instantiation for this m/threads");

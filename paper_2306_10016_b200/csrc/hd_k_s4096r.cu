@@ -6,7 +6,7 @@
 namespace hd {
 
 static cudaError_t launch_s4096r(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
-  auto kern = s4096r::s4096r_kernel;
+  auto kern = a.out.j0 != 0 ? s4096r::s4096r_kernel<true> : s4096r::s4096r_kernel<false>;
   if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt != s4096r::NT) return cudaErrorInvalidConfiguration;
   const int sms = device_sm_count();

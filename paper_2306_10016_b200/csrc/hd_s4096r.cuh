@@ -141,6 +141,9 @@ __device__ __forceinline__ void stage_item(V* Ef, V* Eg, const V* f, int Lf, int
 // f area (last read before this item's bar2), its g into EB once every warp has
 // read its EB slice (an mbarrier with one arrival per warp, so the writers wait for
 // the early reads, not for the other warps' transforms).
+// WIN: an output window with a nonzero start (separate instantiation: the window-free
+// kernel keeps its registers)
+template <bool WIN>
 __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V* EA = reinterpret_cast<V*>(smem_raw);
@@ -169,7 +172,9 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
   const LineIn& fi = a.in_f;
   const LineIn& gi = a.in_g;
   const LineOut& o = a.out;
-  const int Lf = (int)fi.L, Lg = (int)gi.L, Lout = (int)o.L, T = o.T;
+  // output window: positions [j0, j0 + Lout) of the full result,
+  // element j at h[j - j0]; T = ceil((j0 + Lout) / 4096) blocks are unfolded
+  const int Lf = (int)fi.L, Lg = (int)gi.L, T = o.T, j0 = WIN ? (int)o.j0 : 0, jend = j0 + (int)o.L;
   const double scale = a.scale;
   V* slots = reinterpret_cast<V*>(a.scr) + (int64_t)blockIdx.x * (kQMax - 1) * M;
   const uint64_t pol = policy_evict_last(), pol_ef = policy_evict_first();
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
     }
     cta_sync();  // bar3: this item's inverse outputs are visible
     // this item: conjugate twiddles and DFT-8^-1 over k2 for the thread's two n1
-    V* h = reinterpret_cast<V*>(o.ptr[0]) + line_off(o, l);
+    V* hw = reinterpret_cast<V*>(o.ptr[0]) + line_off(o, l) - j0;  // element j at hw[j]
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int n1 = tid + 256 * c;
@@ -253,12 +258,14 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
             w[rr] = rr == q - 1 ? v[n2] : (rr < q - 1 ? ld_slot(slots + rr * M + s, pol_ef) : cmk<V>(0, 0));
 #pragma unroll
           for (int t = 0; t < kQMax; ++t) {
-            if (t >= T || M * t + s >= Lout) break;
+            const int j = M * t + s;
+            if (t >= T || j >= jend) break;
+            if (WIN && j < j0) continue;
             V val = w[0];
 #pragma unroll
             for (int rr = 1; rr < kQMax; ++rr)
               if (rr < q) val = cfmac(val, w[rr], coefs[rr * (kPMax * 8) + 8 * t + n2]);
-            __stcs(h + M * t + s, val);
+            __stcs(hw + j, val);
           }
         }
       }

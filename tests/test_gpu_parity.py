@@ -939,3 +939,22 @@ def test_s4096r_shared_g_and_default_plan(ctx, H):
     for b in range(B):
         assert oracle.rel_l2(h[b], oracle.conv(f[b], g)) < 1e-11
 
+
+@pytest.mark.parametrize("m,lo,n", [(4096, 0, 11191),      # the whole output through the window path
+                                    (4096, 5, 300),        # inside the first block
+                                    (4096, 4000, 5000),    # across blocks 0-2
+                                    (4096, 11000, 191),    # the tail
+                                    (2048, 3000, 6000)])   # m = 2048: the generic fallback (D lowered)
+def test_long_line_windows(ctx, H, m, lo, n):
+    """1-D output windows of config 2's line shape on the one-CTA-per-line engine (m = 4096)
+    and through the generic fallback of an m = 2048 plan."""
+    B, Lf, Lg = 3, 8192, 3000
+    f, g = synth.random_pair(4600 + lo, (B, Lf), (B, Lg))
+    eng = H.HD_ENGINE_S4096R if m == 4096 else H.HD_ENGINE_GENERIC
+    n0 = ctx.engine_launches(eng)
+    h = host(ctx.conv_window([dev(f)], [dev(g)], [lo], [n], batch=True, plan=H.Plan.make(1, [{"m": m}])))
+    assert ctx.engine_launches(eng) - n0 == 1
+    for b in range(B):
+        ref = oracle.conv(f[b], g[b])[lo:lo + n]
+        assert h[b].shape == ref.shape and oracle.rel_l2(h[b], ref) < 1e-11, b
+
