@@ -309,6 +309,38 @@ __device__ __forceinline__ void fft_fwd(V* a, V* buf, const Ex& e, int c, int u,
   dft8<V, +1>(a + 8);
 }
 
+// two forward FFT-128s (rows of their own: exchanges ea, eb) interleaved stage by stage
+// -- independent chains for the convolution pass's F and G
+__device__ __forceinline__ void fft_fwd2(V* a, V* b, V* buf, const Ex& ea, const Ex& eb, int c, int u,
+                                         const V* t128) {
+  w512::dft16<+1, false, V>(a);
+  w512::dft16<+1, false, V>(b);
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) {
+    const V w = t128[(u * k1) & (M - 1)];
+    a[k1] = cmul(a[k1], w);
+    b[k1] = cmul(b[k1], w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) {
+    buf[ea.at(c, k1, u)] = a[k1];
+    buf[eb.at(c, k1, u)] = b[k1];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      a[8 * j + v] = buf[ea.at(c, 2 * u + j, v)];
+      b[8 * j + v] = buf[eb.at(c, 2 * u + j, v)];
+    }
+  dft8<V, +1>(a);
+  dft8<V, +1>(a + 8);
+  dft8<V, +1>(b);
+  dft8<V, +1>(b + 8);
+}
+
 // inverse (adjoint): a[8 j + k2] = Y[2u + j + 16 k2] in; out: a[i] = sum_f zeta^{-(u + 8i) f} Y[f]
 __device__ __forceinline__ void fft_inv(V* a, V* buf, const Ex& e, int c, int u, const V* t128) {
   dft8<V, -1>(a);
@@ -518,9 +550,8 @@ __global__ void __launch_bounds__(NT, MINB) s128_kernel(const __grid_constant__ 
     } else if constexpr (MODE == MODE_CONV) {
       V F[16], G[16];
       load_time(F, buf, li, c, u, r);
-      fft_fwd(F, buf, ex_of(li, il, r), c, u, t128);
       load_time(G, buf, li, c, u, Rg + r);
-      fft_fwd(G, buf, ex_of(li, il, Rg + r), c, u, t128);
+      fft_fwd2(F, G, buf, ex_of(li, il, r), ex_of(li, il, Rg + r), c, u, t128);
       const float sc = (float)a.scale;
 #pragma unroll
       for (int k = 0; k < 16; ++k) F[k] = cscale(cmul(F[k], G[k]), sc);
