@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
   // element j at h[j - j0]; T = ceil((j0 + Lout) / 4096) blocks are unfolded
   const int Lf = (int)fi.L, Lg = (int)gi.L, T = o.T, j0 = WIN ? (int)o.j0 : 0, jend = j0 + (int)o.L;
   const double scale = a.scale;
-  V* slots = reinterpret_cast<V*>(a.scr) + (int64_t)blockIdx.x * (kQMax - 1) * M;
+  // per-CTA residue slots (absent for q = 1: never touched then)
+  V* slots = a.scr ? reinterpret_cast<V*>(a.scr) + (int64_t)blockIdx.x * (kQMax - 1) * M : nullptr;
   const uint64_t pol = policy_evict_last(), pol_ef = policy_evict_first();
   const V* F0 = reinterpret_cast<const V*>(fi.ptr[0]);
   const V* G0 = reinterpret_cast<const V*>(gi.ptr[0]);
