@@ -130,3 +130,15 @@ def test_filter_dictionary_matches_paper(H, golden):
         assert w.shape == ref.shape and np.array_equal(w, ref)
     with pytest.raises(H.HDError):
         H.filter_kernel(8)
+
+
+def test_default_plan_long_1d_lines(H):
+    """Config 2's lines (8192 (*) 3000, c128): the default plan is m = 4096 with every
+    residue in one pass (q = 3, the one-CTA-per-line engine hd_s4096r.cuh), p_f = 2,
+    p_g = 1 (PAPER.md:564-567 at m = 4096, M = 11191); lines of q > 4 at m = 4096 keep
+    the cost model's pick."""
+    p = H.hd_plan_complete(H.HD_C128, [8192], [3000], H.hd_plan_default(H.HD_C128, [8192], [3000]))
+    a = p.axis[0]
+    assert (a.m, a.q, a.D, a.p_f, a.p_g, a.M1) == (4096, 3, 3, 2, 1, 12288)
+    p = H.hd_plan_complete(H.HD_C128, [30000], [3000], H.hd_plan_default(H.HD_C128, [30000], [3000]))
+    assert p.axis[0].m != 4096 or p.axis[0].q <= 4
