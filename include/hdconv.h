@@ -375,7 +375,7 @@ hd_status_t hd_conv1d_dist(hd_ctx_t ctx, hd_dtype_t dtype, int64_t batch, const 
  * 2-D overlap: pass A (forward along x) runs by row chunks and each chunk's all-to-all
  * starts on the communication stream as soon as its chunk is written; pass B
  * (convolution along y) runs by column chunks, each chunk's all-to-all likewise; pass C
- * (inverse along x) waits for the second exchange.  nchunks = 0: 4 (1 at nranks = 1). */
+ * (inverse along x) waits for the second exchange.  nchunks = 0: 2 (1 at nranks = 1). */
 typedef struct {
   int32_t ndim, nranks, rank, nchunks;
   int64_t in_lo, in_hi, out_lo, out_hi, spec_lo, spec_hi;

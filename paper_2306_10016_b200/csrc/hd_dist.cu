@@ -331,7 +331,7 @@ hd_status_t hd_dist_slab_plan(hd_dtype_t dtype, int32_t ndim, int32_t nranks, in
   const size_t eb = dtype == HD_C128 ? 16 : 8;
   const int64_t O0 = Lf[0] + Lg[0] - 1;
   if (ndim == 2) {
-    const int C = nchunks > 0 ? nchunks : (nranks > 1 ? 4 : 1);
+    const int C = nchunks > 0 ? nchunks : (nranks > 1 ? 2 : 1);  // 2 balances launch count and overlap
     o.nchunks = C;
     const int64_t Kx = p.axis[1].M1;
     o.chunk_rows = cdiv(cdiv(Lf[0], nranks), C);

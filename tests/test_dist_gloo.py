@@ -243,7 +243,7 @@ def test_slab2d_plan_config3(H):
     for world in (1, 2, 3, 4, 8):
         sps = [H.slab_plan(H.HD_C128, [4096, 4096], [255, 255], world, k) for k in range(world)]
         s0 = sps[0]
-        assert s0.nchunks == (4 if world > 1 else 1)
+        assert s0.nchunks == (2 if world > 1 else 1)
         assert s0.R == s0.nchunks * s0.chunk_rows and s0.Ks == s0.nchunks * s0.chunk_cols
         assert s0.R * world >= 4096 and s0.Ro * world >= 4350 and s0.Ks * world >= 4608
         for key, n in (("in", 4096), ("out", 4350), ("spec", 4608)):
