@@ -233,13 +233,13 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
     cta_sync();  // bar3: this item's inverse outputs are visible
     // this item: conjugate twiddles and DFT-8^-1 over k2 for the thread's two n1
     V* hw = reinterpret_cast<V*>(o.ptr[0]) + line_off(o, l) - j0;  // element j at hw[j]
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       const int n1 = tid + 256 * c;
       V v[8];
       {
         V t[8];
-        tw_regs(t, zpow(z[c], r), om[c]);
+        tw_regs(t, zpow(c ? z[1] : z[0], r), c ? om[1] : om[0]);
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) v[k2] = cmulc(Ecur[k2 * 512 + n1], t[k2]);
       }
