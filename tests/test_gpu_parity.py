@@ -958,3 +958,22 @@ def test_long_line_windows(ctx, H, m, lo, n):
         ref = oracle.conv(f[b], g[b])[lo:lo + n]
         assert h[b].shape == ref.shape and oracle.rel_l2(h[b], ref) < 1e-11, b
 
+
+
+def test_s4096r_graph_replay(ctx, H):
+    """HD_FLAG_GRAPH on the m = 4096 1-D engine (its residue slots live in the context
+    workspace): the replay matches the oracle and reads new inputs."""
+    B, Lf, Lg = 4, 8192, 3000
+    f, g = synth.random_pair(4700, (B, Lf), (B, Lg))
+    plan = H.Plan.make(1, [{"m": 4096}], flags=H.HD_FLAG_GRAPH)
+    fd, gd = dev(f), dev(g)
+    h = ctx.conv(fd, gd, plan=plan, batch=True)
+    r0 = ctx.graph_replays()
+    f2, g2 = synth.random_pair(4701, (B, Lf), (B, Lg))
+    fd.copy_(torch.from_numpy(f2).cuda())
+    gd.copy_(torch.from_numpy(g2).cuda())
+    ctx.conv(fd, gd, plan=plan, h=h, batch=True)
+    assert ctx.graph_replays() == r0 + 1
+    hh = host(h)
+    for b in range(B):
+        assert oracle.rel_l2(hh[b], oracle.conv(f2[b], g2[b])) < 1e-11, b
