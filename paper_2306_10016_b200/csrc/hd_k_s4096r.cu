@@ -6,7 +6,8 @@
 namespace hd {
 
 static cudaError_t launch_s4096r(const PassArgs& a, dim3 grid, int nt, size_t smem, cudaStream_t st) {
-  auto kern = a.out.j0 != 0 ? s4096r::s4096r_kernel<true> : s4096r::s4096r_kernel<false>;
+  auto kern = a.q <= 3 ? (a.out.j0 != 0 ? s4096r::s4096r_kernel<true, 3> : s4096r::s4096r_kernel<false, 3>)
+                       : (a.out.j0 != 0 ? s4096r::s4096r_kernel<true, 4> : s4096r::s4096r_kernel<false, 4>);
   if (cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
   if (nt != s4096r::NT) return cudaErrorInvalidConfiguration;
   const int sms = device_sm_count();

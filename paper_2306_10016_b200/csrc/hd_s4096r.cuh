@@ -105,17 +105,19 @@ __device__ __forceinline__ void tw_regs(V* t, V c_, V om) {
   t[1] = cmul(c_, om); t[2] = cmul(c_, w2); t[3] = cmul(c_, w3); t[4] = cmul(c_, w4);
   t[5] = cmul(c_, cmul(w4, om)); t[6] = cmul(c_, cmul(w4, w2)); t[7] = cmul(c_, cmul(w4, w3));
 }
-// z^e for 0 <= e < kQMax
+// z^e for 0 <= e < QM
+template <int QM>
 __device__ __forceinline__ V zpow(V z, int e) {
   V p = cmk<V>(1, 0);
 #pragma unroll
-  for (int i = 0; i < kQMax - 1; ++i)
+  for (int i = 0; i < QM - 1; ++i)
     if (i < e) p = cmul(p, z);
   return p;
 }
 
 // stage A of one item (fold, DFT-8, twiddles) for f into Ef and g into Eg, at the
 // thread's own slots [k2 * 512 + n1]
+template <int QM>
 __device__ __forceinline__ void stage_item(V* Ef, V* Eg, const V* f, int Lf, int pf, const V* g, int Lg, int pg,
                                            int r, int tid, const V* cf, const V* z, const V* om) {
   V uf[2][8], ug[2][8];
@@ -124,7 +126,7 @@ __device__ __forceinline__ void stage_item(V* Ef, V* Eg, const V* f, int Lf, int
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     V t[8];
-    tw_regs(t, zpow(z[c], r), om[c]);
+    tw_regs(t, zpow<QM>(z[c], r), om[c]);
 #pragma unroll
     for (int k2 = 0; k2 < 8; ++k2) {
       const int i = k2 * 512 + tid + 256 * c;
@@ -143,7 +145,9 @@ __device__ __forceinline__ void stage_item(V* Ef, V* Eg, const V* f, int Lf, int
 // the early reads, not for the other warps' transforms).
 // WIN: an output window with a nonzero start (separate instantiation: the window-free
 // kernel keeps its registers)
-template <bool WIN>
+// QM: compile-time bound on q (3: config 2's lines; the smaller unfold measured 3.6 %
+// faster than the general QM = 4)
+template <bool WIN, int QM>
 __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V* EA = reinterpret_cast<V*>(smem_raw);
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
     bulk_prefetch_l2(F0 + line_off(fi, l + gridDim.x), (uint32_t)Lf * 16u);
     bulk_prefetch_l2(G0 + line_off(gi, l + gridDim.x), (uint32_t)Lg * 16u);
   }
-  stage_item(EA, EB, F0 + line_off(fi, l), Lf, fi.p, G0 + line_off(gi, l), Lg, gi.p, 0, tid, coefs, z, om);
+  stage_item<QM>(EA, EB, F0 + line_off(fi, l), Lf, fi.p, G0 + line_off(gi, l), Lg, gi.p, 0, tid, coefs, z, om);
   int r = 0;
   uint32_t it = 0;
   bool cur_a = true;
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
         bulk_prefetch_l2(G0 + line_off(gi, ln + gridDim.x), (uint32_t)Lg * 16u);
       }
       mbar_wait(bar_b, it & 1u);  // every warp has read its EB slice
-      stage_item(Enxt, EB, F0 + line_off(fi, ln), Lf, fi.p, G0 + line_off(gi, ln), Lg, gi.p, rn, tid,
+      stage_item<QM>(Enxt, EB, F0 + line_off(fi, ln), Lf, fi.p, G0 + line_off(gi, ln), Lg, gi.p, rn, tid,
                  coefs + rn * (kPMax * 8), z, om);
     }
     cta_sync();  // bar3: this item's inverse outputs are visible
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
       V v[8];
       {
         V t[8];
-        tw_regs(t, zpow(c ? z[1] : z[0], r), c ? om[1] : om[0]);
+        tw_regs(t, zpow<QM>(c ? z[1] : z[0], r), c ? om[1] : om[0]);
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) v[k2] = cmulc(Ecur[k2 * 512 + n1], t[k2]);
       }
@@ -253,18 +257,18 @@ __global__ void __launch_bounds__(NT, 1) s4096r_kernel(const __grid_constant__ P
 #pragma unroll
         for (int n2 = 0; n2 < 8; ++n2) {
           const int s = n1 + 512 * n2;
-          V w[kQMax];
+          V w[QM];
 #pragma unroll
-          for (int rr = 0; rr < kQMax; ++rr)
+          for (int rr = 0; rr < QM; ++rr)
             w[rr] = rr == q - 1 ? v[n2] : (rr < q - 1 ? ld_slot(slots + rr * M + s, pol_ef) : cmk<V>(0, 0));
 #pragma unroll
-          for (int t = 0; t < kQMax; ++t) {
+          for (int t = 0; t < QM; ++t) {
             const int j = M * t + s;
             if (t >= T || j >= jend) break;
             if (WIN && j < j0) continue;
             V val = w[0];
 #pragma unroll
-            for (int rr = 1; rr < kQMax; ++rr)
+            for (int rr = 1; rr < QM; ++rr)
               if (rr < q) val = cfmac(val, w[rr], coefs[rr * (kPMax * 8) + 8 * t + n2]);
             __stcs(hw + j, val);
           }
